@@ -1,0 +1,22 @@
+"""CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
+
+A plain, slow, obviously-correct CPU implementation of the veScale-FSDP
+RaggedShard/DBuffer collective step (arxiv 2602.22437), written from
+/root/reference/PAPER.md (cited as P:<line>) and the readings of SURVEY.md
+§8(c) (listed in DESIGN.md "Readings").
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2602_22437_b200`` + ``librsdb.so``) never imports it, and this
+package imports nothing from the product path; the only shared module is
+``synth`` (seeded inputs and model shapes, no method arithmetic).
+
+Modules
+  planner  -- a1 granularity, a2 Alg. 1 planner (O1), validator, brute force,
+              a3 per-rank segment / quantization-block tables
+  dbuffer  -- a4/a5 AllGather + views, a6 grouped cast/scale, a7 ReduceScatter (O2, O3)
+  adam8    -- a8 block-wise 8-bit Adam (O4)
+
+Parity status of every function is stated in its docstring; all are pinned
+(tests/test_oracle_*.py) -- there is no "parity unpinned" function.
+"""

@@ -1,0 +1,134 @@
+"""Oracle block-wise 8-bit Adam: step a8.  SURVEY.md §8(c) O4.
+TEST INFRASTRUCTURE ONLY.
+
+PAPER.md P:419: "8-bit Adam applies *block-wise* INT8 quantization to the
+gradient statistics ... each device quantizes its local shard independently
+without any communication".  P:344: FP32 master weights.  The paper does not
+print the update; the readings are SURVEY R9 (linear absmax code, zero absmax
+-> zero codes), R10 (contiguous q-element blocks per tensor), R11 (torch
+AdamW order, host fp64 scalars rounded to fp32, the update uses the fresh
+fp32 m, v before requantization).
+
+Per quant block (block = contiguous elements of one tensor, tail shorter),
+every op below is one IEEE fp32 operation, in this order:
+  1. mt = q_m * fl(A_m / 127)                 dequantize first moment (signed)
+  2. vt = q_v * fl(A_v / 255)                 dequantize second moment (unsigned)
+  3. m  = mt + w1 * (g - mt)                  w1 = fl(1 - beta1)   (torch lerp, weight < 0.5)
+  4. v  = b2 * vt + w2 * (g * g)              b2 = fl(beta2), w2 = fl(1 - beta2)
+  5. p  = p * c_wd                            c_wd = fl(1 - lr * wd)   (decoupled decay)
+  6. p  = p - step_size * (m / (sqrt(v) / bc2s + eps))
+                                              step_size = fl(lr / (1 - beta1^t)),
+                                              bc2s = fl(sqrt(1 - beta2^t))
+  7. A_m' = max |m|,  A_v' = max v            over the block
+  8. q_m = clamp(rint(m / fl(A_m'/127)), -127, 127)   (int8)
+     q_v = clamp(rint(v / fl(A_v'/255)),    0, 255)   (uint8); A' = 0 -> codes 0
+  9. param shard for the next AllGather = bf16_RNE(p)  (or p itself for fp32 units)
+
+Parity pins (tests/test_oracle_adam8.py): step-1 closed form from the zero
+state, the identity-codec variant equals torch.optim.AdamW (library routine),
+codec round trip / error bound / zero block, shard-local = unsharded result
+(containment).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence, Tuple
+
+import numpy as np
+
+from .dbuffer import to_bf16_rne
+
+f32 = np.float32
+
+
+@dataclass(frozen=True)
+class AdamCfg:
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 1e-2
+
+
+def host_scalars(cfg: AdamCfg, step: int) -> dict:
+    """Per-step scalars, computed in fp64 then rounded to fp32 (R11)."""
+    if step < 1:
+        raise ValueError("step must be >= 1")
+    return {
+        "w1": f32(1.0 - cfg.beta1),
+        "b2": f32(cfg.beta2),
+        "w2": f32(1.0 - cfg.beta2),
+        "eps": f32(cfg.eps),
+        "c_wd": f32(1.0 - cfg.lr * cfg.weight_decay),
+        "step_size": f32(cfg.lr / (1.0 - cfg.beta1 ** step)),
+        "bc2s": f32(np.sqrt(1.0 - cfg.beta2 ** step)),
+    }
+
+
+def dequantize(codes: np.ndarray, absmax: f32, signed: bool) -> np.ndarray:
+    levels = f32(127.0) if signed else f32(255.0)
+    scale = f32(f32(absmax) / levels)
+    return (codes.astype(np.float32) * scale).astype(np.float32)
+
+
+def quantize(x: np.ndarray, signed: bool) -> Tuple[np.ndarray, f32]:
+    """Linear absmax code of one block (R9); returns (codes, absmax)."""
+    x = np.asarray(x, dtype=np.float32)
+    a = f32(np.max(np.abs(x))) if x.size else f32(0)
+    if a == 0:
+        return np.zeros(x.shape, np.int8 if signed else np.uint8), f32(0)
+    if signed:
+        scale = f32(a / f32(127.0))
+        q = np.clip(np.rint((x / scale).astype(np.float32)), -127, 127).astype(np.int8)
+    else:
+        scale = f32(a / f32(255.0))
+        q = np.clip(np.rint((x / scale).astype(np.float32)), 0, 255).astype(np.uint8)
+    return q, a
+
+
+def adam_block_update(p, g, mt, vt, sc):
+    """Steps 3-6 on fp32 arrays (shared by the 8-bit and identity-codec
+    variants); returns (p_new, m, v)."""
+    g = np.asarray(g, dtype=np.float32)
+    m = (mt + sc["w1"] * (g - mt).astype(np.float32)).astype(np.float32)
+    v = (sc["b2"] * vt + sc["w2"] * (g * g).astype(np.float32)).astype(np.float32)
+    p = (p * sc["c_wd"]).astype(np.float32)
+    denom = (np.sqrt(v).astype(np.float32) / sc["bc2s"] + sc["eps"]).astype(np.float32)
+    p = (p - sc["step_size"] * (m / denom).astype(np.float32)).astype(np.float32)
+    return p, m, v
+
+
+def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: np.ndarray,
+                   m_abs: np.ndarray, v_abs: np.ndarray, blocks: Sequence[Tuple[int, int]],
+                   cfg: AdamCfg, step: int, out_bf16: bool = True):
+    """One 8-bit Adam step on a rank's local shard, block by block.
+
+    master/grad: fp32 [S]; m_q int8 [S]; v_q uint8 [S]; m_abs/v_abs fp32
+    [len(blocks)]; blocks = rank_blocks(...) table of (local offset, len).
+    Returns new copies (master, m_q, v_q, m_abs, v_abs, param_shard) where
+    param_shard is bf16 bit patterns (uint16) or fp32; positions outside any
+    block are left unchanged (param shard: 0)."""
+    sc = host_scalars(cfg, step)
+    master = np.array(master, dtype=np.float32, copy=True)
+    m_q, v_q = np.array(m_q, copy=True), np.array(v_q, copy=True)
+    m_abs = np.array(m_abs, dtype=np.float32, copy=True)
+    v_abs = np.array(v_abs, dtype=np.float32, copy=True)
+    param = np.zeros(master.shape, np.uint16 if out_bf16 else np.float32)
+    for b, (off, n) in enumerate(blocks):
+        s = slice(off, off + n)
+        mt = dequantize(m_q[s], m_abs[b], signed=True)
+        vt = dequantize(v_q[s], v_abs[b], signed=False)
+        p, m, v = adam_block_update(master[s], grad[s], mt, vt, sc)
+        master[s] = p
+        m_q[s], m_abs[b] = quantize(m, signed=True)
+        v_q[s], v_abs[b] = quantize(v, signed=False)
+        param[s] = to_bf16_rne(p) if out_bf16 else p
+    return master, m_q, v_q, m_abs, v_abs, param
+
+
+def step_adam_fp32_states(master, grad, m, v, cfg: AdamCfg, step: int):
+    """Identity-codec variant (states kept in fp32, no quantization): the
+    special case that must reduce to torch.optim.AdamW (pin)."""
+    sc = host_scalars(cfg, step)
+    return adam_block_update(np.asarray(master, np.float32), grad,
+                             np.asarray(m, np.float32), np.asarray(v, np.float32), sc)

@@ -1,0 +1,164 @@
+"""Pins for oracle/adam8.py: step-1 closed form (bias corrections cancel),
+identity-codec variant = torch.optim.AdamW (library routine), codec round
+trip / bound / zero block, and containment: the sharded
+step equals the unsharded step bit for bit."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import adam8 as A
+from oracle import dbuffer as D
+from oracle import planner as P
+from synth import hashgen as H
+
+
+def _zero_state(S, nb):
+    return (np.zeros(S, np.int8), np.zeros(S, np.uint8),
+            np.zeros(nb, np.float32), np.zeros(nb, np.float32))
+
+
+def test_step1_closed_form():
+    """From the zero state: p1 = p0 (1 - lr wd) - lr g / (|g| + eps)."""
+    cfg = A.AdamCfg()
+    S = 4 * 2048 + 100
+    p0 = H.params_np(0, 0, S)
+    g = H.grads_np(0, 0, 0, S)
+    blocks = [(i * 2048, min(2048, S - i * 2048)) for i in range(-(-S // 2048))]
+    mq, vq, ma, va = _zero_state(S, len(blocks))
+    p1 = A.step_8bit_adam(p0, g, mq, vq, ma, va, blocks, cfg, 1)[0]
+    exp = p0.astype(np.float64) * (1 - cfg.lr * cfg.weight_decay) \
+        - cfg.lr * g.astype(np.float64) / (np.abs(g.astype(np.float64)) + cfg.eps)
+    assert np.max(np.abs(p1 - exp)) < 1e-8
+
+
+def test_identity_codec_matches_torch_adamw():
+    cfg = A.AdamCfg(lr=3e-3, weight_decay=0.05)
+    n = 5000
+    rng = np.random.default_rng(0)
+    p = rng.normal(0, 0.02, n).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    tp = torch.nn.Parameter(torch.from_numpy(p.copy()))
+    opt = torch.optim.AdamW([tp], lr=cfg.lr, betas=(cfg.beta1, cfg.beta2), eps=cfg.eps,
+                            weight_decay=cfg.weight_decay, foreach=False, fused=False)
+    for step in range(1, 6):
+        g = rng.normal(0, 1e-3, n).astype(np.float32)
+        p, m, v = A.step_adam_fp32_states(p, g, m, v, cfg, step)
+        tp.grad = torch.from_numpy(g.copy())
+        opt.step()
+        ref = tp.detach().numpy()
+        assert np.max(np.abs(p - ref) / (np.abs(ref) + cfg.lr)) < 1e-6
+
+
+def test_codec_properties():
+    # zero block -> zero codes, zero absmax, exact round trip
+    q, a = A.quantize(np.zeros(2048, np.float32), signed=True)
+    assert a == 0 and not q.any()
+    assert not A.dequantize(q, a, True).any()
+    # block = c * [-127..127] -> exact round trip
+    c = np.float32(2.0 ** -9)
+    x = (np.arange(-127, 128, dtype=np.float32) * c).astype(np.float32)
+    q, a = A.quantize(x, signed=True)
+    assert a == 127 * c and np.array_equal(A.dequantize(q, a, True), x)
+    x = (np.arange(0, 256, dtype=np.float32) * c).astype(np.float32)
+    q, a = A.quantize(x, signed=False)
+    assert np.array_equal(A.dequantize(q, a, False), x)
+    # |x - deq(q(x))| <= A/254 (signed), A/510 (unsigned), up to fp32 rounding
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        x = (rng.normal(0, 1, 2048) * np.exp2(rng.integers(-30, 5))).astype(np.float32)
+        q, a = A.quantize(x, True)
+        assert np.all(np.abs(x - A.dequantize(q, a, True)) <= a / 254 * (1 + 1e-6))
+        q, a = A.quantize(np.abs(x), False)
+        assert np.all(np.abs(np.abs(x) - A.dequantize(q, a, False)) <= a / 510 * (1 + 1e-6))
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 8])
+def test_sharded_step_equals_unsharded(m):
+    """Containment: with 2048-element blocks kept whole by the
+    planner, each rank's local step equals the single-rank step exactly."""
+    es = [256 * 128, 256, 5000, 2048 * 3, 77]
+    q = 2048
+    gs = [min(q, e) for e in es]
+    cfg = A.AdamCfg()
+    E = sum(es)
+    p_log = H.params_np(1, 0, E)
+    g_log = H.grads_np(1, 0, 0, E)
+    mq_log = H.codes_np(1, H.STREAM_MCODE, 0, E, True)
+    vq_log = H.codes_np(1, H.STREAM_VCODE, 0, E, False)
+
+    def run(mm):
+        lay = P.plan(es, gs, mm, 4)
+        bufs = {k: D.place_logical(lay, v) for k, v in
+                dict(p=p_log, g=g_log, mq=mq_log, vq=vq_log).items()}
+        out = {k: np.zeros_like(v) for k, v in bufs.items() if k != "g"}
+        out["bf"] = np.zeros(mm * lay.S, np.uint16)
+        for r in range(mm):
+            blocks = P.rank_blocks(lay, r, q)
+            sl = slice(r * lay.S, (r + 1) * lay.S)
+            # absmax indexed per block: derive from a per-(tensor,block) id so
+            # both layouts see the same initial state
+            ids = _block_ids(lay, r, q)
+            ma = H.absmax_np(1, H.STREAM_ABSM, 0, 10 ** 4, 14)[ids]
+            va = H.absmax_np(1, H.STREAM_ABSV, 0, 10 ** 4, 20)[ids]
+            res = A.step_8bit_adam(bufs["p"][sl], bufs["g"][sl], bufs["mq"][sl], bufs["vq"][sl],
+                                   ma, va, blocks, cfg, 4)
+            out["p"][sl], out["mq"][sl], out["vq"][sl] = res[0], res[1], res[2]
+            out["bf"][sl] = res[5]
+        return lay, out
+
+    lay1, o1 = run(1)
+    layk, ok = run(m)
+    for key in o1:
+        v1 = np.concatenate(D.views(lay1, o1[key]))
+        vk = np.concatenate(D.views(layk, ok[key]))
+        assert np.array_equal(v1.view(np.uint8), vk.view(np.uint8)), key
+
+
+def _block_ids(lay, rank, q):
+    ids = []
+    lo = rank * lay.S
+    base = 0
+    for l, e in zip(lay.starts, lay.numel):
+        for j in range(-(-e // q)):
+            a = l + j * q
+            if lo <= a < lo + lay.S:
+                ids.append(base + j)
+        base += -(-e // q)
+    return np.array(ids, dtype=np.int64)
+
+
+def test_8bit_step_composes_codec_and_torch_pinned_update():
+    """The 8-bit step = dequantize (pinned by the codec tests) -> the fp32
+    update (pinned to torch AdamW) -> quantize, block by block: catches wiring
+    mistakes (swapped m/v absmax, wrong block index, wrong signedness)."""
+    cfg = A.AdamCfg()
+    S, q = 5 * 2048 + 300, 2048
+    blocks = [(i * q, min(q, S - i * q)) for i in range(-(-S // q))]
+    p0 = H.params_np(5, 0, S)
+    g = H.grads_np(5, 0, 0, S)
+    mq = H.codes_np(5, H.STREAM_MCODE, 0, S, True)
+    vq = H.codes_np(5, H.STREAM_VCODE, 0, S, False)
+    ma = H.absmax_np(5, H.STREAM_ABSM, 0, len(blocks), 12)
+    va = H.absmax_np(5, H.STREAM_ABSV, 0, len(blocks), 22)
+    out = A.step_8bit_adam(p0, g, mq, vq, ma, va, blocks, cfg, 7)
+    for b, (off, n) in enumerate(blocks):
+        s = slice(off, off + n)
+        mt = A.dequantize(mq[s], ma[b], True)
+        vt = A.dequantize(vq[s], va[b], False)
+        p, m, v = A.step_adam_fp32_states(p0[s], g[s], mt, vt, cfg, 7)
+        assert np.array_equal(out[0][s], p)
+        qm, am = A.quantize(m, True)
+        qv, av = A.quantize(v, False)
+        assert np.array_equal(out[1][s], qm) and out[3][b] == am
+        assert np.array_equal(out[2][s], qv) and out[4][b] == av
+
+
+def test_bf16_output_is_rne_of_master():
+    S = 2048
+    p0 = H.params_np(2, 0, S)
+    g = H.grads_np(2, 0, 0, S)
+    mq, vq, ma, va = _zero_state(S, 1)
+    res = A.step_8bit_adam(p0, g, mq, vq, ma, va, [(0, S)], A.AdamCfg(), 1)
+    t = torch.from_numpy(res[0]).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(res[5], t)

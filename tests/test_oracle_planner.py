@@ -1,0 +1,318 @@
+"""Pins for oracle/planner.py against what the paper and mathematics fix
+(not against itself): SPEC worked examples (hand-checked), closed forms,
+the textbook linear-partition special case, exhaustive brute force with the
+2-approximation bound of P:287, and the Fig. 9 padding claims of P:489."""
+import random
+import time
+
+import numpy as np
+import pytest
+
+from oracle import planner as P
+from synth import workloads as W
+
+
+# ---------------------------------------------------------------- validator
+def test_validator_constraints():
+    # valid plan -> []; boundary 4 at offset 4 of a g=3 tensor; overlap.
+    ok = P.Layout(2, 1, [4, 4], [4, 4], 4, [0, 4])
+    assert P.validate(ok) == []
+    bad = P.Layout(2, 1, [6], [3], 4, [0])
+    v = P.validate(bad)
+    assert len(v) == 1 and "sharded block" in v[0]
+    ov = P.Layout(2, 1, [4, 4], [1, 1], 4, [0, 2])
+    assert any("overlap" in s for s in P.validate(ov))
+    cap = P.Layout(2, 1, [4], [1], 2, [1])
+    assert any("capacity" in s for s in P.validate(cap))
+    al = P.Layout(2, 4, [4], [1], 6, [0])
+    assert any("g_coll" in s for s in P.validate(al))
+
+
+# ----------------------------------------------------------- SPEC examples
+def test_spec_check_valid_shard_examples():
+    # S:145 exact fit; S:146 capacity bound.
+    ok, ls = P.feasible([4, 4], [4, 4], 2, 4)
+    assert ok and ls == [0, 4]
+    assert not P.feasible([6, 4], [3, 2], 2, 4)[0]
+    # S:147 claims S=5 feasible with t2 in [8,10) -- a 2-element interval for a
+    # 4-element tensor.  Exhaustive search: infeasible.
+    assert not P.exists_layout([6, 4], [3, 2], 2, 5)
+    assert not P.feasible([6, 4], [3, 2], 2, 5)[0]
+
+
+def test_spec_plan_examples():
+    lay = P.plan([6, 4], [3, 2], 2, 1)            # S:155 (S*=6), S:166 layout
+    assert lay.S == 6 and lay.starts == [0, 6] and lay.padding_intervals() == [(10, 12)]
+    assert lay.padding_ratio == pytest.approx(0.2)
+    lay = P.plan([8], [1], 2, 1)
+    assert lay.S == 4 and lay.padding == 0
+    lay = P.plan([4, 4], [4, 4], 2, 1)
+    assert lay.starts == [0, 4] and lay.padding == 0
+    lay = P.plan([10], [5], 3, 1)
+    assert lay.S == 5 and lay.starts == [0] and lay.padding_intervals() == [(10, 15)]
+
+
+def test_spec_brute_force_examples():
+    assert P.brute_force_min_shard([8], [1], 2, 1) == 4
+    assert P.brute_force_min_shard([9], [9], 2, 1) == 9
+    assert P.brute_force_min_shard([6, 4], [3, 2], 2, 1) == 6  # S:185 corrected (App. B)
+
+
+def test_empty_and_errors():
+    lay = P.plan([], [], 4, 8)
+    assert lay.S == 0 and lay.padding == 0
+    with pytest.raises(ValueError):
+        P.plan([4], [0], 2, 1)
+    with pytest.raises(ValueError):
+        P.plan([0], [1], 2, 1)
+    with pytest.raises(ValueError):
+        P.plan([4], [1], 0, 1)
+
+
+# ------------------------------------------------------------- closed forms
+def test_element_granularity_closed_form():
+    rng = random.Random(1)
+    for _ in range(300):
+        n = rng.randint(1, 12)
+        es = [rng.randint(1, 5000) for _ in range(n)]
+        m = rng.choice([1, 2, 3, 4, 7, 8, 16])
+        gc = rng.choice([1, 2, 4, 8, 16])
+        lay = P.plan(es, [1] * n, m, gc)
+        E = sum(es)
+        assert lay.S == -(-(-(-E // m)) // gc) * gc
+        assert P.validate(lay) == []
+        assert lay.padding < m * gc
+
+
+def _painter(es, m):
+    """Textbook linear partition: min over <= m contiguous groups of the max
+    group sum (O(n^2 m) DP)."""
+    n = len(es)
+    pre = [0]
+    for e in es:
+        pre.append(pre[-1] + e)
+    INF = float("inf")
+    best = [[INF] * (n + 1) for _ in range(m + 1)]
+    best[0][0] = 0
+    for j in range(1, m + 1):
+        for i in range(n + 1):
+            best[j][i] = best[j - 1][i]
+            for k in range(i):
+                best[j][i] = min(best[j][i], max(best[j - 1][k], pre[i] - pre[k]))
+    return best[m][n]
+
+
+def test_whole_tensor_blocks_is_linear_partition():
+    rng = random.Random(2)
+    for _ in range(300):
+        n = rng.randint(1, 9)
+        es = [rng.randint(1, 300) for _ in range(n)]
+        m = rng.randint(1, 6)
+        gc = rng.choice([1, 2, 4, 8])
+        lay = P.plan(es, es, m, gc)
+        assert P.validate(lay) == []
+        opt = _painter(es, m)
+        assert lay.S == -(-opt // gc) * gc
+
+
+# ------------------------------------------------------------- brute force
+def _rand_instance(rng):
+    n = rng.randint(1, 6)
+    es, gs = [], []
+    budget = 256
+    for _ in range(n):
+        g = rng.randint(1, 8)
+        u = rng.randint(1, max(1, min(8, (budget - n) // (g * n))))
+        e = g * u
+        if rng.random() < 0.25 and e > 1:      # non-dividing tail block (R5)
+            e -= rng.randint(1, min(g - 1, e - 1)) if g > 1 else 0
+        es.append(max(1, e))
+        gs.append(g)
+    return es, gs, rng.randint(1, 4), rng.choice([1, 2, 4])
+
+
+def test_greedy_check_is_exact():
+    """R1: leftmost placement decides CheckValidShard exactly (fixed order)."""
+    rng = random.Random(3)
+    checks = 0
+    for _ in range(300):
+        es, gs, m, gc = _rand_instance(rng)
+        E = sum(es)
+        for S in range(max(1, -(-E // m)), E + 9):
+            assert P.feasible(es, gs, m, S)[0] == P.exists_layout(es, gs, m, S), (es, gs, m, S)
+            checks += 1
+    assert checks > 2000
+
+
+def test_two_approximation_vs_brute_force():
+    """Acceptance S:504 / P:287: S_opt <= S* <= 2 S_opt on >= 1000 instances."""
+    rng = random.Random(4)
+    exact = 0
+    N = 1000
+    for _ in range(N):
+        es, gs, m, gc = _rand_instance(rng)
+        lay = P.plan(es, gs, m, gc)
+        assert P.validate(lay) == []
+        opt = P.brute_force_min_shard(es, gs, m, gc)
+        assert opt <= lay.S <= 2 * opt, (es, gs, m, gc, lay.S, opt)
+        exact += lay.S == opt
+    assert exact / N > 0.97
+
+
+def test_non_monotone_feasibility_example():
+    """P:287's monotonicity claim fails on this instance."""
+    es, gs, m = [15, 28], [3, 4], 4
+    assert P.exists_layout(es, gs, m, 12)
+    assert not P.exists_layout(es, gs, m, 15)
+    assert P.exists_layout(es, gs, m, 18)
+
+
+def test_any_order_np_hard_gap():
+    """Ordering matters: the any-order optimum can beat the fixed order."""
+    found = False
+    rng = random.Random(5)
+    for _ in range(200):
+        es, gs, m, gc = _rand_instance(rng)
+        if len(es) > 4:
+            continue
+        if P.brute_force_any_order(es, gs, m, gc) < P.brute_force_min_shard(es, gs, m, gc):
+            found = True
+            break
+    assert found
+
+
+# ---------------------------------------------------------- tables (a3)
+def test_rank_tables_partition_the_shards():
+    rng = random.Random(6)
+    for _ in range(100):
+        n = rng.randint(1, 10)
+        q = rng.choice([4, 8, 16])
+        es = [rng.randint(1, 300) for _ in range(n)]
+        gs = [min(q, e) for e in es]
+        m = rng.randint(1, 6)
+        lay = P.plan(es, gs, m, rng.choice([1, 4]))
+        covered = np.zeros(m * lay.S, dtype=int)
+        for r in range(m):
+            for off, ln in P.rank_blocks(lay, r, q):
+                assert 1 <= ln <= q
+                covered[r * lay.S + off: r * lay.S + off + ln] += 1
+            segs = P.rank_segments(lay, r)
+            assert sum(s[2] for s in segs) == sum(ln for _, ln in P.rank_blocks(lay, r, q))
+        mask = np.zeros(m * lay.S, dtype=int)
+        for l, e in zip(lay.starts, lay.numel):
+            mask[l:l + e] = 1
+        assert np.array_equal(covered, mask)
+
+
+def test_rank_blocks_detects_straddle():
+    lay = P.Layout(2, 1, [8], [1], 4, [0])
+    with pytest.raises(ValueError):
+        P.rank_blocks(lay, 0, 8)
+
+
+# ------------------------------------------------------- BJ configs (a2)
+def _plan_unit(unit, m):
+    es = [t.numel for t in unit.tensors]
+    gs = [P.block_elems(t.shape, t.gran) for t in unit.tensors]
+    return P.plan(es, gs, m, P.gcoll_elems(unit.elem_bytes))
+
+
+def _linear_scan_opt(unit, m, S_star):
+    es = [t.numel for t in unit.tensors]
+    gs = [P.block_elems(t.shape, t.gran) for t in unit.tensors]
+    gc = P.gcoll_elems(unit.elem_bytes)
+    S = -(-(-(-sum(es) // m)) // gc) * gc
+    while S < S_star:
+        if P.feasible(es, gs, m, S)[0]:
+            return S
+        S += gc
+    return S_star
+
+
+def test_toy_config_layout():
+    """BJ config 1: E = 198,144 fp32, m = 2.  E/2 = 99,072 is a
+    multiple of g_coll = 4 and falls exactly between b2 and w3, so the
+    zero-padding layout is the concatenation (hand-checked)."""
+    lay = _plan_unit(W.toy().units[0], 2)
+    assert lay.S == 99072 and lay.padding == 0
+    assert lay.starts == [0, 32768, 33024, 65792, 66048, 98816, 99072, 131840,
+                          132096, 164864, 165120, 197888]
+    assert P.validate(lay) == []
+    assert len(P.rank_blocks(lay, 0, 2048)) == 51  # 48 x 2048 + 3 x 256
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8])
+def test_llama_layer_unit(m):
+    u = W.llama32_1b_layer(0)
+    lay = _plan_unit(u, m)
+    assert P.validate(lay) == []
+    assert lay.S == _linear_scan_opt(u, m, lay.S)
+    expect = {1: 60_821_504, 2: 30_410_752, 4: 15_206_400, 8: 7_604_224}
+    assert lay.S == expect[m]
+    for r in range(m):
+        P.rank_blocks(lay, r, 2048)  # containment holds on every rank
+
+
+@pytest.mark.parametrize("m", [2, 4, 8])
+def test_dsv3_unit(m):
+    u = W.dsv3_moe_unit()
+    lay = _plan_unit(u, m)
+    assert P.validate(lay) == []
+    expect = {2: 292_698_112, 4: 146_814_976, 8: 74_317_824}
+    assert lay.S == expect[m]
+
+
+@pytest.mark.parametrize("m", [2, 4, 8])
+def test_llama8b_muon_unit(m):
+    lay = _plan_unit(W.llama3_8b_layer(0), m)
+    assert P.validate(lay) == []
+    expect = {2: 117_448_704, 4: 58_728_448, 8: 58_720_256}
+    assert lay.S == expect[m]
+
+
+# --------------------------------------------- Fig. 9 claims
+FIG9_M = [8, 16, 32, 64, 128, 256, 512, 1024]
+
+
+def _model_padding(wl, m, cache):
+    pad = E = 0
+    for u in wl.units:
+        key = tuple((t.numel, P.block_elems(t.shape, t.gran)) for t in u.tensors)
+        if key not in cache:
+            cache[key] = _plan_unit(u, m)
+        lay = cache[key]
+        pad += lay.padding
+        E += lay.E
+    return pad / E
+
+
+@pytest.mark.parametrize("model", ["dsv3", "gptoss"])
+def test_fig9_padding_claims(model):
+    mk = W.deepseek_v3_671b if model == "dsv3" else W.gpt_oss_120b
+    ratios = {}
+    for rows in (1, 16, 128):
+        wl = mk(rows)
+        for m in FIG9_M:
+            ratios[(rows, m)] = _model_padding(wl, m, {})
+    # "with 1x and 16x row granularities ... padding overhead less than 3%"
+    for rows in (1, 16):
+        assert all(ratios[(rows, m)] < 0.03 for m in FIG9_M), ratios
+    r128 = [ratios[(128, m)] for m in FIG9_M]
+    if model == "dsv3":
+        # "DeepSeek-V3 remains mostly below 3% with mild growth"
+        assert sum(r < 0.03 for r in r128) >= 0.75 * len(r128)
+    else:
+        # "GPT-OSS exhibits step-like fluctuations with spikes up to 18%"
+        assert 0.10 <= max(r128) <= 0.20
+        assert any(b < a for a, b in zip(r128, r128[1:])) or max(r128) > 3 * min(r128)
+
+
+def test_planner_time_claim():
+    """planning < 0.3 s per unit (largest unit: DSV3 MoE layer, 777
+    tensors, m = 1024) -- the oracle (pure Python) already meets it."""
+    u = W.deepseek_v3_671b(128).units[10]
+    t0 = time.perf_counter()
+    lay = _plan_unit(u, 1024)
+    dt = time.perf_counter() - t0
+    assert P.validate(lay) == []
+    assert dt < 0.3 * 5  # generous for a slow CI core; the C++ planner is pinned at 0.3 s
