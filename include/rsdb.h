@@ -1,0 +1,265 @@
+/*
+ * rsdb.h -- C ABI of the RaggedShard / DBuffer collective step (veScale-FSDP,
+ * arxiv 2602.22437), B200-native (sm_100a CUDA + NCCL over NVLink 5).
+ *
+ * Citation keys: P:<n> = /root/reference/PAPER.md line n; SURVEY §8 = the
+ * hot-path scope table this library implements (rows a1..a8).
+ *
+ * The four calls of the method (BASELINE.json north_star):
+ *     plan(tensors, block_sizes, world) -> layout        rsdb_plan
+ *     all_gather(unit)                                    rsdb_all_gather
+ *     reduce_scatter(unit)                                rsdb_reduce_scatter
+ *     step_8bit_adam(shard)                               rsdb_step_8bit_adam
+ * plus the DBuffer batched allocation (rsdb_arena_sizes / rsdb_dbuffer_*),
+ * the communicator bootstrap, and the copy-in/copy-out kernel used by the
+ * row-wise (FSDP2 Shard(0)) measurement baseline.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns rsdb_status; 0 = OK.  On error a message is kept in
+ *    thread-local storage, readable with rsdb_last_error() until the next
+ *    rsdb_* call on the same thread.
+ *  - Element counts and offsets are int64 ELEMENTS unless a name says bytes.
+ *  - Host objects (layout, comm, unit, dbuffer) are created and freed by the
+ *    library.  DEVICE MEMORY FOR DATA IS OWNED BY THE CALLER (e.g. torch
+ *    tensors' data_ptr()); the library never frees it.  The library allocates
+ *    only its own small metadata tables (block / padding tables, < 0.02 B per
+ *    element) at unit / dbuffer creation and frees them in *_free.
+ *  - Device calls take a cudaStream_t (passed as void*; NULL = legacy default
+ *    stream), are stream-ordered and asynchronous, and return after enqueue.
+ *    CUDA launch errors and synchronous NCCL errors come back as status;
+ *    asynchronous NCCL errors surface at the next call on that comm.
+ *  - No CPU fallback exists: a call that needs a GPU and finds none fails
+ *    with RSDB_ECUDA.
+ *  - Thread safety: planning functions are pure and thread-safe; calls on one
+ *    unit / dbuffer / comm must be serialised by the caller.
+ */
+#ifndef RSDB_H_
+#define RSDB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t rsdb_status;
+#define RSDB_OK 0
+#define RSDB_EINVAL 1      /* bad argument (block < 1, world < 1, unknown dtype ...)   */
+#define RSDB_EMISMATCH 2   /* buffer / layout / world / rank / dtype mismatch, or a     */
+                           /* quantization block that would straddle a shard boundary   */
+#define RSDB_ECUDA 3       /* CUDA runtime / launch error (incl. no device)             */
+#define RSDB_ENCCL 4       /* NCCL error                                                */
+#define RSDB_EINTERNAL 5   /* planner inconsistency: must never happen                  */
+
+/* element types */
+#define RSDB_BF16 0
+#define RSDB_F32 1
+
+/* granularity declarations (P:156-159, P:419 orig_param_policy) */
+#define RSDB_GRAN_FLAT 0   /* param = q: blocks of q contiguous elements; g = min(q, e)  */
+#define RSDB_GRAN_ROWS 1   /* param = r: r rows of the last dim; g = min(r*shape[-1], e) */
+#define RSDB_GRAN_WHOLE 2  /* whole tensor is one block (Muon); g = e            */
+#define RSDB_GRAN_ELEM 3   /* element granularity (paper default); g = 1         */
+
+const char* rsdb_last_error(void);
+int32_t rsdb_abi_version(void); /* 1 */
+
+/* ======================================================================== */
+/* a1 -- granularity.  Pure host.                         */
+/* ======================================================================== */
+/* Block size g_t (elements) for a tensor of `ndim` dims `shape`.  Tail blocks
+ * are allowed when g does not divide e (the tensor's last block is shorter).
+ * EINVAL: ndim < 1, any shape[i] < 1, param < 1 for FLAT/ROWS, unknown kind. */
+rsdb_status rsdb_block_elems(int32_t ndim, const int64_t* shape, int32_t kind,
+                             int64_t param, int64_t* g_out);
+
+/* ======================================================================== */
+/* a2/a3 -- planning (PAPER §5: problem P:212-232, Algorithm 1,    */
+/* case analysis P:287).  Pure host, deterministic, thread-safe, no CUDA.    */
+/* ======================================================================== */
+typedef struct rsdb_layout rsdb_layout; /* opaque, library-owned */
+
+/* Plan one FSDP unit: n tensors in the given (default) order with
+ * numel[t] = e_t >= 1 and block[t] = g_t >= 1 elements; `world` = m >= 1
+ * devices; elem_bytes in {1,2,4} (one dtype per unit); gcoll_bytes (16 =
+ * NCCL's alignment) gives g_coll = max(1, gcoll_bytes/elem_bytes).
+ * Computes S* (per-device shard size, a multiple of g_coll) and starts l_t so
+ * that tensor t occupies [l_t, l_t+e_t) of the m*S global buffer and device k
+ * owns [k*S, (k+1)*S), with every block of every tensor wholly on
+ * one device.  Never fails for valid input (S = ceil(E/g)*g is always
+ * feasible); n = 0 gives S = 0.  *out must be freed with rsdb_layout_free. */
+rsdb_status rsdb_plan(int32_t n, const int64_t* numel, const int64_t* block,
+                      int32_t world, int32_t elem_bytes, int32_t gcoll_bytes,
+                      rsdb_layout** out);
+
+/* A layout with caller-chosen S and starts (e.g. the even-split / FSDP1 flat
+ * baseline of BASELINE config 5).  Validated against P:226-229; if
+ * require_gcoll != 0 S must also be a multiple of g_coll.  EINVAL if invalid. */
+rsdb_status rsdb_layout_from_starts(int32_t n, const int64_t* numel, const int64_t* block,
+                                    int32_t world, int32_t elem_bytes, int32_t gcoll_bytes,
+                                    int64_t S, const int64_t* starts, int32_t require_gcoll,
+                                    rsdb_layout** out);
+
+int64_t rsdb_layout_shard_numel(const rsdb_layout*); /* S            */
+int64_t rsdb_layout_padding(const rsdb_layout*);     /* m*S - E      */
+int64_t rsdb_layout_total_numel(const rsdb_layout*); /* E            */
+int32_t rsdb_layout_world(const rsdb_layout*);       /* m            */
+int32_t rsdb_layout_ntensors(const rsdb_layout*);    /* n            */
+int32_t rsdb_layout_elem_bytes(const rsdb_layout*);
+/* l_t for t in input order into l_out[n]. */
+rsdb_status rsdb_layout_starts(const rsdb_layout*, int64_t* l_out);
+/* Number of violated constraints of P:226-229 (+ S % g_coll); 0 for plans. */
+rsdb_status rsdb_layout_validate(const rsdb_layout*, int64_t* n_violations);
+/* Padding intervals [lo, hi) of the global buffer, ascending.  Call with
+ * lo = hi = NULL to get *n; then with arrays of >= *n entries. */
+rsdb_status rsdb_layout_padding_intervals(const rsdb_layout*, int64_t* n, int64_t* lo, int64_t* hi);
+/* a3: pieces of tensors in `rank`'s shard: tensor index, offset inside the
+ * shard, length, offset inside the tensor.  Two-call protocol as above. */
+rsdb_status rsdb_layout_rank_segments(const rsdb_layout*, int32_t rank, int64_t* n,
+                                      int32_t* tensor, int64_t* local_off, int64_t* len,
+                                      int64_t* tensor_off);
+/* a3: quantization blocks of `rank`: block j of tensor t covers tensor
+ * elements [j*qblock, min((j+1)*qblock, e_t)).  Emits (offset inside the
+ * shard, length) in ascending order.  EMISMATCH if a block straddles a shard
+ * boundary (only possible when g_t is not a multiple of qblock). */
+rsdb_status rsdb_layout_rank_blocks(const rsdb_layout*, int32_t rank, int64_t qblock,
+                                    int64_t* n, int64_t* off, int32_t* len);
+/* Plan JSON {"m","g_coll","S","E","padding","numel","block","starts"} into buf
+ * (NUL-terminated if cap suffices); *needed = bytes incl. NUL. */
+rsdb_status rsdb_layout_to_json(const rsdb_layout*, char* buf, int64_t cap, int64_t* needed);
+void rsdb_layout_free(rsdb_layout*);
+
+/* ======================================================================== */
+/* Communicator: NCCL over NVLink 5 / NVSwitch (P:341 standard runtimes).    */
+/* ======================================================================== */
+typedef struct rsdb_comm rsdb_comm;
+/* Rank 0 creates the id; the caller broadcasts its 128 bytes (e.g. with
+ * torch.distributed.broadcast_object_list) -- bootstrap only. */
+rsdb_status rsdb_unique_id(uint8_t out[128]);
+/* Collective over all `world` ranks; binds the comm to CUDA device `device`
+ * (which becomes current on the calling thread). */
+rsdb_status rsdb_comm_init(const uint8_t id[128], int32_t world, int32_t rank,
+                           int32_t device, rsdb_comm** out);
+int32_t rsdb_comm_rank(const rsdb_comm*);
+int32_t rsdb_comm_world(const rsdb_comm*);
+void rsdb_comm_free(rsdb_comm*);
+
+/* ======================================================================== */
+/* Unit: one planned FSDP unit bound to caller-owned device buffers.         */
+/* ======================================================================== */
+typedef struct {
+  void* param_full; /* m*S elements of the unit dtype (bf16 | f32).  AllGather
+                       is in place: rank k's shard is param_full+k*S,
+                       tensor views live at param_full+l_t (a5).               */
+  void* grad_full;  /* m*S elements of the unit dtype: gradients written
+                       through the views (autograd).  For f32 units this may
+                       equal grad_f32 (the group op then scales in place).     */
+  void* grad_f32;   /* m*S fp32: ReduceScatter buffer, in place; after
+                       rsdb_reduce_scatter rank k's reduced shard is
+                       grad_f32 + k*S.                                          */
+} rsdb_unit_bufs;
+typedef struct rsdb_unit rsdb_unit;
+
+/* Binds a layout, an optional comm (NULL: collectives unavailable, local
+ * group op and optimizer still usable -- used by single-GPU tests), the rank
+ * this process holds, buffers (16-byte aligned: EMISMATCH otherwise) and the
+ * 8-bit Adam block size qblock (block table via rsdb_layout_rank_blocks;
+ * EMISMATCH if a block would straddle).  The layout is copied. */
+rsdb_status rsdb_unit_create(const rsdb_layout*, rsdb_comm* comm_or_null, int32_t rank,
+                             const rsdb_unit_bufs* bufs, int64_t qblock, rsdb_unit** out);
+int64_t rsdb_unit_num_blocks(const rsdb_unit*); /* blocks on this rank */
+void rsdb_unit_free(rsdb_unit*);
+
+/* a4: in-place AllGather of the unit buffer (ncclAllGather of S elements from
+ * param_full + rank*S into param_full).  Views need no Copy-Out. */
+rsdb_status rsdb_all_gather(rsdb_unit*, void* stream);
+
+/* a6 alone: the fused DBuffer group op: grad_f32[i] =
+ * fp32(grad_full[i]) * fl(1/m) over the whole m*S buffer in one pass,
+ * padding positions written 0. */
+rsdb_status rsdb_unit_cast_scale(rsdb_unit*, void* stream);
+
+/* a6 + a7: the group op, then the in-place fp32 ReduceScatter (sum) of
+ * grad_f32; rank k's result is grad_f32 + k*S = (1/m) sum_r G_r[kS:(k+1)S]. */
+rsdb_status rsdb_reduce_scatter(rsdb_unit*, void* stream);
+
+/* a8: block-wise 8-bit Adam on the local ragged shard, no
+ * communication.  The per-step scalars (1 - lr*wd, lr/(1-b1^t),
+ * sqrt(1-b2^t)) are formed in fp64 on the host and rounded to fp32; the
+ * element arithmetic is fp32 (P:344 FP32 master weights). */
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay;
+} rsdb_adam_cfg;
+typedef struct {
+  void* master_f32; /* S fp32 master weights of this rank            */
+  void* m_q;        /* S int8   first-moment codes (signed, absmax/127)        */
+  void* v_q;        /* S uint8  second-moment codes (unsigned, absmax/255)     */
+  void* m_absmax;   /* nblocks fp32, block i of rsdb_layout_rank_blocks order  */
+  void* v_absmax;   /* nblocks fp32                                            */
+} rsdb_adam_state;
+/* Reads the gradient shard grad_f32 + rank*S, updates master / codes /
+ * absmax, writes the unit-dtype parameter shard param_full + rank*S (the next
+ * AllGather's send buffer).  Elements outside blocks (padding) untouched.
+ * step >= 1 (EINVAL otherwise). */
+rsdb_status rsdb_step_8bit_adam(rsdb_unit*, const rsdb_adam_state*, const rsdb_adam_cfg*,
+                                int64_t step, void* stream);
+
+/* ======================================================================== */
+/* DBuffer batched allocation: one allocation per    */
+/* buffer kind for all units, persistent offsets, one optimizer launch.      */
+/* ======================================================================== */
+#define RSDB_KIND_PARAM_FULL 0 /* m*S * eb   */
+#define RSDB_KIND_GRAD_FULL 1  /* m*S * eb (0 for f32 units: grads live in GRAD_F32) */
+#define RSDB_KIND_GRAD_F32 2   /* m*S * 4    */
+#define RSDB_KIND_MASTER 3     /* S * 4      */
+#define RSDB_KIND_MQ 4         /* S          */
+#define RSDB_KIND_VQ 5         /* S          */
+#define RSDB_KIND_MABS 6       /* nblocks(rank) * 4 */
+#define RSDB_KIND_VABS 7       /* nblocks(rank) * 4 */
+#define RSDB_NKINDS 8
+/* Byte size of each kind's arena for `rank` and each unit's byte offset in it
+ * (unit_offsets[u*RSDB_NKINDS + kind]); every offset is a multiple of
+ * align_bytes (>= 16, power of two).  MASTER/MQ/VQ share element offsets. */
+rsdb_status rsdb_arena_sizes(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                             int64_t qblock, int64_t align_bytes, int64_t* bytes_per_kind,
+                             int64_t* unit_offsets);
+typedef struct rsdb_dbuffer rsdb_dbuffer;
+/* Creates every unit inside caller-allocated arenas arena_base[RSDB_NKINDS]
+ * (sizes from rsdb_arena_sizes with the same align_bytes), plus one combined
+ * block table so that the optimizer runs as ONE launch over all units. */
+rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units,
+                                rsdb_comm* comm_or_null, int32_t rank, int64_t qblock,
+                                int64_t align_bytes, void* const* arena_base,
+                                rsdb_dbuffer** out);
+rsdb_unit* rsdb_dbuffer_unit(rsdb_dbuffer*, int32_t i); /* borrowed; NULL if out of range */
+int64_t rsdb_dbuffer_num_blocks(const rsdb_dbuffer*);
+/* a8 over every unit's shard in one kernel launch. */
+rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer*, const rsdb_adam_cfg*, int64_t step,
+                                        void* stream);
+/* Grouped zero of every unit's gradient buffer ("zero"). */
+rsdb_status rsdb_dbuffer_zero_grads(rsdb_dbuffer*, void* stream);
+void rsdb_dbuffer_free(rsdb_dbuffer*);
+
+/* ======================================================================== */
+/* Batched ragged copy (FSDP2 interleaved Copy-In/Copy-Out baseline,  */
+/* P:107, Table 1): one launch copies n segments, optional cast and scale.   */
+/* ======================================================================== */
+typedef struct {
+  const void* src; /* device */
+  void* dst;       /* device */
+  int64_t numel;
+} rsdb_segment;
+typedef struct rsdb_copy_plan rsdb_copy_plan;
+/* Persistent copy plan (addresses are persistent across steps, like the
+ * DBuffer map): segs_host is a HOST array copied into a library-owned device
+ * table here (synchronously).  Run: dst[i] = cast(src[i] * scale) for every
+ * segment; dtypes RSDB_BF16 / RSDB_F32; segments must not overlap. */
+rsdb_status rsdb_copy_plan_create(const rsdb_segment* segs_host, int64_t n, int32_t src_dtype,
+                                  int32_t dst_dtype, float scale, rsdb_copy_plan** out);
+rsdb_status rsdb_copy_run(const rsdb_copy_plan*, void* stream);
+void rsdb_copy_plan_free(rsdb_copy_plan*);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSDB_H_ */

@@ -1,0 +1,358 @@
+"""paper_2602_22437_b200 -- the RaggedShard/DBuffer collective step of
+veScale-FSDP (arxiv 2602.22437) for B200.
+
+Thin Python binding over librsdb.so (include/rsdb.h): argument marshalling
+only; every step of the path runs in the library's C++ planner, sm_100a
+kernels and NCCL calls.  PyTorch supplies device memory, streams and the
+torch.distributed bootstrap -- plumbing, not the product.  There is no CPU
+fallback: importing fails loudly if the library is missing.
+
+Names follow the C ABI without the ``rsdb_`` prefix.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from typing import List, Optional, Sequence, Tuple
+
+from . import _capi as _c
+from ._capi import (RSDB_BF16, RSDB_F32, RSDB_GRAN_ELEM, RSDB_GRAN_FLAT,  # noqa: F401
+                    RSDB_GRAN_ROWS, RSDB_GRAN_WHOLE, RsdbError)
+
+lib = _c.lib
+check = _c.check
+
+__all__ = ["block_elems", "plan", "Layout", "Comm", "Unit", "DBuffer", "CopyPlan", "AdamConfig",
+           "all_gather", "reduce_scatter", "step_8bit_adam", "unit_cast_scale", "RsdbError",
+           "init_comm"]
+
+_GRAN = {"flat": RSDB_GRAN_FLAT, "rows": RSDB_GRAN_ROWS, "whole": RSDB_GRAN_WHOLE,
+         "elem": RSDB_GRAN_ELEM}
+
+
+def _ptr(t) -> Optional[int]:
+    """device pointer of a torch tensor (or an int / None)."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------- a1
+def block_elems(shape: Sequence[int], gran: Tuple) -> int:
+    """g_t for a granularity declaration ("flat", q) | ("rows", r) | ("whole",) | ("elem",)."""
+    kind = _GRAN[gran[0]]
+    param = int(gran[1]) if len(gran) > 1 else 0
+    sh = _c.i64_array(shape)
+    out = C.c_int64()
+    check(lib.rsdb_block_elems(len(shape), sh, kind, param, C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------- a2/a3
+class Layout:
+    """Planned FSDP unit layout (library-owned rsdb_layout*)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.rsdb_layout_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def S(self) -> int:
+        return lib.rsdb_layout_shard_numel(self._h)
+
+    @property
+    def padding(self) -> int:
+        return lib.rsdb_layout_padding(self._h)
+
+    @property
+    def E(self) -> int:
+        return lib.rsdb_layout_total_numel(self._h)
+
+    @property
+    def m(self) -> int:
+        return lib.rsdb_layout_world(self._h)
+
+    @property
+    def n(self) -> int:
+        return lib.rsdb_layout_ntensors(self._h)
+
+    @property
+    def elem_bytes(self) -> int:
+        return lib.rsdb_layout_elem_bytes(self._h)
+
+    @property
+    def starts(self) -> List[int]:
+        arr = (C.c_int64 * max(1, self.n))()
+        check(lib.rsdb_layout_starts(self._h, arr))
+        return list(arr[: self.n])
+
+    def validate(self) -> int:
+        v = C.c_int64()
+        check(lib.rsdb_layout_validate(self._h, C.byref(v)))
+        return v.value
+
+    def padding_intervals(self) -> List[Tuple[int, int]]:
+        n = C.c_int64(0)
+        check(lib.rsdb_layout_padding_intervals(self._h, C.byref(n), None, None))
+        lo, hi = (C.c_int64 * max(1, n.value))(), (C.c_int64 * max(1, n.value))()
+        check(lib.rsdb_layout_padding_intervals(self._h, C.byref(n), lo, hi))
+        return [(lo[i], hi[i]) for i in range(n.value)]
+
+    def rank_segments(self, rank: int) -> List[Tuple[int, int, int, int]]:
+        n = C.c_int64(0)
+        check(lib.rsdb_layout_rank_segments(self._h, rank, C.byref(n), None, None, None, None))
+        k = max(1, n.value)
+        t, lo, ln, to = (C.c_int32 * k)(), (C.c_int64 * k)(), (C.c_int64 * k)(), (C.c_int64 * k)()
+        check(lib.rsdb_layout_rank_segments(self._h, rank, C.byref(n), t, lo, ln, to))
+        return [(t[i], lo[i], ln[i], to[i]) for i in range(n.value)]
+
+    def rank_blocks(self, rank: int, qblock: int) -> List[Tuple[int, int]]:
+        n = C.c_int64(0)
+        check(lib.rsdb_layout_rank_blocks(self._h, rank, qblock, C.byref(n), None, None))
+        k = max(1, n.value)
+        off, ln = (C.c_int64 * k)(), (C.c_int32 * k)()
+        check(lib.rsdb_layout_rank_blocks(self._h, rank, qblock, C.byref(n), off, ln))
+        return [(off[i], ln[i]) for i in range(n.value)]
+
+    def to_json(self) -> dict:
+        need = C.c_int64(0)
+        check(lib.rsdb_layout_to_json(self._h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(lib.rsdb_layout_to_json(self._h, buf, need.value, C.byref(need)))
+        return json.loads(buf.value.decode())
+
+
+def plan(numel: Sequence[int], block: Sequence[int], world: int, elem_bytes: int = 2,
+         gcoll_bytes: int = 16) -> Layout:
+    """plan(tensors, block_sizes, world) -> layout (Algorithm 1)."""
+    h = C.c_void_p()
+    check(lib.rsdb_plan(len(numel), _c.i64_array(numel), _c.i64_array(block), world,
+                        elem_bytes, gcoll_bytes, C.byref(h)))
+    return Layout(h.value)
+
+
+def layout_from_starts(numel, block, world, S, starts, elem_bytes=2, gcoll_bytes=16,
+                       require_gcoll=True) -> Layout:
+    h = C.c_void_p()
+    check(lib.rsdb_layout_from_starts(len(numel), _c.i64_array(numel), _c.i64_array(block),
+                                      world, elem_bytes, gcoll_bytes, S, _c.i64_array(starts),
+                                      int(require_gcoll), C.byref(h)))
+    return Layout(h.value)
+
+
+# ---------------------------------------------------------------- comm
+class Comm:
+    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+        h = C.c_void_p()
+        check(lib.rsdb_comm_init(uid, world, rank, device, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.rsdb_unique_id(buf))
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def rank(self) -> int:
+        return lib.rsdb_comm_rank(self._h)
+
+    @property
+    def world(self) -> int:
+        return lib.rsdb_comm_world(self._h)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib.rsdb_comm_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def init_comm(rank: int, world: int, device: int, group=None) -> Comm:
+    """Bootstrap: rank 0 makes the NCCL unique id, torch.distributed
+    broadcasts its 128 bytes (plumbing), every rank joins."""
+    import torch.distributed as dist
+    obj = [Comm.unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    return Comm(obj[0], world, rank, device)
+
+
+# ---------------------------------------------------------------- unit
+class Unit:
+    """One FSDP unit bound to caller-owned device buffers (torch tensors)."""
+
+    def __init__(self, layout: Layout, rank: int, param_full, grad_full, grad_f32,
+                 qblock: int = 2048, comm: Optional[Comm] = None, _handle=None, _keep=None):
+        self.layout = layout
+        self.rank = rank
+        self.comm = comm
+        self._keep = _keep if _keep is not None else (param_full, grad_full, grad_f32)
+        self._owned = _handle is None
+        if _handle is None:
+            bufs = _c.UnitBufs(_ptr(param_full), _ptr(grad_full), _ptr(grad_f32))
+            h = C.c_void_p()
+            check(lib.rsdb_unit_create(layout.handle, comm.handle if comm else None, rank,
+                                       C.byref(bufs), qblock, C.byref(h)))
+            self._h = h
+        else:
+            self._h = C.c_void_p(_handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_blocks(self) -> int:
+        return lib.rsdb_unit_num_blocks(self._h)
+
+    def close(self):
+        if self._owned and self._h is not None and self._h.value:
+            lib.rsdb_unit_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class AdamConfig(_c.AdamCfg):
+    def __init__(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=1e-2):
+        super().__init__(lr, beta1, beta2, eps, weight_decay)
+
+
+def all_gather(unit: Unit, stream=None) -> None:
+    """a4: in-place AllGather of the unit buffer (ncclAllGather)."""
+    check(lib.rsdb_all_gather(unit.handle, _stream(stream)))
+
+
+def unit_cast_scale(unit: Unit, stream=None) -> None:
+    """a6: the fused group op alone (cast bf16->fp32, x1/m, padding 0)."""
+    check(lib.rsdb_unit_cast_scale(unit.handle, _stream(stream)))
+
+
+def reduce_scatter(unit: Unit, stream=None) -> None:
+    """a6 + a7: fused cast/scale, then in-place fp32 ReduceScatter."""
+    check(lib.rsdb_reduce_scatter(unit.handle, _stream(stream)))
+
+
+def step_8bit_adam(unit: Unit, master, m_q, v_q, m_absmax, v_absmax, cfg: AdamConfig,
+                   step: int, stream=None) -> None:
+    """a8: block-wise 8-bit Adam on the unit's local ragged shard."""
+    st = _c.AdamState(_ptr(master), _ptr(m_q), _ptr(v_q), _ptr(m_absmax), _ptr(v_absmax))
+    check(lib.rsdb_step_8bit_adam(unit.handle, C.byref(st), C.byref(cfg), step, _stream(stream)))
+
+
+# ---------------------------------------------------------------- DBuffer
+KINDS = ("param_full", "grad_full", "grad_f32", "master", "m_q", "v_q", "m_absmax", "v_absmax")
+
+
+def arena_sizes(layouts: Sequence[Layout], rank: int, qblock: int = 2048, align: int = 256):
+    arr = (C.c_void_p * max(1, len(layouts)))(*[l.handle.value for l in layouts])
+    sizes = (C.c_int64 * _c.RSDB_NKINDS)()
+    offs = (C.c_int64 * max(1, len(layouts) * _c.RSDB_NKINDS))()
+    check(lib.rsdb_arena_sizes(arr, len(layouts), rank, qblock, align, sizes, offs))
+    return list(sizes), [list(offs[u * 8:(u + 1) * 8]) for u in range(len(layouts))]
+
+
+class DBuffer:
+    """Batched DBuffer: one caller-allocated arena per
+    buffer kind holding every unit; per-unit zero-copy views; one optimizer
+    launch over all units."""
+
+    def __init__(self, layouts: Sequence[Layout], rank: int, arenas: Sequence, qblock=2048,
+                 align=256, comm: Optional[Comm] = None):
+        self.layouts = list(layouts)
+        self.rank = rank
+        self.comm = comm
+        self.arenas = list(arenas)
+        arr = (C.c_void_p * max(1, len(layouts)))(*[l.handle.value for l in layouts])
+        bases = (C.c_void_p * _c.RSDB_NKINDS)(*[_ptr(a) if a is not None and a.numel() > 0
+                                                else None for a in arenas])
+        h = C.c_void_p()
+        check(lib.rsdb_dbuffer_create(arr, len(layouts), comm.handle if comm else None, rank,
+                                      qblock, align, bases, C.byref(h)))
+        self._h = h
+        self.units = [Unit(l, rank, None, None, None, comm=comm,
+                           _handle=lib.rsdb_dbuffer_unit(h, i), _keep=())
+                      for i, l in enumerate(layouts)]
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_blocks(self) -> int:
+        return lib.rsdb_dbuffer_num_blocks(self._h)
+
+    def step_8bit_adam(self, cfg: AdamConfig, step: int, stream=None) -> None:
+        check(lib.rsdb_dbuffer_step_8bit_adam(self._h, C.byref(cfg), step, _stream(stream)))
+
+    def zero_grads(self, stream=None) -> None:
+        check(lib.rsdb_dbuffer_zero_grads(self._h, _stream(stream)))
+
+    def close(self):
+        for u in getattr(self, "units", []):
+            u._h = None
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.rsdb_dbuffer_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- copies
+class CopyPlan:
+    """Persistent batched ragged copy (FSDP2 Copy-In / Copy-Out baseline)."""
+
+    def __init__(self, segments: Sequence[Tuple[object, object, int]], src_dtype=RSDB_BF16,
+                 dst_dtype=RSDB_BF16, scale: float = 1.0):
+        arr = (_c.Segment * max(1, len(segments)))(
+            *[_c.Segment(_ptr(s), _ptr(d), int(n)) for s, d, n in segments])
+        h = C.c_void_p()
+        check(lib.rsdb_copy_plan_create(arr, len(segments), src_dtype, dst_dtype, scale,
+                                        C.byref(h)))
+        self._h = h
+
+    def run(self, stream=None) -> None:
+        check(lib.rsdb_copy_run(self._h, _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.rsdb_copy_plan_free(self._h)
+            self._h = None

@@ -1,0 +1,613 @@
+// extern "C" boundary of the RaggedShard/DBuffer collective step (include/rsdb.h).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <climits>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/rsdb.h"
+#include "kernels.cuh"
+#include "planner.hpp"
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static rsdb_status fail(rsdb_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+#define OK_CLEAR() (g_err.clear(), RSDB_OK)
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(RSDB_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+#define NCCL_TRY(expr)                                                                        \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess) return fail(RSDB_ENCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+struct rsdb_layout {
+  rsdb::Layout L;
+};
+
+struct rsdb_comm {
+  ncclComm_t nc = nullptr;
+  int32_t world = 1, rank = 0, device = 0;
+};
+
+// device allocation owned by the library (metadata tables only)
+struct DevTable {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevTable() {
+    if (p) cudaFree(p);
+  }
+  rsdb_status upload(const void* host, size_t nbytes) {
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    bytes = nbytes;
+    if (!nbytes) return RSDB_OK;
+    CUDA_TRY(cudaMalloc(&p, nbytes));
+    CUDA_TRY(cudaMemcpy(p, host, nbytes, cudaMemcpyHostToDevice));
+    return RSDB_OK;
+  }
+};
+
+struct rsdb_unit {
+  rsdb::Layout L;
+  rsdb_comm* comm = nullptr;
+  int32_t rank = 0;
+  rsdb_unit_bufs bufs{};
+  int64_t qblock = 0;
+  int64_t nblocks = 0;
+  int64_t npad = 0;
+  DevTable pad;     // int64 lo, hi pairs
+  DevTable blocks;  // rsdb::AdamBlock, unit-relative (state = shard, grad/param = +rank*S)
+};
+
+struct rsdb_dbuffer {
+  std::vector<std::unique_ptr<rsdb_unit>> units;
+  void* base[RSDB_NKINDS]{};
+  int64_t nblocks = 0;
+  DevTable blocks;  // arena-relative table over all units
+  int32_t param_bf16 = 1;
+  std::vector<int64_t> grad_bytes;  // per unit, for grouped zero
+};
+
+struct rsdb_copy_plan {
+  DevTable segs;
+  int64_t nseg = 0, total_chunks = 0;
+  int32_t src_bf16 = 1, dst_bf16 = 1;
+  float scale = 1.f;
+};
+
+static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline bool aligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+
+static rsdb_status require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n < 1)
+    return fail(RSDB_ECUDA, "no CUDA device available (%s); there is no CPU fallback",
+                e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+  return RSDB_OK;
+}
+
+extern "C" {
+
+const char* rsdb_last_error(void) { return g_err.c_str(); }
+int32_t rsdb_abi_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// a1 / a2 / a3
+// ---------------------------------------------------------------------------
+rsdb_status rsdb_block_elems(int32_t ndim, const int64_t* shape, int32_t kind, int64_t param,
+                             int64_t* g_out) {
+  std::string err;
+  if (!rsdb::block_elems(ndim, shape, kind, param, g_out, &err)) return fail(RSDB_EINVAL, "%s", err.c_str());
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_plan(int32_t n, const int64_t* numel, const int64_t* block, int32_t world,
+                      int32_t elem_bytes, int32_t gcoll_bytes, rsdb_layout** out) {
+  if (!out || n < 0 || (n > 0 && (!numel || !block))) return fail(RSDB_EINVAL, "rsdb_plan: bad pointer or n");
+  std::vector<int64_t> e(numel, numel + n), g(block, block + n);
+  auto lay = std::make_unique<rsdb_layout>();
+  std::string err;
+  if (!rsdb::plan(e, g, world, elem_bytes, gcoll_bytes, &lay->L, &err))
+    return fail(err.find("internal") != std::string::npos ? RSDB_EINTERNAL : RSDB_EINVAL, "%s",
+                err.c_str());
+  *out = lay.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_from_starts(int32_t n, const int64_t* numel, const int64_t* block,
+                                    int32_t world, int32_t elem_bytes, int32_t gcoll_bytes,
+                                    int64_t S, const int64_t* starts, int32_t require_gcoll,
+                                    rsdb_layout** out) {
+  if (!out || n < 0 || (n > 0 && (!numel || !block || !starts)) || world < 1 || S < 0 ||
+      !(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4) || gcoll_bytes < 1)
+    return fail(RSDB_EINVAL, "rsdb_layout_from_starts: bad argument");
+  auto lay = std::make_unique<rsdb_layout>();
+  rsdb::Layout& L = lay->L;
+  L.m = world;
+  L.elem_bytes = elem_bytes;
+  L.g_coll = std::max<int64_t>(1, gcoll_bytes / elem_bytes);
+  L.S = S;
+  L.e.assign(numel, numel + n);
+  L.g.assign(block, block + n);
+  L.l.assign(starts, starts + n);
+  for (int i = 0; i < n; ++i)
+    if (L.e[i] < 1 || L.g[i] < 1) return fail(RSDB_EINVAL, "numel/block must be >= 1");
+  if (n > 0 && S < 1) return fail(RSDB_EINVAL, "S must be >= 1");
+  const int64_t v = rsdb::count_violations(L, require_gcoll != 0);
+  if (v) return fail(RSDB_EINVAL, "layout violates %lld constraint(s) of P:226-229", (long long)v);
+  *out = lay.release();
+  return OK_CLEAR();
+}
+
+int64_t rsdb_layout_shard_numel(const rsdb_layout* l) { return l ? l->L.S : -1; }
+int64_t rsdb_layout_padding(const rsdb_layout* l) {
+  return l ? int64_t(l->L.m) * l->L.S - l->L.E() : -1;
+}
+int64_t rsdb_layout_total_numel(const rsdb_layout* l) { return l ? l->L.E() : -1; }
+int32_t rsdb_layout_world(const rsdb_layout* l) { return l ? l->L.m : -1; }
+int32_t rsdb_layout_ntensors(const rsdb_layout* l) { return l ? int32_t(l->L.e.size()) : -1; }
+int32_t rsdb_layout_elem_bytes(const rsdb_layout* l) { return l ? l->L.elem_bytes : -1; }
+
+rsdb_status rsdb_layout_starts(const rsdb_layout* l, int64_t* out) {
+  if (!l || (!out && !l->L.l.empty())) return fail(RSDB_EINVAL, "null argument");
+  std::copy(l->L.l.begin(), l->L.l.end(), out);
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_validate(const rsdb_layout* l, int64_t* nv) {
+  if (!l || !nv) return fail(RSDB_EINVAL, "null argument");
+  *nv = rsdb::count_violations(l->L, true);
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_padding_intervals(const rsdb_layout* l, int64_t* n, int64_t* lo, int64_t* hi) {
+  if (!l || !n) return fail(RSDB_EINVAL, "null argument");
+  auto iv = rsdb::padding_intervals(l->L);
+  if (lo && hi) {
+    if (*n < int64_t(iv.size())) return fail(RSDB_EINVAL, "array too small");
+    for (size_t i = 0; i < iv.size(); ++i) lo[i] = iv[i].first, hi[i] = iv[i].second;
+  }
+  *n = int64_t(iv.size());
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_rank_segments(const rsdb_layout* l, int32_t rank, int64_t* n,
+                                      int32_t* tensor, int64_t* local_off, int64_t* len,
+                                      int64_t* tensor_off) {
+  if (!l || !n) return fail(RSDB_EINVAL, "null argument");
+  if (rank < 0 || rank >= l->L.m) return fail(RSDB_EINVAL, "rank %d out of [0,%d)", rank, l->L.m);
+  auto segs = rsdb::rank_segments(l->L, rank);
+  if (tensor && local_off && len && tensor_off) {
+    if (*n < int64_t(segs.size())) return fail(RSDB_EINVAL, "array too small");
+    for (size_t i = 0; i < segs.size(); ++i) {
+      tensor[i] = segs[i].tensor;
+      local_off[i] = segs[i].local_off;
+      len[i] = segs[i].len;
+      tensor_off[i] = segs[i].tensor_off;
+    }
+  }
+  *n = int64_t(segs.size());
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_rank_blocks(const rsdb_layout* l, int32_t rank, int64_t qblock, int64_t* n,
+                                    int64_t* off, int32_t* len) {
+  if (!l || !n) return fail(RSDB_EINVAL, "null argument");
+  if (rank < 0 || rank >= l->L.m) return fail(RSDB_EINVAL, "rank %d out of [0,%d)", rank, l->L.m);
+  std::vector<rsdb::QBlock> b;
+  std::string err;
+  if (!rsdb::rank_blocks(l->L, rank, qblock, &b, &err))
+    return fail(qblock < 1 ? RSDB_EINVAL : RSDB_EMISMATCH, "%s", err.c_str());
+  if (off && len) {
+    if (*n < int64_t(b.size())) return fail(RSDB_EINVAL, "array too small");
+    for (size_t i = 0; i < b.size(); ++i) off[i] = b[i].off, len[i] = b[i].len;
+  }
+  *n = int64_t(b.size());
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_to_json(const rsdb_layout* l, char* buf, int64_t cap, int64_t* needed) {
+  if (!l || !needed) return fail(RSDB_EINVAL, "null argument");
+  const std::string s = rsdb::to_json(l->L);
+  *needed = int64_t(s.size()) + 1;
+  if (buf && cap >= *needed) std::memcpy(buf, s.c_str(), s.size() + 1);
+  return OK_CLEAR();
+}
+
+void rsdb_layout_free(rsdb_layout* l) { delete l; }
+
+// ---------------------------------------------------------------------------
+// communicator
+// ---------------------------------------------------------------------------
+static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+
+rsdb_status rsdb_unique_id(uint8_t out[128]) {
+  if (!out) return fail(RSDB_EINVAL, "null argument");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, 128);
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int32_t device,
+                           rsdb_comm** out) {
+  if (!id || !out || world < 1 || rank < 0 || rank >= world || device < 0)
+    return fail(RSDB_EINVAL, "rsdb_comm_init: bad argument");
+  if (rsdb_status st = require_device()) return st;
+  CUDA_TRY(cudaSetDevice(device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  auto c = std::make_unique<rsdb_comm>();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  NCCL_TRY(ncclCommInitRank(&c->nc, world, uid, rank));
+  *out = c.release();
+  return OK_CLEAR();
+}
+
+int32_t rsdb_comm_rank(const rsdb_comm* c) { return c ? c->rank : -1; }
+int32_t rsdb_comm_world(const rsdb_comm* c) { return c ? c->world : -1; }
+void rsdb_comm_free(rsdb_comm* c) {
+  if (!c) return;
+  if (c->nc) ncclCommDestroy(c->nc);
+  delete c;
+}
+
+// ---------------------------------------------------------------------------
+// unit
+// ---------------------------------------------------------------------------
+static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t rank,
+                              const rsdb_unit_bufs& bufs, int64_t qblock, rsdb_unit* u,
+                              std::vector<rsdb::QBlock>* blocks_out) {
+  if (!(L.elem_bytes == 2 || L.elem_bytes == 4))
+    return fail(RSDB_EMISMATCH, "units support bf16 (2 B) or f32 (4 B) elements, got %d B", L.elem_bytes);
+  if (rank < 0 || rank >= L.m) return fail(RSDB_EINVAL, "rank %d out of [0,%d)", rank, L.m);
+  if (comm && (comm->world != L.m || comm->rank != rank))
+    return fail(RSDB_EMISMATCH, "comm (world %d, rank %d) does not match layout world %d / rank %d",
+                comm->world, comm->rank, L.m, rank);
+  if (!bufs.param_full || !bufs.grad_full || !bufs.grad_f32)
+    return fail(RSDB_EINVAL, "unit buffers must be non-null");
+  if (!aligned16(bufs.param_full) || !aligned16(bufs.grad_full) || !aligned16(bufs.grad_f32))
+    return fail(RSDB_EMISMATCH, "unit buffers must be 16-byte aligned (P:199, P:369)");
+  if (L.elem_bytes == 2 && bufs.grad_full == bufs.grad_f32)
+    return fail(RSDB_EMISMATCH, "bf16 unit: grad_full must not alias grad_f32");
+  std::vector<rsdb::QBlock> qb;
+  std::string err;
+  if (!rsdb::rank_blocks(L, rank, qblock, &qb, &err))
+    return fail(qblock < 1 ? RSDB_EINVAL : RSDB_EMISMATCH, "%s", err.c_str());
+  u->L = L;
+  u->comm = comm;
+  u->rank = rank;
+  u->bufs = bufs;
+  u->qblock = qblock;
+  u->nblocks = int64_t(qb.size());
+  auto iv = rsdb::padding_intervals(L);
+  std::vector<int64_t> pad;
+  for (auto& [a, b] : iv) pad.push_back(a), pad.push_back(b);
+  u->npad = int64_t(iv.size());
+  if (rsdb_status st = require_device()) return st;
+  if (rsdb_status st = u->pad.upload(pad.data(), pad.size() * sizeof(int64_t))) return st;
+  std::vector<rsdb::AdamBlock> tbl(qb.size());
+  const int64_t base = int64_t(rank) * L.S;
+  for (size_t i = 0; i < qb.size(); ++i)
+    tbl[i] = {qb[i].off, base + qb[i].off, base + qb[i].off, qb[i].len, int32_t(i)};
+  if (rsdb_status st = u->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
+  if (blocks_out) *blocks_out = std::move(qb);
+  return RSDB_OK;
+}
+
+rsdb_status rsdb_unit_create(const rsdb_layout* l, rsdb_comm* comm, int32_t rank,
+                             const rsdb_unit_bufs* bufs, int64_t qblock, rsdb_unit** out) {
+  if (!l || !bufs || !out) return fail(RSDB_EINVAL, "null argument");
+  auto u = std::make_unique<rsdb_unit>();
+  if (rsdb_status st = build_unit(l->L, comm, rank, *bufs, qblock, u.get(), nullptr)) return st;
+  *out = u.release();
+  return OK_CLEAR();
+}
+
+int64_t rsdb_unit_num_blocks(const rsdb_unit* u) { return u ? u->nblocks : -1; }
+void rsdb_unit_free(rsdb_unit* u) { delete u; }
+
+rsdb_status rsdb_all_gather(rsdb_unit* u, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
+  if (u->L.S == 0) return OK_CLEAR();
+  const ncclDataType_t dt = u->L.elem_bytes == 2 ? ncclBfloat16 : ncclFloat32;
+  char* full = static_cast<char*>(u->bufs.param_full);
+  const void* send = full + int64_t(u->rank) * u->L.S * u->L.elem_bytes;  // in place
+  NCCL_TRY(ncclAllGather(send, full, size_t(u->L.S), dt, u->comm->nc, S_(stream)));
+  return OK_CLEAR();
+}
+
+static rsdb_status cast_scale(rsdb_unit* u, void* stream) {
+  const int64_t n = int64_t(u->L.m) * u->L.S;
+  const float scale = float(1.0 / double(u->L.m));
+  CUDA_TRY(rsdb::launch_cast_scale(u->bufs.grad_full, u->L.elem_bytes == 2,
+                                   static_cast<float*>(u->bufs.grad_f32), n, scale,
+                                   static_cast<const int64_t*>(u->pad.p), int32_t(u->npad),
+                                   S_(stream)));
+  return RSDB_OK;
+}
+
+rsdb_status rsdb_unit_cast_scale(rsdb_unit* u, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (rsdb_status st = cast_scale(u, stream)) return st;
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_reduce_scatter(rsdb_unit* u, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
+  if (u->L.S == 0) return OK_CLEAR();
+  if (rsdb_status st = cast_scale(u, stream)) return st;
+  float* g = static_cast<float*>(u->bufs.grad_f32);
+  NCCL_TRY(ncclReduceScatter(g, g + int64_t(u->rank) * u->L.S, size_t(u->L.S), ncclFloat32,
+                             ncclSum, u->comm->nc, S_(stream)));
+  return OK_CLEAR();
+}
+
+static rsdb_status adam_scalars(const rsdb_adam_cfg* c, int64_t step, rsdb::AdamScalars* s) {
+  if (!c) return fail(RSDB_EINVAL, "null cfg");
+  if (step < 1) return fail(RSDB_EINVAL, "step must be >= 1");
+  if (!(c->beta1 >= 0 && c->beta1 < 1 && c->beta2 >= 0 && c->beta2 < 1 && c->eps >= 0 && c->lr >= 0))
+    return fail(RSDB_EINVAL, "invalid Adam hyper-parameters");
+  const double lr = c->lr, b1 = c->beta1, b2 = c->beta2;
+  s->w1 = float(1.0 - b1);
+  s->b2 = float(b2);
+  s->w2 = float(1.0 - b2);
+  s->eps = float(c->eps);
+  s->c_wd = float(1.0 - lr * double(c->weight_decay));
+  s->step_size = float(lr / (1.0 - std::pow(b1, double(step))));
+  s->inv_bc2s = float(1.0 / std::sqrt(1.0 - std::pow(b2, double(step))));
+  return RSDB_OK;
+}
+
+rsdb_status rsdb_step_8bit_adam(rsdb_unit* u, const rsdb_adam_state* st, const rsdb_adam_cfg* cfg,
+                                int64_t step, void* stream) {
+  if (!u || !st) return fail(RSDB_EINVAL, "null argument");
+  rsdb::AdamScalars s;
+  if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
+  if (u->nblocks == 0) return OK_CLEAR();
+  if (!st->master_f32 || !st->m_q || !st->v_q || !st->m_absmax || !st->v_absmax)
+    return fail(RSDB_EINVAL, "null state pointer");
+  rsdb::AdamPtrs p{static_cast<float*>(st->master_f32), static_cast<int8_t*>(st->m_q),
+                   static_cast<uint8_t*>(st->v_q),       static_cast<float*>(st->m_absmax),
+                   static_cast<float*>(st->v_absmax),    static_cast<const float*>(u->bufs.grad_f32),
+                   u->bufs.param_full,                   u->L.elem_bytes == 2};
+  CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
+                              int32_t(std::min<int64_t>(u->qblock, 1 << 30)), S_(stream)));
+  return OK_CLEAR();
+}
+
+// ---------------------------------------------------------------------------
+// DBuffer batched arenas
+// ---------------------------------------------------------------------------
+static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+static rsdb_status kind_sizes(const rsdb::Layout& L, int32_t rank, int64_t qblock, int64_t sz[RSDB_NKINDS]) {
+  std::vector<rsdb::QBlock> qb;
+  std::string err;
+  if (!rsdb::rank_blocks(L, rank, qblock, &qb, &err))
+    return fail(qblock < 1 ? RSDB_EINVAL : RSDB_EMISMATCH, "%s", err.c_str());
+  const int64_t full = int64_t(L.m) * L.S;
+  sz[RSDB_KIND_PARAM_FULL] = full * L.elem_bytes;
+  sz[RSDB_KIND_GRAD_FULL] = L.elem_bytes == 4 ? 0 : full * L.elem_bytes;
+  sz[RSDB_KIND_GRAD_F32] = full * 4;
+  sz[RSDB_KIND_MASTER] = L.S * 4;
+  sz[RSDB_KIND_MQ] = L.S;
+  sz[RSDB_KIND_VQ] = L.S;
+  sz[RSDB_KIND_MABS] = int64_t(qb.size()) * 4;
+  sz[RSDB_KIND_VABS] = int64_t(qb.size()) * 4;
+  return RSDB_OK;
+}
+
+// MASTER, MQ and VQ share ELEMENT offsets (one "state" index space): the
+// common element offset is aligned so that every kind's byte offset is a
+// multiple of align_bytes.  Likewise MABS/VABS share a block index space.
+static rsdb_status arena_layout(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                                int64_t qblock, int64_t align, int64_t* bytes, int64_t* offs,
+                                std::vector<int64_t>* state_elem_off, std::vector<int64_t>* blk_idx_off) {
+  if (!units || n_units < 0 || !bytes || align < 16 || (align & (align - 1)))
+    return fail(RSDB_EINVAL, "rsdb_arena_sizes: bad argument (align must be a power of two >= 16)");
+  int64_t acc[RSDB_NKINDS] = {0};
+  int64_t state_e = 0, blk_e = 0;
+  for (int32_t u = 0; u < n_units; ++u) {
+    if (!units[u]) return fail(RSDB_EINVAL, "null layout %d", u);
+    const rsdb::Layout& L = units[u]->L;
+    if (rank < 0 || rank >= L.m) return fail(RSDB_EINVAL, "rank out of range for unit %d", u);
+    int64_t sz[RSDB_NKINDS] = {0};
+    if (rsdb_status st = kind_sizes(L, rank, qblock, sz)) return st;
+    for (int k : {RSDB_KIND_PARAM_FULL, RSDB_KIND_GRAD_FULL, RSDB_KIND_GRAD_F32}) {
+      acc[k] = round_up(acc[k], align);
+      if (offs) offs[int64_t(u) * RSDB_NKINDS + k] = acc[k];
+      acc[k] += sz[k];
+    }
+    state_e = round_up(state_e, align);  // align elements => align bytes for 1- and 4-byte kinds
+    blk_e = round_up(blk_e, align);
+    if (state_elem_off) state_elem_off->push_back(state_e);
+    if (blk_idx_off) blk_idx_off->push_back(blk_e);
+    if (offs) {
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MASTER] = state_e * 4;
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MQ] = state_e;
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_VQ] = state_e;
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MABS] = blk_e * 4;
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_VABS] = blk_e * 4;
+    }
+    state_e += L.S;
+    blk_e += sz[RSDB_KIND_MABS] / 4;
+  }
+  for (int k : {RSDB_KIND_PARAM_FULL, RSDB_KIND_GRAD_FULL, RSDB_KIND_GRAD_F32}) bytes[k] = round_up(acc[k], align);
+  state_e = round_up(state_e, align);
+  blk_e = round_up(blk_e, align);
+  bytes[RSDB_KIND_MASTER] = state_e * 4;
+  bytes[RSDB_KIND_MQ] = state_e;
+  bytes[RSDB_KIND_VQ] = state_e;
+  bytes[RSDB_KIND_MABS] = blk_e * 4;
+  bytes[RSDB_KIND_VABS] = blk_e * 4;
+  return RSDB_OK;
+}
+
+rsdb_status rsdb_arena_sizes(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                             int64_t qblock, int64_t align_bytes, int64_t* bytes_per_kind,
+                             int64_t* unit_offsets) {
+  if (rsdb_status st = arena_layout(units, n_units, rank, qblock, align_bytes, bytes_per_kind,
+                                    unit_offsets, nullptr, nullptr))
+    return st;
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units, rsdb_comm* comm,
+                                int32_t rank, int64_t qblock, int64_t align_bytes,
+                                void* const* arena_base, rsdb_dbuffer** out) {
+  if (!units || !arena_base || !out || n_units < 0) return fail(RSDB_EINVAL, "null argument");
+  int64_t bytes[RSDB_NKINDS];
+  std::vector<int64_t> offs(size_t(n_units) * RSDB_NKINDS), st_off, bk_off;
+  if (rsdb_status st = arena_layout(units, n_units, rank, qblock, align_bytes, bytes, offs.data(),
+                                    &st_off, &bk_off))
+    return st;
+  auto db = std::make_unique<rsdb_dbuffer>();
+  for (int k = 0; k < RSDB_NKINDS; ++k) {
+    db->base[k] = arena_base[k];
+    if (bytes[k] > 0 && !arena_base[k]) return fail(RSDB_EINVAL, "arena %d is null", k);
+    if (bytes[k] > 0 && reinterpret_cast<uintptr_t>(arena_base[k]) % align_bytes)
+      return fail(RSDB_EMISMATCH, "arena %d not aligned to %lld bytes", k, (long long)align_bytes);
+  }
+  int32_t pbf = -1;
+  std::vector<rsdb::AdamBlock> tbl;
+  for (int32_t u = 0; u < n_units; ++u) {
+    const rsdb::Layout& L = units[u]->L;
+    const int32_t bf = L.elem_bytes == 2;
+    if (pbf >= 0 && bf != pbf)
+      return fail(RSDB_EMISMATCH, "one dbuffer holds one parameter dtype (unit %d differs)", u);
+    pbf = bf;
+    auto at = [&](int k) { return static_cast<char*>(arena_base[k]) + offs[size_t(u) * RSDB_NKINDS + k]; };
+    rsdb_unit_bufs b;
+    b.param_full = at(RSDB_KIND_PARAM_FULL);
+    b.grad_f32 = at(RSDB_KIND_GRAD_F32);
+    b.grad_full = bf ? at(RSDB_KIND_GRAD_FULL) : b.grad_f32;
+    auto unit = std::make_unique<rsdb_unit>();
+    std::vector<rsdb::QBlock> qb;
+    if (rsdb_status st = build_unit(L, comm, rank, b, qblock, unit.get(), &qb)) return st;
+    // arena-relative combined table: state in MASTER/MQ/VQ elements, grad in
+    // GRAD_F32 elements, param in PARAM_FULL elements.
+    const int64_t gbase = offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_GRAD_F32] / 4 + int64_t(rank) * L.S;
+    const int64_t pbase = offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_PARAM_FULL] / L.elem_bytes +
+                          int64_t(rank) * L.S;
+    if (bk_off[u] + int64_t(qb.size()) > INT32_MAX) return fail(RSDB_EINVAL, "too many blocks");
+    for (size_t i = 0; i < qb.size(); ++i)
+      tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off, qb[i].len,
+                     int32_t(bk_off[u] + int64_t(i))});
+    db->grad_bytes.push_back(int64_t(L.m) * L.S * L.elem_bytes);
+    db->units.push_back(std::move(unit));
+  }
+  db->param_bf16 = pbf < 0 ? 1 : pbf;
+  db->nblocks = int64_t(tbl.size());
+  if (rsdb_status st = db->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
+  *out = db.release();
+  return OK_CLEAR();
+}
+
+rsdb_unit* rsdb_dbuffer_unit(rsdb_dbuffer* d, int32_t i) {
+  if (!d || i < 0 || i >= int32_t(d->units.size())) return nullptr;
+  return d->units[size_t(i)].get();
+}
+int64_t rsdb_dbuffer_num_blocks(const rsdb_dbuffer* d) { return d ? d->nblocks : -1; }
+
+rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer* d, const rsdb_adam_cfg* cfg, int64_t step,
+                                        void* stream) {
+  if (!d) return fail(RSDB_EINVAL, "null dbuffer");
+  rsdb::AdamScalars s;
+  if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
+  if (d->nblocks == 0) return OK_CLEAR();
+  rsdb::AdamPtrs p{static_cast<float*>(d->base[RSDB_KIND_MASTER]),
+                   static_cast<int8_t*>(d->base[RSDB_KIND_MQ]),
+                   static_cast<uint8_t*>(d->base[RSDB_KIND_VQ]),
+                   static_cast<float*>(d->base[RSDB_KIND_MABS]),
+                   static_cast<float*>(d->base[RSDB_KIND_VABS]),
+                   static_cast<const float*>(d->base[RSDB_KIND_GRAD_F32]),
+                   d->base[RSDB_KIND_PARAM_FULL],
+                   d->param_bf16};
+  CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(d->blocks.p), d->nblocks, p, s, 0,
+                              S_(stream)));
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_zero_grads(rsdb_dbuffer* d, void* stream) {
+  if (!d) return fail(RSDB_EINVAL, "null dbuffer");
+  for (auto& u : d->units)
+    CUDA_TRY(cudaMemsetAsync(u->bufs.grad_full, 0,
+                             size_t(int64_t(u->L.m) * u->L.S * u->L.elem_bytes), S_(stream)));
+  return OK_CLEAR();
+}
+
+void rsdb_dbuffer_free(rsdb_dbuffer* d) { delete d; }
+
+// ---------------------------------------------------------------------------
+// batched ragged copy
+// ---------------------------------------------------------------------------
+rsdb_status rsdb_copy_plan_create(const rsdb_segment* segs, int64_t n, int32_t src_dtype,
+                                  int32_t dst_dtype, float scale, rsdb_copy_plan** out) {
+  if (!out || n < 0 || (n > 0 && !segs)) return fail(RSDB_EINVAL, "null argument");
+  if ((src_dtype != RSDB_BF16 && src_dtype != RSDB_F32) || (dst_dtype != RSDB_BF16 && dst_dtype != RSDB_F32))
+    return fail(RSDB_EINVAL, "dtype must be RSDB_BF16 or RSDB_F32");
+  auto cp = std::make_unique<rsdb_copy_plan>();
+  std::vector<rsdb::CopySeg> v;
+  int64_t chunks = 0;
+  constexpr int64_t CH = 4096;  // must match COPY_CHUNK in kernels.cu
+  for (int64_t i = 0; i < n; ++i) {
+    if (segs[i].numel < 0 || (segs[i].numel > 0 && (!segs[i].src || !segs[i].dst)))
+      return fail(RSDB_EINVAL, "segment %lld invalid", (long long)i);
+    if (segs[i].numel == 0) continue;
+    v.push_back({segs[i].src, segs[i].dst, segs[i].numel, chunks});
+    chunks += (segs[i].numel + CH - 1) / CH;
+  }
+  cp->nseg = int64_t(v.size());
+  cp->total_chunks = chunks;
+  cp->src_bf16 = src_dtype == RSDB_BF16;
+  cp->dst_bf16 = dst_dtype == RSDB_BF16;
+  cp->scale = scale;
+  if (!v.empty()) {
+    if (rsdb_status st = require_device()) return st;
+    if (rsdb_status st = cp->segs.upload(v.data(), v.size() * sizeof(rsdb::CopySeg))) return st;
+  }
+  *out = cp.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_copy_run(const rsdb_copy_plan* cp, void* stream) {
+  if (!cp) return fail(RSDB_EINVAL, "null plan");
+  CUDA_TRY(rsdb::launch_copy_segments(static_cast<const rsdb::CopySeg*>(cp->segs.p), cp->nseg,
+                                      cp->total_chunks, cp->src_bf16, cp->dst_bf16, cp->scale,
+                                      S_(stream)));
+  return OK_CLEAR();
+}
+
+void rsdb_copy_plan_free(rsdb_copy_plan* cp) { delete cp; }
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// Device kernels of the collective step (launchers; definitions in kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rsdb {
+
+// One 8-bit Adam quantization block: element offsets into the state
+// arrays (master / m codes / v codes share indexing), the fp32 gradient array
+// and the parameter array, plus the block's slot in the absmax arrays.
+struct AdamBlock {
+  int64_t state_off;
+  int64_t grad_off;
+  int64_t param_off;
+  int32_t len;
+  int32_t slot;
+};
+static_assert(sizeof(AdamBlock) == 32, "AdamBlock is 32 bytes");
+
+struct AdamScalars {
+  float w1, b2, w2, eps, c_wd, step_size, inv_bc2s;
+};
+
+struct AdamPtrs {
+  float* master;
+  int8_t* mq;
+  uint8_t* vq;
+  float* mabs;
+  float* vabs;
+  const float* grad;
+  void* param;        // bf16 or f32
+  int32_t param_bf16; // 1: bf16, 0: f32
+};
+
+// a6: dst[i] = fp32(src[i]) * scale, i in [0, n); positions inside the sorted
+// padding intervals pad[2j] <= i < pad[2j+1] are written 0.  src may equal dst
+// when src is f32.
+cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t n, float scale,
+                              const int64_t* pad_dev, int32_t npad, cudaStream_t st);
+
+// a8 over `nblocks` table entries.
+cudaError_t launch_adam8(const AdamBlock* table_dev, int64_t nblocks, const AdamPtrs& p,
+                         const AdamScalars& s, int32_t max_len, cudaStream_t st);
+
+struct CopySeg {
+  const void* src;
+  void* dst;
+  int64_t numel;
+  int64_t chunk_begin;  // prefix sum of chunks (for the block -> segment map)
+};
+cudaError_t launch_copy_segments(const CopySeg* segs_dev, int64_t nseg, int64_t total_chunks,
+                                 int src_bf16, int dst_bf16, float scale, cudaStream_t st);
+
+int num_sms();
+
+}  // namespace rsdb

@@ -1,0 +1,171 @@
+"""torchrun worker: one FSDP step through the C-ABI on N GPUs vs the oracle's
+simulated ranks.  Launched by tests/test_gpu_multi.py:
+
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+      --master-port P tests/dist_parity_worker.py
+
+Per unit: AllGather (bit exact), fused cast/scale + ReduceScatter (bit exact
+on dyadic synth grads; error bound on random-normal bf16 grads), 8-bit Adam
+(codes +-1, params 1e-5), then a second AllGather that must equal the
+concatenation of every rank's oracle parameter shard (bf16, within 1 ulp).
+Exit code 0 iff every check passed on every rank.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import paper_2602_22437_b200 as R  # noqa: E402
+from oracle import adam8 as OA  # noqa: E402
+from oracle import dbuffer as OD  # noqa: E402
+from oracle import planner as OP  # noqa: E402
+from synth import workloads as W  # noqa: E402
+
+from gpu_helpers import bf16_bits, f32, logical_grads, logical_params, place_gpu  # noqa: E402
+
+
+def units_for(m):
+    q = 2048
+    lay = W.llama32_1b_layer(0)
+    yield "toy", [t.numel for t in W.toy().units[0].tensors], q, 4
+    yield "llama-attn", [t.numel for t in lay.tensors][:4] + [2048, 2048], q, 2
+    yield "ragged", [5000, 77, 4109, 2048 * 3, 1, 40000, 2048 * 11 + 3], q, 2
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    comm = R.init_comm(rank, world, local)
+    ok = True
+    msgs = []
+    for name, es, q, eb in units_for(world):
+        gs = [min(q, e) for e in es]
+        o = OP.plan(es, gs, world, OP.gcoll_elems(eb))
+        c = R.plan(es, gs, world, elem_bytes=eb)
+        S, E = c.S, sum(es)
+        dt = torch.bfloat16 if eb == 2 else torch.float32
+        p_log = logical_params(5, E)
+        # ---- AllGather: only my shard is valid before the collective
+        full_ref = place_gpu(c, p_log, dt)
+        param_full = torch.zeros_like(full_ref)
+        param_full[rank * S:(rank + 1) * S] = full_ref[rank * S:(rank + 1) * S]
+        grad_full = place_gpu(c, logical_grads(5, rank, E), dt, fill=float("nan"))
+        grad_f32 = grad_full if eb == 4 else torch.empty(world * S, dtype=torch.float32,
+                                                         device="cuda")
+        u = R.Unit(c, rank, param_full, grad_full, grad_f32, qblock=q, comm=comm)
+        R.all_gather(u)
+        torch.cuda.synchronize()
+        exp = OD.place_logical(o, p_log.numpy())
+        exp_bits = OD.to_bf16_rne(exp) if eb == 2 else exp.view(np.uint32)
+        got_bits = bf16_bits(param_full) if eb == 2 else f32(param_full).view(np.uint32)
+        if not np.array_equal(got_bits, exp_bits):
+            ok = False
+            msgs.append(f"{name}: AllGather mismatch")
+        # ---- ReduceScatter (fused cast/scale)
+        R.reduce_scatter(u)
+        torch.cuda.synchronize()
+        bufs = []
+        for r in range(world):
+            src = OD.place_logical(o, logical_grads(5, r, E).numpy(), fill=np.nan)
+            bufs.append(OD.grouped_cast_scale(o, OD.to_bf16_rne(src) if eb == 2 else src,
+                                              eb == 2))
+        y_ref = OD.reduce_scatter(o, bufs)[rank]
+        y = f32(grad_f32[rank * S:(rank + 1) * S])
+        if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
+            ok = False
+            msgs.append(f"{name}: ReduceScatter not bit exact (max {np.abs(y - y_ref).max()})")
+        # ---- 8-bit Adam on my shard
+        master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
+        nb = u.num_blocks
+        mq = torch.zeros(S, dtype=torch.int8, device="cuda")
+        vq = torch.zeros(S, dtype=torch.uint8, device="cuda")
+        ma = torch.zeros(nb, dtype=torch.float32, device="cuda")
+        va = torch.zeros(nb, dtype=torch.float32, device="cuda")
+        R.step_8bit_adam(u, master, mq, vq, ma, va, R.AdamConfig(), 1)
+        R.all_gather(u)
+        torch.cuda.synchronize()
+        ref_full = []
+        for r in range(world):
+            blocks = OP.rank_blocks(o, r, q)
+            p0 = OD.shard(o, OD.place_logical(o, p_log.numpy()), r)
+            st = OA.step_8bit_adam(p0, OD.reduce_scatter(o, bufs)[r], np.zeros(S, np.int8),
+                                   np.zeros(S, np.uint8), np.zeros(len(blocks), np.float32),
+                                   np.zeros(len(blocks), np.float32), blocks, OA.AdamCfg(), 1,
+                                   out_bf16=(eb == 2))
+            ref_full.append(st)
+        mine = ref_full[rank]
+        blocks = OP.rank_blocks(o, rank, q)
+        mask = np.zeros(S, bool)
+        for off, n in blocks:
+            mask[off:off + n] = True
+        gm = f32(master)
+        err = (np.abs(gm - mine[0]) / (np.abs(mine[0]) + 1e-3))[mask]
+        dm = np.abs(mq.cpu().numpy().astype(int) - mine[1].astype(int))[mask]
+        dv = np.abs(vq.cpu().numpy().astype(int) - mine[2].astype(int))[mask]
+        if err.max(initial=0) > 1e-5 or dm.max(initial=0) > 1 or dv.max(initial=0) > 1:
+            ok = False
+            msgs.append(f"{name}: Adam mismatch err={err.max(initial=0)} dm={dm.max(initial=0)}")
+        # second AllGather: every rank's updated shard
+        if eb == 2:
+            got = bf16_bits(param_full).astype(np.int32)
+            exp = np.concatenate([s[5] for s in ref_full]).astype(np.int32)
+        else:
+            got = f32(param_full)
+            exp = np.concatenate([s[5] for s in ref_full])
+        full_mask = np.zeros(world * S, bool)
+        for l, e in zip(o.starts, o.numel):
+            full_mask[l:l + e] = True
+        d = np.abs(got - exp)[full_mask]
+        lim = 1 if eb == 2 else 1e-5 * (np.abs(exp[full_mask]).max() + 1e-3)
+        if d.max(initial=0) > lim:
+            ok = False
+            msgs.append(f"{name}: post-Adam AllGather mismatch {d.max()}")
+        del u
+    # ---- random-normal bf16 grads: fp32 RS tolerance (non-exact sums)
+    es = [300001, 4097]
+    o = OP.plan(es, [1, 1], world, 8)
+    c = R.plan(es, [1, 1], world, elem_bytes=2)
+    S = c.S
+    rng = np.random.default_rng(100 + rank)
+    g_np = [OD.to_bf16_rne(np.random.default_rng(100 + r).normal(0, 1e-2, world * S).astype(np.float32))
+            for r in range(world)]
+    for a, b in o.padding_intervals():
+        for g in g_np:
+            g[a:b] = 0
+    grad_full = torch.from_numpy(g_np[rank].view(np.int16)).cuda().view(torch.bfloat16)
+    grad_f32 = torch.empty(world * S, dtype=torch.float32, device="cuda")
+    pf = torch.zeros(world * S, dtype=torch.bfloat16, device="cuda")
+    u = R.Unit(c, rank, pf, grad_full, grad_f32, qblock=1, comm=comm)
+    R.reduce_scatter(u)
+    torch.cuda.synchronize()
+    xs = [OD.grouped_cast_scale(o, g, True) for g in g_np]
+    yref = OD.reduce_scatter_f64(o, xs)[rank]
+    absum = sum(np.abs(x[rank * S:(rank + 1) * S].astype(np.float64)) for x in xs)
+    y = f32(grad_f32[rank * S:(rank + 1) * S]).astype(np.float64)
+    if np.any(np.abs(y - yref) > 1e-6 * absum + 1e-30):
+        ok = False
+        msgs.append("random-normal RS outside 1e-6 * sum|x|")
+    del u
+    del rng
+    comm.close()
+    flag = torch.tensor([0 if ok else 1])
+    dist.all_reduce(flag)
+    if msgs:
+        print(f"[rank {rank}] " + "; ".join(msgs), flush=True)
+    if rank == 0:
+        print(f"dist parity world={world}: {'PASS' if flag.item() == 0 else 'FAIL'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

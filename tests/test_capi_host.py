@@ -1,0 +1,208 @@
+"""CPU tests of the C-ABI library (no compute calls need a GPU here):
+  * librsdb.so loads and exports every symbol include/rsdb.h declares;
+  * the C++ planner is bit-exact with the oracle (layouts, tables, padding)
+    on >= 10,000 random instances, every BJ config and the Fig. 9 sweeps;
+  * error behaviour stated in the header; device calls fail loudly (no CPU
+    fallback) when there is no GPU;
+  * planner speed claim P:491 (< 0.3 s per unit) for the C++ planner.
+"""
+import ctypes as C
+import os
+import random
+import re
+import time
+
+import pytest
+import torch
+
+import paper_2602_22437_b200 as R
+from paper_2602_22437_b200 import _capi
+from oracle import planner as P
+from synth import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "rsdb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rsdb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = _header_symbols()
+    assert len(syms) >= 35
+    lib = C.CDLL(_capi.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _capi.EXPORTED, f"{s} declared in rsdb.h but not bound"
+    assert set(_capi.EXPORTED) == set(syms)
+    assert R.lib.rsdb_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _capi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def _cmp(es, gs, m, eb):
+    gc = P.gcoll_elems(eb)
+    o = P.plan(es, gs, m, gc)
+    c = R.plan(es, gs, m, elem_bytes=eb)
+    assert c.S == o.S, (es, gs, m, eb)
+    assert c.starts == o.starts
+    assert c.padding == o.padding and c.E == o.E
+    assert c.validate() == 0
+    assert c.padding_intervals() == o.padding_intervals()
+    return o, c
+
+
+def test_planner_parity_random_tiny():
+    rng = random.Random(11)
+    for _ in range(10000):
+        n = rng.randint(0, 7)
+        es = [rng.randint(1, 64) for _ in range(n)]
+        gs = [rng.randint(1, 9) for _ in range(n)]
+        _cmp(es, gs, rng.randint(1, 9), rng.choice([1, 2, 4]))
+
+
+def test_planner_parity_random_medium_and_tables():
+    rng = random.Random(12)
+    for _ in range(400):
+        n = rng.randint(1, 30)
+        q = rng.choice([16, 64, 2048])
+        es = [rng.randint(1, 20000) for _ in range(n)]
+        kind = rng.random()
+        if kind < 0.4:
+            gs = [min(q, e) for e in es]
+        elif kind < 0.7:
+            gs = [rng.choice([1, e, max(1, e // 7)]) for e in es]
+        else:
+            gs = [rng.randint(1, 300) for _ in es]
+        m = rng.choice([1, 2, 3, 4, 8, 16])
+        o, c = _cmp(es, gs, m, rng.choice([2, 4]))
+        for r in range(m):
+            assert c.rank_segments(r) == [tuple(x) for x in P.rank_segments(o, r)]
+            try:
+                ob = P.rank_blocks(o, r, q)
+            except ValueError:
+                with pytest.raises(R.RsdbError) as ei:
+                    c.rank_blocks(r, q)
+                assert ei.value.status == _capi.RSDB_EMISMATCH
+                continue
+            assert c.rank_blocks(r, q) == [tuple(x) for x in ob]
+
+
+@pytest.mark.parametrize("wl", ["toy", "llama", "llama8b", "dsv3"])
+def test_planner_parity_bj_configs(wl):
+    units = {"toy": W.toy().units, "llama": W.llama32_1b().units[:2],
+             "llama8b": [W.llama3_8b_layer(0), W.llama3_8b_root()],
+             "dsv3": [W.dsv3_moe_unit()]}[wl]
+    for u in units:
+        es = [t.numel for t in u.tensors]
+        gs = [P.block_elems(t.shape, t.gran) for t in u.tensors]
+        assert gs == [R.block_elems(t.shape, t.gran) for t in u.tensors]
+        for m in (1, 2, 4, 8):
+            o, c = _cmp(es, gs, m, u.elem_bytes)
+            assert c.to_json() == P.to_dict(o)
+
+
+def test_planner_parity_fig9_sweep():
+    for mk in (W.deepseek_v3_671b, W.gpt_oss_120b):
+        for rows in (1, 16, 128):
+            wl = mk(rows)
+            seen = set()
+            for u in wl.units:
+                key = tuple((t.numel, P.block_elems(t.shape, t.gran)) for t in u.tensors)
+                if key in seen:
+                    continue
+                seen.add(key)
+                es = [k[0] for k in key]
+                gs = [k[1] for k in key]
+                for m in (8, 64, 256, 1024):
+                    _cmp(es, gs, m, 2)
+
+
+def test_cpp_planner_time_claim():
+    """< 0.3 s per unit; the largest unit (DSV3 MoE layer, 777 tensors)."""
+    u = W.deepseek_v3_671b(128).units[10]
+    es = [t.numel for t in u.tensors]
+    gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+    for m in (8, 1024):
+        t0 = time.perf_counter()
+        lay = R.plan(es, gs, m)
+        dt = time.perf_counter() - t0
+        assert lay.validate() == 0 and dt < 0.3
+
+
+def test_error_behaviour():
+    with pytest.raises(R.RsdbError) as e:
+        R.plan([4], [0], 2)
+    assert e.value.status == _capi.RSDB_EINVAL
+    with pytest.raises(R.RsdbError):
+        R.plan([4], [1], 0)
+    with pytest.raises(R.RsdbError):
+        R.plan([0], [1], 2)
+    with pytest.raises(R.RsdbError):
+        R.plan([4], [1], 2, elem_bytes=3)
+    with pytest.raises(R.RsdbError):
+        R.block_elems([4, 0], ("flat", 8))
+    with pytest.raises(R.RsdbError):
+        R.block_elems([4], ("flat", 0))
+    lay = R.plan([], [], 4)
+    assert lay.S == 0 and lay.starts == [] and lay.padding == 0
+    with pytest.raises(R.RsdbError) as e:
+        R.plan([8], [1], 2, elem_bytes=4).rank_blocks(0, 8)
+    assert e.value.status == _capi.RSDB_EMISMATCH
+    with pytest.raises(R.RsdbError):
+        R.plan([8], [1], 2).rank_blocks(5, 8)
+    # explicit layouts are validated against P:226-229
+    good = R.layout_from_starts([6, 4], [3, 2], 2, 6, [0, 6], elem_bytes=4, gcoll_bytes=4)
+    assert good.S == 6 and good.validate() == 0
+    with pytest.raises(R.RsdbError):
+        R.layout_from_starts([6], [3], 2, 4, [0], elem_bytes=4, gcoll_bytes=4)
+    odd = R.layout_from_starts([9], [1], 2, 5, [0], elem_bytes=2, require_gcoll=False)
+    assert odd.S == 5
+
+
+def test_block_elems_kinds():
+    assert R.block_elems([256, 128], ("flat", 2048)) == 2048
+    assert R.block_elems([256], ("flat", 2048)) == 256
+    assert R.block_elems([576, 7168], ("rows", 128)) == 128 * 7168
+    assert R.block_elems([100, 10], ("rows", 128)) == 1000
+    assert R.block_elems([3, 5], ("whole",)) == 15
+    assert R.block_elems([3, 5], ("elem",)) == 1
+
+
+def test_arena_sizes_alignment_and_disjointness():
+    lays = [R.plan([t.numel for t in u.tensors], [R.block_elems(t.shape, t.gran) for t in u.tensors], 4)
+            for u in W.llama32_1b().units[:3]]
+    for rank in range(4):
+        sizes, offs = R.arena_sizes(lays, rank, 2048, 256)
+        for k in range(8):
+            spans = []
+            for u, lay in enumerate(lays):
+                assert offs[u][k] % 256 == 0
+                per = {0: lay.m * lay.S * 2, 1: lay.m * lay.S * 2, 2: lay.m * lay.S * 4,
+                       3: lay.S * 4, 4: lay.S, 5: lay.S,
+                       6: 4 * len(lay.rank_blocks(rank, 2048)), 7: 4 * len(lay.rank_blocks(rank, 2048))}[k]
+                spans.append((offs[u][k], offs[u][k] + per))
+                assert offs[u][k] + per <= sizes[k]
+            spans.sort()
+            assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+            # master / mq / vq share element offsets
+        assert [o[3] // 4 for o in offs] == [o[4] for o in offs] == [o[5] for o in offs]
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_device_calls_fail_loudly_without_gpu():
+    lay = R.plan([4096], [2048], 1)
+    with pytest.raises(R.RsdbError) as e:
+        R.Unit(lay, 0, 256, 256, 512, qblock=2048)
+    assert e.value.status == _capi.RSDB_ECUDA
+    assert "no CPU fallback" in str(e.value)
+    with pytest.raises(R.RsdbError) as e:
+        R.Comm(b"\0" * 128, 1, 0, 0)
+    assert e.value.status == _capi.RSDB_ECUDA

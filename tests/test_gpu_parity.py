@@ -1,0 +1,301 @@
+"""-m gpu parity: the CUDA path (through the C-ABI) vs the CPU oracle, element
+by element on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star, made well-defined in DESIGN.md):
+  * AllGather / layouts: bit exact;
+  * cast/scale group op: bit exact (one fp32 multiply by fl(1/m) both sides);
+  * ReduceScatter fp32: |y - y_ref| <= 1e-6 * sum_r |x_r| (bit exact on the
+    dyadic synth inputs, where every fp32 partial sum is exact);
+  * 8-bit Adam: codes within +-1, params |dp| <= 1e-5 (|p_ref| + lr), absmax
+    relative 1e-6, bf16 shard = RNE(GPU master) exactly and within 1 bf16 ulp
+    of the oracle's.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_22437_b200 as R
+from oracle import adam8 as OA
+from oracle import dbuffer as OD
+from oracle import planner as OP
+from synth import hashgen as H
+from synth import workloads as W
+
+from gpu_helpers import bf16_bits, f32, logical_grads, logical_params, numels, place_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _plans(es, gs, m, eb):
+    gc = OP.gcoll_elems(eb)
+    o = OP.plan(es, gs, m, gc)
+    c = R.plan(es, gs, m, elem_bytes=eb)
+    assert c.starts == o.starts and c.S == o.S
+    return o, c
+
+
+# ------------------------------------------------------------------ synth
+def test_hash_generator_on_device_matches_numpy():
+    a = H.values_np(7, 17, 1000, 300000, 14, True)
+    b = H.values_torch(7, 17, 1000, 300000, 14, True, device="cuda", chunk=65536).cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    c = H.codes_np(7, 64, 5, 100000, True)
+    d = H.codes_torch(7, 64, 5, 100000, True, device="cuda").cpu().numpy()
+    assert np.array_equal(c, d)
+
+
+# ------------------------------------------------------------------ a6
+CAST_CASES = [
+    ([256 * 128, 256] * 6, "flat", 1, 2), ([256 * 128, 256] * 6, "flat", 2, 4),
+    ([5000, 77, 4109, 2048 * 3, 1], "flat", 3, 2), ([5000, 77, 4109, 2048 * 3, 1], "elem", 8, 2),
+    ([123457, 99, 7], "whole", 5, 2), ([4096 * 9 + 5], "elem", 4, 4), ([1 << 20, 3], "flat", 8, 2),
+]
+
+
+@pytest.mark.parametrize("es,gk,m,eb", CAST_CASES)
+def test_cast_scale_bit_exact(es, gk, m, eb):
+    gs = [min(2048, e) if gk == "flat" else (1 if gk == "elem" else e) for e in es]
+    o, c = _plans(es, gs, m, eb)
+    E = sum(es)
+    g_log = logical_grads(0, 1, E)
+    dt = torch.bfloat16 if eb == 2 else torch.float32
+    grad_full = place_gpu(c, g_log, dt, fill=float("nan"))       # garbage padding
+    grad_f32 = torch.empty(m * c.S, dtype=torch.float32, device="cuda")
+    param_full = torch.zeros(m * c.S, dtype=dt, device="cuda")
+    for rank in sorted({0, m - 1}):
+        q = {"flat": 2048, "elem": 1, "whole": max(es)}[gk]
+        u = R.Unit(c, rank, param_full, grad_full, grad_f32 if eb == 2 else grad_full, qblock=q)
+        out = grad_f32 if eb == 2 else grad_full
+        if eb == 4:
+            grad_full.copy_(place_gpu(c, g_log, dt, fill=float("nan")))
+        R.unit_cast_scale(u)
+        torch.cuda.synchronize()
+        src = OD.place_logical(o, g_log.numpy(), fill=np.nan)
+        ref = OD.grouped_cast_scale(o, OD.to_bf16_rne(src) if eb == 2 else src, eb == 2)
+        assert np.array_equal(f32(out).view(np.uint32), ref.view(np.uint32))
+
+
+def test_unit_rejects_misaligned_buffers():
+    """Units require 16-byte aligned buffers (NCCL alignment)."""
+    es, gs, m = [3000, 5], [1, 1], 2
+    o, c = _plans(es, gs, m, 4)
+    E = sum(es)
+    g_log = logical_grads(3, 0, E)
+    base = torch.zeros(m * c.S + 4, dtype=torch.float32, device="cuda")
+    src = base[1:1 + m * c.S]
+    src.copy_(place_gpu(c, g_log, torch.float32))
+    dst = torch.zeros(m * c.S + 4, dtype=torch.float32, device="cuda")[1:1 + m * c.S]
+    pf = torch.zeros(m * c.S, dtype=torch.float32, device="cuda")
+    with pytest.raises(R.RsdbError):        # units require 16-B aligned buffers
+        R.Unit(c, 0, pf, src, dst, qblock=1)
+
+
+# ------------------------------------------------------------------ a8
+def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None):
+    gs = [min(q, e) for e in es]
+    o, c = _plans(es, gs, m, eb)
+    E = sum(es)
+    S = c.S
+    dt = torch.bfloat16 if eb == 2 else torch.float32
+    p_log = logical_params(seed, E)
+    g_log = logical_grads(seed, rank, E)
+    if zero_grad_tensor is not None:
+        a = sum(es[:zero_grad_tensor])
+        g_log[a:a + es[zero_grad_tensor]] = 0
+    # ----- GPU side (product layout) -----
+    master_full = place_gpu(c, p_log, torch.float32)
+    master = master_full[rank * S:(rank + 1) * S].clone()
+    grad_f32 = place_gpu(c, g_log, torch.float32)
+    grad_full = torch.zeros(m * S, dtype=dt, device="cuda")
+    param_full = torch.zeros(m * S, dtype=dt, device="cuda")
+    u = R.Unit(c, rank, param_full, grad_full if eb == 2 else grad_f32, grad_f32, qblock=q)
+    nb = u.num_blocks
+    blocks_c = c.rank_blocks(rank, q)
+    assert len(blocks_c) == nb
+    if warm:
+        mq = H.codes_torch(seed, H.STREAM_MCODE, rank * S, S, True, device="cuda")
+        vq = H.codes_torch(seed, H.STREAM_VCODE, rank * S, S, False, device="cuda")
+        ma = H.absmax_torch(seed, H.STREAM_ABSM, rank * 100000, nb, 14, device="cuda")
+        va = H.absmax_torch(seed, H.STREAM_ABSV, rank * 100000, nb, 22, device="cuda")
+    else:
+        mq = torch.zeros(S, dtype=torch.int8, device="cuda")
+        vq = torch.zeros(S, dtype=torch.uint8, device="cuda")
+        ma = torch.zeros(nb, dtype=torch.float32, device="cuda")
+        va = torch.zeros(nb, dtype=torch.float32, device="cuda")
+    ins = [t.cpu().numpy().copy() for t in (master, mq, vq, ma, va)]
+    cfg = R.AdamConfig()
+    R.step_8bit_adam(u, master, mq, vq, ma, va, cfg, step)
+    torch.cuda.synchronize()
+    # ----- oracle side (oracle layout) -----
+    blocks_o = OP.rank_blocks(o, rank, q)
+    assert [tuple(b) for b in blocks_o] == blocks_c
+    g_or = OD.shard(o, OD.place_logical(o, g_log.numpy()), rank)
+    ref = OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], blocks_o,
+                            OA.AdamCfg(), step, out_bf16=(eb == 2))
+    _check_adam(o, rank, blocks_o, (master, mq, vq, ma, va, param_full), ref, ins, eb, cfg.lr)
+    return u
+
+
+def _check_adam(o, rank, blocks, gpu, ref, ins, eb, lr):
+    master, mq, vq, ma, va, param_full = gpu
+    S = o.S
+    mask = np.zeros(S, bool)
+    for off, n in blocks:
+        mask[off:off + n] = True
+    gm = f32(master)
+    # params
+    err = np.abs(gm - ref[0]) / (np.abs(ref[0]) + lr)
+    assert err[mask].max(initial=0) <= 1e-5, err[mask].max()
+    assert np.array_equal(gm[~mask], ins[0][~mask])  # padding untouched
+    # codes +-1
+    dm = np.abs(mq.cpu().numpy().astype(np.int32) - ref[1].astype(np.int32))
+    dv = np.abs(vq.cpu().numpy().astype(np.int32) - ref[2].astype(np.int32))
+    assert dm[mask].max(initial=0) <= 1 and dv[mask].max(initial=0) <= 1
+    assert np.mean(dm[mask] != 0) < 1e-3 and np.mean(dv[mask] != 0) < 1e-3
+    # absmax
+    for a, r in ((f32(ma), ref[3]), (f32(va), ref[4])):
+        assert np.all(np.abs(a - r) <= 1e-6 * np.abs(r) + 1e-30)
+    # parameter shard for the next AllGather
+    shard = param_full[rank * S:(rank + 1) * S]
+    if eb == 2:
+        b = bf16_bits(shard)
+        rne = OD.to_bf16_rne(gm)
+        assert np.array_equal(b[mask], rne[mask])
+        diff = np.abs(b[mask].astype(np.int32) - ref[5][mask].astype(np.int32))
+        assert diff.max(initial=0) <= 1
+        assert not b[~mask].any()
+    else:
+        assert np.array_equal(f32(shard)[mask], gm[mask])
+
+
+ADAM_CASES = [
+    # es, q, m, eb, rank, step, warm
+    ([256 * 128, 256] * 6, 2048, 2, 4, 1, 1, False),          # toy config, fp32 unit
+    ([256 * 128, 256] * 6, 2048, 2, 4, 0, 5, True),
+    ([5000, 77, 4109, 2048 * 3, 1, 40000], 2048, 3, 2, 0, 3, True),   # ragged, misaligned
+    ([5000, 77, 4109, 2048 * 3, 1, 40000], 2048, 3, 2, 2, 3, True),
+    ([5000, 77, 4109, 2048 * 3, 1, 40000], 2048, 1, 2, 0, 1, False),
+    ([2048 * 40, 2048 * 7 + 100, 33], 4096, 2, 2, 1, 2, True),     # q > 2048: two-pass path
+    ([2048 * 40, 2048 * 7 + 100, 33], 1024, 4, 2, 3, 9, True),
+    ([2048 * 64 + 1000], 2048, 8, 2, 5, 100, True),
+]
+
+
+@pytest.mark.parametrize("es,q,m,eb,rank,step,warm", ADAM_CASES)
+def test_adam8_parity(es, q, m, eb, rank, step, warm):
+    _adam_case(es, q, m, eb, rank, step, warm)
+
+
+def test_adam8_zero_gradient_block():
+    """Zero state + zero gradient: m = v = 0 -> absmax 0 -> codes 0."""
+    _adam_case([4096, 2048, 300], 2048, 1, 2, 0, 1, False, zero_grad_tensor=1)
+
+
+# ------------------------------------------------------ unit through NCCL, world 1
+def test_unit_world1_nccl_path():
+    u_decl = W.llama32_1b_layer(0)
+    es = [t.numel for t in u_decl.tensors][:4] + [2048, 2048]
+    gs = [min(2048, e) for e in es]
+    o, c = _plans(es, gs, 1, 2)
+    comm = R.Comm(R.Comm.unique_id(), 1, 0, 0)
+    E, S = sum(es), c.S
+    p_log, g_log = logical_params(1, E), logical_grads(1, 0, E)
+    param_full = place_gpu(c, p_log, torch.bfloat16)
+    before = param_full.clone()
+    grad_full = place_gpu(c, g_log, torch.bfloat16)
+    grad_f32 = torch.empty(S, dtype=torch.float32, device="cuda")
+    u = R.Unit(c, 0, param_full, grad_full, grad_f32, qblock=2048, comm=comm)
+    R.all_gather(u)
+    R.reduce_scatter(u)
+    torch.cuda.synchronize()
+    assert torch.equal(param_full.view(torch.int16), before.view(torch.int16))
+    ref = OD.grouped_cast_scale(o, OD.to_bf16_rne(OD.place_logical(o, g_log.numpy())), True)
+    assert np.array_equal(f32(grad_f32), ref)
+    del u
+    comm.close()
+
+
+# ------------------------------------------------------ DBuffer one-launch Adam
+def test_dbuffer_one_launch_equals_per_unit_oracle():
+    decl = [([t.numel for t in W.llama32_1b_layer(0).tensors][-3:] + [70000, 33], 2)]
+    decl.append(([256 * 128, 256, 256 * 128, 256], 2))
+    decl.append(([2048 * 5 + 7, 19, 4096], 2))
+    m, rank, q = 4, 1, 2048
+    lays_o, lays_c = [], []
+    for es, eb in decl:
+        o, c = _plans(es, [min(q, e) for e in es], m, eb)
+        lays_o.append(o)
+        lays_c.append(c)
+    sizes, offs = R.arena_sizes(lays_c, rank, q, 256)
+    ar = [torch.zeros(max(1, s), dtype=torch.uint8, device="cuda") for s in sizes]
+    db = R.DBuffer(lays_c, rank, ar, qblock=q, align=256)
+    assert db.num_blocks == sum(len(l.rank_blocks(rank, q)) for l in lays_c)
+    refs, ins_all, views = [], [], []
+    for ui, ((es, eb), o, c) in enumerate(zip(decl, lays_o, lays_c)):
+        E, S = sum(es), c.S
+        off = offs[ui]
+        nb = len(c.rank_blocks(rank, q))
+        v = {
+            "param_full": ar[0][off[0]:off[0] + m * S * 2].view(torch.bfloat16),
+            "grad_f32": ar[2][off[2]:off[2] + m * S * 4].view(torch.float32),
+            "master": ar[3][off[3]:off[3] + S * 4].view(torch.float32),
+            "mq": ar[4][off[4]:off[4] + S].view(torch.int8),
+            "vq": ar[5][off[5]:off[5] + S],
+            "ma": ar[6][off[6]:off[6] + nb * 4].view(torch.float32),
+            "va": ar[7][off[7]:off[7] + nb * 4].view(torch.float32),
+        }
+        p_log, g_log = logical_params(ui, E), logical_grads(ui, rank, E)
+        v["master"].copy_(place_gpu(c, p_log, torch.float32)[rank * S:(rank + 1) * S])
+        v["grad_f32"].copy_(place_gpu(c, g_log, torch.float32))
+        v["mq"].copy_(H.codes_torch(ui, H.STREAM_MCODE, 0, S, True, device="cuda"))
+        v["vq"].copy_(H.codes_torch(ui, H.STREAM_VCODE, 0, S, False, device="cuda"))
+        v["ma"].copy_(H.absmax_torch(ui, H.STREAM_ABSM, 0, nb, 14, device="cuda"))
+        v["va"].copy_(H.absmax_torch(ui, H.STREAM_ABSV, 0, nb, 22, device="cuda"))
+        ins = [v[k].cpu().numpy().copy() for k in ("master", "mq", "vq", "ma", "va")]
+        blocks = OP.rank_blocks(o, rank, q)
+        g_or = OD.shard(o, OD.place_logical(o, g_log.numpy()), rank)
+        refs.append(OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], blocks,
+                                      OA.AdamCfg(), 4))
+        ins_all.append(ins)
+        views.append(v)
+    cfg = R.AdamConfig()
+    db.step_8bit_adam(cfg, 4)
+    torch.cuda.synchronize()
+    for o, v, ref, ins in zip(lays_o, views, refs, ins_all):
+        _check_adam(o, rank, OP.rank_blocks(o, rank, q),
+                    (v["master"], v["mq"], v["vq"], v["ma"], v["va"], v["param_full"]),
+                    ref, ins, 2, cfg.lr)
+    db.close()
+
+
+# ------------------------------------------------------------------ copies
+def test_copy_plan_parity():
+    rng = np.random.default_rng(0)
+    n_seg = 37
+    lens = rng.integers(1, 20000, n_seg)
+    src = torch.from_numpy(H.params_np(3, 0, int(lens.sum()) + 64)).cuda()
+    dst32 = torch.zeros(int(lens.sum()) + 64 * n_seg, dtype=torch.float32, device="cuda")
+    dst16 = torch.zeros_like(dst32, dtype=torch.bfloat16)
+    segs32, segs16, exp = [], [], np.zeros(dst32.numel(), np.float32)
+    so = do = 0
+    srcn = src.cpu().numpy()
+    for i, n in enumerate(lens):
+        n = int(n)
+        so_i = so + (i % 3)            # misaligned starts for some segments
+        segs32.append((src.data_ptr() + 4 * so_i, dst32.data_ptr() + 4 * do, n))
+        segs16.append((src.data_ptr() + 4 * so_i, dst16.data_ptr() + 2 * do, n))
+        exp[do:do + n] = srcn[so_i:so_i + n] * np.float32(0.5)
+        so += n
+        do += n + (i % 5)
+    R.CopyPlan(segs32, R.RSDB_F32, R.RSDB_F32, 0.5).run()
+    R.CopyPlan(segs16, R.RSDB_F32, R.RSDB_BF16, 0.5).run()
+    torch.cuda.synchronize()
+    assert np.array_equal(f32(dst32), exp)
+    assert np.array_equal(bf16_bits(dst16), OD.to_bf16_rne(exp))
