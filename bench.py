@@ -1,0 +1,537 @@
+#!/usr/bin/env python
+"""Benchmark of the RaggedShard/DBuffer collective step (veScale-FSDP, arxiv
+2602.22437) on B200.  Contract: see DESIGN.md "Measurement".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): Llama-3.2-1B-shaped bf16 parameter set,
+one FSDP unit per decoder layer plus a root unit (embed + final norm), 2048-
+element 8-bit-Adam blocks, all 17 units in one batched DBuffer per rank.
+Synthetic, seeded inputs (synth/), random-init weights.
+
+One step (all per-step rows of SURVEY §8(a); a1-a3 planning is one-time at
+init, reported as plan_ms):
+    for unit in units:            a4  AllGather (in place, zero-copy views a5)
+    for unit in reversed(units):  a6  fused cast bf16->fp32 x 1/m, padding 0
+                                  a7  ReduceScatter fp32 (in place)
+    one launch over every shard:  a8  block-wise 8-bit Adam (+ bf16 shard)
+
+value = whole-job algorithmic GB/s of the step = sum over ranks of
+        [AG bus bytes + RS bus bytes + cast bytes + Adam bytes] / max-rank time
+        (per-rank bytes: AG (m-1) S 2, RS (m-1) S 4, cast m S 6, Adam 18 per
+        owned element + 16 per block), per unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AG+RS bus GB/s per FSDP unit at 1/2/4/8 B200; 8-bit Adam shard HBM GB/s"
+UNIT = "GB/s"
+WORKLOAD = "llama-3.2-1b"
+QBLOCK = 2048
+ALIGN = 256
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--layers", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: max(3, steps // 10)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+NVLINK_PEAK_GBS = 770.0  # measured per-direction peer bandwidth, B200_PROFILING.md
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = set(gpus)
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.12)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons, n = [], 0.0, set(), 0
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) not in self.gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            n += 1
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": n}
+
+
+# ---------------------------------------------------------------- setup
+def build_units(n_layers):
+    from synth import workloads as W
+    wl = W.llama32_1b(QBLOCK, n_layers)
+    return wl.units
+
+
+def setup(rank, world, local, units, comm):
+    import torch
+
+    import paper_2602_22437_b200 as R
+    from synth import hashgen as H
+
+    t0 = time.perf_counter()
+    lays = []
+    for u in units:
+        es = [t.numel for t in u.tensors]
+        gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+        lays.append(R.plan(es, gs, world, elem_bytes=2))
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    sizes, offs = R.arena_sizes(lays, rank, QBLOCK, ALIGN)
+    dev = torch.device("cuda", local)
+    arenas = [torch.zeros(max(1, s), dtype=torch.uint8, device=dev) for s in sizes]
+    db = R.DBuffer(lays, rank, arenas, qblock=QBLOCK, align=ALIGN, comm=comm)
+    # fill: logical params / grads from the counter hash, placed through the views
+    views = []
+    for ui, (u, lay) in enumerate(zip(units, lays)):
+        S, m = lay.S, lay.m
+        off = offs[ui]
+        nb = len(lay.rank_blocks(rank, QBLOCK))
+        v = {
+            "param_full": arenas[0][off[0]:off[0] + m * S * 2].view(torch.bfloat16),
+            "grad_full": arenas[1][off[1]:off[1] + m * S * 2].view(torch.bfloat16),
+            "grad_f32": arenas[2][off[2]:off[2] + m * S * 4].view(torch.float32),
+            "master": arenas[3][off[3]:off[3] + S * 4].view(torch.float32),
+            "mq": arenas[4][off[4]:off[4] + S].view(torch.int8),
+            "vq": arenas[5][off[5]:off[5] + S],
+            "ma": arenas[6][off[6]:off[6] + nb * 4].view(torch.float32),
+            "va": arenas[7][off[7]:off[7] + nb * 4].view(torch.float32),
+        }
+        E = lay.E
+        p = H.params_torch(ui, 0, E, device=dev)
+        g = H.grads_torch(ui, rank, 0, E, device=dev)
+        full_p = torch.zeros(m * S, dtype=torch.float32, device=dev)
+        o = 0
+        for l, e in zip(lay.starts, [t.numel for t in u.tensors]):
+            full_p[l:l + e] = p[o:o + e]
+            v["grad_full"][l:l + e] = g[o:o + e].to(torch.bfloat16)
+            o += e
+        v["param_full"].copy_(full_p.to(torch.bfloat16))
+        v["master"].copy_(full_p[rank * S:(rank + 1) * S])
+        # warm synthetic 8-bit Adam state (codes + per-block absmax)
+        v["mq"].copy_(H.codes_torch(ui, H.STREAM_MCODE, rank * S, S, True, device=dev))
+        v["vq"].copy_(H.codes_torch(ui, H.STREAM_VCODE, rank * S, S, False, device=dev))
+        v["ma"].copy_(H.absmax_torch(ui, H.STREAM_ABSM, rank * 10 ** 7, nb, 14, device=dev))
+        v["va"].copy_(H.absmax_torch(ui, H.STREAM_ABSV, rank * 10 ** 7, nb, 22, device=dev))
+        del p, g, full_p
+        views.append(v)
+    torch.cuda.synchronize()
+    return lays, db, arenas, views, plan_ms, sizes
+
+
+def algorithmic_bytes(lays, rank):
+    """Per-rank algorithmic bytes of one step, by row."""
+    ag = rs = cast = adam = 0
+    n_el = n_blk = 0
+    for lay in lays:
+        m, S = lay.m, lay.S
+        ag += (m - 1) * S * 2
+        rs += (m - 1) * S * 4
+        cast += m * S * 6
+        blocks = lay.rank_blocks(rank, QBLOCK)
+        el = sum(n for _, n in blocks)
+        n_el += el
+        n_blk += len(blocks)
+    adam = 18 * n_el + 16 * n_blk
+    return {"ag": ag, "rs": rs, "cast": cast, "adam": adam, "adam_elems": n_el,
+            "adam_blocks": n_blk}
+
+
+# ---------------------------------------------------------------- step
+class Timers:
+    """CUDA event pairs on the launching stream around each op kind."""
+
+    def __init__(self):
+        self.pairs = {"ag": [], "cast": [], "rs": [], "adam": []}
+
+    def rec(self, kind, stream):
+        import torch
+        a = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        return a
+
+    def add(self, kind, a, b):
+        self.pairs[kind].append((a, b))
+
+    def totals_ms(self):
+        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.pairs.items()}
+
+    def counts(self):
+        return {k: len(v) for k, v in self.pairs.items()}
+
+
+def step(R, db, cfg, t, stream, timers=None):
+    import torch
+    units = db.units
+
+    def timed(kind, fn):
+        if timers is None:
+            fn()
+            return
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        timers.add(kind, a, b)
+
+    for u in units:
+        timed("ag", lambda u=u: R.all_gather(u, stream))
+    for u in reversed(units):
+        timed("cast", lambda u=u: R.unit_cast_scale(u, stream))
+        timed("rs", lambda u=u: R.unit_reduce_scatter_f32(u, stream))
+    timed("adam", lambda: db.step_8bit_adam(cfg, t, stream))
+
+
+def barrier(world):
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.item()
+
+
+def profile_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(kernel)
+        if e and e.get("workload") == WORKLOAD and e.get("n_gpus") == 1:
+            return e["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle)
+def oracle_sample_step(world, n_blocks, seed=0):
+    """The oracle (as it stands) on a bounded sample of the workload: a slice
+    of n_blocks 2048-element blocks of the layer unit, planned for `world`
+    simulated ranks; AG, cast/scale, RS and 8-bit Adam for EVERY rank.
+    Returns (seconds, whole-job algorithmic bytes, elements)."""
+    import numpy as np
+
+    from oracle import adam8 as OA
+    from oracle import dbuffer as OD
+    from oracle import planner as OP
+    from synth import hashgen as H
+
+    es = [n_blocks * QBLOCK]
+    E = es[0]
+    o = OP.plan(es, [QBLOCK], world, OP.gcoll_elems(2))
+    S = o.S
+    p_log = H.params_np(seed, 0, E)
+    grads = [OD.to_bf16_rne(OD.place_logical(o, H.grads_np(seed, r, 0, E))) for r in range(world)]
+    params16 = OD.to_bf16_rne(OD.place_logical(o, p_log))
+    master = OD.place_logical(o, p_log)
+    t0 = time.perf_counter()
+    OD.all_gather([OD.shard(o, params16, k) for k in range(world)])
+    xs = [OD.grouped_cast_scale(o, g, True) for g in grads]
+    ys = OD.reduce_scatter(o, xs)
+    for r in range(world):
+        blocks = OP.rank_blocks(o, r, QBLOCK)
+        nb = len(blocks)
+        OA.step_8bit_adam(OD.shard(o, master, r), ys[r], np.zeros(S, np.int8),
+                          np.zeros(S, np.uint8), np.zeros(nb, np.float32),
+                          np.zeros(nb, np.float32), blocks, OA.AdamCfg(), 1)
+    dt = time.perf_counter() - t0
+    nbytes = world * ((world - 1) * S * 2 + (world - 1) * S * 4 + world * S * 6) + 18 * E + 16 * n_blocks
+    return dt, nbytes, E
+
+
+def cpu_baseline(world, target_s=10.0):
+    dt, nb, E = oracle_sample_step(world, 256)
+    blocks = max(256, int(256 * target_s / max(dt, 1e-3)))
+    blocks = min(blocks, 1 << 16)
+    dt, nb, E = oracle_sample_step(world, blocks)
+    return {"value": nb / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{E} params ({blocks} x 2048-elem blocks of the layer unit), "
+                      f"{world} simulated rank(s), AG+cast+RS+8-bit Adam, numpy single thread, "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    # calibrate: the whole --steps K --warmup W run should take ~2 minutes
+    dt, _, _ = oracle_sample_step(world, 64)
+    per_step = 120.0 / max(1, args.steps + args.warmup)
+    blocks = max(16, min(1 << 15, int(64 * per_step / max(dt, 1e-4))))
+    for _ in range(args.warmup):
+        oracle_sample_step(world, blocks)
+    tot_t = tot_b = 0.0
+    E = 0
+    for _ in range(args.steps):
+        dt, nb, E = oracle_sample_step(world, blocks)
+        tot_t += dt
+        tot_b += nb
+    value = tot_b / tot_t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{WORKLOAD} per-layer FSDP units (bounded oracle sample)",
+                       "qblock": QBLOCK, "parallelism": f"fsdp{world} (simulated ranks)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{E} params per step ({blocks} blocks), {world} "
+                                       "simulated rank(s), numpy single thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- main arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_22437_b200 as R
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    comm = R.init_comm(rank, world, local)
+    units = build_units(args.layers)
+    lays, db, arenas, views, plan_ms, sizes = setup(rank, world, local, units, comm)
+    ab = algorithmic_bytes(lays, rank)
+    per_rank_bytes = ab["ag"] + ab["rs"] + ab["cast"] + ab["adam"]
+    job_bytes = sum_over_ranks(per_rank_bytes, world)
+    cfg = R.AdamConfig()
+    stream = torch.cuda.Stream()
+    t = 1
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(R, db, cfg, t, stream)
+            t += 1
+    stream.synchronize()
+    # ---------------- timed region: inputs resident in HBM
+    timers = Timers()
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = Clocks(range(world)) if rank == 0 else None
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step(R, db, cfg, t, stream, timers)
+            t += 1
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop() if clocks else None
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, world)
+    tot = timers.totals_ms()
+    cnt = timers.counts()
+    K = args.steps
+    # per-op rates on this rank (per launch averages)
+    adam_ms = tot["adam"] / max(1, cnt["adam"])
+    cast_ms = tot["cast"] / K
+    ag_ms, rs_ms = tot["ag"] / K, tot["rs"] / K
+    adam_gbs = ab["adam"] / (adam_ms * 1e-3) / 1e9
+    cast_gbs = ab["cast"] / (cast_ms * 1e-3) / 1e9
+    ag_bus = ab["ag"] / (ag_ms * 1e-3) / 1e9 if world > 1 else None
+    rs_bus = ab["rs"] / (rs_ms * 1e-3) / 1e9 if world > 1 else None
+    hbm_peak, peak_src = load_peaks()
+    # dominant kernel of the step (largest share of device time)
+    shares = {"adam8_kernel": tot["adam"], "cast_scale_kernel": tot["cast"],
+              "nccl_reduce_scatter": tot["rs"], "nccl_all_gather": tot["ag"]}
+    dom = max(shares, key=shares.get)
+    if dom in ("adam8_kernel", "cast_scale_kernel"):
+        ach = adam_gbs if dom == "adam8_kernel" else cast_gbs
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": profile_traffic(dom), "peak_source": peak_src}
+    else:
+        ach = rs_bus if dom == "nccl_reduce_scatter" else ag_bus
+        roof = {"kernel": dom, "bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK_GBS,
+                "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "traffic": None,
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
+    roof["share_of_step"] = shares[dom] / max(1e-9, ms_local)
+    value = job_bytes / (ms / K * 1e-3) / 1e9
+
+    # ---------------- e2e: host buffers through the C-ABI, copies inside
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes)
+    # ---------------- CPU baseline (oracle) on rank 0
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(world)
+    barrier(world)
+    if rank == 0:
+        E = sum(l.E for l in lays)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{WORKLOAD}: {len(lays)} FSDP units (root + {args.layers} "
+                                   f"layers), {E} params, bf16 params/grads, 2048-elem 8-bit "
+                                   "Adam blocks, warm synthetic states",
+                       "units": len(lays), "params": E, "qblock": QBLOCK,
+                       "parallelism": f"fsdp{world}",
+                       "l2": f"no flush: per-step working set {sum(sizes) / 2 ** 30:.1f} GiB "
+                             f"per rank >> L2 ({L2_BYTES >> 20} MiB)",
+                       "plan_ms": plan_ms},
+            "per_op": {"adam_hbm_gbs": adam_gbs, "adam_ms_per_launch": adam_ms,
+                       "cast_hbm_gbs": cast_gbs, "cast_ms_per_step": cast_ms,
+                       "ag_busbw_gbs": ag_bus, "rs_busbw_gbs": rs_bus,
+                       "ag_ms_per_step": ag_ms, "rs_ms_per_step": rs_ms,
+                       "bytes_per_rank": ab},
+            "roofline": roof,
+            "clocks": clk,
+            "gpu_launches": (cnt["cast"] + cnt["adam"]),
+            "nccl_calls": cnt["ag"] + cnt["rs"],
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    db.close()
+    comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes):
+    """Same step, through the public C-ABI calls, with the step's inputs (this
+    rank's bf16 gradient buffers) copied host->device from pinned memory and
+    the step's result (the updated bf16 parameter shards) copied back, every
+    step, inside the timed region."""
+    import torch
+    K = args.e2e_steps or max(3, args.steps // 10)
+    host_g, host_p = [], []
+    for v, lay in zip(views, lays):
+        host_g.append(v["grad_full"].cpu().pin_memory())
+        host_p.append(torch.empty(lay.S, dtype=torch.bfloat16).pin_memory())
+    h2d = sum(h.numel() * 2 for h in host_g)
+    d2h = sum(h.numel() * 2 for h in host_p)
+
+    def e2e_step(tt):
+        for v, h in zip(views, host_g):
+            v["grad_full"].copy_(h, non_blocking=True)
+        for u in db.units:
+            R.all_gather(u, stream)
+        for u in reversed(db.units):
+            R.reduce_scatter(u, stream)
+        db.step_8bit_adam(cfg, tt, stream)
+        for v, h, lay in zip(views, host_p, lays):
+            h.copy_(v["param_full"][rank * lay.S:(rank + 1) * lay.S], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        e2e_step(t)
+        t += 1
+    torch.cuda.synchronize()
+    barrier(world)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(K):
+            e2e_step(t)
+            t += 1
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    return {"value": job_bytes / (ms / K * 1e-3) / 1e9, "unit": UNIT, "steps": K,
+            "ms_per_step": ms / K, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,6 +183,11 @@ rsdb_status rsdb_unit_cast_scale(rsdb_unit*, void* stream);
  * grad_f32; rank k's result is grad_f32 + k*S = (1/m) sum_r G_r[kS:(k+1)S]. */
 rsdb_status rsdb_reduce_scatter(rsdb_unit*, void* stream);
 
+/* a7 alone: the in-place fp32 ReduceScatter (sum) of grad_f32 as it stands
+ * (rsdb_reduce_scatter == rsdb_unit_cast_scale + this; split so that the two
+ * can be timed separately). */
+rsdb_status rsdb_unit_reduce_scatter_f32(rsdb_unit*, void* stream);
+
 /* a8: block-wise 8-bit Adam on the local ragged shard, no
  * communication.  The per-step scalars (1 - lr*wd, lr/(1-b1^t),
  * sqrt(1-b2^t)) are formed in fp64 on the host and rounded to fp32; the

@@ -267,6 +267,11 @@ def reduce_scatter(unit: Unit, stream=None) -> None:
     check(lib.rsdb_reduce_scatter(unit.handle, _stream(stream)))
 
 
+def unit_reduce_scatter_f32(unit: Unit, stream=None) -> None:
+    """a7 alone: in-place fp32 ReduceScatter of grad_f32 as it stands."""
+    check(lib.rsdb_unit_reduce_scatter_f32(unit.handle, _stream(stream)))
+
+
 def step_8bit_adam(unit: Unit, master, m_q, v_q, m_absmax, v_absmax, cfg: AdamConfig,
                    step: int, stream=None) -> None:
     """a8: block-wise 8-bit Adam on the unit's local ragged shard."""

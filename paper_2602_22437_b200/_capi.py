@@ -72,6 +72,7 @@ _SIGS = {
     "rsdb_all_gather": (i32, [vp, vp]),
     "rsdb_unit_cast_scale": (i32, [vp, vp]),
     "rsdb_reduce_scatter": (i32, [vp, vp]),
+    "rsdb_unit_reduce_scatter_f32": (i32, [vp, vp]),
     "rsdb_step_8bit_adam": (i32, [vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64, vp]),
     "rsdb_arena_sizes": (i32, [C.POINTER(vp), i32, i32, i64, i64, P_i64, P_i64]),
     "rsdb_dbuffer_create": (i32, [C.POINTER(vp), i32, vp, i32, i64, i64, C.POINTER(vp),
@@ -98,7 +99,7 @@ class RsdbError(RuntimeError):
 def load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2602_22437_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2602_22437_b200/build.py` "
             "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():

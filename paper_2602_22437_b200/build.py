@@ -1,6 +1,6 @@
 """Build librsdb.so in-tree with nvcc for sm_100a (B200).
 
-python -m paper_2602_22437_b200.build      (or __graft_entry__.build())
+python paper_2602_22437_b200/build.py      (or __graft_entry__.build())
 
 Flags: -gencode arch=compute_100a,code=sm_100a (SASS only, no PTX JIT),
 -O3 -lineinfo (ncu source view), -Xptxas -v (register / spill report kept in

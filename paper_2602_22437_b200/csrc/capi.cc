@@ -361,14 +361,27 @@ rsdb_status rsdb_unit_cast_scale(rsdb_unit* u, void* stream) {
   return OK_CLEAR();
 }
 
+static rsdb_status rs_f32(rsdb_unit* u, void* stream) {
+  float* g = static_cast<float*>(u->bufs.grad_f32);
+  NCCL_TRY(ncclReduceScatter(g, g + int64_t(u->rank) * u->L.S, size_t(u->L.S), ncclFloat32,
+                             ncclSum, u->comm->nc, S_(stream)));
+  return RSDB_OK;
+}
+
 rsdb_status rsdb_reduce_scatter(rsdb_unit* u, void* stream) {
   if (!u) return fail(RSDB_EINVAL, "null unit");
   if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
   if (u->L.S == 0) return OK_CLEAR();
   if (rsdb_status st = cast_scale(u, stream)) return st;
-  float* g = static_cast<float*>(u->bufs.grad_f32);
-  NCCL_TRY(ncclReduceScatter(g, g + int64_t(u->rank) * u->L.S, size_t(u->L.S), ncclFloat32,
-                             ncclSum, u->comm->nc, S_(stream)));
+  if (rsdb_status st = rs_f32(u, stream)) return st;
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_unit_reduce_scatter_f32(rsdb_unit* u, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
+  if (u->L.S == 0) return OK_CLEAR();
+  if (rsdb_status st = rs_f32(u, stream)) return st;
   return OK_CLEAR();
 }
 

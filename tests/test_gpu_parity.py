@@ -7,8 +7,8 @@ Tolerances (BASELINE.json north_star, made well-defined in DESIGN.md):
   * ReduceScatter fp32: |y - y_ref| <= 1e-6 * sum_r |x_r| (bit exact on the
     dyadic synth inputs, where every fp32 partial sum is exact);
   * 8-bit Adam: codes within +-1, params |dp| <= 1e-5 (|p_ref| + lr), absmax
-    relative 1e-6, bf16 shard = RNE(GPU master) exactly and within 1 bf16 ulp
-    of the oracle's.
+    relative 1e-6, bf16 shard = RNE(GPU master) exactly and, by value, within
+    the param tolerance plus one bf16 ulp of the oracle's.
 """
 import numpy as np
 import pytest
@@ -168,8 +168,12 @@ def _check_adam(o, rank, blocks, gpu, ref, ins, eb, lr):
         b = bf16_bits(shard)
         rne = OD.to_bf16_rne(gm)
         assert np.array_equal(b[mask], rne[mask])
-        diff = np.abs(b[mask].astype(np.int32) - ref[5][mask].astype(np.int32))
-        assert diff.max(initial=0) <= 1
+        # by value: the fp32 param tolerance plus one bf16 ulp (bit patterns
+        # of near-zero params, |p| << lr, are not comparable)
+        bv = OD.bf16_to_f32(b[mask]).astype(np.float64)
+        rv = OD.bf16_to_f32(ref[5][mask]).astype(np.float64)
+        r0 = np.abs(ref[0][mask]).astype(np.float64)
+        assert np.all(np.abs(bv - rv) <= 1e-5 * (r0 + lr) + 2.0 ** -8 * r0)
         assert not b[~mask].any()
     else:
         assert np.array_equal(f32(shard)[mask], gm[mask])
