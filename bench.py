@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: max(3, steps // 10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
+                    help="p2p: fused single-kernel collectives over NVLink peer memory "
+                         "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
     return ap.parse_args()
 
 
@@ -225,7 +228,10 @@ class Timers:
         return {k: len(v) for k, v in self.pairs.items()}
 
 
-def step(R, db, cfg, t, stream, timers=None):
+def step(R, db, cfg, t, stream, timers=None, p2p=None):
+    """One step.  p2p=None: NCCL AllGather, cast kernel + NCCL fp32
+    ReduceScatter.  p2p given: the fused single-kernel collectives over NVLink
+    peer memory; the cast is inside the ReduceScatter kernel."""
     import torch
     units = db.units
 
@@ -240,11 +246,17 @@ def step(R, db, cfg, t, stream, timers=None):
         b.record(stream)
         timers.add(kind, a, b)
 
-    for u in units:
-        timed("ag", lambda u=u: R.all_gather(u, stream))
-    for u in reversed(units):
-        timed("cast", lambda u=u: R.unit_cast_scale(u, stream))
-        timed("rs", lambda u=u: R.unit_reduce_scatter_f32(u, stream))
+    if p2p is None:
+        for u in units:
+            timed("ag", lambda u=u: R.all_gather(u, stream))
+        for u in reversed(units):
+            timed("cast", lambda u=u: R.unit_cast_scale(u, stream))
+            timed("rs", lambda u=u: R.unit_reduce_scatter_f32(u, stream))
+    else:
+        for u in units:
+            timed("ag", lambda u=u: R.all_gather_p2p(u, p2p, stream))
+        for u in reversed(units):
+            timed("rs", lambda u=u: R.reduce_scatter_p2p(u, p2p, stream))
     timed("adam", lambda: db.step_8bit_adam(cfg, t, stream))
 
 
@@ -382,6 +394,9 @@ def run_ours(args):
     comm = R.init_comm(rank, world, local)
     units = build_units(args.layers)
     lays, db, arenas, views, plan_ms, sizes = setup(rank, world, local, units, comm)
+    p2p = None
+    if args.collectives == "p2p":
+        p2p = R.P2P(comm, [arenas[0], arenas[1]])  # PARAM_FULL, GRAD_FULL arenas
     ab = algorithmic_bytes(lays, rank)
     per_rank_bytes = ab["ag"] + ab["rs"] + ab["cast"] + ab["adam"]
     job_bytes = sum_over_ranks(per_rank_bytes, world)
@@ -390,7 +405,7 @@ def run_ours(args):
     t = 1
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            step(R, db, cfg, t, stream)
+            step(R, db, cfg, t, stream, p2p=p2p)
             t += 1
     stream.synchronize()
     # ---------------- timed region: inputs resident in HBM
@@ -403,7 +418,7 @@ def run_ours(args):
     ev0.record(stream)
     with torch.cuda.stream(stream):
         for _ in range(args.steps):
-            step(R, db, cfg, t, stream, timers)
+            step(R, db, cfg, t, stream, timers, p2p=p2p)
             t += 1
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -420,21 +435,30 @@ def run_ours(args):
     ag_ms, rs_ms = tot["ag"] / K, tot["rs"] / K
     adam_gbs = ab["adam"] / (adam_ms * 1e-3) / 1e9
     cast_gbs = ab["cast"] / (cast_ms * 1e-3) / 1e9
-    ag_bus = ab["ag"] / (ag_ms * 1e-3) / 1e9 if world > 1 else None
-    rs_bus = ab["rs"] / (rs_ms * 1e-3) / 1e9 if world > 1 else None
+    # physical bytes crossing NVLink into each rank per step: AG (m-1) S 2;
+    # RS (m-1) S 4 on the NCCL fp32 path, (m-1) S 2 on the fused p2p path
+    wire_ag = ab["ag"]
+    wire_rs = ab["rs"] if p2p is None else ab["rs"] // 2
+    ag_bus = wire_ag / (ag_ms * 1e-3) / 1e9 if world > 1 else None
+    rs_bus = wire_rs / (rs_ms * 1e-3) / 1e9 if world > 1 else None
     hbm_peak, peak_src = load_peaks()
     # dominant kernel of the step (largest share of device time)
+    names = ({"ag": "nccl_all_gather", "rs": "nccl_reduce_scatter"} if p2p is None else
+             {"ag": "ag_p2p_kernel", "rs": "rs_p2p_kernel"})
     shares = {"adam8_kernel": tot["adam"], "cast_scale_kernel": tot["cast"],
-              "nccl_reduce_scatter": tot["rs"], "nccl_all_gather": tot["ag"]}
+              names["rs"]: tot["rs"], names["ag"]: tot["ag"]}
     dom = max(shares, key=shares.get)
-    if dom in ("adam8_kernel", "cast_scale_kernel"):
+    if dom in ("adam8_kernel", "cast_scale_kernel") or world == 1:
+        if dom not in ("adam8_kernel", "cast_scale_kernel"):
+            dom = "adam8_kernel"
         ach = adam_gbs if dom == "adam8_kernel" else cast_gbs
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "traffic": profile_traffic(dom), "peak_source": peak_src}
     else:
-        ach = rs_bus if dom == "nccl_reduce_scatter" else ag_bus
+        ach = rs_bus if dom == names["rs"] else ag_bus
         roof = {"kernel": dom, "bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "traffic": None,
+                "bytes": "physical wire bytes into each rank per launch",
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
     roof["share_of_step"] = shares[dom] / max(1e-9, ms_local)
     value = job_bytes / (ms / K * 1e-3) / 1e9
@@ -442,7 +466,7 @@ def run_ours(args):
     # ---------------- e2e: host buffers through the C-ABI, copies inside
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes)
+        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p)
     # ---------------- CPU baseline (oracle) on rank 0
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -459,29 +483,34 @@ def run_ours(args):
                                    "Adam blocks, warm synthetic states",
                        "units": len(lays), "params": E, "qblock": QBLOCK,
                        "parallelism": f"fsdp{world}",
+                       "collectives": args.collectives,
                        "l2": f"no flush: per-step working set {sum(sizes) / 2 ** 30:.1f} GiB "
                              f"per rank >> L2 ({L2_BYTES >> 20} MiB)",
                        "plan_ms": plan_ms},
             "per_op": {"adam_hbm_gbs": adam_gbs, "adam_ms_per_launch": adam_ms,
                        "cast_hbm_gbs": cast_gbs, "cast_ms_per_step": cast_ms,
-                       "ag_busbw_gbs": ag_bus, "rs_busbw_gbs": rs_bus,
+                       "ag_wire_gbs": ag_bus, "rs_wire_gbs": rs_bus,
+                       "ag_wire_bytes_per_rank": wire_ag, "rs_wire_bytes_per_rank": wire_rs,
                        "ag_ms_per_step": ag_ms, "rs_ms_per_step": rs_ms,
                        "bytes_per_rank": ab},
             "roofline": roof,
             "clocks": clk,
-            "gpu_launches": (cnt["cast"] + cnt["adam"]),
-            "nccl_calls": cnt["ag"] + cnt["rs"],
+            "gpu_launches": (cnt["cast"] + cnt["adam"] + (0 if p2p is None else cnt["ag"] + cnt["rs"])),
+            "nccl_calls": 0 if p2p is not None else cnt["ag"] + cnt["rs"],
             "cpu_baseline": cpu,
             "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
+    if p2p is not None:
+        torch.cuda.synchronize()
+        p2p.close()
     db.close()
     comm.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes):
+def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p=None):
     """Same step, through the public C-ABI calls, with the step's inputs (this
     rank's bf16 gradient buffers) copied host->device from pinned memory and
     the step's result (the updated bf16 parameter shards) copied back, every
@@ -492,16 +521,22 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes):
     for v, lay in zip(views, lays):
         host_g.append(v["grad_full"].cpu().pin_memory())
         host_p.append(torch.empty(lay.S, dtype=torch.bfloat16).pin_memory())
-    h2d = sum(h.numel() * 2 for h in host_g)
-    d2h = sum(h.numel() * 2 for h in host_p)
+    h2d = sum_over_ranks(sum(h.numel() * 2 for h in host_g), world)  # whole job
+    d2h = sum_over_ranks(sum(h.numel() * 2 for h in host_p), world)
 
     def e2e_step(tt):
         for v, h in zip(views, host_g):
             v["grad_full"].copy_(h, non_blocking=True)
         for u in db.units:
-            R.all_gather(u, stream)
+            if p2p is None:
+                R.all_gather(u, stream)
+            else:
+                R.all_gather_p2p(u, p2p, stream)
         for u in reversed(db.units):
-            R.reduce_scatter(u, stream)
+            if p2p is None:
+                R.reduce_scatter(u, stream)
+            else:
+                R.reduce_scatter_p2p(u, p2p, stream)
         db.step_8bit_adam(cfg, tt, stream)
         for v, h, lay in zip(views, host_p, lays):
             h.copy_(v["param_full"][rank * lay.S:(rank + 1) * lay.S], non_blocking=True)

@@ -210,6 +210,45 @@ rsdb_status rsdb_step_8bit_adam(rsdb_unit*, const rsdb_adam_state*, const rsdb_a
                                 int64_t step, void* stream);
 
 /* ======================================================================== */
+/* Fused collectives over NVLink peer memory.              */
+/* Each rank maps the other ranks' buffers (CUDA IPC over NVLink 5 /         */
+/* NVSwitch) and the collective runs inside ONE sm_100a kernel per call:     */
+/*  - rsdb_reduce_scatter_p2p: a6+a7 fused -- rank k reads G_r[kS:(k+1)S]    */
+/*    (bf16) from every rank r, sums fp32(G_r)*fl(1/m) in rank order 0..m-1  */
+/*    in fp32 (bit-identical to the oracle), zeroes padding, writes          */
+/*    grad_f32 + k*S.  Wire bytes (m-1)*S*2 per rank (half of fp32 RS).      */
+/*  - rsdb_all_gather_p2p: a4 -- rank k copies every peer's shard into its   */
+/*    own param_full (same offsets).                                         */
+/* Ordering: a start barrier (every rank has issued the call, so all prior  */
+/* stream work -- grads / optimizer writes -- is complete) and a done        */
+/* barrier (every rank finished reading its peers) through a signal buffer;  */
+/* the kernel returns only after the done barrier, so later stream work may  */
+/* overwrite the buffers.  All ranks must issue the same p2p calls in the    */
+/* same order (SPMD).  World <= 8 (one NVLink domain).                       */
+/* ======================================================================== */
+#define RSDB_IPC_BYTES 72          /* cudaIpcMemHandle_t (64) + offset (8)   */
+#define RSDB_P2P_SIGNAL_BYTES 4096 /* signal buffer size per rank            */
+typedef struct rsdb_p2p rsdb_p2p;
+/* IPC handle + offset of the device allocation containing dev_ptr. */
+rsdb_status rsdb_ipc_handle(const void* dev_ptr, uint8_t out[RSDB_IPC_BYTES]);
+/* Maps n_bufs buffers of every rank.  local_bufs[0] MUST be a zero-filled
+ * device buffer of >= RSDB_P2P_SIGNAL_BYTES (the signal buffer, caller
+ * owned); local_bufs[i] / sizes[i] are this rank's buffers (e.g. the
+ * GRAD_FULL and PARAM_FULL arenas); all_handles holds world * n_bufs
+ * handles from rsdb_ipc_handle, rank-major (the caller all-gathers them,
+ * e.g. with torch.distributed.all_gather_object).  EINVAL on bad sizes,
+ * ECUDA if a handle cannot be opened (no P2P path). */
+rsdb_status rsdb_p2p_create(rsdb_comm* comm, int32_t n_bufs, void* const* local_bufs,
+                            const int64_t* sizes, const uint8_t* all_handles, rsdb_p2p** out);
+void rsdb_p2p_free(rsdb_p2p*);
+/* The unit's grad_full (bf16 units) / param_full must lie inside one of the
+ * registered buffers at the same offset on every rank (true for DBuffer
+ * arenas: offsets are rank-independent for PARAM_FULL / GRAD_FULL).
+ * EMISMATCH otherwise. */
+rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
+rsdb_status rsdb_all_gather_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
+
+/* ======================================================================== */
 /* DBuffer batched allocation: one allocation per    */
 /* buffer kind for all units, persistent offsets, one optimizer launch.      */
 /* ======================================================================== */

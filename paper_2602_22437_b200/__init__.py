@@ -279,6 +279,65 @@ def step_8bit_adam(unit: Unit, master, m_q, v_q, m_absmax, v_absmax, cfg: AdamCo
     check(lib.rsdb_step_8bit_adam(unit.handle, C.byref(st), C.byref(cfg), step, _stream(stream)))
 
 
+# ---------------------------------------------------------------- N1: NVLink peer memory
+def ipc_handle(t) -> bytes:
+    buf = C.create_string_buffer(_c.RSDB_IPC_BYTES)
+    check(lib.rsdb_ipc_handle(_ptr(t), buf))
+    return buf.raw
+
+
+class P2P:
+    """Every rank's `bufs` (torch tensors, e.g. the GRAD_FULL and PARAM_FULL
+    arenas) mapped into this process over NVLink (CUDA IPC), plus a signal
+    buffer, for the fused p2p collectives.  The IPC handles are exchanged with
+    torch.distributed.all_gather_object (plumbing).  Keeps the tensors alive."""
+
+    def __init__(self, comm: Comm, bufs: Sequence, group=None):
+        import torch
+        import torch.distributed as dist
+        dev = bufs[0].device
+        self.signal = torch.zeros(_c.RSDB_P2P_SIGNAL_BYTES, dtype=torch.uint8, device=dev)
+        self.bufs = [self.signal] + list(bufs)
+        mine = b"".join(ipc_handle(t) for t in self.bufs)
+        allh = [None] * comm.world
+        if comm.world > 1:
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        n = len(self.bufs)
+        ptrs = (C.c_void_p * n)(*[t.data_ptr() for t in self.bufs])
+        sizes = (C.c_int64 * n)(*[t.numel() * t.element_size() for t in self.bufs])
+        h = C.c_void_p()
+        check(lib.rsdb_p2p_create(comm.handle, n, ptrs, sizes, b"".join(allh), C.byref(h)))
+        self._h = h
+        self.comm = comm
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.rsdb_p2p_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def reduce_scatter_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
+    """a6 + a7 fused in one kernel over NVLink peer memory (bf16 on the wire)."""
+    check(lib.rsdb_reduce_scatter_p2p(unit.handle, p2p.handle, _stream(stream)))
+
+
+def all_gather_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
+    """a4 as one kernel pulling every peer's shard over NVLink."""
+    check(lib.rsdb_all_gather_p2p(unit.handle, p2p.handle, _stream(stream)))
+
+
 # ---------------------------------------------------------------- DBuffer
 KINDS = ("param_full", "grad_full", "grad_f32", "master", "m_q", "v_q", "m_absmax", "v_absmax")
 

@@ -18,6 +18,8 @@ RSDB_GRAN_FLAT, RSDB_GRAN_ROWS, RSDB_GRAN_WHOLE, RSDB_GRAN_ELEM = range(4)
 (RSDB_KIND_PARAM_FULL, RSDB_KIND_GRAD_FULL, RSDB_KIND_GRAD_F32, RSDB_KIND_MASTER,
  RSDB_KIND_MQ, RSDB_KIND_VQ, RSDB_KIND_MABS, RSDB_KIND_VABS) = range(8)
 RSDB_NKINDS = 8
+RSDB_IPC_BYTES = 72
+RSDB_P2P_SIGNAL_BYTES = 4096
 
 i32, i64, vp = C.c_int32, C.c_int64, C.c_void_p
 P_i64, P_i32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
@@ -74,6 +76,11 @@ _SIGS = {
     "rsdb_reduce_scatter": (i32, [vp, vp]),
     "rsdb_unit_reduce_scatter_f32": (i32, [vp, vp]),
     "rsdb_step_8bit_adam": (i32, [vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64, vp]),
+    "rsdb_ipc_handle": (i32, [vp, C.c_char_p]),
+    "rsdb_p2p_create": (i32, [vp, i32, C.POINTER(vp), P_i64, C.c_char_p, C.POINTER(vp)]),
+    "rsdb_p2p_free": (None, [vp]),
+    "rsdb_reduce_scatter_p2p": (i32, [vp, vp, vp]),
+    "rsdb_all_gather_p2p": (i32, [vp, vp, vp]),
     "rsdb_arena_sizes": (i32, [C.POINTER(vp), i32, i32, i64, i64, P_i64, P_i64]),
     "rsdb_dbuffer_create": (i32, [C.POINTER(vp), i32, vp, i32, i64, i64, C.POINTER(vp),
                                   C.POINTER(vp)]),

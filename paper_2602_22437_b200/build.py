@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "librsdb.so")
-SOURCES = ["planner.cc", "capi.cc", "kernels.cu"]
+SOURCES = ["planner.cc", "capi.cc", "kernels.cu", "p2p.cu"]
 HEADERS = ["planner.hpp", "kernels.cuh"]
 
 

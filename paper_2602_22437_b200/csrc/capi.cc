@@ -92,6 +92,16 @@ struct rsdb_dbuffer {
   std::vector<int64_t> grad_bytes;  // per unit, for grouped zero
 };
 
+struct rsdb_p2p {
+  rsdb_comm* comm = nullptr;
+  int32_t n = 0;
+  std::vector<char*> local;          // [n]
+  std::vector<int64_t> size;         // [n]
+  std::vector<std::vector<char*>> peer;  // [n][world], own rank = local
+  std::vector<void*> opened;         // IPC mappings to close
+  uint64_t epoch = 0;
+};
+
 struct rsdb_copy_plan {
   DevTable segs;
   int64_t nseg = 0, total_chunks = 0;
@@ -415,6 +425,160 @@ rsdb_status rsdb_step_8bit_adam(rsdb_unit* u, const rsdb_adam_state* st, const r
                    u->bufs.param_full,                   u->L.elem_bytes == 2};
   CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
                               int32_t(std::min<int64_t>(u->qblock, 1 << 30)), S_(stream)));
+  return OK_CLEAR();
+}
+
+// ---------------------------------------------------------------------------
+// fused collectives over NVLink peer memory (N1)
+// ---------------------------------------------------------------------------
+typedef int (*cuMemGetAddressRange_t)(unsigned long long* base, size_t* size, unsigned long long ptr);
+
+static rsdb_status alloc_base(const void* p, char** base, int64_t* size) {
+  static cuMemGetAddressRange_t fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) return fail(RSDB_ECUDA, "cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<cuMemGetAddressRange_t>(f);
+  }
+  unsigned long long b = 0;
+  size_t s = 0;
+  if (fn(&b, &s, reinterpret_cast<unsigned long long>(p)) != 0)
+    return fail(RSDB_EINVAL, "pointer %p is not a device allocation", p);
+  *base = reinterpret_cast<char*>(b);
+  *size = int64_t(s);
+  return RSDB_OK;
+}
+
+rsdb_status rsdb_ipc_handle(const void* dev_ptr, uint8_t out[RSDB_IPC_BYTES]) {
+  if (!dev_ptr || !out) return fail(RSDB_EINVAL, "null argument");
+  if (rsdb_status st = require_device()) return st;
+  char* base = nullptr;
+  int64_t sz = 0;
+  if (rsdb_status st = alloc_base(dev_ptr, &base, &sz)) return st;
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, base));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  const int64_t off = static_cast<const char*>(dev_ptr) - base;
+  std::memcpy(out, &h, 64);
+  std::memcpy(out + 64, &off, 8);
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_p2p_create(rsdb_comm* comm, int32_t n_bufs, void* const* local_bufs,
+                            const int64_t* sizes, const uint8_t* all_handles, rsdb_p2p** out) {
+  if (!comm || n_bufs < 1 || !local_bufs || !sizes || !all_handles || !out)
+    return fail(RSDB_EINVAL, "rsdb_p2p_create: null argument or n_bufs < 1");
+  if (comm->world > rsdb::P2P_MAX_RANKS)
+    return fail(RSDB_EINVAL, "p2p collectives support world <= %d", rsdb::P2P_MAX_RANKS);
+  if (sizes[0] < RSDB_P2P_SIGNAL_BYTES) return fail(RSDB_EINVAL, "signal buffer too small");
+  auto p = std::make_unique<rsdb_p2p>();
+  p->comm = comm;
+  p->n = n_bufs;
+  p->peer.assign(size_t(n_bufs), std::vector<char*>(size_t(comm->world), nullptr));
+  for (int32_t i = 0; i < n_bufs; ++i) {
+    if (!local_bufs[i] || sizes[i] < 0) return fail(RSDB_EINVAL, "buffer %d invalid", i);
+    p->local.push_back(static_cast<char*>(local_bufs[i]));
+    p->size.push_back(sizes[i]);
+  }
+  CUDA_TRY(cudaSetDevice(comm->device));
+  auto cleanup = [&]() {
+    for (void* q : p->opened) cudaIpcCloseMemHandle(q);
+    p->opened.clear();
+  };
+  for (int32_t r = 0; r < comm->world; ++r) {
+    for (int32_t i = 0; i < n_bufs; ++i) {
+      if (r == comm->rank) {
+        p->peer[size_t(i)][size_t(r)] = p->local[size_t(i)];
+        continue;
+      }
+      const uint8_t* h = all_handles + (int64_t(r) * n_bufs + i) * RSDB_IPC_BYTES;
+      cudaIpcMemHandle_t mh;
+      int64_t off;
+      std::memcpy(&mh, h, 64);
+      std::memcpy(&off, h + 64, 8);
+      void* base = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        cleanup();
+        return fail(RSDB_ECUDA, "cudaIpcOpenMemHandle(rank %d, buffer %d): %s", r, i,
+                    cudaGetErrorString(e));
+      }
+      p->opened.push_back(base);
+      p->peer[size_t(i)][size_t(r)] = static_cast<char*>(base) + off;
+    }
+  }
+  *out = p.release();
+  return OK_CLEAR();
+}
+
+void rsdb_p2p_free(rsdb_p2p* p) {
+  if (!p) return;
+  for (void* q : p->opened) cudaIpcCloseMemHandle(q);
+  delete p;
+}
+
+// locate `ptr` (with `bytes` behind it) inside a registered buffer i (>= 1)
+static rsdb_status p2p_find(const rsdb_p2p* p, const void* ptr, int64_t bytes, int32_t* idx,
+                            int64_t* off) {
+  const char* c = static_cast<const char*>(ptr);
+  for (int32_t i = 1; i < p->n; ++i) {
+    const char* b = p->local[size_t(i)];
+    if (c >= b && c + bytes <= b + p->size[size_t(i)]) {
+      *idx = i;
+      *off = c - b;
+      return RSDB_OK;
+    }
+  }
+  return fail(RSDB_EMISMATCH, "unit buffer is not inside a registered p2p buffer");
+}
+
+static rsdb_status p2p_common(rsdb_unit* u, rsdb_p2p* p, rsdb::P2PSignals* sg) {
+  if (!u || !p) return fail(RSDB_EINVAL, "null argument");
+  if (!u->comm || u->comm != p->comm) return fail(RSDB_EMISMATCH, "unit and p2p use different comms");
+  const int m = u->L.m;
+  if ((u->L.S * u->L.elem_bytes) % 16 != 0)
+    return fail(RSDB_EMISMATCH, "p2p collectives need 16-byte aligned shards (S*elem %% 16 == 0; "
+                                "planner layouts always are, P:199)");
+  sg->local = reinterpret_cast<uint64_t*>(p->local[0]);
+  for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
+    sg->peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+  return RSDB_OK;
+}
+
+rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
+  rsdb::P2PSignals sg;
+  if (rsdb_status st = p2p_common(u, p, &sg)) return st;
+  if (u->L.elem_bytes != 2) return fail(RSDB_EMISMATCH, "p2p ReduceScatter needs a bf16 unit");
+  if (u->L.S == 0) return OK_CLEAR();
+  const int m = u->L.m;
+  int32_t bi = 0;
+  int64_t off = 0;
+  if (rsdb_status st = p2p_find(p, u->bufs.grad_full, int64_t(m) * u->L.S * 2, &bi, &off)) return st;
+  rsdb::P2PPtrs g{};
+  for (int r = 0; r < m; ++r) g.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+  const float scale = float(1.0 / double(m));
+  ++p->epoch;
+  CUDA_TRY(rsdb::launch_rs_p2p(g, static_cast<float*>(u->bufs.grad_f32) + int64_t(u->rank) * u->L.S,
+                               u->L.S, u->rank, m, scale, static_cast<const int64_t*>(u->pad.p),
+                               int32_t(u->npad), sg, p->epoch, S_(stream)));
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
+  rsdb::P2PSignals sg;
+  if (rsdb_status st = p2p_common(u, p, &sg)) return st;
+  if (u->L.S == 0) return OK_CLEAR();
+  const int m = u->L.m;
+  const int64_t bytes_S = u->L.S * u->L.elem_bytes;
+  int32_t bi = 0;
+  int64_t off = 0;
+  if (rsdb_status st = p2p_find(p, u->bufs.param_full, int64_t(m) * bytes_S, &bi, &off)) return st;
+  rsdb::P2PPtrs q{};
+  for (int r = 0; r < m; ++r) q.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+  ++p->epoch;
+  CUDA_TRY(rsdb::launch_ag_p2p(q, bytes_S, u->rank, m, sg, p->epoch, S_(stream)));
   return OK_CLEAR();
 }
 

@@ -11,6 +11,9 @@
 // on a persistent grid of (resident CTAs per SM) x (148 SMs).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "kernels.cuh"
 
 namespace rsdb {
@@ -47,6 +50,11 @@ __device__ __forceinline__ uint2 ld_na_v2(const void* p) {
                : "l"(p));
   return r;
 }
+__device__ __forceinline__ uint32_t ld_na_u32(const void* p) {
+  uint32_t r;
+  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
@@ -69,9 +77,16 @@ __device__ __forceinline__ float s8_to_f(uint32_t byte) {  // two's complement b
 __device__ __forceinline__ int rne_int(float x) {
   return __float_as_int(__fadd_rn(x, 12582912.0f)) - 0x4B400000;
 }
+// .ftz approximations: v = 0 or denormal gives sqrt = 0 (the denominator is
+// then eps = 1e-8 either way); denom >= eps is never denormal.
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -98,7 +113,7 @@ static int resident_blocks(K kernel, int threads, size_t smem) {
 // a6: fused cast + scale + padding zero
 // ----------------------------------------------------------------------------
 constexpr int CAST_THREADS = 256;
-constexpr int CAST_UNROLL = 4;
+constexpr int CAST_UNROLL = 8;
 constexpr int CAST_SMEM_PAD = 256;  // padding intervals cached in shared memory
 
 // first interval j with hi_j > x (pad = lo0, hi0, lo1, hi1, ... ascending)
@@ -132,48 +147,51 @@ __global__ void __launch_bounds__(CAST_THREADS) cast_scale_kernel(const void* __
     __syncthreads();
     pad = spad;
   }
-  constexpr int V = SRC_BF16 ? 8 : 4;  // elements per 16-byte source vector
+  // Each thread moves 4 elements per vector: an 8-byte (bf16) or 16-byte
+  // (f32) load and ONE 16-byte store, so every warp instruction covers a
+  // contiguous span (no half-sector strided stores).
+  constexpr int V = 4;
   const int64_t nvec = n / V;
   const int64_t stride = int64_t(gridDim.x) * CAST_THREADS * CAST_UNROLL;
   for (int64_t base = int64_t(blockIdx.x) * CAST_THREADS * CAST_UNROLL + threadIdx.x; base < nvec;
        base += stride) {
-    int4 raw[CAST_UNROLL];
+    float f[CAST_UNROLL][V];
 #pragma unroll
     for (int u = 0; u < CAST_UNROLL; ++u) {
       const int64_t c = base + u * CAST_THREADS;
-      if (c < nvec) raw[u] = ld_nc_v4(static_cast<const int4*>(src) + c);
+      if (c < nvec) {
+        if constexpr (SRC_BF16) {
+          const uint2 w = ld_nc_v2(static_cast<const uint2*>(src) + c);
+          f[u][0] = bf16lo(w.x);
+          f[u][1] = bf16hi(w.x);
+          f[u][2] = bf16lo(w.y);
+          f[u][3] = bf16hi(w.y);
+        } else {
+          const int4 w = ld_nc_v4(static_cast<const int4*>(src) + c);
+          f[u][0] = __int_as_float(w.x);
+          f[u][1] = __int_as_float(w.y);
+          f[u][2] = __int_as_float(w.z);
+          f[u][3] = __int_as_float(w.w);
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < CAST_UNROLL; ++u) {
       const int64_t c = base + u * CAST_THREADS;
       if (c >= nvec) break;
-      float f[V];
-      if constexpr (SRC_BF16) {
-        const uint32_t w[4] = {uint32_t(raw[u].x), uint32_t(raw[u].y), uint32_t(raw[u].z),
-                               uint32_t(raw[u].w)};
+      float x[V];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          f[2 * k] = bf16lo(w[k]) * scale;
-          f[2 * k + 1] = bf16hi(w[k]) * scale;
-        }
-      } else {
-        f[0] = __int_as_float(raw[u].x) * scale;
-        f[1] = __int_as_float(raw[u].y) * scale;
-        f[2] = __int_as_float(raw[u].z) * scale;
-        f[3] = __int_as_float(raw[u].w) * scale;
-      }
+      for (int k = 0; k < V; ++k) x[k] = f[u][k] * scale;
       const int64_t e0 = c * V;
       if (npad > 0) {
         const int j = first_pad_after(pad, npad, e0);
         if (j < npad && pad[2 * j] < e0 + V) {
 #pragma unroll
           for (int k = 0; k < V; ++k)
-            if (in_pad_from(pad, npad, j, e0 + k)) f[k] = 0.f;
+            if (in_pad_from(pad, npad, j, e0 + k)) x[k] = 0.f;
         }
       }
-      float4* d = reinterpret_cast<float4*>(dst + e0);
-#pragma unroll
-      for (int k = 0; k < V / 4; ++k) d[k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+      *reinterpret_cast<float4*>(dst + e0) = make_float4(x[0], x[1], x[2], x[3]);
     }
   }
   // scalar tail (n % V elements) by block 0
@@ -206,8 +224,7 @@ cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t
   if (n <= 0) return cudaSuccess;
   const bool aligned = (reinterpret_cast<uintptr_t>(src) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
-  const int V = src_bf16 ? 8 : 4;
-  const int64_t nvec = n / V;
+  const int64_t nvec = n / 4;
   if (!aligned) {
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 16);
     if (src_bf16)
@@ -231,27 +248,53 @@ cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t
 
 // ----------------------------------------------------------------------------
 // a8: block-wise 8-bit Adam
+//
+// One CTA of NT threads per 2048-element quantization block; thread t owns
+// Q = 512/NT quads [4t + 4*NT*k, +4), k < Q, so every warp-wide access is one
+// contiguous span.  Two kernels share the per-block body:
+//   adam8_kernel      loads straight from global memory (16-B vectors);
+//   adam8_tma_kernel  persistent CTAs with a ring of shared-memory stages
+//                     filled by 1-D bulk TMA (cp.async.bulk, mbarrier
+//                     complete_tx): the next blocks stream in while the
+//                     current one is reduced, quantized and stored.
+// Blocks that are not full (tails) or not 16-B aligned take a masked
+// element path; blocks longer than 2048 take a two-pass path.
+//
+// Instruction diet (the kernel is HBM-bound only if it issues < ~30
+// instructions per element): codes are widened with one PRMT per byte into
+// the float 2^23 + code (exact; then FADD/FMUL = the oracle's q * fl(A/127)),
+// requantised with the magic-add RNE whose float bits carry the code in
+// their low byte (3 PRMT per 4 codes), and no clamp is needed because
+// |m| <= A  =>  |m * fl(127/A)| < 127.5 (and 0 <= v * fl(255/A) < 255.5).
 // ----------------------------------------------------------------------------
-constexpr int ADAM_THREADS = 256;
-constexpr int ADAM_EPT = 8;                            // elements per thread
-constexpr int ADAM_TILE = ADAM_THREADS * ADAM_EPT;     // 2048: single-pass block size
-constexpr int ADAM_WARPS = ADAM_THREADS / 32;
+constexpr int ADAM_TILE = 2048;  // single-pass block size
 
 struct ElemOut {
   float p, m, v;
 };
 
-// Steps 1-6 of the update for one element (O4); FMA-contracted where noted.
+template <int NT>
+struct AdamGeom {
+  static constexpr int Q = ADAM_TILE / (4 * NT);  // quads per thread
+  static constexpr int EPT = 4 * Q;               // elements per thread
+  static constexpr int WARPS = NT / 32;
+  // element index (inside the block) of this thread's e-th element
+  __device__ static __forceinline__ int idx(int e) { return 4 * int(threadIdx.x) + (e >> 2) * 4 * NT + (e & 3); }
+  __device__ static __forceinline__ int quad(int k) { return 4 * int(threadIdx.x) + 4 * NT * k; }
+};
+
+// Steps 1-6 of the update for one element (O4); FMA-contracted.
 __device__ __forceinline__ ElemOut adam_elem(float p, float g, float mt, float vt,
                                              const AdamScalars& s) {
   ElemOut o;
   o.m = fmaf(s.w1, g - mt, mt);                    // mt + (1-b1)(g - mt)     (lerp)
   o.v = fmaf(s.b2, vt, s.w2 * (g * g));            // b2 vt + (1-b2) g^2
   const float denom = fmaf(sqrt_approx(o.v), s.inv_bc2s, s.eps);  // sqrt(v)/bc2s + eps
-  o.p = fmaf(-s.step_size, __fdividef(o.m, denom), p * s.c_wd);   // p*c_wd - ss*m/denom
+  o.p = fmaf(-s.step_size, o.m * rcp_approx(denom), p * s.c_wd);  // p*c_wd - ss*m/denom
   return o;
 }
 
+template <int WARPS>
 __device__ __forceinline__ void block_max2(float& a, float& b, float* sa, float* sb) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -267,186 +310,429 @@ __device__ __forceinline__ void block_max2(float& a, float& b, float* sa, float*
   a = sa[0];
   b = sb[0];
 #pragma unroll
-  for (int i = 1; i < ADAM_WARPS; ++i) {
+  for (int i = 1; i < WARPS; ++i) {
     a = fmaxf(a, sa[i]);
     b = fmaxf(b, sb[i]);
   }
 }
 
-__device__ __forceinline__ uint32_t qm_code(float m, float inv) {  // -> byte of int8
-  int q = rne_int(m * inv);
-  q = max(-127, min(127, q));
-  return uint32_t(q) & 0xffu;
+// byte k of w as the float 2^23 + byte (exact)
+__device__ __forceinline__ float byte_f(uint32_t w, int k) {
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + k));
 }
-__device__ __forceinline__ uint32_t qv_code(float v, float inv) {
-  int q = rne_int(v * inv);
-  q = max(0, min(255, q));
-  return uint32_t(q);
+// 4 dequantized moments from a word of codes: m signed (bias 128), v unsigned
+__device__ __forceinline__ void dq4_m(uint32_t w, float sm, float* out) {
+  w ^= 0x80808080u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = (byte_f(w, k) - 8388736.0f) * sm;  // (code) * fl(A/127)
 }
+__device__ __forceinline__ void dq4_v(uint32_t w, float sv, float* out) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = (byte_f(w, k) - 8388608.0f) * sv;  // (code) * fl(A/255)
+}
+// RNE code in the low byte of the float bits of x + 1.5*2^23 (|x| < 2^22)
+__device__ __forceinline__ uint32_t rne_bits(float x) {
+  return __float_as_uint(__fadd_rn(x, 12582912.0f));
+}
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040u), __byte_perm(c, d, 0x0040u), 0x5410u);
+}
+// scalar code (masked path), with the same rounding
+__device__ __forceinline__ uint8_t code1(float x) { return uint8_t(rne_bits(x) & 0xffu); }
 
-template <bool PARAM_BF16>
-__global__ void __launch_bounds__(ADAM_THREADS) adam8_kernel(const AdamBlock* __restrict__ tbl,
-                                                             int64_t nblocks, AdamPtrs P,
-                                                             AdamScalars s) {
-  __shared__ float red_m[ADAM_WARPS], red_v[ADAM_WARPS];
-  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
-    const AdamBlock blk = tbl[b];
-    const int64_t slot = blk.slot;
-    const float sm = P.mabs[slot] / 127.0f;  // dequantization scales (IEEE div)
-    const float sv = P.vabs[slot] / 255.0f;
-    float* __restrict__ master = P.master + blk.state_off;
-    int8_t* __restrict__ mq = P.mq + blk.state_off;
-    uint8_t* __restrict__ vq = P.vq + blk.state_off;
-    const float* __restrict__ grad = P.grad + blk.grad_off;
-    const int len = blk.len;
+template <int NT>
+struct BlockRegs {
+  float p[AdamGeom<NT>::EPT], g[AdamGeom<NT>::EPT], mt[AdamGeom<NT>::EPT], vt[AdamGeom<NT>::EPT];
+};
 
-    if (len <= ADAM_TILE) {
-      // ---------------- single pass: the block lives in registers ----------
-      const int i0 = threadIdx.x * ADAM_EPT;
-      const bool vec = (i0 + ADAM_EPT <= len) && ((blk.state_off & 7) == 0) &&
-                       ((blk.grad_off & 3) == 0) && ((blk.param_off & 7) == 0);
-      float p[ADAM_EPT], g[ADAM_EPT], mt[ADAM_EPT], vt[ADAM_EPT];
-      if (vec) {
-        const int4 p0 = ld_na_v4(master + i0), p1 = ld_na_v4(master + i0 + 4);
-        const int4 g0 = ld_nc_v4(grad + i0), g1 = ld_nc_v4(grad + i0 + 4);
-        const uint2 cm = ld_na_v2(mq + i0), cv = ld_na_v2(vq + i0);
-        p[0] = __int_as_float(p0.x); p[1] = __int_as_float(p0.y);
-        p[2] = __int_as_float(p0.z); p[3] = __int_as_float(p0.w);
-        p[4] = __int_as_float(p1.x); p[5] = __int_as_float(p1.y);
-        p[6] = __int_as_float(p1.z); p[7] = __int_as_float(p1.w);
-        g[0] = __int_as_float(g0.x); g[1] = __int_as_float(g0.y);
-        g[2] = __int_as_float(g0.z); g[3] = __int_as_float(g0.w);
-        g[4] = __int_as_float(g1.x); g[5] = __int_as_float(g1.y);
-        g[6] = __int_as_float(g1.z); g[7] = __int_as_float(g1.w);
+// full, 16-B aligned block from 4 element arrays (global or shared)
+template <int NT, bool GLOBAL>
+__device__ __forceinline__ void load_fast(BlockRegs<NT>& r, const float* master, const float* grad,
+                                          const void* mq, const void* vq, float sm, float sv) {
+  using G = AdamGeom<NT>;
+  int4 pv[G::Q], gv[G::Q];
+  uint32_t cm[G::Q], cv[G::Q];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          mt[k] = s8_to_f((cm.x >> (8 * k)) & 0xffu) * sm;
-          mt[k + 4] = s8_to_f((cm.y >> (8 * k)) & 0xffu) * sm;
-          vt[k] = u8_to_f((cv.x >> (8 * k)) & 0xffu) * sv;
-          vt[k + 4] = u8_to_f((cv.y >> (8 * k)) & 0xffu) * sv;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < ADAM_EPT; ++k) {
-          const int i = i0 + k;
-          if (i < len) {
-            p[k] = master[i];
-            g[k] = grad[i];
-            mt[k] = s8_to_f(uint32_t(uint8_t(mq[i]))) * sm;
-            vt[k] = u8_to_f(uint32_t(vq[i])) * sv;
-          } else {
-            p[k] = g[k] = mt[k] = vt[k] = 0.f;
-          }
-        }
-      }
-      float m[ADAM_EPT], v[ADAM_EPT];
-      float am = 0.f, av = 0.f;
-#pragma unroll
-      for (int k = 0; k < ADAM_EPT; ++k) {
-        const ElemOut o = adam_elem(p[k], g[k], mt[k], vt[k], s);
-        const bool live = (i0 + k) < len;
-        p[k] = o.p;
-        m[k] = live ? o.m : 0.f;
-        v[k] = live ? o.v : 0.f;
-        am = fmaxf(am, fabsf(m[k]));
-        av = fmaxf(av, v[k]);
-      }
-      block_max2(am, av, red_m, red_v);
-      const float im = am > 0.f ? 127.0f / am : 0.f;
-      const float iv = av > 0.f ? 255.0f / av : 0.f;
-      if (vec) {
-        uint2 cm, cv;
-        cm.x = qm_code(m[0], im) | (qm_code(m[1], im) << 8) | (qm_code(m[2], im) << 16) |
-               (qm_code(m[3], im) << 24);
-        cm.y = qm_code(m[4], im) | (qm_code(m[5], im) << 8) | (qm_code(m[6], im) << 16) |
-               (qm_code(m[7], im) << 24);
-        cv.x = qv_code(v[0], iv) | (qv_code(v[1], iv) << 8) | (qv_code(v[2], iv) << 16) |
-               (qv_code(v[3], iv) << 24);
-        cv.y = qv_code(v[4], iv) | (qv_code(v[5], iv) << 8) | (qv_code(v[6], iv) << 16) |
-               (qv_code(v[7], iv) << 24);
-        reinterpret_cast<float4*>(master + i0)[0] = make_float4(p[0], p[1], p[2], p[3]);
-        reinterpret_cast<float4*>(master + i0)[1] = make_float4(p[4], p[5], p[6], p[7]);
-        *reinterpret_cast<uint2*>(mq + i0) = cm;
-        *reinterpret_cast<uint2*>(vq + i0) = cv;
-        if constexpr (PARAM_BF16) {
-          uint4 o;
-          o.x = pack_bf16x2(p[0], p[1]);
-          o.y = pack_bf16x2(p[2], p[3]);
-          o.z = pack_bf16x2(p[4], p[5]);
-          o.w = pack_bf16x2(p[6], p[7]);
-          *reinterpret_cast<uint4*>(static_cast<uint16_t*>(P.param) + blk.param_off + i0) = o;
-        } else {
-          float* pp = static_cast<float*>(P.param) + blk.param_off + i0;
-          reinterpret_cast<float4*>(pp)[0] = make_float4(p[0], p[1], p[2], p[3]);
-          reinterpret_cast<float4*>(pp)[1] = make_float4(p[4], p[5], p[6], p[7]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < ADAM_EPT; ++k) {
-          const int i = i0 + k;
-          if (i < len) {
-            master[i] = p[k];
-            mq[i] = int8_t(qm_code(m[k], im));
-            vq[i] = uint8_t(qv_code(v[k], iv));
-            if constexpr (PARAM_BF16) {
-              const __nv_bfloat16 h = __float2bfloat16_rn(p[k]);
-              static_cast<__nv_bfloat16*>(P.param)[blk.param_off + i] = h;
-            } else {
-              static_cast<float*>(P.param)[blk.param_off + i] = p[k];
-            }
-          }
-        }
-      }
-      if (threadIdx.x == 0) {
-        P.mabs[slot] = am;
-        P.vabs[slot] = av;
-      }
+  for (int k = 0; k < G::Q; ++k) {
+    const int a = G::quad(k);
+    if constexpr (GLOBAL) {
+      pv[k] = ld_na_v4(master + a);
+      gv[k] = ld_nc_v4(grad + a);
+      cm[k] = ld_na_u32(static_cast<const uint8_t*>(mq) + a);
+      cv[k] = ld_na_u32(static_cast<const uint8_t*>(vq) + a);
     } else {
-      // ---------------- two passes for blocks longer than 2048 -------------
-      float am = 0.f, av = 0.f;
-      for (int i = threadIdx.x; i < len; i += ADAM_THREADS) {
-        const ElemOut o = adam_elem(0.f, grad[i], s8_to_f(uint32_t(uint8_t(mq[i]))) * sm,
-                                    u8_to_f(uint32_t(vq[i])) * sv, s);
-        am = fmaxf(am, fabsf(o.m));
-        av = fmaxf(av, o.v);
-      }
-      block_max2(am, av, red_m, red_v);
-      const float im = am > 0.f ? 127.0f / am : 0.f;
-      const float iv = av > 0.f ? 255.0f / av : 0.f;
-      __syncthreads();  // every thread has read the old codes of ITS elements
-                        // only, so no cross-thread hazard; keep reduction smem safe
-      for (int i = threadIdx.x; i < len; i += ADAM_THREADS) {
-        const ElemOut o = adam_elem(master[i], grad[i], s8_to_f(uint32_t(uint8_t(mq[i]))) * sm,
-                                    u8_to_f(uint32_t(vq[i])) * sv, s);
-        master[i] = o.p;
-        mq[i] = int8_t(qm_code(o.m, im));
-        vq[i] = uint8_t(qv_code(o.v, iv));
-        if constexpr (PARAM_BF16)
-          static_cast<__nv_bfloat16*>(P.param)[blk.param_off + i] = __float2bfloat16_rn(o.p);
-        else
-          static_cast<float*>(P.param)[blk.param_off + i] = o.p;
-      }
-      if (threadIdx.x == 0) {
-        P.mabs[slot] = am;
-        P.vabs[slot] = av;
+      pv[k] = *reinterpret_cast<const int4*>(master + a);
+      gv[k] = *reinterpret_cast<const int4*>(grad + a);
+      cm[k] = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(mq) + a);
+      cv[k] = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(vq) + a);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < G::Q; ++k) {
+    r.p[4 * k + 0] = __int_as_float(pv[k].x);
+    r.p[4 * k + 1] = __int_as_float(pv[k].y);
+    r.p[4 * k + 2] = __int_as_float(pv[k].z);
+    r.p[4 * k + 3] = __int_as_float(pv[k].w);
+    r.g[4 * k + 0] = __int_as_float(gv[k].x);
+    r.g[4 * k + 1] = __int_as_float(gv[k].y);
+    r.g[4 * k + 2] = __int_as_float(gv[k].z);
+    r.g[4 * k + 3] = __int_as_float(gv[k].w);
+    dq4_m(cm[k], sm, &r.mt[4 * k]);
+    dq4_v(cv[k], sv, &r.vt[4 * k]);
+  }
+}
+
+// masked element loads (tails, misaligned blocks)
+template <int NT>
+__device__ __forceinline__ void load_generic(BlockRegs<NT>& r, const float* master, const float* grad,
+                                             const int8_t* mq, const uint8_t* vq, int len, float sm,
+                                             float sv) {
+  using G = AdamGeom<NT>;
+#pragma unroll
+  for (int e = 0; e < G::EPT; ++e) {
+    const int i = G::idx(e);
+    if (i < len) {
+      r.p[e] = master[i];
+      r.g[e] = grad[i];
+      r.mt[e] = (byte_f(uint32_t(uint8_t(mq[i])) ^ 0x80u, 0) - 8388736.0f) * sm;
+      r.vt[e] = (byte_f(uint32_t(vq[i]), 0) - 8388608.0f) * sv;
+    } else {
+      r.p[e] = r.g[e] = r.mt[e] = r.vt[e] = 0.f;
+    }
+  }
+}
+
+// Update + block absmax + (hook) + requantize + stores, for a block held in
+// registers.  `after_reduce` runs once every thread of the CTA has its inputs
+// in registers (right after the absmax reduction's barrier).
+template <int NT, bool PARAM_BF16, bool FAST, typename Hook>
+__device__ __forceinline__ void adam_block_tail(BlockRegs<NT>& r, const AdamBlock& blk,
+                                                const AdamPtrs& P, const AdamScalars& s,
+                                                float* red_m, float* red_v, Hook after_reduce) {
+  using G = AdamGeom<NT>;
+  const int len = blk.len;
+  float m[G::EPT], v[G::EPT];
+  float am = 0.f, av = 0.f;
+#pragma unroll
+  for (int e = 0; e < G::EPT; ++e) {
+    const ElemOut o = adam_elem(r.p[e], r.g[e], r.mt[e], r.vt[e], s);
+    const bool live = FAST || G::idx(e) < len;
+    r.p[e] = o.p;
+    m[e] = live ? o.m : 0.f;
+    v[e] = live ? o.v : 0.f;
+    am = fmaxf(am, fabsf(m[e]));
+    av = fmaxf(av, v[e]);
+  }
+  block_max2<G::WARPS>(am, av, red_m, red_v);
+  after_reduce();
+  const float im = am > 0.f ? 127.0f / am : 0.f;
+  const float iv = av > 0.f ? 255.0f / av : 0.f;
+  float* __restrict__ master = P.master + blk.state_off;
+  uint8_t* __restrict__ mq = reinterpret_cast<uint8_t*>(P.mq) + blk.state_off;
+  uint8_t* __restrict__ vq = P.vq + blk.state_off;
+  if constexpr (FAST) {
+#pragma unroll
+    for (int k = 0; k < G::Q; ++k) {
+      const int a = G::quad(k);
+      const float* pk = &r.p[4 * k];
+      const float* mk = &m[4 * k];
+      const float* vk = &v[4 * k];
+      *reinterpret_cast<float4*>(master + a) = make_float4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint32_t*>(mq + a) = pack4(rne_bits(mk[0] * im), rne_bits(mk[1] * im),
+                                                   rne_bits(mk[2] * im), rne_bits(mk[3] * im));
+      *reinterpret_cast<uint32_t*>(vq + a) = pack4(rne_bits(vk[0] * iv), rne_bits(vk[1] * iv),
+                                                   rne_bits(vk[2] * iv), rne_bits(vk[3] * iv));
+      if constexpr (PARAM_BF16) {
+        uint16_t* pp = static_cast<uint16_t*>(P.param) + blk.param_off;
+        *reinterpret_cast<uint2*>(pp + a) =
+            make_uint2(pack_bf16x2(pk[0], pk[1]), pack_bf16x2(pk[2], pk[3]));
+      } else {
+        float* pp = static_cast<float*>(P.param) + blk.param_off;
+        *reinterpret_cast<float4*>(pp + a) = make_float4(pk[0], pk[1], pk[2], pk[3]);
       }
     }
-    __syncthreads();  // red_m/red_v reused by the next block
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::EPT; ++e) {
+      const int i = G::idx(e);
+      if (i < len) {
+        master[i] = r.p[e];
+        mq[i] = code1(m[e] * im);
+        vq[i] = code1(v[e] * iv);
+        if constexpr (PARAM_BF16)
+          static_cast<__nv_bfloat16*>(P.param)[blk.param_off + i] = __float2bfloat16_rn(r.p[e]);
+        else
+          static_cast<float*>(P.param)[blk.param_off + i] = r.p[e];
+      }
+    }
   }
+  if (threadIdx.x == 0) {
+    P.mabs[blk.slot] = am;
+    P.vabs[blk.slot] = av;
+  }
+}
+
+// blocks longer than 2048: pass 1 computes the absmax, pass 2 recomputes and stores
+template <int NT, bool PARAM_BF16, typename Hook>
+__device__ __forceinline__ void adam_block_two_pass(const AdamBlock& blk, float sm, float sv,
+                                                    const AdamPtrs& P, const AdamScalars& s,
+                                                    float* red_m, float* red_v, Hook after_reduce) {
+  float* __restrict__ master = P.master + blk.state_off;
+  uint8_t* __restrict__ mq = reinterpret_cast<uint8_t*>(P.mq) + blk.state_off;
+  uint8_t* __restrict__ vq = P.vq + blk.state_off;
+  const float* __restrict__ grad = P.grad + blk.grad_off;
+  auto mt_of = [&](int i) { return (byte_f(uint32_t(mq[i]) ^ 0x80u, 0) - 8388736.0f) * sm; };
+  auto vt_of = [&](int i) { return (byte_f(uint32_t(vq[i]), 0) - 8388608.0f) * sv; };
+  float am = 0.f, av = 0.f;
+  for (int i = threadIdx.x; i < blk.len; i += NT) {
+    const ElemOut o = adam_elem(0.f, grad[i], mt_of(i), vt_of(i), s);
+    am = fmaxf(am, fabsf(o.m));
+    av = fmaxf(av, o.v);
+  }
+  block_max2<AdamGeom<NT>::WARPS>(am, av, red_m, red_v);
+  after_reduce();
+  const float im = am > 0.f ? 127.0f / am : 0.f;
+  const float iv = av > 0.f ? 255.0f / av : 0.f;
+  // each thread rewrites exactly the elements it read in pass 1: no hazard
+  for (int i = threadIdx.x; i < blk.len; i += NT) {
+    const ElemOut o = adam_elem(master[i], grad[i], mt_of(i), vt_of(i), s);
+    master[i] = o.p;
+    mq[i] = code1(o.m * im);
+    vq[i] = code1(o.v * iv);
+    if constexpr (PARAM_BF16)
+      static_cast<__nv_bfloat16*>(P.param)[blk.param_off + i] = __float2bfloat16_rn(o.p);
+    else
+      static_cast<float*>(P.param)[blk.param_off + i] = o.p;
+  }
+  if (threadIdx.x == 0) {
+    P.mabs[blk.slot] = am;
+    P.vabs[blk.slot] = av;
+  }
+}
+
+__device__ __forceinline__ bool adam_fast(const AdamBlock& b) {
+  return b.len == ADAM_TILE && ((b.state_off | b.grad_off | b.param_off) & 3) == 0;
+}
+
+struct NoHook {
+  __device__ void operator()() const {}
+};
+
+template <int NT, bool PARAM_BF16>
+__device__ __forceinline__ void adam_block_global(const AdamBlock& blk, const AdamPtrs& P,
+                                                  const AdamScalars& s, float sm, float sv,
+                                                  float* rm, float* rv) {
+  if (blk.len <= ADAM_TILE) {
+    BlockRegs<NT> r;
+    if (adam_fast(blk)) {
+      load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
+                          P.vq + blk.state_off, sm, sv);
+      adam_block_tail<NT, PARAM_BF16, true>(r, blk, P, s, rm, rv, NoHook{});
+    } else {
+      load_generic<NT>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
+                       P.vq + blk.state_off, blk.len, sm, sv);
+      adam_block_tail<NT, PARAM_BF16, false>(r, blk, P, s, rm, rv, NoHook{});
+    }
+  } else {
+    adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, NoHook{});
+  }
+}
+
+template <int NT, bool PARAM_BF16>
+__global__ void __launch_bounds__(NT) adam8_kernel(const AdamBlock* __restrict__ tbl,
+                                                   int64_t nblocks, AdamPtrs P, AdamScalars s) {
+  __shared__ float red_m[2][AdamGeom<NT>::WARPS], red_v[2][AdamGeom<NT>::WARPS];
+  int it = 0;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+    const AdamBlock blk = tbl[b];
+    const float sm = P.mabs[blk.slot] / 127.0f;  // dequantization scales (IEEE div)
+    const float sv = P.vabs[blk.slot] / 255.0f;
+    // red_m/red_v are double-buffered: a thread can be at most one block
+    // ahead (every block has a barrier), so no trailing __syncthreads.
+    adam_block_global<NT, PARAM_BF16>(blk, P, s, sm, sv, red_m[it & 1], red_v[it & 1]);
+  }
+}
+
+// ---------------- TMA-pipelined variant ----------------
+struct __align__(128) AdamStage {
+  float p[ADAM_TILE];
+  float g[ADAM_TILE];
+  uint8_t mq[ADAM_TILE];
+  uint8_t vq[ADAM_TILE];
+};
+constexpr uint32_t ADAM_STAGE_TX = sizeof(float) * ADAM_TILE * 2 + ADAM_TILE * 2;  // 20480
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// bulk copies need 16-B aligned global addresses: codes at state_off % 16
+__device__ __forceinline__ bool adam_tma_ok(const AdamBlock& b) {
+  return b.len == ADAM_TILE && (b.state_off & 15) == 0 && ((b.grad_off | b.param_off) & 3) == 0;
+}
+
+template <int NT, bool PARAM_BF16, int STAGES>
+__global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restrict__ tbl,
+                                                       int64_t nblocks, AdamPtrs P, AdamScalars s) {
+  extern __shared__ __align__(128) uint8_t adam_smem[];
+  AdamStage* stage = reinterpret_cast<AdamStage*>(adam_smem);
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ float red_m[2][AdamGeom<NT>::WARPS], red_v[2][AdamGeom<NT>::WARPS];
+
+  // thread 0 fills stage `st` with block b (or just arrives if b is not TMA-able)
+  auto issue = [&](int64_t b, int st) {
+    const AdamBlock nb = tbl[b];
+    if (adam_tma_ok(nb)) {
+      mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
+      bulk_g2s(stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
+    } else {
+      mbar_arrive(&full[st]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < STAGES; ++st) {
+      const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
+      if (b < nblocks) issue(b, st);
+    }
+  }
+  __syncthreads();
+  int it = 0;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+    const int st = it % STAGES;
+    const uint32_t ph = uint32_t(it / STAGES) & 1u;
+    const AdamBlock blk = tbl[b];
+    const float sm = P.mabs[blk.slot] / 127.0f;
+    const float sv = P.vabs[blk.slot] / 255.0f;
+    float* rm = red_m[it & 1];
+    float* rv = red_v[it & 1];
+    // refill this stage with block b + STAGES*grid once every thread has
+    // consumed it (called right after the absmax barrier)
+    auto refill = [&]() {
+      if (threadIdx.x == 0) {
+        const int64_t nb = b + int64_t(STAGES) * gridDim.x;
+        if (nb < nblocks) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async writes
+          issue(nb, st);
+        }
+      }
+    };
+    mbar_wait(&full[st], ph);
+    if (adam_tma_ok(blk)) {
+      const AdamStage& S = stage[st];
+      BlockRegs<NT> r;
+      load_fast<NT, false>(r, S.p, S.g, S.mq, S.vq, sm, sv);
+      adam_block_tail<NT, PARAM_BF16, true>(r, blk, P, s, rm, rv, refill);
+    } else if (blk.len <= ADAM_TILE) {
+      BlockRegs<NT> r;
+      if (adam_fast(blk)) {
+        load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off,
+                            P.mq + blk.state_off, P.vq + blk.state_off, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, true>(r, blk, P, s, rm, rv, refill);
+      } else {
+        load_generic<NT>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
+                         P.vq + blk.state_off, blk.len, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, false>(r, blk, P, s, rm, rv, refill);
+      }
+    } else {
+      adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, refill);
+    }
+  }
+}
+
+// Variant switch (experiments; the default is the measured best):
+// RSDB_ADAM_KERNEL = direct128 | direct256 | tma2 | tma3 | tma4  (TMA: 128 threads)
+static int adam_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RSDB_ADAM_KERNEL");
+    v = 128;
+    if (e && !strcmp(e, "direct128")) v = 128;
+    if (e && !strcmp(e, "direct256")) v = 256;
+    if (e && !strcmp(e, "tma2")) v = 2;
+    if (e && !strcmp(e, "tma3")) v = 3;
+    if (e && !strcmp(e, "tma4")) v = 4;
+  }
+  return v;
+}
+
+template <int NT, bool BF, int ST>
+static cudaError_t launch_adam8_tma(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
+                                    const AdamScalars& s, cudaStream_t st) {
+  const size_t smem = sizeof(AdamStage) * ST;
+  static int occ = [&] {
+    cudaFuncSetAttribute(adam8_tma_kernel<NT, BF, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    return resident_blocks(adam8_tma_kernel<NT, BF, ST>, NT, smem);
+  }();
+  const int64_t blocks = std::min<int64_t>(nblocks, int64_t(num_sms()) * occ);
+  adam8_tma_kernel<NT, BF, ST><<<blocks, NT, smem, st>>>(tbl, nblocks, p, s);
+  return cudaGetLastError();
+}
+
+template <int NT, bool BF>
+static cudaError_t launch_adam8_direct(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
+                                       const AdamScalars& s, cudaStream_t st) {
+  static int occ = resident_blocks(adam8_kernel<NT, BF>, NT, 0);
+  const int64_t blocks = std::min<int64_t>(nblocks, int64_t(num_sms()) * occ);
+  adam8_kernel<NT, BF><<<blocks, NT, 0, st>>>(tbl, nblocks, p, s);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_adam8(const AdamBlock* table_dev, int64_t nblocks, const AdamPtrs& p,
                          const AdamScalars& s, int32_t /*max_len*/, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
-  static int occ_bf = resident_blocks(adam8_kernel<true>, ADAM_THREADS, 0);
-  static int occ_f = resident_blocks(adam8_kernel<false>, ADAM_THREADS, 0);
-  const int64_t cap = int64_t(num_sms()) * (p.param_bf16 ? occ_bf : occ_f);
-  const int64_t blocks = std::min<int64_t>(nblocks, cap);
-  if (p.param_bf16)
-    adam8_kernel<true><<<blocks, ADAM_THREADS, 0, st>>>(table_dev, nblocks, p, s);
-  else
-    adam8_kernel<false><<<blocks, ADAM_THREADS, 0, st>>>(table_dev, nblocks, p, s);
-  return cudaGetLastError();
+  const bool bf = p.param_bf16;
+  switch (adam_variant()) {
+    case 2:
+      return bf ? launch_adam8_tma<128, true, 2>(table_dev, nblocks, p, s, st)
+                : launch_adam8_tma<128, false, 2>(table_dev, nblocks, p, s, st);
+    case 3:
+      return bf ? launch_adam8_tma<128, true, 3>(table_dev, nblocks, p, s, st)
+                : launch_adam8_tma<128, false, 3>(table_dev, nblocks, p, s, st);
+    case 4:
+      return bf ? launch_adam8_tma<128, true, 4>(table_dev, nblocks, p, s, st)
+                : launch_adam8_tma<128, false, 4>(table_dev, nblocks, p, s, st);
+    case 256:
+      return bf ? launch_adam8_direct<256, true>(table_dev, nblocks, p, s, st)
+                : launch_adam8_direct<256, false>(table_dev, nblocks, p, s, st);
+    default:
+      return bf ? launch_adam8_direct<128, true>(table_dev, nblocks, p, s, st)
+                : launch_adam8_direct<128, false>(table_dev, nblocks, p, s, st);
+  }
 }
 
 // ----------------------------------------------------------------------------

@@ -54,4 +54,19 @@ cudaError_t launch_copy_segments(const CopySeg* segs_dev, int64_t nseg, int64_t 
 
 int num_sms();
 
+// ---- fused collectives over NVLink peer memory (p2p.cu) ----
+constexpr int P2P_MAX_RANKS = 8;
+struct P2PPtrs {
+  const void* p[P2P_MAX_RANKS];  // per-rank device pointers (own rank: local)
+};
+struct P2PSignals {
+  uint64_t* local;                  // this rank's signal buffer
+  uint64_t* peer[P2P_MAX_RANKS];    // every rank's signal buffer, mapped here
+};
+cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,
+                          const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
+                          cudaStream_t st);
+cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
+                          const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
+
 }  // namespace rsdb

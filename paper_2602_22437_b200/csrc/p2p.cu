@@ -1,0 +1,247 @@
+// Fused collectives over NVLink peer memory.
+//
+//  rs_p2p_kernel  a6+a7: rank k pulls G_r[kS + i] (bf16) from every rank r
+//                 over NVLink, y = sum_{r=0..m-1} fp32(G_r) * scale in rank
+//                 order (fp32), padding -> 0, writes its fp32 shard.  Bytes on
+//                 the wire per rank: (m-1) S 2 (bf16), vs (m-1) S 4 for the
+//                 fp32 NCCL ReduceScatter, and no separate m*S cast pass.
+//  ag_p2p_kernel  a4: rank k pulls every peer's shard into its own buffer.
+//
+// Synchronisation through a per-rank signal buffer (uint64 words):
+//   [0, 8)   start[r] = epoch written by rank r when it enters the call
+//   [8, 16)  done[r]  = epoch written by rank r when all its CTAs finished
+//                       reading its peers
+//   [16]     CTA completion counter of this rank's running kernel
+// Start: block 0 publishes `epoch` to every peer (after a system fence), every
+// CTA waits until all peers have published.  Done: the last CTA of the rank
+// publishes to every peer and waits for all peers, so the kernel -- and the
+// stream -- only moves on once nobody reads this rank's buffers any more.
+#include <cuda_bf16.h>
+
+#include "kernels.cuh"
+
+namespace rsdb {
+
+constexpr int P2P_THREADS = 512;
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_peer_v2(const void* p) {  // 8 bytes from a peer (bypass L1)
+  uint2 r;
+  asm volatile("ld.global.cv.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_peer_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.cv.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
+  if (blockIdx.x == 0 && threadIdx.x < m && int(threadIdx.x) != rank) {
+    __threadfence_system();
+    st_release_sys(sg.peer[threadIdx.x] + rank, epoch);
+  }
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < m; ++r) {
+      if (r == rank) continue;
+      while (ld_acquire_sys(sg.local + r) < epoch) {
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
+  __syncthreads();  // this CTA's peer reads are complete (values consumed)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(sg.local + 16);
+    const unsigned int old = atomicAdd(ctr, 1u);
+    if (old == gridDim.x - 1) {
+      atomicExch(ctr, 0u);
+      __threadfence_system();
+      for (int r = 0; r < m; ++r)
+        if (r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);
+      for (int r = 0; r < m; ++r) {
+        if (r == rank) continue;
+        while (ld_acquire_sys(sg.local + 8 + r) < epoch) {
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int first_pad_after_p(const int64_t* pad, int npad, int64_t x) {
+  int lo = 0, hi = npad;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (pad[2 * mid + 1] > x)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ bool in_pad_p(const int64_t* pad, int npad, int j, int64_t i) {
+  for (; j < npad && pad[2 * j] <= i; ++j)
+    if (i < pad[2 * j + 1]) return true;
+  return false;
+}
+
+// grads: M pointers to each rank's unit grad_full base (bf16).  out = this
+// rank's grad_f32 + rank*S.  pad: padding intervals of the global buffer.
+// Templated on the world size so the peer loop unrolls with static indices
+// (no local-memory copy of the pointer table) and all M x U peer loads are
+// in flight before the rank-ordered accumulation.
+template <int M>
+__global__ void __launch_bounds__(P2P_THREADS) rs_p2p_kernel(P2PPtrs grads, float* __restrict__ out,
+                                                            int64_t S, int rank, float scale,
+                                                            const int64_t* __restrict__ pad, int npad,
+                                                            P2PSignals sg, uint64_t epoch) {
+  constexpr int U = M <= 2 ? 8 : (M <= 4 ? 4 : 2);  // vectors per thread per iteration
+  p2p_start(sg, rank, M, epoch);
+  const int64_t base = int64_t(rank) * S;
+  const int64_t nvec = S / 4;  // S is a multiple of g_coll = 8 for bf16 units
+  const int64_t stride = int64_t(gridDim.x) * P2P_THREADS * U;
+  const uint16_t* g[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) g[r] = static_cast<const uint16_t*>(grads.p[r]) + base;
+  for (int64_t v0 = int64_t(blockIdx.x) * P2P_THREADS * U + threadIdx.x; v0 < nvec; v0 += stride) {
+    uint2 w[M][U];
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+        w[r][u] = v < nvec ? ld_peer_v2(g[r] + 4 * v) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+      if (v >= nvec) break;
+      // rank-order accumulation: acc = ((0 + x_0) + x_1) + ... (fp32), x_r = fp32(G_r) * scale
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        a0 += __uint_as_float(w[r][u].x << 16) * scale;
+        a1 += __uint_as_float(w[r][u].x & 0xffff0000u) * scale;
+        a2 += __uint_as_float(w[r][u].y << 16) * scale;
+        a3 += __uint_as_float(w[r][u].y & 0xffff0000u) * scale;
+      }
+      const int64_t e0 = base + 4 * v;
+      if (npad > 0) {
+        const int j = first_pad_after_p(pad, npad, e0);
+        if (j < npad && pad[2 * j] < e0 + 4) {
+          if (in_pad_p(pad, npad, j, e0 + 0)) a0 = 0.f;
+          if (in_pad_p(pad, npad, j, e0 + 1)) a1 = 0.f;
+          if (in_pad_p(pad, npad, j, e0 + 2)) a2 = 0.f;
+          if (in_pad_p(pad, npad, j, e0 + 3)) a3 = 0.f;
+        }
+      }
+      *reinterpret_cast<float4*>(out + 4 * v) = make_float4(a0, a1, a2, a3);
+    }
+  }
+  p2p_done(sg, rank, M, epoch);
+}
+
+// params: M pointers to each rank's unit param_full base; copies peer shards
+// [r*S, (r+1)*S) for r != rank into this rank's buffer.  bytes_S = S * elem.
+template <int M>
+__global__ void __launch_bounds__(P2P_THREADS) ag_p2p_kernel(P2PPtrs params, int64_t bytes_S, int rank,
+                                                            P2PSignals sg, uint64_t epoch) {
+  constexpr int U = 4;
+  p2p_start(sg, rank, M, epoch);
+  char* dst = static_cast<char*>(const_cast<void*>(params.p[0]));
+  const char* src[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    src[r] = static_cast<const char*>(params.p[r]);
+    if (r == rank) dst = const_cast<char*>(src[r]);
+  }
+  const int64_t nvec = bytes_S / 16;  // S * elem is a multiple of 16 (g_coll)
+  const int64_t stride = int64_t(gridDim.x) * P2P_THREADS * U;
+  for (int64_t v0 = int64_t(blockIdx.x) * P2P_THREADS * U + threadIdx.x; v0 < nvec; v0 += stride) {
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      if (r == rank) continue;
+      int4 w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+        if (v < nvec) w[u] = ld_peer_v4(src[r] + int64_t(r) * bytes_S + 16 * v);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+        if (v < nvec) *reinterpret_cast<int4*>(dst + int64_t(r) * bytes_S + 16 * v) = w[u];
+      }
+    }
+  }
+  p2p_done(sg, rank, M, epoch);
+}
+
+template <typename K>
+static int p2p_grid(K kernel) {
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, P2P_THREADS, 0);
+  return num_sms() * (b < 1 ? 1 : b);
+}
+
+template <int M>
+static cudaError_t rs_p2p_m(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
+                            const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
+                            cudaStream_t st) {
+  static const int grid = p2p_grid(rs_p2p_kernel<M>);
+  const int64_t per = int64_t(P2P_THREADS) * (M <= 2 ? 8 : (M <= 4 ? 4 : 2));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((S / 4 + per - 1) / per, grid));
+  rs_p2p_kernel<M><<<blocks, P2P_THREADS, 0, st>>>(grads, out, S, rank, scale, pad, npad, sg, epoch);
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t ag_p2p_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
+                            uint64_t epoch, cudaStream_t st) {
+  static const int grid = p2p_grid(ag_p2p_kernel<M>);
+  const int64_t per = int64_t(P2P_THREADS) * 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((bytes_S / 16 + per - 1) / per, grid));
+  ag_p2p_kernel<M><<<blocks, P2P_THREADS, 0, st>>>(params, bytes_S, rank, sg, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,
+                          const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
+                          cudaStream_t st) {
+  switch (m) {
+#define RS_CASE(M) \
+  case M:          \
+    return rs_p2p_m<M>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    RS_CASE(1) RS_CASE(2) RS_CASE(3) RS_CASE(4) RS_CASE(5) RS_CASE(6) RS_CASE(7) RS_CASE(8)
+#undef RS_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
+                          const P2PSignals& sg, uint64_t epoch, cudaStream_t st) {
+  switch (m) {
+#define AG_CASE(M) \
+  case M:          \
+    return ag_p2p_m<M>(params, bytes_S, rank, sg, epoch, st);
+    AG_CASE(1) AG_CASE(2) AG_CASE(3) AG_CASE(4) AG_CASE(5) AG_CASE(6) AG_CASE(7) AG_CASE(8)
+#undef AG_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rsdb

@@ -1,0 +1,11 @@
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()"
+timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -5 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo bench_rc=$?
+tail -3 gpurun_out/bench1.err; cat gpurun_out/bench1.json
+B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 600 $B > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"adam8|cast_scale|nccl|Nccl" --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo ncu1_rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"adam8|cast_scale" -c 4 -o gpurun_out/prof_r1 $B > gpurun_out/ncu_full.log 2>&1; echo ncu2_rc=$?
+tail -3 gpurun_out/ncu_full.log

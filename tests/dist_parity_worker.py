@@ -83,6 +83,34 @@ def main():
         if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
             ok = False
             msgs.append(f"{name}: ReduceScatter not bit exact (max {np.abs(y - y_ref).max()})")
+        # ---- N1: the same two collectives as single kernels over NVLink peer memory
+        p2p = R.P2P(comm, [param_full, grad_full] if eb == 2 else [param_full])
+        param_full.zero_()
+        param_full[rank * S:(rank + 1) * S] = full_ref[rank * S:(rank + 1) * S]
+        R.all_gather_p2p(u, p2p)
+        torch.cuda.synchronize()
+        got_bits = bf16_bits(param_full) if eb == 2 else f32(param_full).view(np.uint32)
+        if not np.array_equal(got_bits, exp_bits):
+            ok = False
+            msgs.append(f"{name}: p2p AllGather mismatch")
+        if eb == 2:
+            grad_f32.fill_(float("nan"))
+            R.reduce_scatter_p2p(u, p2p)
+            torch.cuda.synchronize()
+            y = f32(grad_f32[rank * S:(rank + 1) * S])
+            if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
+                ok = False
+                msgs.append(f"{name}: p2p ReduceScatter not bit exact")
+            # repeated calls (epochs advance, barriers re-arm)
+            for _ in range(3):
+                R.reduce_scatter_p2p(u, p2p)
+                R.all_gather_p2p(u, p2p)
+            torch.cuda.synchronize()
+            y = f32(grad_f32[rank * S:(rank + 1) * S])
+            if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
+                ok = False
+                msgs.append(f"{name}: repeated p2p ReduceScatter drifted")
+        p2p.close()
         # ---- 8-bit Adam on my shard
         master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
         nb = u.num_blocks
@@ -125,7 +153,7 @@ def main():
         full_mask = np.zeros(world * S, bool)
         for l, e in zip(o.starts, o.numel):
             full_mask[l:l + e] = True
-        tol = 1e-5 * (p32 + 1e-3) + (2.0 ** -8 * p32 if eb == 2 else 0)
+        tol = 1e-5 * (p32 + 1e-3) + (2.0 ** -7 * p32 if eb == 2 else 0)
         if np.any((np.abs(got - exp) > tol)[full_mask]):
             ok = False
             msgs.append(f"{name}: post-Adam AllGather mismatch {np.abs(got - exp)[full_mask].max()}")
@@ -154,6 +182,17 @@ def main():
     if np.any(np.abs(y - yref) > 1e-6 * absum + 1e-30):
         ok = False
         msgs.append("random-normal RS outside 1e-6 * sum|x|")
+    # fused p2p path: rank-order fp32 sum == the oracle's rank-order sum bit for bit
+    p2p = R.P2P(comm, [grad_full])
+    grad_f32.zero_()
+    R.reduce_scatter_p2p(u, p2p)
+    torch.cuda.synchronize()
+    y32 = f32(grad_f32[rank * S:(rank + 1) * S])
+    yord = OD.reduce_scatter(o, xs)[rank]
+    if not np.array_equal(y32.view(np.uint32), yord.view(np.uint32)):
+        ok = False
+        msgs.append("random-normal p2p RS differs from the rank-order oracle sum")
+    p2p.close()
     del u
     del rng
     comm.close()
