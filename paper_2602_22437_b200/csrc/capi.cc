@@ -488,6 +488,8 @@ rsdb_status rsdb_p2p_create(rsdb_comm* comm, int32_t n_bufs, void* const* local_
     p->opened.clear();
   };
   for (int32_t r = 0; r < comm->world; ++r) {
+    // buffers of one rank may share an allocation (same handle): open it once
+    std::vector<std::pair<std::string, void*>> seen;
     for (int32_t i = 0; i < n_bufs; ++i) {
       if (r == comm->rank) {
         p->peer[size_t(i)][size_t(r)] = p->local[size_t(i)];
@@ -498,14 +500,20 @@ rsdb_status rsdb_p2p_create(rsdb_comm* comm, int32_t n_bufs, void* const* local_
       int64_t off;
       std::memcpy(&mh, h, 64);
       std::memcpy(&off, h + 64, 8);
+      const std::string key(reinterpret_cast<const char*>(h), 64);
       void* base = nullptr;
-      cudaError_t e = cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess) {
-        cleanup();
-        return fail(RSDB_ECUDA, "cudaIpcOpenMemHandle(rank %d, buffer %d): %s", r, i,
-                    cudaGetErrorString(e));
+      for (auto& kv : seen)
+        if (kv.first == key) base = kv.second;
+      if (!base) {
+        cudaError_t e = cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          cleanup();
+          return fail(RSDB_ECUDA, "cudaIpcOpenMemHandle(rank %d, buffer %d): %s", r, i,
+                      cudaGetErrorString(e));
+        }
+        p->opened.push_back(base);
+        seen.emplace_back(key, base);
       }
-      p->opened.push_back(base);
       p->peer[size_t(i)][size_t(r)] = static_cast<char*>(base) + off;
     }
   }
