@@ -434,7 +434,7 @@ def run_ours(args):
     cast_ms = tot["cast"] / K
     ag_ms, rs_ms = tot["ag"] / K, tot["rs"] / K
     adam_gbs = ab["adam"] / (adam_ms * 1e-3) / 1e9
-    cast_gbs = ab["cast"] / (cast_ms * 1e-3) / 1e9
+    cast_gbs = ab["cast"] / (cast_ms * 1e-3) / 1e9 if cast_ms > 0 else None  # p2p: fused into RS
     # physical bytes crossing NVLink into each rank per step: AG (m-1) S 2;
     # RS (m-1) S 4 on the NCCL fp32 path, (m-1) S 2 on the fused p2p path
     wire_ag = ab["ag"]

@@ -679,7 +679,7 @@ static int adam_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("RSDB_ADAM_KERNEL");
-    v = 128;
+    v = 3;  // measured best on B200: TMA ring of 3 stages, 128 threads (profiles/r1)
     if (e && !strcmp(e, "direct128")) v = 128;
     if (e && !strcmp(e, "direct256")) v = 256;
     if (e && !strcmp(e, "tma2")) v = 2;
