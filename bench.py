@@ -47,7 +47,7 @@ L2_BYTES = 126 * 2 ** 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--layers", type=int, default=16)
@@ -80,13 +80,17 @@ NVLINK_PEAK_GBS = 770.0  # measured per-direction peer bandwidth, B200_PROFILING
 
 # ---------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampler (the B200_PROFILING.md clocks line) started before the
+    warm-up -- nvidia-smi needs ~0.1-0.3 s to start -- and filtered to samples
+    whose own timestamps fall inside [begin(), end()] (the timed region)."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpus):
         self.gpus = set(gpus)
         self.p = None
+        self.t0 = self.t1 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS,
                                        "--format=csv,noheader,nounits", "-lms", "50"],
@@ -94,9 +98,16 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+
     def stop(self):
         if self.p is None:
             return None
+        import datetime
         time.sleep(0.12)
         self.p.terminate()
         try:
@@ -108,8 +119,15 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9 or not f[0].isdigit() or int(f[0]) not in self.gpus:
+            if len(f) < 10 or not f[1].isdigit() or int(f[1]) not in self.gpus:
                 continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if ts is not None and self.t0 is not None and not (self.t0 - 0.06 <= ts <= self.t1 + 0.06):
+                continue
+            f = f[1:]
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
@@ -402,6 +420,7 @@ def run_ours(args):
     job_bytes = sum_over_ranks(per_rank_bytes, world)
     cfg = R.AdamConfig()
     stream = torch.cuda.Stream()
+    clocks = Clocks(range(world)) if rank == 0 else None  # started early: nvidia-smi is slow to start
     t = 1
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -412,7 +431,8 @@ def run_ours(args):
     timers = Timers()
     barrier(world)
     torch.cuda.synchronize()
-    clocks = Clocks(range(world)) if rank == 0 else None
+    if clocks:
+        clocks.begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -422,6 +442,8 @@ def run_ours(args):
             t += 1
     ev1.record(stream)
     torch.cuda.synchronize()
+    if clocks:
+        clocks.end()
     barrier(world)
     clk = clocks.stop() if clocks else None
     ms_local = ev0.elapsed_time(ev1)

@@ -561,6 +561,10 @@ rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   if (u->L.elem_bytes != 2) return fail(RSDB_EMISMATCH, "p2p ReduceScatter needs a bf16 unit");
   if (u->L.S == 0) return OK_CLEAR();
   const int m = u->L.m;
+  if (m == 1) {  // no peers: the reduction is the group op alone (a6)
+    if (rsdb_status st = cast_scale(u, stream)) return st;
+    return OK_CLEAR();
+  }
   int32_t bi = 0;
   int64_t off = 0;
   if (rsdb_status st = p2p_find(p, u->bufs.grad_full, int64_t(m) * u->L.S * 2, &bi, &off)) return st;
@@ -577,7 +581,7 @@ rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
 rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   rsdb::P2PSignals sg;
   if (rsdb_status st = p2p_common(u, p, &sg)) return st;
-  if (u->L.S == 0) return OK_CLEAR();
+  if (u->L.S == 0 || u->L.m == 1) return OK_CLEAR();  // world 1: AllGather is the identity
   const int m = u->L.m;
   const int64_t bytes_S = u->L.S * u->L.elem_bytes;
   int32_t bi = 0;

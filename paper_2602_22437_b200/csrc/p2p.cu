@@ -18,6 +18,9 @@
 // stream -- only moves on once nobody reads this rank's buffers any more.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "kernels.cuh"
 
 namespace rsdb {
@@ -32,16 +35,31 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint2 ld_peer_v2(const void* p) {  // 8 bytes from a peer (bypass L1)
+// peer loads; FL = 0: ld.global.cv (uncached), 1: ld.global.nc (read-only
+// path; the peer does not write its buffer between the barriers), 2: weak ld.global
+template <int FL>
+__device__ __forceinline__ uint2 ld_peer_v2(const void* p) {
   uint2 r;
-  asm volatile("ld.global.cv.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  if constexpr (FL == 0)
+    asm volatile("ld.global.cv.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  else if constexpr (FL == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
+template <int FL>
 __device__ __forceinline__ int4 ld_peer_v4(const void* p) {
   int4 r;
-  asm volatile("ld.global.cv.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if constexpr (FL == 0)
+    asm volatile("ld.global.cv.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  else if constexpr (FL == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 
@@ -63,7 +81,7 @@ __device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m,
 __device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
   __syncthreads();  // this CTA's peer reads are complete (values consumed)
   if (threadIdx.x == 0) {
-    __threadfence();
+    __threadfence_system();  // this CTA's (possibly remote, push variant) stores
     unsigned int* ctr = reinterpret_cast<unsigned int*>(sg.local + 16);
     const unsigned int old = atomicAdd(ctr, 1u);
     if (old == gridDim.x - 1) {
@@ -97,92 +115,135 @@ __device__ __forceinline__ bool in_pad_p(const int64_t* pad, int npad, int j, in
   return false;
 }
 
+// Zero the padding positions of 4 consecutive outputs starting at e0.
+__device__ __forceinline__ void pad_zero4(const int64_t* pad, int npad, int64_t e0, float& a0,
+                                          float& a1, float& a2, float& a3) {
+  if (npad <= 0) return;
+  const int j = first_pad_after_p(pad, npad, e0);
+  if (j < npad && pad[2 * j] < e0 + 4) {
+    if (in_pad_p(pad, npad, j, e0 + 0)) a0 = 0.f;
+    if (in_pad_p(pad, npad, j, e0 + 1)) a1 = 0.f;
+    if (in_pad_p(pad, npad, j, e0 + 2)) a2 = 0.f;
+    if (in_pad_p(pad, npad, j, e0 + 3)) a3 = 0.f;
+  }
+}
+
 // grads: M pointers to each rank's unit grad_full base (bf16).  out = this
 // rank's grad_f32 + rank*S.  pad: padding intervals of the global buffer.
-// Templated on the world size so the peer loop unrolls with static indices
-// (no local-memory copy of the pointer table) and all M x U peer loads are
-// in flight before the rank-ordered accumulation.
-template <int M>
+// Templated on the world size M so the peer loop unrolls with static indices
+// (no local-memory copy of the pointer table) and all M x U peer loads are in
+// flight before the rank-ordered accumulation.  VEC = bf16 elements per load
+// (4: 8-byte loads, one coalesced float4 store; 8: 16-byte loads, two float4
+// stores), FL = peer-load flavour.
+template <int M, int VEC, int FL>
 __global__ void __launch_bounds__(P2P_THREADS) rs_p2p_kernel(P2PPtrs grads, float* __restrict__ out,
                                                             int64_t S, int rank, float scale,
                                                             const int64_t* __restrict__ pad, int npad,
                                                             P2PSignals sg, uint64_t epoch) {
-  constexpr int U = M <= 2 ? 8 : (M <= 4 ? 4 : 2);  // vectors per thread per iteration
+  constexpr int U = (M <= 2 ? 8 : (M <= 4 ? 4 : 2)) * 4 / VEC;  // vectors per thread per iteration
   p2p_start(sg, rank, M, epoch);
   const int64_t base = int64_t(rank) * S;
-  const int64_t nvec = S / 4;  // S is a multiple of g_coll = 8 for bf16 units
+  const int64_t nvec = S / VEC;  // S is a multiple of g_coll = 8 for bf16 units
   const int64_t stride = int64_t(gridDim.x) * P2P_THREADS * U;
   const uint16_t* g[M];
 #pragma unroll
   for (int r = 0; r < M; ++r) g[r] = static_cast<const uint16_t*>(grads.p[r]) + base;
   for (int64_t v0 = int64_t(blockIdx.x) * P2P_THREADS * U + threadIdx.x; v0 < nvec; v0 += stride) {
-    uint2 w[M][U];
+    uint32_t w[M][U][VEC / 2];
 #pragma unroll
     for (int r = 0; r < M; ++r)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-        w[r][u] = v < nvec ? ld_peer_v2(g[r] + 4 * v) : make_uint2(0u, 0u);
+        if constexpr (VEC == 4) {
+          const uint2 x = v < nvec ? ld_peer_v2<FL>(g[r] + 4 * v) : make_uint2(0u, 0u);
+          w[r][u][0] = x.x;
+          w[r][u][1] = x.y;
+        } else {
+          const int4 x = v < nvec ? ld_peer_v4<FL>(g[r] + 8 * v) : make_int4(0, 0, 0, 0);
+          w[r][u][0] = uint32_t(x.x);
+          w[r][u][1] = uint32_t(x.y);
+          w[r][u][2] = uint32_t(x.z);
+          w[r][u][3] = uint32_t(x.w);
+        }
       }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t v = v0 + int64_t(u) * P2P_THREADS;
       if (v >= nvec) break;
       // rank-order accumulation: acc = ((0 + x_0) + x_1) + ... (fp32), x_r = fp32(G_r) * scale
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      float a[VEC];
 #pragma unroll
-      for (int r = 0; r < M; ++r) {
-        a0 += __uint_as_float(w[r][u].x << 16) * scale;
-        a1 += __uint_as_float(w[r][u].x & 0xffff0000u) * scale;
-        a2 += __uint_as_float(w[r][u].y << 16) * scale;
-        a3 += __uint_as_float(w[r][u].y & 0xffff0000u) * scale;
-      }
-      const int64_t e0 = base + 4 * v;
-      if (npad > 0) {
-        const int j = first_pad_after_p(pad, npad, e0);
-        if (j < npad && pad[2 * j] < e0 + 4) {
-          if (in_pad_p(pad, npad, j, e0 + 0)) a0 = 0.f;
-          if (in_pad_p(pad, npad, j, e0 + 1)) a1 = 0.f;
-          if (in_pad_p(pad, npad, j, e0 + 2)) a2 = 0.f;
-          if (in_pad_p(pad, npad, j, e0 + 3)) a3 = 0.f;
+      for (int k = 0; k < VEC; ++k) a[k] = 0.f;
+#pragma unroll
+      for (int r = 0; r < M; ++r)
+#pragma unroll
+        for (int k = 0; k < VEC / 2; ++k) {
+          a[2 * k] += __uint_as_float(w[r][u][k] << 16) * scale;
+          a[2 * k + 1] += __uint_as_float(w[r][u][k] & 0xffff0000u) * scale;
         }
+#pragma unroll
+      for (int k = 0; k < VEC / 4; ++k) {
+        const int64_t e0 = base + VEC * v + 4 * k;
+        pad_zero4(pad, npad, e0, a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]);
+        *reinterpret_cast<float4*>(out + VEC * v + 4 * k) =
+            make_float4(a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]);
       }
-      *reinterpret_cast<float4*>(out + 4 * v) = make_float4(a0, a1, a2, a3);
     }
   }
   p2p_done(sg, rank, M, epoch);
 }
 
-// params: M pointers to each rank's unit param_full base; copies peer shards
-// [r*S, (r+1)*S) for r != rank into this rank's buffer.  bytes_S = S * elem.
-template <int M>
+// params: M pointers to each rank's unit param_full base.  PUSH = false: copy
+// every peer's shard [r*S, (r+1)*S) into this rank's buffer (peer loads);
+// PUSH = true: write this rank's shard into every peer's buffer (peer stores,
+// made visible by the system fence of the done barrier).  bytes_S = S * elem.
+template <int M, bool PUSH, int FL>
 __global__ void __launch_bounds__(P2P_THREADS) ag_p2p_kernel(P2PPtrs params, int64_t bytes_S, int rank,
                                                             P2PSignals sg, uint64_t epoch) {
   constexpr int U = 4;
   p2p_start(sg, rank, M, epoch);
-  char* dst = static_cast<char*>(const_cast<void*>(params.p[0]));
-  const char* src[M];
+  char* buf[M];
 #pragma unroll
-  for (int r = 0; r < M; ++r) {
-    src[r] = static_cast<const char*>(params.p[r]);
-    if (r == rank) dst = const_cast<char*>(src[r]);
-  }
+  for (int r = 0; r < M; ++r) buf[r] = static_cast<char*>(const_cast<void*>(params.p[r]));
+  char* mine = static_cast<char*>(const_cast<void*>(params.p[0]));
+#pragma unroll
+  for (int r = 0; r < M; ++r)
+    if (r == rank) mine = buf[r];
   const int64_t nvec = bytes_S / 16;  // S * elem is a multiple of 16 (g_coll)
   const int64_t stride = int64_t(gridDim.x) * P2P_THREADS * U;
   for (int64_t v0 = int64_t(blockIdx.x) * P2P_THREADS * U + threadIdx.x; v0 < nvec; v0 += stride) {
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      if (r == rank) continue;
+    if constexpr (PUSH) {
       int4 w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-        if (v < nvec) w[u] = ld_peer_v4(src[r] + int64_t(r) * bytes_S + 16 * v);
+        if (v < nvec) w[u] = ld_peer_v4<1>(mine + int64_t(rank) * bytes_S + 16 * v);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-        if (v < nvec) *reinterpret_cast<int4*>(dst + int64_t(r) * bytes_S + 16 * v) = w[u];
+      for (int r = 0; r < M; ++r) {
+        if (r == rank) continue;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+          if (v < nvec) *reinterpret_cast<int4*>(buf[r] + int64_t(rank) * bytes_S + 16 * v) = w[u];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        if (r == rank) continue;
+        int4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+          if (v < nvec) w[u] = ld_peer_v4<FL>(buf[r] + int64_t(r) * bytes_S + 16 * v);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t v = v0 + int64_t(u) * P2P_THREADS;
+          if (v < nvec) *reinterpret_cast<int4*>(mine + int64_t(r) * bytes_S + 16 * v) = w[u];
+        }
       }
     }
   }
@@ -196,25 +257,70 @@ static int p2p_grid(K kernel) {
   return num_sms() * (b < 1 ? 1 : b);
 }
 
+// Variant switch (experiments; defaults = measured best):
+// RSDB_P2P_RS = v4cv | v4nc | v4ld | v8cv | v8nc | v8ld ;  RSDB_P2P_AG = pullcv | pullnc | push
+static int p2p_env(const char* name, const char* const* opts, int n, int dflt) {
+  const char* e = getenv(name);
+  if (!e) return dflt;
+  for (int i = 0; i < n; ++i)
+    if (!strcmp(e, opts[i])) return i;
+  return dflt;
+}
+static int rs_variant() {
+  static const char* o[] = {"v4cv", "v4nc", "v4ld", "v8cv", "v8nc", "v8ld"};
+  static int v = p2p_env("RSDB_P2P_RS", o, 6, 0);
+  return v;
+}
+static int ag_variant() {
+  static const char* o[] = {"pullcv", "pullnc", "push"};
+  static int v = p2p_env("RSDB_P2P_AG", o, 3, 0);
+  return v;
+}
+
+template <int M, int VEC, int FL>
+static cudaError_t rs_p2p_mvf(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
+                              const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
+                              cudaStream_t st) {
+  static const int grid = p2p_grid(rs_p2p_kernel<M, VEC, FL>);
+  const int64_t per = int64_t(P2P_THREADS) * VEC * ((M <= 2 ? 8 : (M <= 4 ? 4 : 2)) * 4 / VEC);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((S + per - 1) / per, grid));
+  rs_p2p_kernel<M, VEC, FL><<<blocks, P2P_THREADS, 0, st>>>(grads, out, S, rank, scale, pad, npad, sg,
+                                                             epoch);
+  return cudaGetLastError();
+}
+
 template <int M>
 static cudaError_t rs_p2p_m(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
                             const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
                             cudaStream_t st) {
-  static const int grid = p2p_grid(rs_p2p_kernel<M>);
-  const int64_t per = int64_t(P2P_THREADS) * (M <= 2 ? 8 : (M <= 4 ? 4 : 2));
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((S / 4 + per - 1) / per, grid));
-  rs_p2p_kernel<M><<<blocks, P2P_THREADS, 0, st>>>(grads, out, S, rank, scale, pad, npad, sg, epoch);
+  switch (rs_variant()) {
+    case 1: return rs_p2p_mvf<M, 4, 1>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    case 2: return rs_p2p_mvf<M, 4, 2>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    case 3: return rs_p2p_mvf<M, 8, 0>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    case 4: return rs_p2p_mvf<M, 8, 1>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    case 5: return rs_p2p_mvf<M, 8, 2>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    default: return rs_p2p_mvf<M, 4, 0>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+  }
+}
+
+template <int M, bool PUSH, int FL>
+static cudaError_t ag_p2p_mvf(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
+                              uint64_t epoch, cudaStream_t st) {
+  static const int grid = p2p_grid(ag_p2p_kernel<M, PUSH, FL>);
+  const int64_t per = int64_t(P2P_THREADS) * 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((bytes_S / 16 + per - 1) / per, grid));
+  ag_p2p_kernel<M, PUSH, FL><<<blocks, P2P_THREADS, 0, st>>>(params, bytes_S, rank, sg, epoch);
   return cudaGetLastError();
 }
 
 template <int M>
 static cudaError_t ag_p2p_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
                             uint64_t epoch, cudaStream_t st) {
-  static const int grid = p2p_grid(ag_p2p_kernel<M>);
-  const int64_t per = int64_t(P2P_THREADS) * 4;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((bytes_S / 16 + per - 1) / per, grid));
-  ag_p2p_kernel<M><<<blocks, P2P_THREADS, 0, st>>>(params, bytes_S, rank, sg, epoch);
-  return cudaGetLastError();
+  switch (ag_variant()) {
+    case 1: return ag_p2p_mvf<M, false, 1>(params, bytes_S, rank, sg, epoch, st);
+    case 2: return ag_p2p_mvf<M, true, 1>(params, bytes_S, rank, sg, epoch, st);
+    default: return ag_p2p_mvf<M, false, 0>(params, bytes_S, rank, sg, epoch, st);
+  }
 }
 
 cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,
