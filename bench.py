@@ -467,13 +467,16 @@ def run_ours(args):
     # dominant kernel of the step (largest share of device time)
     names = ({"ag": "nccl_all_gather", "rs": "nccl_reduce_scatter"} if p2p is None else
              {"ag": "ag_p2p_kernel", "rs": "rs_p2p_kernel"})
-    shares = {"adam8_kernel": tot["adam"], "cast_scale_kernel": tot["cast"],
+    # the default 8-bit Adam kernel is the TMA-pipelined one (RSDB_ADAM_KERNEL overrides)
+    adam_name = ("adam8_tma_kernel" if os.environ.get("RSDB_ADAM_KERNEL", "tma3").startswith("tma")
+                 else "adam8_kernel")
+    shares = {adam_name: tot["adam"], "cast_scale_kernel": tot["cast"],
               names["rs"]: tot["rs"], names["ag"]: tot["ag"]}
     dom = max(shares, key=shares.get)
-    if dom in ("adam8_kernel", "cast_scale_kernel") or world == 1:
-        if dom not in ("adam8_kernel", "cast_scale_kernel"):
-            dom = "adam8_kernel"
-        ach = adam_gbs if dom == "adam8_kernel" else cast_gbs
+    if dom in (adam_name, "cast_scale_kernel") or world == 1:
+        if dom not in (adam_name, "cast_scale_kernel"):
+            dom = adam_name
+        ach = adam_gbs if dom == adam_name else cast_gbs
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "traffic": profile_traffic(dom), "peak_source": peak_src}
     else:
