@@ -250,6 +250,254 @@ __global__ void __launch_bounds__(P2P_THREADS) ag_p2p_kernel(P2PPtrs params, int
   p2p_done(sg, rank, M, epoch);
 }
 
+// ---------------- TMA (bulk-copy) variants over NVLink ----------------
+// The data movement is issued by ONE thread per CTA as 1-D bulk copies
+// (cp.async.bulk) straight from the peers' mapped memory into a ring of
+// shared-memory stages (mbarrier complete_tx), so NVLink sees large
+// transactions and the SMs issue almost no load instructions.
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+}
+__device__ __forceinline__ void tbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+constexpr int AG_TMA_CHUNK = 16384;  // bytes per stage
+constexpr int AG_TMA_STAGES = 4;
+
+template <int M>
+__global__ void __launch_bounds__(32) ag_tma_kernel(P2PPtrs params, int64_t bytes_S, int rank,
+                                                   P2PSignals sg, uint64_t epoch) {
+  extern __shared__ __align__(128) uint8_t ag_smem[];
+  __shared__ __align__(8) uint64_t bar[AG_TMA_STAGES];
+  p2p_start(sg, rank, M, epoch);
+  if (threadIdx.x == 0) {
+    char* buf[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) buf[r] = static_cast<char*>(const_cast<void*>(params.p[r]));
+    char* mine = buf[0];
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      if (r == rank) mine = buf[r];
+    for (int s = 0; s < AG_TMA_STAGES; ++s) tbar_init(&bar[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int64_t per = (bytes_S + AG_TMA_CHUNK - 1) / AG_TMA_CHUNK;  // chunks per peer shard
+    const int64_t total = per * (M - 1);
+    // chunk j -> (peer r, byte offset inside the global buffer, length)
+    auto chunk = [&](int64_t j, int& r, int64_t& off, uint32_t& len) {
+      r = int(j / per);
+      const int64_t c = j - int64_t(r) * per;
+      r += r >= rank;
+      off = int64_t(r) * bytes_S + c * AG_TMA_CHUNK;
+      len = uint32_t(imin64(AG_TMA_CHUNK, bytes_S - c * AG_TMA_CHUNK));
+    };
+    auto issue = [&](int64_t j, int s) {
+      int r;
+      int64_t off;
+      uint32_t len;
+      chunk(j, r, off, len);
+      const char* src = buf[0];
+#pragma unroll
+      for (int q = 0; q < M; ++q)
+        if (q == r) src = buf[q];
+      tbar_expect(&bar[s], len);
+      tma_g2s(ag_smem + s * AG_TMA_CHUNK, src + off, len, &bar[s]);
+    };
+    for (int s = 0; s < AG_TMA_STAGES; ++s) {
+      const int64_t j = blockIdx.x + int64_t(s) * gridDim.x;
+      if (j < total) issue(j, s);
+    }
+    int it = 0;
+    for (int64_t j = blockIdx.x; j < total; j += gridDim.x, ++it) {
+      const int s = it % AG_TMA_STAGES;
+      tbar_wait(&bar[s], uint32_t(it / AG_TMA_STAGES) & 1u);
+      int r;
+      int64_t off;
+      uint32_t len;
+      chunk(j, r, off, len);
+      tma_s2g(mine + off, ag_smem + s * AG_TMA_CHUNK, len);
+      const int64_t jn = j + int64_t(AG_TMA_STAGES) * gridDim.x;
+      if (jn < total) {
+        tma_wait_read_all();  // the store above has read stage s
+        issue(jn, s);
+      }
+    }
+    tma_wait_all();
+  }
+  p2p_done(sg, rank, M, epoch);
+}
+
+constexpr int RS_TMA_THREADS = 256;
+constexpr int RS_TMA_TILE = 2048;  // elements per tile (8 per thread)
+constexpr int RS_TMA_STAGES = 3;
+
+template <int M>
+__global__ void __launch_bounds__(RS_TMA_THREADS) rs_tma_kernel(P2PPtrs grads, float* __restrict__ out,
+                                                               int64_t S, int rank, float scale,
+                                                               const int64_t* __restrict__ pad, int npad,
+                                                               P2PSignals sg, uint64_t epoch) {
+  extern __shared__ __align__(128) uint8_t rs_smem[];
+  __shared__ __align__(8) uint64_t bar[RS_TMA_STAGES];
+  // stage s, rank r: RS_TMA_TILE bf16 at rs_smem + (s*M + r) * RS_TMA_TILE*2
+  uint16_t* stage = reinterpret_cast<uint16_t*>(rs_smem);
+  p2p_start(sg, rank, M, epoch);
+  const int64_t base = int64_t(rank) * S;
+  const int64_t ntiles = (S + RS_TMA_TILE - 1) / RS_TMA_TILE;
+  auto issue = [&](int64_t t, int s) {
+    const int64_t e0 = t * RS_TMA_TILE;
+    const uint32_t len = uint32_t(imin64(RS_TMA_TILE, S - e0)) * 2;  // bytes, multiple of 16
+    tbar_expect(&bar[s], len * M);
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      tma_g2s(stage + (s * M + r) * RS_TMA_TILE,
+              static_cast<const uint16_t*>(grads.p[r]) + base + e0, len, &bar[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS_TMA_STAGES; ++s) tbar_init(&bar[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < RS_TMA_STAGES; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  }
+  __syncthreads();
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % RS_TMA_STAGES;
+    tbar_wait(&bar[s], uint32_t(it / RS_TMA_STAGES) & 1u);
+    const int64_t e0 = t * RS_TMA_TILE;
+    const int len = int(imin64(RS_TMA_TILE, S - e0));
+    // two quads per thread: [4t, 4t+4) and [1024 + 4t, ...)
+    float a[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[q][k] = 0.f;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      const uint16_t* src = stage + (s * M + r) * RS_TMA_TILE;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = 4 * threadIdx.x + q * (RS_TMA_TILE / 2);
+        const uint2 w = *reinterpret_cast<const uint2*>(src + i);
+        a[q][0] += __uint_as_float(w.x << 16) * scale;
+        a[q][1] += __uint_as_float(w.x & 0xffff0000u) * scale;
+        a[q][2] += __uint_as_float(w.y << 16) * scale;
+        a[q][3] += __uint_as_float(w.y & 0xffff0000u) * scale;
+      }
+    }
+    __syncthreads();  // every thread has read stage s
+    if (threadIdx.x == 0) {
+      const int64_t tn = t + int64_t(RS_TMA_STAGES) * gridDim.x;
+      if (tn < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(tn, s);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = 4 * threadIdx.x + q * (RS_TMA_TILE / 2);
+      if (i < len) {  // len is a multiple of 8: whole quads
+        pad_zero4(pad, npad, base + e0 + i, a[q][0], a[q][1], a[q][2], a[q][3]);
+        *reinterpret_cast<float4*>(out + e0 + i) = make_float4(a[q][0], a[q][1], a[q][2], a[q][3]);
+      }
+    }
+  }
+  p2p_done(sg, rank, M, epoch);
+}
+
+template <int M>
+static cudaError_t ag_tma_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
+                            uint64_t epoch, cudaStream_t st) {
+  const size_t smem = size_t(AG_TMA_CHUNK) * AG_TMA_STAGES;
+  static const int grid = [&] {
+    cudaFuncSetAttribute(ag_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ag_tma_kernel<M>, 32, smem);
+    return num_sms() * (b < 1 ? 1 : b);
+  }();
+  const int64_t chunks = (bytes_S + AG_TMA_CHUNK - 1) / AG_TMA_CHUNK * (M - 1);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(chunks, grid));
+  ag_tma_kernel<M><<<blocks, 32, smem, st>>>(params, bytes_S, rank, sg, epoch);
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
+                            const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
+                            cudaStream_t st) {
+  const size_t smem = size_t(RS_TMA_TILE) * 2 * M * RS_TMA_STAGES;
+  static const int grid = [&] {
+    cudaFuncSetAttribute(rs_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_tma_kernel<M>, RS_TMA_THREADS, smem);
+    return num_sms() * (b < 1 ? 1 : b);
+  }();
+  const int64_t tiles = (S + RS_TMA_TILE - 1) / RS_TMA_TILE;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, grid));
+  rs_tma_kernel<M><<<blocks, RS_TMA_THREADS, smem, st>>>(grads, out, S, rank, scale, pad, npad, sg, epoch);
+  return cudaGetLastError();
+}
+
+// Start (phase 0) or done (phase 1) barrier alone, one CTA: brackets the
+// copy-engine AllGather variant (cudaMemcpyAsync over the IPC mappings).
+template <int M>
+__global__ void __launch_bounds__(32) p2p_barrier_kernel(P2PSignals sg, int rank, uint64_t epoch, int phase) {
+  if (phase == 0)
+    p2p_start(sg, rank, M, epoch);
+  else
+    p2p_done(sg, rank, M, epoch);
+}
+
+template <int M>
+static cudaError_t ag_ce_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
+                           uint64_t epoch, cudaStream_t st) {
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
+  char* mine = static_cast<char*>(const_cast<void*>(params.p[rank]));
+  for (int r = 0; r < M; ++r) {
+    if (r == rank) continue;
+    const char* src = static_cast<const char*>(params.p[r]) + int64_t(r) * bytes_S;
+    cudaError_t e = cudaMemcpyAsync(mine + int64_t(r) * bytes_S, src, size_t(bytes_S),
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
+  return cudaGetLastError();
+}
+
 template <typename K>
 static int p2p_grid(K kernel) {
   int b = 0;
@@ -258,7 +506,8 @@ static int p2p_grid(K kernel) {
 }
 
 // Variant switch (experiments; defaults = measured best):
-// RSDB_P2P_RS = v4cv | v4nc | v4ld | v8cv | v8nc | v8ld ;  RSDB_P2P_AG = pullcv | pullnc | push
+// RSDB_P2P_RS = v4cv | v4nc | v4ld | v8cv | v8nc | v8ld | tma ;
+// RSDB_P2P_AG = pullcv | pullnc | push | tma | ce   (defaults v8cv / push: profiles/r1)
 static int p2p_env(const char* name, const char* const* opts, int n, int dflt) {
   const char* e = getenv(name);
   if (!e) return dflt;
@@ -267,13 +516,13 @@ static int p2p_env(const char* name, const char* const* opts, int n, int dflt) {
   return dflt;
 }
 static int rs_variant() {
-  static const char* o[] = {"v4cv", "v4nc", "v4ld", "v8cv", "v8nc", "v8ld"};
-  static int v = p2p_env("RSDB_P2P_RS", o, 6, 0);
+  static const char* o[] = {"v4cv", "v4nc", "v4ld", "v8cv", "v8nc", "v8ld", "tma"};
+  static int v = p2p_env("RSDB_P2P_RS", o, 7, 3);
   return v;
 }
 static int ag_variant() {
-  static const char* o[] = {"pullcv", "pullnc", "push"};
-  static int v = p2p_env("RSDB_P2P_AG", o, 3, 0);
+  static const char* o[] = {"pullcv", "pullnc", "push", "tma", "ce"};
+  static int v = p2p_env("RSDB_P2P_AG", o, 5, 2);
   return v;
 }
 
@@ -299,6 +548,7 @@ static cudaError_t rs_p2p_m(const P2PPtrs& grads, float* out, int64_t S, int ran
     case 3: return rs_p2p_mvf<M, 8, 0>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
     case 4: return rs_p2p_mvf<M, 8, 1>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
     case 5: return rs_p2p_mvf<M, 8, 2>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    case 6: return rs_tma_m<M>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
     default: return rs_p2p_mvf<M, 4, 0>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
   }
 }
@@ -319,6 +569,8 @@ static cudaError_t ag_p2p_m(const P2PPtrs& params, int64_t bytes_S, int rank, co
   switch (ag_variant()) {
     case 1: return ag_p2p_mvf<M, false, 1>(params, bytes_S, rank, sg, epoch, st);
     case 2: return ag_p2p_mvf<M, true, 1>(params, bytes_S, rank, sg, epoch, st);
+    case 3: return ag_tma_m<M>(params, bytes_S, rank, sg, epoch, st);
+    case 4: return ag_ce_m<M>(params, bytes_S, rank, sg, epoch, st);
     default: return ag_p2p_mvf<M, false, 0>(params, bytes_S, rank, sg, epoch, st);
   }
 }
