@@ -317,10 +317,13 @@ __global__ void __launch_bounds__(32) ag_tma_kernel(P2PPtrs params, int64_t byte
     const int64_t per = (bytes_S + AG_TMA_CHUNK - 1) / AG_TMA_CHUNK;  // chunks per peer shard
     const int64_t total = per * (M - 1);
     // chunk j -> (peer r, byte offset inside the global buffer, length)
+    // peer slot p = j / per reads from rank (rank + 1 + p) % M: at any moment the
+    // ranks read from distinct peers (a permutation), so no GPU's links are
+    // shared by several readers while others idle
     auto chunk = [&](int64_t j, int& r, int64_t& off, uint32_t& len) {
-      r = int(j / per);
-      const int64_t c = j - int64_t(r) * per;
-      r += r >= rank;
+      const int p = int(j / per);
+      const int64_t c = j - int64_t(p) * per;
+      r = (rank + 1 + p) % M;
       off = int64_t(r) * bytes_S + c * AG_TMA_CHUNK;
       len = uint32_t(imin64(AG_TMA_CHUNK, bytes_S - c * AG_TMA_CHUNK));
     };
@@ -487,8 +490,8 @@ static cudaError_t ag_ce_m(const P2PPtrs& params, int64_t bytes_S, int rank, con
                            uint64_t epoch, cudaStream_t st) {
   p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
   char* mine = static_cast<char*>(const_cast<void*>(params.p[rank]));
-  for (int r = 0; r < M; ++r) {
-    if (r == rank) continue;
+  for (int p = 1; p < M; ++p) {  // rotated peer order: a permutation per step (see ag_tma_kernel)
+    const int r = (rank + p) % M;
     const char* src = static_cast<const char*>(params.p[r]) + int64_t(r) * bytes_S;
     cudaError_t e = cudaMemcpyAsync(mine + int64_t(r) * bytes_S, src, size_t(bytes_S),
                                     cudaMemcpyDeviceToDevice, st);
