@@ -104,7 +104,9 @@ def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: n
     """One 8-bit Adam step on a rank's local shard, block by block.
 
     master/grad: fp32 [S]; m_q int8 [S]; v_q uint8 [S]; m_abs/v_abs fp32
-    [len(blocks)]; blocks = rank_blocks(...) table of (local offset, len).
+    [len(blocks)]; blocks = rank_blocks(...) table of (local offset, len), or
+    rank_tiles(...) table of 2-D tiles (offset of first element, rows, cols,
+    pitch) -- a block is the set of its elements, the update is the same.
     Returns new copies (master, m_q, v_q, m_abs, v_abs, param_shard) where
     param_shard is bf16 bit patterns (uint16) or fp32; positions outside any
     block are left unchanged (param shard: 0)."""
@@ -114,8 +116,12 @@ def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: n
     m_abs = np.array(m_abs, dtype=np.float32, copy=True)
     v_abs = np.array(v_abs, dtype=np.float32, copy=True)
     param = np.zeros(master.shape, np.uint16 if out_bf16 else np.float32)
-    for b, (off, n) in enumerate(blocks):
-        s = slice(off, off + n)
+    for b, blk in enumerate(blocks):
+        if len(blk) == 2:
+            s = slice(blk[0], blk[0] + blk[1])
+        else:  # 2-D tile: element (a, c) at off + a * pitch + c
+            off, rows, cols, pitch = blk
+            s = (off + np.arange(rows)[:, None] * pitch + np.arange(cols)[None, :]).ravel()
         mt = dequantize(m_q[s], m_abs[b], signed=True)
         vt = dequantize(v_q[s], v_abs[b], signed=False)
         p, m, v = adam_block_update(master[s], grad[s], mt, vt, sc)

@@ -367,6 +367,54 @@ def rank_blocks(lay: Layout, rank: int, qblock: int) -> List[Tuple[int, int]]:
     return out
 
 
+def rank_tiles(lay: Layout, rank: int, specs: Sequence[Tuple]) -> List[Tuple[int, int, int, int]]:
+    """Quantization blocks of `rank` when tensor t is quantized in 2-D tiles
+    (the paper's setup "32x32 blocks ... 32-row block granularity",
+    P:419).  specs[t] = ("tile", row_len C, tile_rows tr, tile_cols tc) views
+    tensor t as [e_t / C, C] and cuts it into tr x tc tiles (edge tiles
+    smaller); ("flat", q) keeps contiguous q-element blocks.  Returns
+    (local offset of the tile's first element, rows, cols, pitch) for every
+    block whose elements lie in rank's shard, tensors in order, tiles
+    row-major; a tile that straddles a shard boundary raises."""
+    lo, hi = rank * lay.S, (rank + 1) * lay.S
+    out = []
+    for t, (l, e) in enumerate(zip(lay.starts, lay.numel)):
+        if l + e <= lo or l >= hi:
+            continue
+        spec = specs[t]
+        if spec[0] == "flat":
+            out += [(off, 1, n, n) for off, n in _flat_blocks(l, e, int(spec[1]), lo, hi, t)]
+            continue
+        C, tr, tc = int(spec[1]), int(spec[2]), int(spec[3])
+        Rw = e // C
+        if Rw * C != e:
+            raise ValueError(f"tensor {t}: numel {e} is not a multiple of row_len {C}")
+        for i in range(_ceil(Rw, tr)):
+            rows = min(tr, Rw - i * tr)
+            for j in range(_ceil(C, tc)):
+                cols = min(tc, C - j * tc)
+                first = l + i * tr * C + j * tc
+                last = first + (rows - 1) * C + cols - 1
+                if last < lo or first >= hi:
+                    continue
+                if first < lo or last >= hi:
+                    raise ValueError(f"tile ({i},{j}) of tensor {t} straddles a shard boundary")
+                out.append((first - lo, rows, cols, C))
+    return out
+
+
+def _flat_blocks(l, e, q, lo, hi, t):
+    out = []
+    for j in range(_ceil(e, q)):
+        a, b = l + j * q, l + min((j + 1) * q, e)
+        if b <= lo or a >= hi:
+            continue
+        if a < lo or b > hi:
+            raise ValueError(f"quant block {j} of tensor {t} straddles a shard boundary")
+        out.append((a - lo, b - a))
+    return out
+
+
 def to_dict(lay: Layout) -> Dict:
     return {"m": lay.m, "g_coll": lay.g_coll, "S": lay.S, "E": lay.E,
             "padding": lay.padding, "numel": list(lay.numel),

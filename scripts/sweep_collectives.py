@@ -50,6 +50,10 @@ def main():
     ap.add_argument("--layouts", default="ragged,even,ideal")
     ap.add_argument("--ops", default="ag,rs")
     ap.add_argument("--path", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--workload", default="bucket",
+                    help="bucket (config 5) | llama8b-layer | llama8b-root (config 3) | "
+                         "dsv3 (config 4) | llama1b-layer | llama1b-root (config 2): whole units "
+                         "with their declared granularity, layout 'ragged' only")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -57,13 +61,18 @@ def main():
     dist.init_process_group("gloo")
     comm = R.init_comm(rank, world, local)
     st = torch.cuda.Stream()
-    for mb in [int(x) for x in args.sizes.split(",")]:
-        u = W.bucket(mb)
+    named = {"llama8b-layer": W.llama3_8b_layer(0), "llama8b-root": W.llama3_8b_root(),
+             "dsv3": W.dsv3_moe_unit(), "llama1b-layer": W.llama32_1b_layer(0),
+             "llama1b-root": W.llama32_1b_root()}
+    sizes = [int(x) for x in args.sizes.split(",")] if args.workload == "bucket" else [0]
+    for mb in sizes:
+        u = W.bucket(mb) if args.workload == "bucket" else named[args.workload]
         es = [t.numel for t in u.tensors]
+        gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
         E = sum(es)
-        for kind in args.layouts.split(","):
+        for kind in (args.layouts.split(",") if args.workload == "bucket" else ["ragged"]):
             if kind == "ragged":
-                lay = R.plan(es, [1] * len(es), world)
+                lay = R.plan(es, gs, world)
             else:
                 S = -(-E // world)
                 if kind == "ideal":
@@ -104,7 +113,8 @@ def main():
                 bus = nbytes / (ms * 1e-3) * (world - 1) / world / 1e9
                 good = E * (2 if op == "ag" else 4) / (ms * 1e-3) * (world - 1) / world / 1e9
                 if rank == 0:
-                    print(json.dumps({"mb": mb, "layout": kind, "op": op, "path": args.path,
+                    print(json.dumps({"workload": args.workload,
+                                      "mb": mb, "layout": kind, "op": op, "path": args.path,
                                       "m": world, "S": S,
                                       "E": E, "ms": ms, "busbw_gbs": bus, "goodput_gbs": good,
                                       "pad": lay.padding, "nccl_env": {k: v for k, v in os.environ.items()

@@ -162,3 +162,66 @@ def test_bf16_output_is_rne_of_master():
     res = A.step_8bit_adam(p0, g, mq, vq, ma, va, [(0, S)], A.AdamCfg(), 1)
     t = torch.from_numpy(res[0]).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(res[5], t)
+
+
+# ----------------------------------------------------------------- N2: 2-D tiles
+def _tile_layout(m, tr=32):
+    # two matrices [96, 64] and [64, 40] + a vector, 32-row sharding granularity
+    shapes = [(96, 64), (64, 40), (130,)]
+    es = [int(np.prod(s)) for s in shapes]
+    gs = [tr * 64, tr * 40, 1]
+    return shapes, P.plan(es, gs, m, 4)
+
+
+def test_tiles_with_one_row_are_flat_blocks():
+    shapes, lay = _tile_layout(3)
+    for r in range(3):
+        specs = [("tile", s[-1], 1, s[-1]) if len(s) == 2 else ("flat", 130) for s in shapes]
+        t = P.rank_tiles(lay, r, specs)
+        fl = P.rank_tiles(lay, r, [("flat", s[-1]) if len(s) == 2 else ("flat", 130) for s in shapes])
+        assert t == fl
+
+
+def test_tiles_partition_every_tensor():
+    for m in (1, 2, 3, 4):
+        shapes, lay = _tile_layout(m)
+        specs = [("tile", 64, 32, 32), ("tile", 40, 32, 32), ("flat", 130)]
+        cover = np.zeros(m * lay.S, int)
+        for r in range(m):
+            for off, rows, cols, pitch in P.rank_tiles(lay, r, specs):
+                idx = r * lay.S + off + np.arange(rows)[:, None] * pitch + np.arange(cols)[None, :]
+                cover[idx.ravel()] += 1
+        exp = np.zeros(m * lay.S, int)
+        for l, e in zip(lay.starts, lay.numel):
+            exp[l:l + e] = 1
+        assert np.array_equal(cover, exp)
+
+
+def test_tile_straddle_detected():
+    lay = P.plan([96 * 64], [1], 5, 4)  # element granularity: S = 1232 cuts row 19
+    with pytest.raises(ValueError):
+        for r in range(5):
+            P.rank_tiles(lay, r, [("tile", 64, 32, 32)])
+
+
+def test_tiled_step_equals_flat_step_on_each_tile():
+    """Independent tile derivation: reshape [R, C] -> [R/32, 32, C/32, 32]."""
+    cfg = A.AdamCfg()
+    R_, C_ = 96, 64
+    lay = P.plan([R_ * C_], [32 * C_], 1, 4)
+    S = lay.S
+    p = H.params_np(9, 0, S)
+    g = H.grads_np(9, 0, 0, S)
+    mq = H.codes_np(9, H.STREAM_MCODE, 0, S, True)
+    vq = H.codes_np(9, H.STREAM_VCODE, 0, S, False)
+    tiles = P.rank_tiles(lay, 0, [("tile", C_, 32, 32)])
+    nb = len(tiles)
+    ma = H.absmax_np(9, H.STREAM_ABSM, 0, nb, 12)
+    va = H.absmax_np(9, H.STREAM_ABSV, 0, nb, 22)
+    out = A.step_8bit_adam(p, g, mq, vq, ma, va, tiles, cfg, 3)
+    idx = np.arange(R_ * C_).reshape(R_ // 32, 32, C_ // 32, 32).transpose(0, 2, 1, 3).reshape(-1, 1024)
+    for b in range(nb):
+        e = idx[b]
+        ref = A.step_8bit_adam(p[e], g[e], mq[e], vq[e], ma[b:b + 1], va[b:b + 1], [(0, 1024)], cfg, 3)
+        assert np.array_equal(out[0][e], ref[0]) and np.array_equal(out[1][e], ref[1])
+        assert np.array_equal(out[2][e], ref[2]) and out[3][b] == ref[3][0] and out[4][b] == ref[4][0]
