@@ -124,6 +124,25 @@ rsdb_status rsdb_layout_rank_segments(const rsdb_layout*, int32_t rank, int64_t*
  * boundary (only possible when g_t is not a multiple of qblock). */
 rsdb_status rsdb_layout_rank_blocks(const rsdb_layout*, int32_t rank, int64_t qblock,
                                     int64_t* n, int64_t* off, int32_t* len);
+/* Quantization block spec per tensor (the paper's 8-bit Adam uses
+ * 32x32 tiles with 32-row sharding granularity):
+ *   tile_rows == 0: contiguous blocks of tile_cols elements of the flattened
+ *                   tensor (row_len ignored) -- the qblock form;
+ *   tile_rows  > 0: the tensor viewed as [e_t / row_len, row_len] is cut into
+ *                   tile_rows x tile_cols tiles, row-major, edge tiles smaller. */
+typedef struct {
+  int64_t row_len;
+  int32_t tile_rows;
+  int32_t tile_cols;
+} rsdb_qspec;
+/* a3 with tiles: blocks of `rank` as (offset of the first element inside the
+ * shard, rows, cols, pitch = elements between rows), tensors in order, tiles
+ * row-major.  specs[n_tensors].  EMISMATCH if a tile straddles a shard
+ * boundary (granularity not a multiple of tile_rows rows); EINVAL if
+ * row_len does not divide e_t or a size is < 1.  Two-call protocol. */
+rsdb_status rsdb_layout_rank_tiles(const rsdb_layout*, int32_t rank, const rsdb_qspec* specs,
+                                   int64_t* n, int64_t* off, int32_t* rows, int32_t* cols,
+                                   int64_t* pitch);
 /* Plan JSON {"m","g_coll","S","E","padding","numel","block","starts"} into buf
  * (NUL-terminated if cap suffices); *needed = bytes incl. NUL. */
 rsdb_status rsdb_layout_to_json(const rsdb_layout*, char* buf, int64_t cap, int64_t* needed);
@@ -167,6 +186,9 @@ typedef struct rsdb_unit rsdb_unit;
  * EMISMATCH if a block would straddle).  The layout is copied. */
 rsdb_status rsdb_unit_create(const rsdb_layout*, rsdb_comm* comm_or_null, int32_t rank,
                              const rsdb_unit_bufs* bufs, int64_t qblock, rsdb_unit** out);
+/* The same with per-tensor quantization specs (2-D tiles, N2): specs[n]. */
+rsdb_status rsdb_unit_create_q(const rsdb_layout*, rsdb_comm* comm_or_null, int32_t rank,
+                               const rsdb_unit_bufs* bufs, const rsdb_qspec* specs, rsdb_unit** out);
 int64_t rsdb_unit_num_blocks(const rsdb_unit*); /* blocks on this rank */
 void rsdb_unit_free(rsdb_unit*);
 
@@ -275,6 +297,15 @@ rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units
                                 rsdb_comm* comm_or_null, int32_t rank, int64_t qblock,
                                 int64_t align_bytes, void* const* arena_base,
                                 rsdb_dbuffer** out);
+/* The same two calls with per-unit, per-tensor quantization specs
+ * (specs[u] points to rsdb_qspec[n_tensors(u)]; N2 tiles). */
+rsdb_status rsdb_arena_sizes_q(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                               const rsdb_qspec* const* specs, int64_t align_bytes,
+                               int64_t* bytes_per_kind, int64_t* unit_offsets);
+rsdb_status rsdb_dbuffer_create_q(const rsdb_layout* const* units, int32_t n_units,
+                                  rsdb_comm* comm_or_null, int32_t rank,
+                                  const rsdb_qspec* const* specs, int64_t align_bytes,
+                                  void* const* arena_base, rsdb_dbuffer** out);
 rsdb_unit* rsdb_dbuffer_unit(rsdb_dbuffer*, int32_t i); /* borrowed; NULL if out of range */
 int64_t rsdb_dbuffer_num_blocks(const rsdb_dbuffer*);
 /* a8 over every unit's shard in one kernel launch. */

@@ -48,6 +48,22 @@ def _stream(stream) -> Optional[int]:
     return stream.cuda_stream
 
 
+# ---------------------------------------------------------------- quantization specs
+def qspecs(specs) -> "C.Array":
+    """Per-tensor quantization block specs -> rsdb_qspec[]:
+    ("flat", q) contiguous q-element blocks; ("tile", row_len, rows, cols)
+    2-D tiles of the [numel/row_len, row_len] view (N2, P:419 32x32)."""
+    arr = (_c.QSpec * max(1, len(specs)))()
+    for i, sp in enumerate(specs):
+        if sp[0] == "flat":
+            arr[i] = _c.QSpec(0, 0, int(sp[1]))
+        elif sp[0] == "tile":
+            arr[i] = _c.QSpec(int(sp[1]), int(sp[2]), int(sp[3]))
+        else:
+            raise ValueError(f"unknown quantization spec {sp!r}")
+    return arr
+
+
 # ---------------------------------------------------------------- a1
 def block_elems(shape: Sequence[int], gran: Tuple) -> int:
     """g_t for a granularity declaration ("flat", q) | ("rows", r) | ("whole",) | ("elem",)."""
@@ -134,6 +150,16 @@ class Layout:
         check(lib.rsdb_layout_rank_blocks(self._h, rank, qblock, C.byref(n), off, ln))
         return [(off[i], ln[i]) for i in range(n.value)]
 
+    def rank_tiles(self, rank: int, specs) -> List[Tuple[int, int, int, int]]:
+        """(offset of first element, rows, cols, pitch) of rank's blocks (N2)."""
+        sp = qspecs(specs)
+        n = C.c_int64(0)
+        check(lib.rsdb_layout_rank_tiles(self._h, rank, sp, C.byref(n), None, None, None, None))
+        k = max(1, n.value)
+        off, rw, cl, pt = (C.c_int64 * k)(), (C.c_int32 * k)(), (C.c_int32 * k)(), (C.c_int64 * k)()
+        check(lib.rsdb_layout_rank_tiles(self._h, rank, sp, C.byref(n), off, rw, cl, pt))
+        return [(off[i], rw[i], cl[i], pt[i]) for i in range(n.value)]
+
     def to_json(self) -> dict:
         need = C.c_int64(0)
         check(lib.rsdb_layout_to_json(self._h, None, 0, C.byref(need)))
@@ -212,7 +238,8 @@ class Unit:
     """One FSDP unit bound to caller-owned device buffers (torch tensors)."""
 
     def __init__(self, layout: Layout, rank: int, param_full, grad_full, grad_f32,
-                 qblock: int = 2048, comm: Optional[Comm] = None, _handle=None, _keep=None):
+                 qblock: int = 2048, comm: Optional[Comm] = None, _handle=None, _keep=None,
+                 qspec=None):
         self.layout = layout
         self.rank = rank
         self.comm = comm
@@ -221,8 +248,12 @@ class Unit:
         if _handle is None:
             bufs = _c.UnitBufs(_ptr(param_full), _ptr(grad_full), _ptr(grad_f32))
             h = C.c_void_p()
-            check(lib.rsdb_unit_create(layout.handle, comm.handle if comm else None, rank,
-                                       C.byref(bufs), qblock, C.byref(h)))
+            if qspec is None:
+                check(lib.rsdb_unit_create(layout.handle, comm.handle if comm else None, rank,
+                                           C.byref(bufs), qblock, C.byref(h)))
+            else:
+                check(lib.rsdb_unit_create_q(layout.handle, comm.handle if comm else None, rank,
+                                             C.byref(bufs), qspecs(qspec), C.byref(h)))
             self._h = h
         else:
             self._h = C.c_void_p(_handle)
@@ -342,11 +373,24 @@ def all_gather_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
 KINDS = ("param_full", "grad_full", "grad_f32", "master", "m_q", "v_q", "m_absmax", "v_absmax")
 
 
-def arena_sizes(layouts: Sequence[Layout], rank: int, qblock: int = 2048, align: int = 256):
+def _spec_ptrs(qspec_per_unit):
+    keep = [qspecs(sp) for sp in qspec_per_unit]
+    ptrs = (C.POINTER(_c.QSpec) * max(1, len(keep)))(
+        *[C.cast(a, C.POINTER(_c.QSpec)) for a in keep])
+    return ptrs, keep
+
+
+def arena_sizes(layouts: Sequence[Layout], rank: int, qblock: int = 2048, align: int = 256,
+                qspec=None):
+    """qspec: None (flat qblock) or one per-tensor spec list per unit (N2)."""
     arr = (C.c_void_p * max(1, len(layouts)))(*[l.handle.value for l in layouts])
     sizes = (C.c_int64 * _c.RSDB_NKINDS)()
     offs = (C.c_int64 * max(1, len(layouts) * _c.RSDB_NKINDS))()
-    check(lib.rsdb_arena_sizes(arr, len(layouts), rank, qblock, align, sizes, offs))
+    if qspec is None:
+        check(lib.rsdb_arena_sizes(arr, len(layouts), rank, qblock, align, sizes, offs))
+    else:
+        ptrs, _keep = _spec_ptrs(qspec)
+        check(lib.rsdb_arena_sizes_q(arr, len(layouts), rank, ptrs, align, sizes, offs))
     return list(sizes), [list(offs[u * 8:(u + 1) * 8]) for u in range(len(layouts))]
 
 
@@ -356,7 +400,7 @@ class DBuffer:
     launch over all units."""
 
     def __init__(self, layouts: Sequence[Layout], rank: int, arenas: Sequence, qblock=2048,
-                 align=256, comm: Optional[Comm] = None):
+                 align=256, comm: Optional[Comm] = None, qspec=None):
         self.layouts = list(layouts)
         self.rank = rank
         self.comm = comm
@@ -365,8 +409,13 @@ class DBuffer:
         bases = (C.c_void_p * _c.RSDB_NKINDS)(*[_ptr(a) if a is not None and a.numel() > 0
                                                 else None for a in arenas])
         h = C.c_void_p()
-        check(lib.rsdb_dbuffer_create(arr, len(layouts), comm.handle if comm else None, rank,
-                                      qblock, align, bases, C.byref(h)))
+        if qspec is None:
+            check(lib.rsdb_dbuffer_create(arr, len(layouts), comm.handle if comm else None, rank,
+                                          qblock, align, bases, C.byref(h)))
+        else:
+            ptrs, _keep = _spec_ptrs(qspec)
+            check(lib.rsdb_dbuffer_create_q(arr, len(layouts), comm.handle if comm else None, rank,
+                                            ptrs, align, bases, C.byref(h)))
         self._h = h
         self.units = [Unit(l, rank, None, None, None, comm=comm,
                            _handle=lib.rsdb_dbuffer_unit(h, i), _keep=())

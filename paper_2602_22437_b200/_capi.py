@@ -38,6 +38,10 @@ class AdamState(C.Structure):
     _fields_ = [("master_f32", vp), ("m_q", vp), ("v_q", vp), ("m_absmax", vp), ("v_absmax", vp)]
 
 
+class QSpec(C.Structure):
+    _fields_ = [("row_len", i64), ("tile_rows", i32), ("tile_cols", i32)]
+
+
 class Segment(C.Structure):
     _fields_ = [("src", vp), ("dst", vp), ("numel", i64)]
 
@@ -62,6 +66,12 @@ _SIGS = {
     "rsdb_layout_rank_segments": (i32, [vp, i32, P_i64, P_i32, P_i64, P_i64, P_i64]),
     "rsdb_layout_rank_blocks": (i32, [vp, i32, i64, P_i64, P_i64, P_i32]),
     "rsdb_layout_to_json": (i32, [vp, C.c_char_p, i64, P_i64]),
+    "rsdb_layout_rank_tiles": (i32, [vp, i32, C.POINTER(QSpec), P_i64, P_i64, P_i32, P_i32, P_i64]),
+    "rsdb_unit_create_q": (i32, [vp, vp, i32, C.POINTER(UnitBufs), C.POINTER(QSpec), C.POINTER(vp)]),
+    "rsdb_arena_sizes_q": (i32, [C.POINTER(vp), i32, i32, C.POINTER(C.POINTER(QSpec)), i64, P_i64,
+                                 P_i64]),
+    "rsdb_dbuffer_create_q": (i32, [C.POINTER(vp), i32, vp, i32, C.POINTER(C.POINTER(QSpec)), i64,
+                                    C.POINTER(vp), C.POINTER(vp)]),
     "rsdb_layout_free": (None, [vp]),
     "rsdb_unique_id": (i32, [C.c_char_p]),
     "rsdb_comm_init": (i32, [C.c_char_p, i32, i32, i32, C.POINTER(vp)]),

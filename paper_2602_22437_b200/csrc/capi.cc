@@ -292,9 +292,34 @@ void rsdb_comm_free(rsdb_comm* c) {
 // ---------------------------------------------------------------------------
 // unit
 // ---------------------------------------------------------------------------
+// per-tensor quantization specs: explicit (rsdb_qspec*, N2 tiles) or flat qblock
+static std::vector<rsdb::QSpec> make_specs(const rsdb::Layout& L, int64_t qblock,
+                                           const rsdb_qspec* specs) {
+  std::vector<rsdb::QSpec> v(L.e.size());
+  for (size_t t = 0; t < v.size(); ++t) {
+    if (specs)
+      v[t] = {specs[t].row_len, specs[t].tile_rows, specs[t].tile_cols};
+    else
+      v[t] = {0, 0, int32_t(std::min<int64_t>(qblock, INT32_MAX))};
+  }
+  return v;
+}
+
+static rsdb_status tiles_of(const rsdb::Layout& L, int32_t rank, const std::vector<rsdb::QSpec>& specs,
+                            std::vector<rsdb::QTile>* out) {
+  std::string err;
+  if (!rsdb::rank_tiles(L, rank, specs, out, &err))
+    return fail(err.find("straddles") != std::string::npos ? RSDB_EMISMATCH : RSDB_EINVAL, "%s",
+                err.c_str());
+  for (auto& t : *out)
+    if (int64_t(t.rows) * t.cols > (int64_t{1} << 30) || t.pitch > INT32_MAX)
+      return fail(RSDB_EINVAL, "quantization block too large");
+  return RSDB_OK;
+}
+
 static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t rank,
-                              const rsdb_unit_bufs& bufs, int64_t qblock, rsdb_unit* u,
-                              std::vector<rsdb::QBlock>* blocks_out) {
+                              const rsdb_unit_bufs& bufs, const std::vector<rsdb::QSpec>& specs,
+                              rsdb_unit* u, std::vector<rsdb::QTile>* blocks_out) {
   if (!(L.elem_bytes == 2 || L.elem_bytes == 4))
     return fail(RSDB_EMISMATCH, "units support bf16 (2 B) or f32 (4 B) elements, got %d B", L.elem_bytes);
   if (rank < 0 || rank >= L.m) return fail(RSDB_EINVAL, "rank %d out of [0,%d)", rank, L.m);
@@ -307,15 +332,12 @@ static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t ra
     return fail(RSDB_EMISMATCH, "unit buffers must be 16-byte aligned (P:199, P:369)");
   if (L.elem_bytes == 2 && bufs.grad_full == bufs.grad_f32)
     return fail(RSDB_EMISMATCH, "bf16 unit: grad_full must not alias grad_f32");
-  std::vector<rsdb::QBlock> qb;
-  std::string err;
-  if (!rsdb::rank_blocks(L, rank, qblock, &qb, &err))
-    return fail(qblock < 1 ? RSDB_EINVAL : RSDB_EMISMATCH, "%s", err.c_str());
+  std::vector<rsdb::QTile> qb;
+  if (rsdb_status st = tiles_of(L, rank, specs, &qb)) return st;
   u->L = L;
   u->comm = comm;
   u->rank = rank;
   u->bufs = bufs;
-  u->qblock = qblock;
   u->nblocks = int64_t(qb.size());
   auto iv = rsdb::padding_intervals(L);
   std::vector<int64_t> pad;
@@ -326,7 +348,8 @@ static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t ra
   std::vector<rsdb::AdamBlock> tbl(qb.size());
   const int64_t base = int64_t(rank) * L.S;
   for (size_t i = 0; i < qb.size(); ++i)
-    tbl[i] = {qb[i].off, base + qb[i].off, base + qb[i].off, qb[i].len, int32_t(i)};
+    tbl[i] = {qb[i].off, base + qb[i].off, base + qb[i].off, qb[i].rows * qb[i].cols, int32_t(i),
+              qb[i].cols, int32_t(qb[i].pitch)};
   if (rsdb_status st = u->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
   if (blocks_out) *blocks_out = std::move(qb);
   return RSDB_OK;
@@ -336,8 +359,36 @@ rsdb_status rsdb_unit_create(const rsdb_layout* l, rsdb_comm* comm, int32_t rank
                              const rsdb_unit_bufs* bufs, int64_t qblock, rsdb_unit** out) {
   if (!l || !bufs || !out) return fail(RSDB_EINVAL, "null argument");
   auto u = std::make_unique<rsdb_unit>();
-  if (rsdb_status st = build_unit(l->L, comm, rank, *bufs, qblock, u.get(), nullptr)) return st;
+  if (rsdb_status st = build_unit(l->L, comm, rank, *bufs, make_specs(l->L, qblock, nullptr), u.get(),
+                                  nullptr))
+    return st;
   *out = u.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_unit_create_q(const rsdb_layout* l, rsdb_comm* comm, int32_t rank,
+                               const rsdb_unit_bufs* bufs, const rsdb_qspec* specs, rsdb_unit** out) {
+  if (!l || !bufs || !out || (!specs && !l->L.e.empty())) return fail(RSDB_EINVAL, "null argument");
+  auto u = std::make_unique<rsdb_unit>();
+  if (rsdb_status st = build_unit(l->L, comm, rank, *bufs, make_specs(l->L, 0, specs), u.get(), nullptr))
+    return st;
+  *out = u.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_layout_rank_tiles(const rsdb_layout* l, int32_t rank, const rsdb_qspec* specs,
+                                   int64_t* n, int64_t* off, int32_t* rows, int32_t* cols,
+                                   int64_t* pitch) {
+  if (!l || !n || (!specs && !l->L.e.empty())) return fail(RSDB_EINVAL, "null argument");
+  if (rank < 0 || rank >= l->L.m) return fail(RSDB_EINVAL, "rank %d out of [0,%d)", rank, l->L.m);
+  std::vector<rsdb::QTile> t;
+  if (rsdb_status st = tiles_of(l->L, rank, make_specs(l->L, 0, specs), &t)) return st;
+  if (off && rows && cols && pitch) {
+    if (*n < int64_t(t.size())) return fail(RSDB_EINVAL, "array too small");
+    for (size_t i = 0; i < t.size(); ++i)
+      off[i] = t[i].off, rows[i] = t[i].rows, cols[i] = t[i].cols, pitch[i] = t[i].pitch;
+  }
+  *n = int64_t(t.size());
   return OK_CLEAR();
 }
 
@@ -424,7 +475,7 @@ rsdb_status rsdb_step_8bit_adam(rsdb_unit* u, const rsdb_adam_state* st, const r
                    static_cast<float*>(st->v_absmax),    static_cast<const float*>(u->bufs.grad_f32),
                    u->bufs.param_full,                   u->L.elem_bytes == 2};
   CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
-                              int32_t(std::min<int64_t>(u->qblock, 1 << 30)), S_(stream)));
+                              0, S_(stream)));
   return OK_CLEAR();
 }
 
@@ -599,11 +650,10 @@ rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
 // ---------------------------------------------------------------------------
 static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-static rsdb_status kind_sizes(const rsdb::Layout& L, int32_t rank, int64_t qblock, int64_t sz[RSDB_NKINDS]) {
-  std::vector<rsdb::QBlock> qb;
-  std::string err;
-  if (!rsdb::rank_blocks(L, rank, qblock, &qb, &err))
-    return fail(qblock < 1 ? RSDB_EINVAL : RSDB_EMISMATCH, "%s", err.c_str());
+static rsdb_status kind_sizes(const rsdb::Layout& L, int32_t rank, const std::vector<rsdb::QSpec>& specs,
+                              int64_t sz[RSDB_NKINDS]) {
+  std::vector<rsdb::QTile> qb;
+  if (rsdb_status st = tiles_of(L, rank, specs, &qb)) return st;
   const int64_t full = int64_t(L.m) * L.S;
   sz[RSDB_KIND_PARAM_FULL] = full * L.elem_bytes;
   sz[RSDB_KIND_GRAD_FULL] = L.elem_bytes == 4 ? 0 : full * L.elem_bytes;
@@ -616,12 +666,26 @@ static rsdb_status kind_sizes(const rsdb::Layout& L, int32_t rank, int64_t qbloc
   return RSDB_OK;
 }
 
+// per-unit spec vectors: explicit (specs[u] = rsdb_qspec[n_u]) or flat qblock
+static rsdb_status unit_specs(const rsdb_layout* const* units, int32_t n_units, int64_t qblock,
+                              const rsdb_qspec* const* specs,
+                              std::vector<std::vector<rsdb::QSpec>>* out) {
+  out->clear();
+  for (int32_t u = 0; u < n_units; ++u) {
+    if (!units[u]) return fail(RSDB_EINVAL, "null layout %d", u);
+    if (specs && !specs[u] && !units[u]->L.e.empty()) return fail(RSDB_EINVAL, "null specs for unit %d", u);
+    out->push_back(make_specs(units[u]->L, qblock, specs ? specs[u] : nullptr));
+  }
+  return RSDB_OK;
+}
+
 // MASTER, MQ and VQ share ELEMENT offsets (one "state" index space): the
 // common element offset is aligned so that every kind's byte offset is a
 // multiple of align_bytes.  Likewise MABS/VABS share a block index space.
 static rsdb_status arena_layout(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
-                                int64_t qblock, int64_t align, int64_t* bytes, int64_t* offs,
-                                std::vector<int64_t>* state_elem_off, std::vector<int64_t>* blk_idx_off) {
+                                const std::vector<std::vector<rsdb::QSpec>>& specs, int64_t align,
+                                int64_t* bytes, int64_t* offs, std::vector<int64_t>* state_elem_off,
+                                std::vector<int64_t>* blk_idx_off) {
   if (!units || n_units < 0 || !bytes || align < 16 || (align & (align - 1)))
     return fail(RSDB_EINVAL, "rsdb_arena_sizes: bad argument (align must be a power of two >= 16)");
   int64_t acc[RSDB_NKINDS] = {0};
@@ -631,7 +695,7 @@ static rsdb_status arena_layout(const rsdb_layout* const* units, int32_t n_units
     const rsdb::Layout& L = units[u]->L;
     if (rank < 0 || rank >= L.m) return fail(RSDB_EINVAL, "rank out of range for unit %d", u);
     int64_t sz[RSDB_NKINDS] = {0};
-    if (rsdb_status st = kind_sizes(L, rank, qblock, sz)) return st;
+    if (rsdb_status st = kind_sizes(L, rank, specs[size_t(u)], sz)) return st;
     for (int k : {RSDB_KIND_PARAM_FULL, RSDB_KIND_GRAD_FULL, RSDB_KIND_GRAD_F32}) {
       acc[k] = round_up(acc[k], align);
       if (offs) offs[int64_t(u) * RSDB_NKINDS + k] = acc[k];
@@ -662,23 +726,43 @@ static rsdb_status arena_layout(const rsdb_layout* const* units, int32_t n_units
   return RSDB_OK;
 }
 
-rsdb_status rsdb_arena_sizes(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
-                             int64_t qblock, int64_t align_bytes, int64_t* bytes_per_kind,
-                             int64_t* unit_offsets) {
-  if (rsdb_status st = arena_layout(units, n_units, rank, qblock, align_bytes, bytes_per_kind,
+static rsdb_status arena_sizes_impl(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                                    int64_t qblock, const rsdb_qspec* const* specs, int64_t align_bytes,
+                                    int64_t* bytes_per_kind, int64_t* unit_offsets) {
+  if (!units || n_units < 0) return fail(RSDB_EINVAL, "null argument");
+  std::vector<std::vector<rsdb::QSpec>> sp;
+  if (rsdb_status st = unit_specs(units, n_units, qblock, specs, &sp)) return st;
+  if (rsdb_status st = arena_layout(units, n_units, rank, sp, align_bytes, bytes_per_kind,
                                     unit_offsets, nullptr, nullptr))
     return st;
   return OK_CLEAR();
 }
 
-rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units, rsdb_comm* comm,
-                                int32_t rank, int64_t qblock, int64_t align_bytes,
-                                void* const* arena_base, rsdb_dbuffer** out) {
+rsdb_status rsdb_arena_sizes(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                             int64_t qblock, int64_t align_bytes, int64_t* bytes_per_kind,
+                             int64_t* unit_offsets) {
+  return arena_sizes_impl(units, n_units, rank, qblock, nullptr, align_bytes, bytes_per_kind,
+                          unit_offsets);
+}
+
+rsdb_status rsdb_arena_sizes_q(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
+                               const rsdb_qspec* const* specs, int64_t align_bytes,
+                               int64_t* bytes_per_kind, int64_t* unit_offsets) {
+  if (!specs) return fail(RSDB_EINVAL, "null specs");
+  return arena_sizes_impl(units, n_units, rank, 0, specs, align_bytes, bytes_per_kind, unit_offsets);
+}
+
+static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t n_units,
+                                       rsdb_comm* comm, int32_t rank, int64_t qblock,
+                                       const rsdb_qspec* const* specs, int64_t align_bytes,
+                                       void* const* arena_base, rsdb_dbuffer** out) {
   if (!units || !arena_base || !out || n_units < 0) return fail(RSDB_EINVAL, "null argument");
+  std::vector<std::vector<rsdb::QSpec>> sp;
+  if (rsdb_status st = unit_specs(units, n_units, qblock, specs, &sp)) return st;
   int64_t bytes[RSDB_NKINDS];
   std::vector<int64_t> offs(size_t(n_units) * RSDB_NKINDS), st_off, bk_off;
-  if (rsdb_status st = arena_layout(units, n_units, rank, qblock, align_bytes, bytes, offs.data(),
-                                    &st_off, &bk_off))
+  if (rsdb_status st = arena_layout(units, n_units, rank, sp, align_bytes, bytes, offs.data(), &st_off,
+                                    &bk_off))
     return st;
   auto db = std::make_unique<rsdb_dbuffer>();
   for (int k = 0; k < RSDB_NKINDS; ++k) {
@@ -701,8 +785,8 @@ rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units
     b.grad_f32 = at(RSDB_KIND_GRAD_F32);
     b.grad_full = bf ? at(RSDB_KIND_GRAD_FULL) : b.grad_f32;
     auto unit = std::make_unique<rsdb_unit>();
-    std::vector<rsdb::QBlock> qb;
-    if (rsdb_status st = build_unit(L, comm, rank, b, qblock, unit.get(), &qb)) return st;
+    std::vector<rsdb::QTile> qb;
+    if (rsdb_status st = build_unit(L, comm, rank, b, sp[size_t(u)], unit.get(), &qb)) return st;
     // arena-relative combined table: state in MASTER/MQ/VQ elements, grad in
     // GRAD_F32 elements, param in PARAM_FULL elements.
     const int64_t gbase = offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_GRAD_F32] / 4 + int64_t(rank) * L.S;
@@ -710,8 +794,9 @@ rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units
                           int64_t(rank) * L.S;
     if (bk_off[u] + int64_t(qb.size()) > INT32_MAX) return fail(RSDB_EINVAL, "too many blocks");
     for (size_t i = 0; i < qb.size(); ++i)
-      tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off, qb[i].len,
-                     int32_t(bk_off[u] + int64_t(i))});
+      tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off,
+                     qb[i].rows * qb[i].cols, int32_t(bk_off[u] + int64_t(i)), qb[i].cols,
+                     int32_t(qb[i].pitch)});
     db->grad_bytes.push_back(int64_t(L.m) * L.S * L.elem_bytes);
     db->units.push_back(std::move(unit));
   }
@@ -720,6 +805,19 @@ rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units
   if (rsdb_status st = db->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
   *out = db.release();
   return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units, rsdb_comm* comm,
+                                int32_t rank, int64_t qblock, int64_t align_bytes,
+                                void* const* arena_base, rsdb_dbuffer** out) {
+  return dbuffer_create_impl(units, n_units, comm, rank, qblock, nullptr, align_bytes, arena_base, out);
+}
+
+rsdb_status rsdb_dbuffer_create_q(const rsdb_layout* const* units, int32_t n_units, rsdb_comm* comm,
+                                  int32_t rank, const rsdb_qspec* const* specs, int64_t align_bytes,
+                                  void* const* arena_base, rsdb_dbuffer** out) {
+  if (!specs) return fail(RSDB_EINVAL, "null specs");
+  return dbuffer_create_impl(units, n_units, comm, rank, 0, specs, align_bytes, arena_base, out);
 }
 
 rsdb_unit* rsdb_dbuffer_unit(rsdb_dbuffer* d, int32_t i) {

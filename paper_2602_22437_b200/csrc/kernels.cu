@@ -382,30 +382,79 @@ __device__ __forceinline__ void load_fast(BlockRegs<NT>& r, const float* master,
   }
 }
 
-// masked element loads (tails, misaligned blocks)
+// element i of a block laid out as rows of `cols` elements `pitch` apart
+__device__ __forceinline__ int64_t blk_off(const AdamBlock& b, int i) {
+  const int row = i / b.cols;
+  return int64_t(row) * b.pitch + (i - row * b.cols);
+}
+
+// masked, strided element loads (tails, misaligned blocks, odd tiles)
 template <int NT>
-__device__ __forceinline__ void load_generic(BlockRegs<NT>& r, const float* master, const float* grad,
-                                             const int8_t* mq, const uint8_t* vq, int len, float sm,
-                                             float sv) {
+__device__ __forceinline__ void load_generic(BlockRegs<NT>& r, const AdamBlock& blk,
+                                             const AdamPtrs& P, float sm, float sv) {
   using G = AdamGeom<NT>;
+  const float* master = P.master + blk.state_off;
+  const float* grad = P.grad + blk.grad_off;
+  const int8_t* mq = P.mq + blk.state_off;
+  const uint8_t* vq = P.vq + blk.state_off;
 #pragma unroll
   for (int e = 0; e < G::EPT; ++e) {
     const int i = G::idx(e);
-    if (i < len) {
-      r.p[e] = master[i];
-      r.g[e] = grad[i];
-      r.mt[e] = (byte_f(uint32_t(uint8_t(mq[i])) ^ 0x80u, 0) - 8388736.0f) * sm;
-      r.vt[e] = (byte_f(uint32_t(vq[i]), 0) - 8388608.0f) * sv;
+    if (i < blk.len) {
+      const int64_t o = blk_off(blk, i);
+      r.p[e] = master[o];
+      r.g[e] = grad[o];
+      r.mt[e] = (byte_f(uint32_t(uint8_t(mq[o])) ^ 0x80u, 0) - 8388736.0f) * sm;
+      r.vt[e] = (byte_f(uint32_t(vq[o]), 0) - 8388608.0f) * sv;
     } else {
       r.p[e] = r.g[e] = r.mt[e] = r.vt[e] = 0.f;
     }
   }
 }
 
+// 2-D tile with cols % 4 == 0 (quads never cross a row) and 16-B aligned rows:
+// every quad is one 16-B vector at its own row address (N2, 32x32 tiles)
+template <int NT>
+__device__ __forceinline__ void load_tile(BlockRegs<NT>& r, const AdamBlock& blk, const AdamPtrs& P,
+                                          float sm, float sv) {
+  using G = AdamGeom<NT>;
+  int4 pv[G::Q], gv[G::Q];
+  uint32_t cm[G::Q], cv[G::Q];
+#pragma unroll
+  for (int k = 0; k < G::Q; ++k) {
+    const int e0 = G::quad(k);
+    if (e0 < blk.len) {
+      const int64_t a = blk_off(blk, e0);
+      pv[k] = ld_na_v4(P.master + blk.state_off + a);
+      gv[k] = ld_nc_v4(P.grad + blk.grad_off + a);
+      cm[k] = ld_na_u32(P.mq + blk.state_off + a);
+      cv[k] = ld_na_u32(P.vq + blk.state_off + a);
+    } else {
+      pv[k] = gv[k] = make_int4(0, 0, 0, 0);
+      cm[k] = 0x80808080u;  // decodes to m = 0
+      cv[k] = 0u;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < G::Q; ++k) {
+    r.p[4 * k + 0] = __int_as_float(pv[k].x);
+    r.p[4 * k + 1] = __int_as_float(pv[k].y);
+    r.p[4 * k + 2] = __int_as_float(pv[k].z);
+    r.p[4 * k + 3] = __int_as_float(pv[k].w);
+    r.g[4 * k + 0] = __int_as_float(gv[k].x);
+    r.g[4 * k + 1] = __int_as_float(gv[k].y);
+    r.g[4 * k + 2] = __int_as_float(gv[k].z);
+    r.g[4 * k + 3] = __int_as_float(gv[k].w);
+    dq4_m(cm[k], sm, &r.mt[4 * k]);
+    dq4_v(cv[k], sv, &r.vt[4 * k]);
+  }
+}
+
 // Update + block absmax + (hook) + requantize + stores, for a block held in
 // registers.  `after_reduce` runs once every thread of the CTA has its inputs
 // in registers (right after the absmax reduction's barrier).
-template <int NT, bool PARAM_BF16, bool FAST, typename Hook>
+// MODE 0: masked strided elements; 1: full contiguous 2048 block; 2: 2-D tile quads
+template <int NT, bool PARAM_BF16, int MODE, typename Hook>
 __device__ __forceinline__ void adam_block_tail(BlockRegs<NT>& r, const AdamBlock& blk,
                                                 const AdamPtrs& P, const AdamScalars& s,
                                                 float* red_m, float* red_v, Hook after_reduce) {
@@ -416,7 +465,7 @@ __device__ __forceinline__ void adam_block_tail(BlockRegs<NT>& r, const AdamBloc
 #pragma unroll
   for (int e = 0; e < G::EPT; ++e) {
     const ElemOut o = adam_elem(r.p[e], r.g[e], r.mt[e], r.vt[e], s);
-    const bool live = FAST || G::idx(e) < len;
+    const bool live = MODE == 1 || G::idx(e) < len;
     r.p[e] = o.p;
     m[e] = live ? o.m : 0.f;
     v[e] = live ? o.v : 0.f;
@@ -430,10 +479,14 @@ __device__ __forceinline__ void adam_block_tail(BlockRegs<NT>& r, const AdamBloc
   float* __restrict__ master = P.master + blk.state_off;
   uint8_t* __restrict__ mq = reinterpret_cast<uint8_t*>(P.mq) + blk.state_off;
   uint8_t* __restrict__ vq = P.vq + blk.state_off;
-  if constexpr (FAST) {
+  if constexpr (MODE != 0) {
 #pragma unroll
     for (int k = 0; k < G::Q; ++k) {
-      const int a = G::quad(k);
+      int64_t a = G::quad(k);
+      if constexpr (MODE == 2) {
+        if (a >= len) continue;
+        a = blk_off(blk, int(a));
+      }
       const float* pk = &r.p[4 * k];
       const float* mk = &m[4 * k];
       const float* vk = &v[4 * k];
@@ -456,13 +509,14 @@ __device__ __forceinline__ void adam_block_tail(BlockRegs<NT>& r, const AdamBloc
     for (int e = 0; e < G::EPT; ++e) {
       const int i = G::idx(e);
       if (i < len) {
-        master[i] = r.p[e];
-        mq[i] = code1(m[e] * im);
-        vq[i] = code1(v[e] * iv);
+        const int64_t o = blk_off(blk, i);
+        master[o] = r.p[e];
+        mq[o] = code1(m[e] * im);
+        vq[o] = code1(v[e] * iv);
         if constexpr (PARAM_BF16)
-          static_cast<__nv_bfloat16*>(P.param)[blk.param_off + i] = __float2bfloat16_rn(r.p[e]);
+          static_cast<__nv_bfloat16*>(P.param)[blk.param_off + o] = __float2bfloat16_rn(r.p[e]);
         else
-          static_cast<float*>(P.param)[blk.param_off + i] = r.p[e];
+          static_cast<float*>(P.param)[blk.param_off + o] = r.p[e];
       }
     }
   }
@@ -481,13 +535,14 @@ __device__ __forceinline__ void adam_block_two_pass(const AdamBlock& blk, float 
   uint8_t* __restrict__ mq = reinterpret_cast<uint8_t*>(P.mq) + blk.state_off;
   uint8_t* __restrict__ vq = P.vq + blk.state_off;
   const float* __restrict__ grad = P.grad + blk.grad_off;
-  auto mt_of = [&](int i) { return (byte_f(uint32_t(mq[i]) ^ 0x80u, 0) - 8388736.0f) * sm; };
-  auto vt_of = [&](int i) { return (byte_f(uint32_t(vq[i]), 0) - 8388608.0f) * sv; };
+  auto mt_of = [&](int64_t o) { return (byte_f(uint32_t(mq[o]) ^ 0x80u, 0) - 8388736.0f) * sm; };
+  auto vt_of = [&](int64_t o) { return (byte_f(uint32_t(vq[o]), 0) - 8388608.0f) * sv; };
   float am = 0.f, av = 0.f;
   for (int i = threadIdx.x; i < blk.len; i += NT) {
-    const ElemOut o = adam_elem(0.f, grad[i], mt_of(i), vt_of(i), s);
-    am = fmaxf(am, fabsf(o.m));
-    av = fmaxf(av, o.v);
+    const int64_t o = blk_off(blk, i);
+    const ElemOut e = adam_elem(0.f, grad[o], mt_of(o), vt_of(o), s);
+    am = fmaxf(am, fabsf(e.m));
+    av = fmaxf(av, e.v);
   }
   block_max2<AdamGeom<NT>::WARPS>(am, av, red_m, red_v);
   after_reduce();
@@ -495,14 +550,15 @@ __device__ __forceinline__ void adam_block_two_pass(const AdamBlock& blk, float 
   const float iv = av > 0.f ? 255.0f / av : 0.f;
   // each thread rewrites exactly the elements it read in pass 1: no hazard
   for (int i = threadIdx.x; i < blk.len; i += NT) {
-    const ElemOut o = adam_elem(master[i], grad[i], mt_of(i), vt_of(i), s);
-    master[i] = o.p;
-    mq[i] = code1(o.m * im);
-    vq[i] = code1(o.v * iv);
+    const int64_t q = blk_off(blk, i);
+    const ElemOut o = adam_elem(master[q], grad[q], mt_of(q), vt_of(q), s);
+    master[q] = o.p;
+    mq[q] = code1(o.m * im);
+    vq[q] = code1(o.v * iv);
     if constexpr (PARAM_BF16)
-      static_cast<__nv_bfloat16*>(P.param)[blk.param_off + i] = __float2bfloat16_rn(o.p);
+      static_cast<__nv_bfloat16*>(P.param)[blk.param_off + q] = __float2bfloat16_rn(o.p);
     else
-      static_cast<float*>(P.param)[blk.param_off + i] = o.p;
+      static_cast<float*>(P.param)[blk.param_off + q] = o.p;
   }
   if (threadIdx.x == 0) {
     P.mabs[blk.slot] = am;
@@ -511,7 +567,11 @@ __device__ __forceinline__ void adam_block_two_pass(const AdamBlock& blk, float 
 }
 
 __device__ __forceinline__ bool adam_fast(const AdamBlock& b) {
-  return b.len == ADAM_TILE && ((b.state_off | b.grad_off | b.param_off) & 3) == 0;
+  return b.len == ADAM_TILE && b.cols == b.len && ((b.state_off | b.grad_off | b.param_off) & 3) == 0;
+}
+__device__ __forceinline__ bool adam_tile_fast(const AdamBlock& b) {
+  return b.cols != b.len && ((b.cols | b.pitch) & 3) == 0 &&
+         ((b.state_off | b.grad_off | b.param_off) & 3) == 0;
 }
 
 struct NoHook {
@@ -527,11 +587,13 @@ __device__ __forceinline__ void adam_block_global(const AdamBlock& blk, const Ad
     if (adam_fast(blk)) {
       load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
                           P.vq + blk.state_off, sm, sv);
-      adam_block_tail<NT, PARAM_BF16, true>(r, blk, P, s, rm, rv, NoHook{});
+      adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, NoHook{});
+    } else if (adam_tile_fast(blk)) {
+      load_tile<NT>(r, blk, P, sm, sv);
+      adam_block_tail<NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, NoHook{});
     } else {
-      load_generic<NT>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
-                       P.vq + blk.state_off, blk.len, sm, sv);
-      adam_block_tail<NT, PARAM_BF16, false>(r, blk, P, s, rm, rv, NoHook{});
+      load_generic<NT>(r, blk, P, sm, sv);
+      adam_block_tail<NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, NoHook{});
     }
   } else {
     adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, NoHook{});
@@ -597,7 +659,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // bulk copies need 16-B aligned global addresses: codes at state_off % 16
 __device__ __forceinline__ bool adam_tma_ok(const AdamBlock& b) {
-  return b.len == ADAM_TILE && (b.state_off & 15) == 0 && ((b.grad_off | b.param_off) & 3) == 0;
+  return b.len == ADAM_TILE && b.cols == b.len && (b.state_off & 15) == 0 &&
+         ((b.grad_off | b.param_off) & 3) == 0;
 }
 
 template <int NT, bool PARAM_BF16, int STAGES>
@@ -655,17 +718,19 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
       const AdamStage& S = stage[st];
       BlockRegs<NT> r;
       load_fast<NT, false>(r, S.p, S.g, S.mq, S.vq, sm, sv);
-      adam_block_tail<NT, PARAM_BF16, true>(r, blk, P, s, rm, rv, refill);
+      adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
     } else if (blk.len <= ADAM_TILE) {
       BlockRegs<NT> r;
       if (adam_fast(blk)) {
         load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off,
                             P.mq + blk.state_off, P.vq + blk.state_off, sm, sv);
-        adam_block_tail<NT, PARAM_BF16, true>(r, blk, P, s, rm, rv, refill);
+        adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
+      } else if (adam_tile_fast(blk)) {
+        load_tile<NT>(r, blk, P, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill);
       } else {
-        load_generic<NT>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
-                         P.vq + blk.state_off, blk.len, sm, sv);
-        adam_block_tail<NT, PARAM_BF16, false>(r, blk, P, s, rm, rv, refill);
+        load_generic<NT>(r, blk, P, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, refill);
       }
     } else {
       adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, refill);
@@ -778,6 +843,28 @@ __global__ void __launch_bounds__(COPY_THREADS) copy_seg_kernel(const CopySeg* _
       for (int64_t i = threadIdx.x; i < nv; i += COPY_THREADS)
         reinterpret_cast<int4*>(d)[i] = ld_nc_v4(reinterpret_cast<const int4*>(s) + i);
       for (int64_t i = nv * 16 + threadIdx.x; i < nbytes; i += COPY_THREADS) d[i] = s[i];
+    } else if ((reinterpret_cast<uintptr_t>(s) % (4 * eb_s) == 0) &&
+               (reinterpret_cast<uintptr_t>(d) % (4 * eb_d) == 0)) {
+      // cast / scale, 4 elements per thread per vector (8- or 16-byte accesses)
+      const int64_t nv = n / 4;
+      for (int64_t i = threadIdx.x; i < nv; i += COPY_THREADS) {
+        float f[4];
+        if (src_bf16) {
+          const uint2 w = reinterpret_cast<const uint2*>(s)[i];
+          f[0] = bf16lo(w.x), f[1] = bf16hi(w.x), f[2] = bf16lo(w.y), f[3] = bf16hi(w.y);
+        } else {
+          const float4 w = reinterpret_cast<const float4*>(s)[i];
+          f[0] = w.x, f[1] = w.y, f[2] = w.z, f[3] = w.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] *= scale;
+        if (dst_bf16)
+          reinterpret_cast<uint2*>(d)[i] = make_uint2(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]));
+        else
+          reinterpret_cast<float4*>(d)[i] = make_float4(f[0], f[1], f[2], f[3]);
+      }
+      for (int64_t i = nv * 4 + threadIdx.x; i < n; i += COPY_THREADS)
+        store_from_f(d, i, load_as_f(s, i, src_bf16) * scale, dst_bf16);
     } else {
       for (int64_t i = threadIdx.x; i < n; i += COPY_THREADS)
         store_from_f(d, i, load_as_f(s, i, src_bf16) * scale, dst_bf16);

@@ -8,15 +8,20 @@ namespace rsdb {
 
 // One 8-bit Adam quantization block: element offsets into the state
 // arrays (master / m codes / v codes share indexing), the fp32 gradient array
-// and the parameter array, plus the block's slot in the absmax arrays.
+// and the parameter array, plus the block's slot in the absmax arrays.  A
+// block is `len` elements laid out as rows of `cols` elements, `pitch`
+// elements apart (contiguous block: cols == pitch == len; 2-D tile, N2:
+// cols = tile width, pitch = row length of the tensor).
 struct AdamBlock {
   int64_t state_off;
   int64_t grad_off;
   int64_t param_off;
   int32_t len;
   int32_t slot;
+  int32_t cols;
+  int32_t pitch;
 };
-static_assert(sizeof(AdamBlock) == 32, "AdamBlock is 32 bytes");
+static_assert(sizeof(AdamBlock) == 40, "AdamBlock is 40 bytes");
 
 struct AdamScalars {
   float w1, b2, w2, eps, c_wd, step_size, inv_bc2s;

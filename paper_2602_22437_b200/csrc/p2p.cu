@@ -510,7 +510,7 @@ static int p2p_grid(K kernel) {
 
 // Variant switch (experiments; defaults = measured best):
 // RSDB_P2P_RS = v4cv | v4nc | v4ld | v8cv | v8nc | v8ld | tma ;
-// RSDB_P2P_AG = pullcv | pullnc | push | tma | ce   (defaults v8cv / push: profiles/r1)
+// RSDB_P2P_AG = pullcv | pullnc | push | tma | ce   (defaults: RS tma, AG ce; profiles/r1)
 static int p2p_env(const char* name, const char* const* opts, int n, int dflt) {
   const char* e = getenv(name);
   if (!e) return dflt;
@@ -520,12 +520,12 @@ static int p2p_env(const char* name, const char* const* opts, int n, int dflt) {
 }
 static int rs_variant() {
   static const char* o[] = {"v4cv", "v4nc", "v4ld", "v8cv", "v8nc", "v8ld", "tma"};
-  static int v = p2p_env("RSDB_P2P_RS", o, 7, 3);
+  static int v = p2p_env("RSDB_P2P_RS", o, 7, 6);  // tma: 604-614 GB/s wire (profiles/r1)
   return v;
 }
 static int ag_variant() {
   static const char* o[] = {"pullcv", "pullnc", "push", "tma", "ce"};
-  static int v = p2p_env("RSDB_P2P_AG", o, 5, 2);
+  static int v = p2p_env("RSDB_P2P_AG", o, 5, 4);  // ce: 701 GB/s at N=2 and 4 (profiles/r1)
   return v;
 }
 

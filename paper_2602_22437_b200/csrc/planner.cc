@@ -249,6 +249,64 @@ bool rank_blocks(const Layout& L, int32_t rank, int64_t q, std::vector<QBlock>* 
   return true;
 }
 
+bool rank_tiles(const Layout& L, int32_t rank, const std::vector<QSpec>& specs,
+                std::vector<QTile>* out, std::string* err) {
+  out->clear();
+  if (specs.size() != L.e.size()) {
+    *err = "rank_tiles: one spec per tensor required";
+    return false;
+  }
+  const int64_t lo = rank * L.S, hi = lo + L.S;
+  for (size_t t = 0; t < L.e.size(); ++t) {
+    const int64_t l = L.l[t], e = L.e[t];
+    if (l + e <= lo || l >= hi) continue;
+    const QSpec& q = specs[t];
+    if (q.tile_rows == 0) {  // contiguous blocks
+      const int64_t n = q.tile_cols;
+      if (n < 1 || n > (int64_t{1} << 30)) {
+        *err = "rank_tiles: flat block size must be in [1, 2^30]";
+        return false;
+      }
+      for (int64_t j = l >= lo ? 0 : (lo - l) / n; j * n < e; ++j) {
+        const int64_t a = l + j * n, b = l + std::min((j + 1) * n, e);
+        if (b <= lo) continue;
+        if (a >= hi) break;
+        if (a < lo || b > hi) {
+          *err = "rank_tiles: block " + std::to_string(j) + " of tensor " + std::to_string(t) +
+                 " straddles a shard boundary";
+          return false;
+        }
+        out->push_back({a - lo, 1, int32_t(b - a), b - a});
+      }
+      continue;
+    }
+    const int64_t C = q.row_len, tr = q.tile_rows, tc = q.tile_cols;
+    if (C < 1 || tr < 1 || tc < 1 || e % C != 0 || tr * std::min<int64_t>(tc, C) > (int64_t{1} << 30)) {
+      *err = "rank_tiles: invalid tile spec for tensor " + std::to_string(t);
+      return false;
+    }
+    const int64_t Rw = e / C;
+    for (int64_t i = 0; i * tr < Rw; ++i) {
+      const int64_t rows = std::min(tr, Rw - i * tr);
+      const int64_t row_first = l + i * tr * C;
+      if (row_first + (rows - 1) * C + C <= lo) continue;  // whole tile-row below the shard
+      if (row_first >= hi) break;
+      for (int64_t j = 0; j * tc < C; ++j) {
+        const int64_t cols = std::min(tc, C - j * tc);
+        const int64_t first = row_first + j * tc, last = first + (rows - 1) * C + cols - 1;
+        if (last < lo || first >= hi) continue;
+        if (first < lo || last >= hi) {
+          *err = "rank_tiles: tile (" + std::to_string(i) + "," + std::to_string(j) + ") of tensor " +
+                 std::to_string(t) + " straddles a shard boundary";
+          return false;
+        }
+        out->push_back({first - lo, int32_t(rows), int32_t(cols), C});
+      }
+    }
+  }
+  return true;
+}
+
 std::string to_json(const Layout& L) {
   auto arr = [](const std::vector<int64_t>& v) {
     std::string s = "[";

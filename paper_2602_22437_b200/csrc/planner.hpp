@@ -42,6 +42,22 @@ std::vector<std::pair<int64_t, int64_t>> padding_intervals(const Layout& L);
 std::vector<Segment> rank_segments(const Layout& L, int32_t rank);
 bool rank_blocks(const Layout& L, int32_t rank, int64_t q, std::vector<QBlock>* out,
                  std::string* err);
+
+// Quantization block spec per tensor: tile_rows == 0 ->
+// contiguous blocks of tile_cols elements; else tile_rows x tile_cols tiles of
+// the [e / row_len, row_len] view (edge tiles smaller).
+struct QSpec {
+  int64_t row_len;
+  int32_t tile_rows;
+  int32_t tile_cols;
+};
+struct QTile {
+  int64_t off;    // first element, offset inside the shard
+  int32_t rows, cols;
+  int64_t pitch;  // elements between rows
+};
+bool rank_tiles(const Layout& L, int32_t rank, const std::vector<QSpec>& specs,
+                std::vector<QTile>* out, std::string* err);
 std::string to_json(const Layout& L);
 
 }  // namespace rsdb

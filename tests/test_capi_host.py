@@ -12,6 +12,7 @@ import random
 import re
 import time
 
+import numpy as np
 import pytest
 import torch
 
@@ -194,6 +195,43 @@ def test_arena_sizes_alignment_and_disjointness():
             assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
             # master / mq / vq share element offsets
         assert [o[3] // 4 for o in offs] == [o[4] for o in offs] == [o[5] for o in offs]
+
+
+def test_tile_tables_match_oracle():
+    """N2: 2-D quantization tiles (32x32 with 32-row granularity) --
+    C++ tables bit-exact with the oracle's; straddles rejected alike."""
+    rng = random.Random(21)
+    for _ in range(150):
+        n = rng.randint(1, 6)
+        shapes, specs, gs = [], [], []
+        for _ in range(n):
+            if rng.random() < 0.7:
+                C_ = rng.choice([16, 40, 64, 96, 130])
+                R_ = rng.choice([7, 32, 45, 64, 100])
+                tr, tc = rng.choice([(32, 32), (8, 16), (1, C_), (32, 128)])
+                shapes.append((R_, C_))
+                specs.append(("tile", C_, tr, tc))
+                gs.append(rng.choice([tr * C_, R_ * C_, 2 * tr * C_]))
+            else:
+                e = rng.randint(1, 3000)
+                q = rng.choice([64, 1024])
+                shapes.append((e,))
+                specs.append(("flat", q))
+                gs.append(min(q, e))
+        es = [int(np.prod(s)) for s in shapes]
+        gs = [min(g, e) for g, e in zip(gs, es)]
+        m = rng.randint(1, 5)
+        o = P.plan(es, gs, m, 4)
+        c = R.plan(es, gs, m, elem_bytes=4)
+        for r in range(m):
+            try:
+                ot = P.rank_tiles(o, r, specs)
+            except ValueError:
+                with pytest.raises(R.RsdbError) as ei:
+                    c.rank_tiles(r, specs)
+                assert ei.value.status == _capi.RSDB_EMISMATCH
+                continue
+            assert c.rank_tiles(r, specs) == [tuple(x) for x in ot]
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")

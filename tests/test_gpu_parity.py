@@ -147,8 +147,12 @@ def _check_adam(o, rank, blocks, gpu, ref, ins, eb, lr):
     master, mq, vq, ma, va, param_full = gpu
     S = o.S
     mask = np.zeros(S, bool)
-    for off, n in blocks:
-        mask[off:off + n] = True
+    for blk in blocks:
+        if len(blk) == 2:
+            mask[blk[0]:blk[0] + blk[1]] = True
+        else:
+            off, rows, cols, pitch = blk
+            mask[(off + np.arange(rows)[:, None] * pitch + np.arange(cols)[None, :]).ravel()] = True
     gm = f32(master)
     # params
     err = np.abs(gm - ref[0]) / (np.abs(ref[0]) + lr)
@@ -196,6 +200,47 @@ ADAM_CASES = [
 @pytest.mark.parametrize("es,q,m,eb,rank,step,warm", ADAM_CASES)
 def test_adam8_parity(es, q, m, eb, rank, step, warm):
     _adam_case(es, q, m, eb, rank, step, warm)
+
+
+TILE_CASES = [
+    # shapes, specs (per tensor), row granularity, m, rank
+    ([(96, 64), (64, 40), (130,)], [("tile", 64, 32, 32), ("tile", 40, 32, 32), ("flat", 130)], 32, 2, 1),
+    ([(2048, 512), (512,), (100, 96)], [("tile", 512, 32, 32), ("flat", 512), ("tile", 96, 32, 32)], 32, 3, 2),
+    ([(256, 128)], [("tile", 128, 128, 128)], 128, 2, 0),          # 128x128 tiles: two-pass path
+    ([(64, 30), (40, 66)], [("tile", 30, 8, 5), ("tile", 66, 8, 6)], 8, 2, 1),  # masked strided path
+]
+
+
+@pytest.mark.parametrize("shapes,specs,rows,m,rank", TILE_CASES)
+def test_adam8_tiles_parity(shapes, specs, rows, m, rank):
+    """N2: the paper's 8-bit Adam setup -- 2-D quantization tiles with row
+    sharding granularity -- vs the oracle, through rsdb_unit_create_q."""
+    es = [int(np.prod(s)) for s in shapes]
+    gs = [rows * s[-1] if len(s) == 2 else min(int(sp[1]), int(np.prod(s)))
+          for s, sp in zip(shapes, specs)]
+    o, c = _plans(es, gs, m, 2)
+    E, S = sum(es), c.S
+    tiles_o = OP.rank_tiles(o, rank, specs)
+    assert c.rank_tiles(rank, specs) == [tuple(t) for t in tiles_o]
+    p_log, g_log = logical_params(4, E), logical_grads(4, rank, E)
+    master = place_gpu(c, p_log, torch.float32)[rank * S:(rank + 1) * S].clone()
+    grad_f32 = place_gpu(c, g_log, torch.float32)
+    grad_full = torch.zeros(m * S, dtype=torch.bfloat16, device="cuda")
+    param_full = torch.zeros(m * S, dtype=torch.bfloat16, device="cuda")
+    u = R.Unit(c, rank, param_full, grad_full, grad_f32, qspec=specs)
+    nb = u.num_blocks
+    assert nb == len(tiles_o)
+    mq = H.codes_torch(4, H.STREAM_MCODE, rank * S, S, True, device="cuda")
+    vq = H.codes_torch(4, H.STREAM_VCODE, rank * S, S, False, device="cuda")
+    ma = H.absmax_torch(4, H.STREAM_ABSM, 0, nb, 14, device="cuda")
+    va = H.absmax_torch(4, H.STREAM_ABSV, 0, nb, 22, device="cuda")
+    ins = [t.cpu().numpy().copy() for t in (master, mq, vq, ma, va)]
+    cfg = R.AdamConfig()
+    R.step_8bit_adam(u, master, mq, vq, ma, va, cfg, 6)
+    torch.cuda.synchronize()
+    g_or = OD.shard(o, OD.place_logical(o, g_log.numpy()), rank)
+    ref = OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], tiles_o, OA.AdamCfg(), 6)
+    _check_adam(o, rank, tiles_o, (master, mq, vq, ma, va, param_full), ref, ins, 2, cfg.lr)
 
 
 def test_adam8_zero_gradient_block():
