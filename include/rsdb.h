@@ -92,6 +92,20 @@ rsdb_status rsdb_plan(int32_t n, const int64_t* numel, const int64_t* block,
                       int32_t world, int32_t elem_bytes, int32_t gcoll_bytes,
                       rsdb_layout** out);
 
+/* The same with one of the tensor orders of P:279 (the paper
+ * adopts the default order): 0 default, 1 sorted by sharding block size
+ * (descending, stable), 2 sorted by the caller's shape keys (descending,
+ * stable; identical shapes adjacent; keys may be NULL otherwise), 3 the best
+ * of these (smallest S, ties to the earlier order).  Tensors are placed in the
+ * chosen order; starts are still reported in input order. */
+#define RSDB_ORDER_DEFAULT 0
+#define RSDB_ORDER_BLOCK 1
+#define RSDB_ORDER_SHAPE 2
+#define RSDB_ORDER_BEST 3
+rsdb_status rsdb_plan_ordered(int32_t n, const int64_t* numel, const int64_t* block,
+                              int32_t world, int32_t elem_bytes, int32_t gcoll_bytes,
+                              int32_t ordering, const int64_t* shape_keys, rsdb_layout** out);
+
 /* A layout with caller-chosen S and starts (e.g. the even-split / FSDP1 flat
  * baseline of BASELINE config 5).  Validated against P:226-229; if
  * require_gcoll != 0 S must also be a multiple of g_coll.  EINVAL if invalid. */

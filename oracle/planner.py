@@ -231,6 +231,42 @@ def plan(es: Sequence[int], gs: Sequence[int], m: int, g_coll: int) -> Layout:
     return Layout(m, g_coll, es, gs, best, ls)
 
 
+ORDER_DEFAULT, ORDER_BLOCK, ORDER_SHAPE, ORDER_BEST = 0, 1, 2, 3
+
+
+def order_perm(es, gs, ordering: int, keys=None) -> List[int]:
+    """Tensor orders of P:279: (i) default; (ii) sorted by sharding block
+    size; (iii) sorted by tensor shape.  Readings (R18): descending,
+    stable; the shape order sorts by a caller-supplied shape key (identical
+    shapes become adjacent)."""
+    idx = list(range(len(es)))
+    if ordering == ORDER_DEFAULT:
+        return idx
+    if ordering == ORDER_BLOCK:
+        return sorted(idx, key=lambda i: -gs[i])
+    if ordering == ORDER_SHAPE:
+        if keys is None:
+            raise ValueError("shape order needs keys")
+        return sorted(idx, key=lambda i: -keys[i])
+    raise ValueError(f"unknown ordering {ordering}")
+
+
+def plan_ordered(es, gs, m, g_coll, ordering: int = ORDER_DEFAULT, keys=None) -> Layout:
+    """Algorithm 1 on a permuted tensor order; starts are returned in
+    input order.  ORDER_BEST plans all three orders and keeps the smallest S
+    (ties: the earlier order)."""
+    if ordering == ORDER_BEST:
+        cands = [plan_ordered(es, gs, m, g_coll, o, keys)
+                 for o in (ORDER_DEFAULT, ORDER_BLOCK, ORDER_SHAPE) if o != ORDER_SHAPE or keys is not None]
+        return min(cands, key=lambda L: L.S)
+    perm = order_perm(es, gs, ordering, keys)
+    lay = plan([es[i] for i in perm], [gs[i] for i in perm], m, g_coll)
+    starts = [0] * len(es)
+    for k, i in enumerate(perm):
+        starts[i] = lay.starts[k]
+    return Layout(m, g_coll, list(es), list(gs), lay.S, starts)
+
+
 # ----------------------------------------------------------------------------
 # Validator: the optimization problem's constraints (P:226-229)
 # ----------------------------------------------------------------------------

@@ -177,6 +177,20 @@ def plan(numel: Sequence[int], block: Sequence[int], world: int, elem_bytes: int
     return Layout(h.value)
 
 
+ORDER = {"default": 0, "block": 1, "shape": 2, "best": 3}
+
+
+def plan_ordered(numel: Sequence[int], block: Sequence[int], world: int, ordering="default",
+                 shape_keys: Optional[Sequence[int]] = None, elem_bytes: int = 2,
+                 gcoll_bytes: int = 16) -> Layout:
+    """Algorithm 1 on one of the tensor orders of P:279 (N4)."""
+    h = C.c_void_p()
+    keys = _c.i64_array(shape_keys) if shape_keys is not None else None
+    check(lib.rsdb_plan_ordered(len(numel), _c.i64_array(numel), _c.i64_array(block), world,
+                                elem_bytes, gcoll_bytes, ORDER[ordering], keys, C.byref(h)))
+    return Layout(h.value)
+
+
 def layout_from_starts(numel, block, world, S, starts, elem_bytes=2, gcoll_bytes=16,
                        require_gcoll=True) -> Layout:
     h = C.c_void_p()

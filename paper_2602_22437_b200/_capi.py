@@ -52,6 +52,7 @@ _SIGS = {
     "rsdb_abi_version": (i32, []),
     "rsdb_block_elems": (i32, [i32, P_i64, i32, i64, P_i64]),
     "rsdb_plan": (i32, [i32, P_i64, P_i64, i32, i32, i32, C.POINTER(vp)]),
+    "rsdb_plan_ordered": (i32, [i32, P_i64, P_i64, i32, i32, i32, i32, P_i64, C.POINTER(vp)]),
     "rsdb_layout_from_starts": (i32, [i32, P_i64, P_i64, i32, i32, i32, i64, P_i64, i32,
                                       C.POINTER(vp)]),
     "rsdb_layout_shard_numel": (i64, [vp]),

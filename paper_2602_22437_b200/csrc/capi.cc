@@ -149,6 +149,23 @@ rsdb_status rsdb_plan(int32_t n, const int64_t* numel, const int64_t* block, int
   return OK_CLEAR();
 }
 
+rsdb_status rsdb_plan_ordered(int32_t n, const int64_t* numel, const int64_t* block, int32_t world,
+                              int32_t elem_bytes, int32_t gcoll_bytes, int32_t ordering,
+                              const int64_t* shape_keys, rsdb_layout** out) {
+  if (!out || n < 0 || (n > 0 && (!numel || !block))) return fail(RSDB_EINVAL, "rsdb_plan_ordered: bad pointer or n");
+  if (ordering == 2 && n > 0 && !shape_keys) return fail(RSDB_EINVAL, "shape ordering needs keys");
+  std::vector<int64_t> e(numel, numel + n), g(block, block + n), k;
+  if (shape_keys) k.assign(shape_keys, shape_keys + n);
+  auto lay = std::make_unique<rsdb_layout>();
+  std::string err;
+  if (!rsdb::plan_ordered(e, g, world, elem_bytes, gcoll_bytes, ordering, shape_keys ? &k : nullptr,
+                          &lay->L, &err))
+    return fail(err.find("internal") != std::string::npos ? RSDB_EINTERNAL : RSDB_EINVAL, "%s",
+                err.c_str());
+  *out = lay.release();
+  return OK_CLEAR();
+}
+
 rsdb_status rsdb_layout_from_starts(int32_t n, const int64_t* numel, const int64_t* block,
                                     int32_t world, int32_t elem_bytes, int32_t gcoll_bytes,
                                     int64_t S, const int64_t* starts, int32_t require_gcoll,

@@ -176,6 +176,48 @@ bool plan(const std::vector<int64_t>& e, const std::vector<int64_t>& g, int32_t 
   return true;
 }
 
+bool plan_ordered(const std::vector<int64_t>& e, const std::vector<int64_t>& g, int32_t m,
+                  int32_t elem_bytes, int32_t gcoll_bytes, int32_t ordering,
+                  const std::vector<int64_t>* keys, Layout* out, std::string* err) {
+  if (ordering == 3) {  // best of the orders
+    Layout best;
+    bool have = false;
+    for (int32_t o = 0; o < 3; ++o) {
+      if (o == 2 && !keys) continue;
+      Layout L;
+      if (!plan_ordered(e, g, m, elem_bytes, gcoll_bytes, o, keys, &L, err)) return false;
+      if (!have || L.S < best.S) best = L, have = true;
+    }
+    *out = best;
+    return true;
+  }
+  std::vector<size_t> perm(e.size());
+  std::iota(perm.begin(), perm.end(), size_t{0});
+  if (ordering == 1) {
+    std::stable_sort(perm.begin(), perm.end(), [&](size_t a, size_t b) { return g[a] > g[b]; });
+  } else if (ordering == 2) {
+    if (!keys || keys->size() != e.size()) {
+      *err = "plan: shape ordering needs one key per tensor";
+      return false;
+    }
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](size_t a, size_t b) { return (*keys)[a] > (*keys)[b]; });
+  } else if (ordering != 0) {
+    *err = "plan: unknown ordering";
+    return false;
+  }
+  std::vector<int64_t> pe(e.size()), pg(g.size());
+  for (size_t k = 0; k < perm.size(); ++k) pe[k] = e[perm[k]], pg[k] = g[perm[k]];
+  Layout L;
+  if (!plan(pe, pg, m, elem_bytes, gcoll_bytes, &L, err)) return false;
+  Layout R = L;
+  R.e = e;
+  R.g = g;
+  for (size_t k = 0; k < perm.size(); ++k) R.l[perm[k]] = L.l[k];
+  *out = R;
+  return true;
+}
+
 int64_t count_violations(const Layout& L, bool require_gcoll) {
   int64_t v = 0;
   const int64_t cap = static_cast<int64_t>(L.m) * L.S;

@@ -33,6 +33,12 @@ bool block_elems(int32_t ndim, const int64_t* shape, int32_t kind, int64_t param
 // a2: returns false (with err) only on invalid input.
 bool plan(const std::vector<int64_t>& e, const std::vector<int64_t>& g, int32_t m,
           int32_t elem_bytes, int32_t gcoll_bytes, Layout* out, std::string* err);
+// Tensor orders of P:279: 0 default, 1 by sharding block size (desc, stable),
+// 2 by caller shape key (desc, stable), 3 best of the three (smallest S,
+// ties to the earlier order).  Starts are reported in input order.
+bool plan_ordered(const std::vector<int64_t>& e, const std::vector<int64_t>& g, int32_t m,
+                  int32_t elem_bytes, int32_t gcoll_bytes, int32_t ordering,
+                  const std::vector<int64_t>* keys, Layout* out, std::string* err);
 // CheckValidShard at one S (leftmost placement); starts filled when feasible.
 bool feasible(const std::vector<int64_t>& e, const std::vector<int64_t>& g, int32_t m, int64_t S,
               std::vector<int64_t>* starts);

@@ -197,6 +197,25 @@ def test_arena_sizes_alignment_and_disjointness():
         assert [o[3] // 4 for o in offs] == [o[4] for o in offs] == [o[5] for o in offs]
 
 
+def test_orderings_match_oracle_and_best_is_best():
+    """N4 / P:279: the three tensor orders and their best; C++ == oracle."""
+    rng = random.Random(31)
+    for _ in range(300):
+        n = rng.randint(1, 9)
+        es = [rng.randint(1, 500) for _ in range(n)]
+        gs = [rng.choice([1, e, max(1, e // 3), 7]) for e in es]
+        gs = [min(g, e) for g, e in zip(gs, es)]
+        keys = [rng.randint(0, 3) for _ in range(n)]
+        m = rng.randint(1, 6)
+        for name, o in (("default", 0), ("block", 1), ("shape", 2), ("best", 3)):
+            ol = P.plan_ordered(es, gs, m, 4, o, keys)
+            cl = R.plan_ordered(es, gs, m, name, keys, elem_bytes=4)
+            assert cl.S == ol.S and cl.starts == ol.starts, (name, es, gs, m)
+            assert cl.validate() == 0 and P.validate(ol) == []
+        best = P.plan_ordered(es, gs, m, 4, 3, keys).S
+        assert best <= min(P.plan_ordered(es, gs, m, 4, o, keys).S for o in (0, 1, 2))
+
+
 def test_tile_tables_match_oracle():
     """N2: 2-D quantization tiles (32x32 with 32-row granularity) --
     C++ tables bit-exact with the oracle's; straddles rejected alike."""
