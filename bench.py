@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: max(3, steps // 10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fuse-adam", action="store_true",
+                    help="p2p path: separate ReduceScatter kernel + one 8-bit Adam launch instead "
+                         "of the fused ReduceScatter+Adam kernel")
     ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
                     help="p2p: fused single-kernel collectives over NVLink peer memory "
                          "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
@@ -246,10 +249,12 @@ class Timers:
         return {k: len(v) for k, v in self.pairs.items()}
 
 
-def step(R, db, cfg, t, stream, timers=None, p2p=None):
+def step(R, db, cfg, t, stream, timers=None, p2p=None, fuse=False):
     """One step.  p2p=None: NCCL AllGather, cast kernel + NCCL fp32
-    ReduceScatter.  p2p given: the fused single-kernel collectives over NVLink
-    peer memory; the cast is inside the ReduceScatter kernel."""
+    ReduceScatter, one 8-bit Adam launch.  p2p given: the single-kernel
+    collectives over NVLink peer memory; the cast is inside the
+    ReduceScatter kernel, and with fuse=True the 8-bit Adam update of each
+    unit's shard is inside it too (rsdb_reduce_scatter_adam_p2p)."""
     import torch
     units = db.units
 
@@ -273,6 +278,10 @@ def step(R, db, cfg, t, stream, timers=None, p2p=None):
     else:
         for u in units:
             timed("ag", lambda u=u: R.all_gather_p2p(u, p2p, stream))
+        if fuse:  # a6 + a7 + a8: one kernel per unit, no separate optimizer launch
+            for u in reversed(units):
+                timed("rs", lambda u=u: R.reduce_scatter_adam_p2p(u, p2p, cfg, t, stream=stream))
+            return
         for u in reversed(units):
             timed("rs", lambda u=u: R.reduce_scatter_p2p(u, p2p, stream))
     timed("adam", lambda: db.step_8bit_adam(cfg, t, stream))
@@ -423,6 +432,7 @@ def run_ours(args):
     p2p = None
     if args.collectives == "p2p":
         p2p = R.P2P(comm, [arenas[0], arenas[1]])  # PARAM_FULL, GRAD_FULL arenas
+    fuse = p2p is not None and not args.no_fuse_adam
     ab = algorithmic_bytes(lays, rank)
     per_rank_bytes = ab["ag"] + ab["rs"] + ab["cast"] + ab["adam"]
     job_bytes = sum_over_ranks(per_rank_bytes, world)
@@ -432,7 +442,7 @@ def run_ours(args):
     t = 1
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            step(R, db, cfg, t, stream, p2p=p2p)
+            step(R, db, cfg, t, stream, p2p=p2p, fuse=fuse)
             t += 1
     stream.synchronize()
     # ---------------- timed region: inputs resident in HBM
@@ -446,7 +456,7 @@ def run_ours(args):
     ev0.record(stream)
     with torch.cuda.stream(stream):
         for _ in range(args.steps):
-            step(R, db, cfg, t, stream, timers, p2p=p2p)
+            step(R, db, cfg, t, stream, timers, p2p=p2p, fuse=fuse)
             t += 1
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -463,7 +473,7 @@ def run_ours(args):
     adam_ms = tot["adam"] / max(1, cnt["adam"])
     cast_ms = tot["cast"] / K
     ag_ms, rs_ms = tot["ag"] / K, tot["rs"] / K
-    adam_gbs = ab["adam"] / (adam_ms * 1e-3) / 1e9
+    adam_gbs = ab["adam"] / (adam_ms * 1e-3) / 1e9 if adam_ms > 0 else None  # fused: inside RS
     cast_gbs = ab["cast"] / (cast_ms * 1e-3) / 1e9 if cast_ms > 0 else None  # p2p: fused into RS
     # physical bytes crossing NVLink into each rank per step: AG (m-1) S 2;
     # RS (m-1) S 4 on the NCCL fp32 path, (m-1) S 2 on the fused p2p path
@@ -472,16 +482,37 @@ def run_ours(args):
     ag_bus = wire_ag / (ag_ms * 1e-3) / 1e9 if world > 1 else None
     rs_bus = wire_rs / (rs_ms * 1e-3) / 1e9 if world > 1 else None
     hbm_peak, peak_src = load_peaks()
+    # fused kernel (a6+a7+a8): HBM bytes per rank per step = every element of
+    # this rank's bf16 gradient buffer read once (by whichever rank owns it)
+    # + 14 B per owned element (fp32 master R+W, codes R+W, bf16 shard W)
+    # + 16 B of absmax per block
+    fused_hbm = (sum(l.m * l.S * 2 for l in lays) + 14 * ab["adam_elems"] + 16 * ab["adam_blocks"])
+    fused_gbs = fused_hbm / (rs_ms * 1e-3) / 1e9 if fuse else None
     # dominant kernel of the step (largest share of device time)
     names = ({"ag": "nccl_all_gather", "rs": "nccl_reduce_scatter"} if p2p is None else
-             {"ag": "ag_p2p_kernel", "rs": "rs_p2p_kernel"})
+             {"ag": "ag_p2p (copy engines)" if os.environ.get("RSDB_P2P_AG", "ce") == "ce"
+              else "ag_p2p_kernel",
+              "rs": "rs_adam_tma_kernel" if fuse else "rs_p2p_kernel"})
     # the default 8-bit Adam kernel is the TMA-pipelined one (RSDB_ADAM_KERNEL overrides)
     adam_name = ("adam8_tma_kernel" if os.environ.get("RSDB_ADAM_KERNEL", "tma3").startswith("tma")
                  else "adam8_kernel")
     shares = {adam_name: tot["adam"], "cast_scale_kernel": tot["cast"],
               names["rs"]: tot["rs"], names["ag"]: tot["ag"]}
     dom = max(shares, key=shares.get)
-    if dom in (adam_name, "cast_scale_kernel") or world == 1:
+    if fuse and dom == names["rs"]:
+        if world == 1:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": fused_gbs, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": fused_gbs / hbm_peak,
+                    "traffic": profile_traffic(dom), "peak_source": peak_src,
+                    "bytes": "16 B per owned element (bf16 grad 2, master 8, codes 4, bf16 out 2) "
+                             "+ 16 B absmax per block"}
+        else:
+            roof = {"kernel": dom, "bound": "nvlink", "achieved": rs_bus, "peak": NVLINK_PEAK_GBS,
+                    "unit": "GB/s", "frac": rs_bus / NVLINK_PEAK_GBS, "traffic": None,
+                    "bytes": "physical wire bytes into each rank per launch ((m-1) S 2)",
+                    "hbm_achieved": fused_gbs, "hbm_frac": fused_gbs / hbm_peak,
+                    "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
+    elif dom in (adam_name, "cast_scale_kernel") or world == 1:
         if dom not in (adam_name, "cast_scale_kernel"):
             dom = adam_name
         ach = adam_gbs if dom == adam_name else cast_gbs
@@ -499,7 +530,7 @@ def run_ours(args):
     # ---------------- e2e: host buffers through the C-ABI, copies inside
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p)
+        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p, fuse)
     # ---------------- CPU baseline (oracle) on rank 0
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -523,6 +554,7 @@ def run_ours(args):
             "per_op": {"adam_hbm_gbs": adam_gbs, "adam_ms_per_launch": adam_ms,
                        "cast_hbm_gbs": cast_gbs, "cast_ms_per_step": cast_ms,
                        "ag_wire_gbs": ag_bus, "rs_wire_gbs": rs_bus,
+                       "fused_rs_adam": fuse, "fused_hbm_gbs": fused_gbs,
                        "ag_wire_bytes_per_rank": wire_ag, "rs_wire_bytes_per_rank": wire_rs,
                        "ag_ms_per_step": ag_ms, "rs_ms_per_step": rs_ms,
                        "bytes_per_rank": ab},
@@ -543,7 +575,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p=None):
+def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p=None, fuse=False):
     """Same step, through the public C-ABI calls, with the step's inputs (this
     rank's bf16 gradient buffers) copied host->device from pinned memory and
     the step's result (the updated bf16 parameter shards) copied back, every
@@ -568,9 +600,12 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2
         for u in reversed(db.units):
             if p2p is None:
                 R.reduce_scatter(u, stream)
+            elif fuse:
+                R.reduce_scatter_adam_p2p(u, p2p, cfg, tt, stream=stream)
             else:
                 R.reduce_scatter_p2p(u, p2p, stream)
-        db.step_8bit_adam(cfg, tt, stream)
+        if not fuse:
+            db.step_8bit_adam(cfg, tt, stream)
         for v, h, lay in zip(views, host_p, lays):
             h.copy_(v["param_full"][rank * lay.S:(rank + 1) * lay.S], non_blocking=True)
 

@@ -283,6 +283,15 @@ void rsdb_p2p_free(rsdb_p2p*);
  * EMISMATCH otherwise. */
 rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
 rsdb_status rsdb_all_gather_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
+/* a6 + a7 + a8 in ONE kernel: the ReduceScatter of the unit's bf16 gradients
+ * over NVLink (rank-order fp32 sum x 1/m, as rsdb_reduce_scatter_p2p) feeds
+ * the block-wise 8-bit Adam update of this rank's shard directly (as
+ * rsdb_step_8bit_adam); the fp32 reduced gradient is not written (grad_f32 is
+ * left untouched).  p2p may be NULL when world == 1.  Results are identical
+ * to rsdb_reduce_scatter_p2p followed by rsdb_step_8bit_adam.  The state
+ * pointers: `st`, or NULL for a unit of a DBuffer (its arenas). */
+rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit*, rsdb_p2p* p2p_or_null, const rsdb_adam_state* st,
+                                         const rsdb_adam_cfg*, int64_t step, void* stream);
 
 /* ======================================================================== */
 /* DBuffer batched allocation: one allocation per    */

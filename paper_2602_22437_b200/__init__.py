@@ -378,6 +378,19 @@ def reduce_scatter_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
     check(lib.rsdb_reduce_scatter_p2p(unit.handle, p2p.handle, _stream(stream)))
 
 
+def reduce_scatter_adam_p2p(unit: Unit, p2p: Optional[P2P], cfg: AdamConfig, step: int,
+                            state=None, stream=None) -> None:
+    """a6 + a7 + a8 in one kernel: ReduceScatter over NVLink feeding the 8-bit
+    Adam update of this rank's shard.  state = (master, m_q, v_q, m_absmax,
+    v_absmax) tensors, or None for a unit of a DBuffer.  p2p may be None at
+    world 1."""
+    st = None
+    if state is not None:
+        st = C.byref(_c.AdamState(*[_ptr(t) for t in state]))
+    check(lib.rsdb_reduce_scatter_adam_p2p(unit.handle, p2p.handle if p2p is not None else None,
+                                           st, C.byref(cfg), step, _stream(stream)))
+
+
 def all_gather_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
     """a4 as one kernel pulling every peer's shard over NVLink."""
     check(lib.rsdb_all_gather_p2p(unit.handle, p2p.handle, _stream(stream)))

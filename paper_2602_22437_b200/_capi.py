@@ -92,6 +92,8 @@ _SIGS = {
     "rsdb_p2p_free": (None, [vp]),
     "rsdb_reduce_scatter_p2p": (i32, [vp, vp, vp]),
     "rsdb_all_gather_p2p": (i32, [vp, vp, vp]),
+    "rsdb_reduce_scatter_adam_p2p": (i32, [vp, vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64,
+                                           vp]),
     "rsdb_arena_sizes": (i32, [C.POINTER(vp), i32, i32, i64, i64, P_i64, P_i64]),
     "rsdb_dbuffer_create": (i32, [C.POINTER(vp), i32, vp, i32, i64, i64, C.POINTER(vp),
                                   C.POINTER(vp)]),

@@ -21,7 +21,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "librsdb.so")
 SOURCES = ["planner.cc", "capi.cc", "kernels.cu", "p2p.cu"]
-HEADERS = ["planner.hpp", "kernels.cuh"]
+HEADERS = ["planner.hpp", "kernels.cuh", "adam_dev.cuh"]
 
 
 def nccl_dir() -> str:

@@ -81,6 +81,8 @@ struct rsdb_unit {
   int64_t npad = 0;
   DevTable pad;     // int64 lo, hi pairs
   DevTable blocks;  // rsdb::AdamBlock, unit-relative (state = shard, grad/param = +rank*S)
+  bool has_bound_state = false;  // unit of a DBuffer: optimizer state in its arenas
+  rsdb_adam_state bound_state{};
 };
 
 struct rsdb_dbuffer {
@@ -662,6 +664,44 @@ rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   return OK_CLEAR();
 }
 
+rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state* st,
+                                         const rsdb_adam_cfg* cfg, int64_t step, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (u->L.elem_bytes != 2) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs a bf16 unit");
+  rsdb::AdamScalars s;
+  if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
+  if (!st) {
+    if (!u->has_bound_state) return fail(RSDB_EINVAL, "null state and the unit is not part of a DBuffer");
+    st = &u->bound_state;
+  }
+  if (!st->master_f32 || !st->m_q || !st->v_q || !st->m_absmax || !st->v_absmax)
+    return fail(RSDB_EINVAL, "null state pointer");
+  const int m = u->L.m;
+  if (u->L.S == 0 || u->nblocks == 0) return OK_CLEAR();
+  rsdb::P2PPtrs g{};
+  rsdb::P2PSignals sg{};
+  if (m > 1) {
+    if (!p) return fail(RSDB_EINVAL, "world > 1 needs a p2p object");
+    if (rsdb_status e = p2p_common(u, p, &sg)) return e;
+    int32_t bi = 0;
+    int64_t off = 0;
+    if (rsdb_status e = p2p_find(p, u->bufs.grad_full, int64_t(m) * u->L.S * 2, &bi, &off)) return e;
+    for (int r = 0; r < m; ++r) g.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+    ++p->epoch;
+  } else {
+    g.p[0] = u->bufs.grad_full;
+  }
+  rsdb::AdamPtrs ap{static_cast<float*>(st->master_f32), static_cast<int8_t*>(st->m_q),
+                    static_cast<uint8_t*>(st->v_q),       static_cast<float*>(st->m_absmax),
+                    static_cast<float*>(st->v_absmax),    nullptr,
+                    u->bufs.param_full,                   1};
+  const float scale = float(1.0 / double(m));
+  CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, g, m,
+                                    scale, ap, s, m > 1 ? &sg : nullptr, u->rank,
+                                    m > 1 ? p->epoch : 0, S_(stream)));
+  return OK_CLEAR();
+}
+
 // ---------------------------------------------------------------------------
 // DBuffer batched arenas
 // ---------------------------------------------------------------------------
@@ -804,6 +844,9 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
     auto unit = std::make_unique<rsdb_unit>();
     std::vector<rsdb::QTile> qb;
     if (rsdb_status st = build_unit(L, comm, rank, b, sp[size_t(u)], unit.get(), &qb)) return st;
+    unit->has_bound_state = true;
+    unit->bound_state = {at(RSDB_KIND_MASTER), at(RSDB_KIND_MQ), at(RSDB_KIND_VQ), at(RSDB_KIND_MABS),
+                         at(RSDB_KIND_VABS)};
     // arena-relative combined table: state in MASTER/MQ/VQ elements, grad in
     // GRAD_F32 elements, param in PARAM_FULL elements.
     const int64_t gbase = offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_GRAD_F32] / 4 + int64_t(rank) * L.S;

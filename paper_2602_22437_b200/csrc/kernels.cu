@@ -14,81 +14,10 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "adam_dev.cuh"
 #include "kernels.cuh"
 
 namespace rsdb {
-
-// ----------------------------------------------------------------------------
-// helpers
-// ----------------------------------------------------------------------------
-__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint2 ld_nc_v2(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
-  return r;
-}
-// coherent streaming loads for data the same kernel later overwrites
-__device__ __forceinline__ int4 ld_na_v4(const void* p) {
-  int4 r;
-  asm volatile("ld.global.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint2 ld_na_v2(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint32_t ld_na_u32(const void* p) {
-  uint32_t r;
-  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-
-// fp32 -> bf16 round-to-nearest-even, packed pair (lo = a, hi = b)
-__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-// small-integer <-> float without the quarter-rate I2F/F2I pipe:
-// 2^23 + x has x in its low mantissa bits for 0 <= x < 2^23.
-__device__ __forceinline__ float u8_to_f(uint32_t byte) {
-  return __uint_as_float(0x4B000000u | byte) - 8388608.0f;
-}
-__device__ __forceinline__ float s8_to_f(uint32_t byte) {  // two's complement byte
-  return __uint_as_float(0x4B000000u | ((byte ^ 0x80u) & 0xffu)) - 8388736.0f;
-}
-// round-to-nearest-even of |x| < 2^22 returned as int: (x + 1.5*2^23) keeps
-// the rounded integer in the mantissa (the FADD rounds RNE).
-__device__ __forceinline__ int rne_int(float x) {
-  return __float_as_int(__fadd_rn(x, 12582912.0f)) - 0x4B400000;
-}
-// .ftz approximations: v = 0 or denormal gives sqrt = 0 (the denominator is
-// then eps = 1e-8 either way); denom >= eps is never denormal.
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float r;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
 
 int num_sms() {
   static int n = 0;
@@ -246,360 +175,6 @@ cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t
   return cudaGetLastError();
 }
 
-// ----------------------------------------------------------------------------
-// a8: block-wise 8-bit Adam
-//
-// One CTA of NT threads per 2048-element quantization block; thread t owns
-// Q = 512/NT quads [4t + 4*NT*k, +4), k < Q, so every warp-wide access is one
-// contiguous span.  Two kernels share the per-block body:
-//   adam8_kernel      loads straight from global memory (16-B vectors);
-//   adam8_tma_kernel  persistent CTAs with a ring of shared-memory stages
-//                     filled by 1-D bulk TMA (cp.async.bulk, mbarrier
-//                     complete_tx): the next blocks stream in while the
-//                     current one is reduced, quantized and stored.
-// Blocks that are not full (tails) or not 16-B aligned take a masked
-// element path; blocks longer than 2048 take a two-pass path.
-//
-// Instruction diet (the kernel is HBM-bound only if it issues < ~30
-// instructions per element): codes are widened with one PRMT per byte into
-// the float 2^23 + code (exact; then FADD/FMUL = the oracle's q * fl(A/127)),
-// requantised with the magic-add RNE whose float bits carry the code in
-// their low byte (3 PRMT per 4 codes), and no clamp is needed because
-// |m| <= A  =>  |m * fl(127/A)| < 127.5 (and 0 <= v * fl(255/A) < 255.5).
-// ----------------------------------------------------------------------------
-constexpr int ADAM_TILE = 2048;  // single-pass block size
-
-struct ElemOut {
-  float p, m, v;
-};
-
-template <int NT>
-struct AdamGeom {
-  static constexpr int Q = ADAM_TILE / (4 * NT);  // quads per thread
-  static constexpr int EPT = 4 * Q;               // elements per thread
-  static constexpr int WARPS = NT / 32;
-  // element index (inside the block) of this thread's e-th element
-  __device__ static __forceinline__ int idx(int e) { return 4 * int(threadIdx.x) + (e >> 2) * 4 * NT + (e & 3); }
-  __device__ static __forceinline__ int quad(int k) { return 4 * int(threadIdx.x) + 4 * NT * k; }
-};
-
-// Steps 1-6 of the update for one element (O4); FMA-contracted.
-__device__ __forceinline__ ElemOut adam_elem(float p, float g, float mt, float vt,
-                                             const AdamScalars& s) {
-  ElemOut o;
-  o.m = fmaf(s.w1, g - mt, mt);                    // mt + (1-b1)(g - mt)     (lerp)
-  o.v = fmaf(s.b2, vt, s.w2 * (g * g));            // b2 vt + (1-b2) g^2
-  const float denom = fmaf(sqrt_approx(o.v), s.inv_bc2s, s.eps);  // sqrt(v)/bc2s + eps
-  o.p = fmaf(-s.step_size, o.m * rcp_approx(denom), p * s.c_wd);  // p*c_wd - ss*m/denom
-  return o;
-}
-
-template <int WARPS>
-__device__ __forceinline__ void block_max2(float& a, float& b, float* sa, float* sb) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
-    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sa[w] = a;
-    sb[w] = b;
-  }
-  __syncthreads();
-  a = sa[0];
-  b = sb[0];
-#pragma unroll
-  for (int i = 1; i < WARPS; ++i) {
-    a = fmaxf(a, sa[i]);
-    b = fmaxf(b, sb[i]);
-  }
-}
-
-// byte k of w as the float 2^23 + byte (exact)
-__device__ __forceinline__ float byte_f(uint32_t w, int k) {
-  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + k));
-}
-// 4 dequantized moments from a word of codes: m signed (bias 128), v unsigned
-__device__ __forceinline__ void dq4_m(uint32_t w, float sm, float* out) {
-  w ^= 0x80808080u;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) out[k] = (byte_f(w, k) - 8388736.0f) * sm;  // (code) * fl(A/127)
-}
-__device__ __forceinline__ void dq4_v(uint32_t w, float sv, float* out) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) out[k] = (byte_f(w, k) - 8388608.0f) * sv;  // (code) * fl(A/255)
-}
-// RNE code in the low byte of the float bits of x + 1.5*2^23 (|x| < 2^22)
-__device__ __forceinline__ uint32_t rne_bits(float x) {
-  return __float_as_uint(__fadd_rn(x, 12582912.0f));
-}
-__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  return __byte_perm(__byte_perm(a, b, 0x0040u), __byte_perm(c, d, 0x0040u), 0x5410u);
-}
-// scalar code (masked path), with the same rounding
-__device__ __forceinline__ uint8_t code1(float x) { return uint8_t(rne_bits(x) & 0xffu); }
-
-template <int NT>
-struct BlockRegs {
-  float p[AdamGeom<NT>::EPT], g[AdamGeom<NT>::EPT], mt[AdamGeom<NT>::EPT], vt[AdamGeom<NT>::EPT];
-};
-
-// full, 16-B aligned block from 4 element arrays (global or shared)
-template <int NT, bool GLOBAL>
-__device__ __forceinline__ void load_fast(BlockRegs<NT>& r, const float* master, const float* grad,
-                                          const void* mq, const void* vq, float sm, float sv) {
-  using G = AdamGeom<NT>;
-  int4 pv[G::Q], gv[G::Q];
-  uint32_t cm[G::Q], cv[G::Q];
-#pragma unroll
-  for (int k = 0; k < G::Q; ++k) {
-    const int a = G::quad(k);
-    if constexpr (GLOBAL) {
-      pv[k] = ld_na_v4(master + a);
-      gv[k] = ld_nc_v4(grad + a);
-      cm[k] = ld_na_u32(static_cast<const uint8_t*>(mq) + a);
-      cv[k] = ld_na_u32(static_cast<const uint8_t*>(vq) + a);
-    } else {
-      pv[k] = *reinterpret_cast<const int4*>(master + a);
-      gv[k] = *reinterpret_cast<const int4*>(grad + a);
-      cm[k] = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(mq) + a);
-      cv[k] = *reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(vq) + a);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < G::Q; ++k) {
-    r.p[4 * k + 0] = __int_as_float(pv[k].x);
-    r.p[4 * k + 1] = __int_as_float(pv[k].y);
-    r.p[4 * k + 2] = __int_as_float(pv[k].z);
-    r.p[4 * k + 3] = __int_as_float(pv[k].w);
-    r.g[4 * k + 0] = __int_as_float(gv[k].x);
-    r.g[4 * k + 1] = __int_as_float(gv[k].y);
-    r.g[4 * k + 2] = __int_as_float(gv[k].z);
-    r.g[4 * k + 3] = __int_as_float(gv[k].w);
-    dq4_m(cm[k], sm, &r.mt[4 * k]);
-    dq4_v(cv[k], sv, &r.vt[4 * k]);
-  }
-}
-
-// element i of a block laid out as rows of `cols` elements `pitch` apart
-__device__ __forceinline__ int64_t blk_off(const AdamBlock& b, int i) {
-  const int row = i / b.cols;
-  return int64_t(row) * b.pitch + (i - row * b.cols);
-}
-
-// masked, strided element loads (tails, misaligned blocks, odd tiles)
-template <int NT>
-__device__ __forceinline__ void load_generic(BlockRegs<NT>& r, const AdamBlock& blk,
-                                             const AdamPtrs& P, float sm, float sv) {
-  using G = AdamGeom<NT>;
-  const float* master = P.master + blk.state_off;
-  const float* grad = P.grad + blk.grad_off;
-  const int8_t* mq = P.mq + blk.state_off;
-  const uint8_t* vq = P.vq + blk.state_off;
-#pragma unroll
-  for (int e = 0; e < G::EPT; ++e) {
-    const int i = G::idx(e);
-    if (i < blk.len) {
-      const int64_t o = blk_off(blk, i);
-      r.p[e] = master[o];
-      r.g[e] = grad[o];
-      r.mt[e] = (byte_f(uint32_t(uint8_t(mq[o])) ^ 0x80u, 0) - 8388736.0f) * sm;
-      r.vt[e] = (byte_f(uint32_t(vq[o]), 0) - 8388608.0f) * sv;
-    } else {
-      r.p[e] = r.g[e] = r.mt[e] = r.vt[e] = 0.f;
-    }
-  }
-}
-
-// 2-D tile with cols % 4 == 0 (quads never cross a row) and 16-B aligned rows:
-// every quad is one 16-B vector at its own row address (N2, 32x32 tiles)
-template <int NT>
-__device__ __forceinline__ void load_tile(BlockRegs<NT>& r, const AdamBlock& blk, const AdamPtrs& P,
-                                          float sm, float sv) {
-  using G = AdamGeom<NT>;
-  int4 pv[G::Q], gv[G::Q];
-  uint32_t cm[G::Q], cv[G::Q];
-#pragma unroll
-  for (int k = 0; k < G::Q; ++k) {
-    const int e0 = G::quad(k);
-    if (e0 < blk.len) {
-      const int64_t a = blk_off(blk, e0);
-      pv[k] = ld_na_v4(P.master + blk.state_off + a);
-      gv[k] = ld_nc_v4(P.grad + blk.grad_off + a);
-      cm[k] = ld_na_u32(P.mq + blk.state_off + a);
-      cv[k] = ld_na_u32(P.vq + blk.state_off + a);
-    } else {
-      pv[k] = gv[k] = make_int4(0, 0, 0, 0);
-      cm[k] = 0x80808080u;  // decodes to m = 0
-      cv[k] = 0u;
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < G::Q; ++k) {
-    r.p[4 * k + 0] = __int_as_float(pv[k].x);
-    r.p[4 * k + 1] = __int_as_float(pv[k].y);
-    r.p[4 * k + 2] = __int_as_float(pv[k].z);
-    r.p[4 * k + 3] = __int_as_float(pv[k].w);
-    r.g[4 * k + 0] = __int_as_float(gv[k].x);
-    r.g[4 * k + 1] = __int_as_float(gv[k].y);
-    r.g[4 * k + 2] = __int_as_float(gv[k].z);
-    r.g[4 * k + 3] = __int_as_float(gv[k].w);
-    dq4_m(cm[k], sm, &r.mt[4 * k]);
-    dq4_v(cv[k], sv, &r.vt[4 * k]);
-  }
-}
-
-// Update + block absmax + (hook) + requantize + stores, for a block held in
-// registers.  `after_reduce` runs once every thread of the CTA has its inputs
-// in registers (right after the absmax reduction's barrier).
-// MODE 0: masked strided elements; 1: full contiguous 2048 block; 2: 2-D tile quads
-template <int NT, bool PARAM_BF16, int MODE, typename Hook>
-__device__ __forceinline__ void adam_block_tail(BlockRegs<NT>& r, const AdamBlock& blk,
-                                                const AdamPtrs& P, const AdamScalars& s,
-                                                float* red_m, float* red_v, Hook after_reduce) {
-  using G = AdamGeom<NT>;
-  const int len = blk.len;
-  float m[G::EPT], v[G::EPT];
-  float am = 0.f, av = 0.f;
-#pragma unroll
-  for (int e = 0; e < G::EPT; ++e) {
-    const ElemOut o = adam_elem(r.p[e], r.g[e], r.mt[e], r.vt[e], s);
-    const bool live = MODE == 1 || G::idx(e) < len;
-    r.p[e] = o.p;
-    m[e] = live ? o.m : 0.f;
-    v[e] = live ? o.v : 0.f;
-    am = fmaxf(am, fabsf(m[e]));
-    av = fmaxf(av, v[e]);
-  }
-  block_max2<G::WARPS>(am, av, red_m, red_v);
-  after_reduce();
-  const float im = am > 0.f ? 127.0f / am : 0.f;
-  const float iv = av > 0.f ? 255.0f / av : 0.f;
-  float* __restrict__ master = P.master + blk.state_off;
-  uint8_t* __restrict__ mq = reinterpret_cast<uint8_t*>(P.mq) + blk.state_off;
-  uint8_t* __restrict__ vq = P.vq + blk.state_off;
-  if constexpr (MODE != 0) {
-#pragma unroll
-    for (int k = 0; k < G::Q; ++k) {
-      int64_t a = G::quad(k);
-      if constexpr (MODE == 2) {
-        if (a >= len) continue;
-        a = blk_off(blk, int(a));
-      }
-      const float* pk = &r.p[4 * k];
-      const float* mk = &m[4 * k];
-      const float* vk = &v[4 * k];
-      *reinterpret_cast<float4*>(master + a) = make_float4(pk[0], pk[1], pk[2], pk[3]);
-      *reinterpret_cast<uint32_t*>(mq + a) = pack4(rne_bits(mk[0] * im), rne_bits(mk[1] * im),
-                                                   rne_bits(mk[2] * im), rne_bits(mk[3] * im));
-      *reinterpret_cast<uint32_t*>(vq + a) = pack4(rne_bits(vk[0] * iv), rne_bits(vk[1] * iv),
-                                                   rne_bits(vk[2] * iv), rne_bits(vk[3] * iv));
-      if constexpr (PARAM_BF16) {
-        uint16_t* pp = static_cast<uint16_t*>(P.param) + blk.param_off;
-        *reinterpret_cast<uint2*>(pp + a) =
-            make_uint2(pack_bf16x2(pk[0], pk[1]), pack_bf16x2(pk[2], pk[3]));
-      } else {
-        float* pp = static_cast<float*>(P.param) + blk.param_off;
-        *reinterpret_cast<float4*>(pp + a) = make_float4(pk[0], pk[1], pk[2], pk[3]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < G::EPT; ++e) {
-      const int i = G::idx(e);
-      if (i < len) {
-        const int64_t o = blk_off(blk, i);
-        master[o] = r.p[e];
-        mq[o] = code1(m[e] * im);
-        vq[o] = code1(v[e] * iv);
-        if constexpr (PARAM_BF16)
-          static_cast<__nv_bfloat16*>(P.param)[blk.param_off + o] = __float2bfloat16_rn(r.p[e]);
-        else
-          static_cast<float*>(P.param)[blk.param_off + o] = r.p[e];
-      }
-    }
-  }
-  if (threadIdx.x == 0) {
-    P.mabs[blk.slot] = am;
-    P.vabs[blk.slot] = av;
-  }
-}
-
-// blocks longer than 2048: pass 1 computes the absmax, pass 2 recomputes and stores
-template <int NT, bool PARAM_BF16, typename Hook>
-__device__ __forceinline__ void adam_block_two_pass(const AdamBlock& blk, float sm, float sv,
-                                                    const AdamPtrs& P, const AdamScalars& s,
-                                                    float* red_m, float* red_v, Hook after_reduce) {
-  float* __restrict__ master = P.master + blk.state_off;
-  uint8_t* __restrict__ mq = reinterpret_cast<uint8_t*>(P.mq) + blk.state_off;
-  uint8_t* __restrict__ vq = P.vq + blk.state_off;
-  const float* __restrict__ grad = P.grad + blk.grad_off;
-  auto mt_of = [&](int64_t o) { return (byte_f(uint32_t(mq[o]) ^ 0x80u, 0) - 8388736.0f) * sm; };
-  auto vt_of = [&](int64_t o) { return (byte_f(uint32_t(vq[o]), 0) - 8388608.0f) * sv; };
-  float am = 0.f, av = 0.f;
-  for (int i = threadIdx.x; i < blk.len; i += NT) {
-    const int64_t o = blk_off(blk, i);
-    const ElemOut e = adam_elem(0.f, grad[o], mt_of(o), vt_of(o), s);
-    am = fmaxf(am, fabsf(e.m));
-    av = fmaxf(av, e.v);
-  }
-  block_max2<AdamGeom<NT>::WARPS>(am, av, red_m, red_v);
-  after_reduce();
-  const float im = am > 0.f ? 127.0f / am : 0.f;
-  const float iv = av > 0.f ? 255.0f / av : 0.f;
-  // each thread rewrites exactly the elements it read in pass 1: no hazard
-  for (int i = threadIdx.x; i < blk.len; i += NT) {
-    const int64_t q = blk_off(blk, i);
-    const ElemOut o = adam_elem(master[q], grad[q], mt_of(q), vt_of(q), s);
-    master[q] = o.p;
-    mq[q] = code1(o.m * im);
-    vq[q] = code1(o.v * iv);
-    if constexpr (PARAM_BF16)
-      static_cast<__nv_bfloat16*>(P.param)[blk.param_off + q] = __float2bfloat16_rn(o.p);
-    else
-      static_cast<float*>(P.param)[blk.param_off + q] = o.p;
-  }
-  if (threadIdx.x == 0) {
-    P.mabs[blk.slot] = am;
-    P.vabs[blk.slot] = av;
-  }
-}
-
-__device__ __forceinline__ bool adam_fast(const AdamBlock& b) {
-  return b.len == ADAM_TILE && b.cols == b.len && ((b.state_off | b.grad_off | b.param_off) & 3) == 0;
-}
-__device__ __forceinline__ bool adam_tile_fast(const AdamBlock& b) {
-  return b.cols != b.len && ((b.cols | b.pitch) & 3) == 0 &&
-         ((b.state_off | b.grad_off | b.param_off) & 3) == 0;
-}
-
-struct NoHook {
-  __device__ void operator()() const {}
-};
-
-template <int NT, bool PARAM_BF16>
-__device__ __forceinline__ void adam_block_global(const AdamBlock& blk, const AdamPtrs& P,
-                                                  const AdamScalars& s, float sm, float sv,
-                                                  float* rm, float* rv) {
-  if (blk.len <= ADAM_TILE) {
-    BlockRegs<NT> r;
-    if (adam_fast(blk)) {
-      load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off, P.mq + blk.state_off,
-                          P.vq + blk.state_off, sm, sv);
-      adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, NoHook{});
-    } else if (adam_tile_fast(blk)) {
-      load_tile<NT>(r, blk, P, sm, sv);
-      adam_block_tail<NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, NoHook{});
-    } else {
-      load_generic<NT>(r, blk, P, sm, sv);
-      adam_block_tail<NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, NoHook{});
-    }
-  } else {
-    adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, NoHook{});
-  }
-}
-
 template <int NT, bool PARAM_BF16>
 __global__ void __launch_bounds__(NT) adam8_kernel(const AdamBlock* __restrict__ tbl,
                                                    int64_t nblocks, AdamPtrs P, AdamScalars s) {
@@ -613,48 +188,6 @@ __global__ void __launch_bounds__(NT) adam8_kernel(const AdamBlock* __restrict__
     // ahead (every block has a barrier), so no trailing __syncthreads.
     adam_block_global<NT, PARAM_BF16>(blk, P, s, sm, sv, red_m[it & 1], red_v[it & 1]);
   }
-}
-
-// ---------------- TMA-pipelined variant ----------------
-struct __align__(128) AdamStage {
-  float p[ADAM_TILE];
-  float g[ADAM_TILE];
-  uint8_t mq[ADAM_TILE];
-  uint8_t vq[ADAM_TILE];
-};
-constexpr uint32_t ADAM_STAGE_TX = sizeof(float) * ADAM_TILE * 2 + ADAM_TILE * 2;  // 20480
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n"
-      "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // bulk copies need 16-B aligned global addresses: codes at state_off % 16

@@ -73,5 +73,10 @@ cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank,
                           cudaStream_t st);
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
+// a6 + a7 + a8 fused: ReduceScatter of the bf16 gradients over NVLink and the
+// 8-bit Adam update of the local shard in one kernel (sg may be null iff m == 1).
+cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
+                               float scale, const AdamPtrs& P, const AdamScalars& s,
+                               const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st);
 
 }  // namespace rsdb

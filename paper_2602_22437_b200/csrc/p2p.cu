@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "adam_dev.cuh"
 #include "kernels.cuh"
 
 namespace rsdb {
@@ -600,6 +601,184 @@ cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int 
     return ag_p2p_m<M>(params, bytes_S, rank, sg, epoch, st);
     AG_CASE(1) AG_CASE(2) AG_CASE(3) AG_CASE(4) AG_CASE(5) AG_CASE(6) AG_CASE(7) AG_CASE(8)
 #undef AG_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------- ReduceScatter fused with the 8-bit Adam step ----------------
+// a6 + a7 + a8 in ONE kernel over NVLink: for every quantization block of
+// this rank's shard, one thread bulk-loads the block's bf16 gradients from all
+// M ranks (TMA over the IPC mappings) plus the local fp32 master and the m / v
+// codes into a shared-memory stage; the CTA sums the M gradients in rank
+// order in fp32 (bit-identical to rs_p2p / the oracle's rank-order sum) and
+// runs the 8-bit Adam update on the block.  The fp32 reduced gradient never
+// reaches HBM (-8 B per owned element) and the optimizer's HBM traffic
+// overlaps the NVLink-bound reduction.  M = 1 (world 1): the cast + Adam.
+constexpr int RSA_NT = 128;
+
+template <int M>
+struct RsaGeom {
+  static constexpr int STAGES = M <= 4 ? 3 : 2;
+  static constexpr int G_BYTES = M * ADAM_TILE * 2;
+  static constexpr int STAGE_BYTES = G_BYTES + ADAM_TILE * 4 + ADAM_TILE * 2;
+};
+
+__device__ __forceinline__ bool rsa_fits(const AdamBlock& b) {
+  return b.cols == b.len && b.len <= ADAM_TILE && (b.len & 15) == 0 && (b.state_off & 15) == 0 &&
+         (b.grad_off & 7) == 0 && (b.param_off & 3) == 0;
+}
+
+template <int M, bool PARAM_BF16, bool SYNC>
+__global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __restrict__ tbl,
+                                                            int64_t nblocks, P2PPtrs grads,
+                                                            float scale, AdamPtrs P, AdamScalars s,
+                                                            P2PSignals sg, int rank, uint64_t epoch) {
+  using Gm = RsaGeom<M>;
+  using G = AdamGeom<RSA_NT>;
+  extern __shared__ __align__(128) uint8_t rsa_smem[];
+  __shared__ __align__(8) uint64_t full[Gm::STAGES];
+  __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
+  if constexpr (SYNC) p2p_start(sg, rank, M, epoch);
+  auto issue = [&](int64_t b, int st) {
+    const AdamBlock nb = tbl[b];
+    uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
+    if (rsa_fits(nb)) {
+      const uint32_t L = uint32_t(nb.len);
+      tbar_expect(&full[st], L * (2 * M + 6));
+#pragma unroll
+      for (int r = 0; r < M; ++r)
+        tma_g2s(S + r * ADAM_TILE * 2, static_cast<const uint16_t*>(grads.p[r]) + nb.grad_off, L * 2,
+                &full[st]);
+      tma_g2s(S + Gm::G_BYTES, P.master + nb.state_off, L * 4, &full[st]);
+      tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + nb.state_off, L, &full[st]);
+      tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + nb.state_off, L, &full[st]);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[st])) : "memory");
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < Gm::STAGES; ++st) tbar_init(&full[st]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < Gm::STAGES; ++st) {
+      const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
+      if (b < nblocks) issue(b, st);
+    }
+  }
+  __syncthreads();
+  int it = 0;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+    const int st = it % Gm::STAGES;
+    const AdamBlock blk = tbl[b];
+    const float sm = P.mabs[blk.slot] / 127.0f;
+    const float sv = P.vabs[blk.slot] / 255.0f;
+    float* rm = red_m[it & 1];
+    float* rv = red_v[it & 1];
+    auto refill = [&]() {
+      if (threadIdx.x == 0) {
+        const int64_t nb = b + int64_t(Gm::STAGES) * gridDim.x;
+        if (nb < nblocks) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(nb, st);
+        }
+      }
+    };
+    tbar_wait(&full[st], uint32_t(it / Gm::STAGES) & 1u);
+    BlockRegs<RSA_NT> r;
+    if (rsa_fits(blk)) {
+      const uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
+      const uint16_t* Sg = reinterpret_cast<const uint16_t*>(S);
+      const float* Sp = reinterpret_cast<const float*>(S + Gm::G_BYTES);
+      const uint8_t* Sm = S + Gm::G_BYTES + ADAM_TILE * 4;
+      const uint8_t* Sv = S + Gm::G_BYTES + ADAM_TILE * 5;
+#pragma unroll
+      for (int k = 0; k < G::Q; ++k) {
+        const int e0 = G::quad(k);
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t cm = 0x80808080u, cv = 0u;  // decode to m = v = 0 for masked quads
+        if (e0 < blk.len) {
+#pragma unroll
+          for (int q = 0; q < M; ++q) {  // rank order
+            const uint2 w = *reinterpret_cast<const uint2*>(Sg + q * ADAM_TILE + e0);
+            a[0] += __uint_as_float(w.x << 16) * scale;
+            a[1] += __uint_as_float(w.x & 0xffff0000u) * scale;
+            a[2] += __uint_as_float(w.y << 16) * scale;
+            a[3] += __uint_as_float(w.y & 0xffff0000u) * scale;
+          }
+          pv = *reinterpret_cast<const float4*>(Sp + e0);
+          cm = *reinterpret_cast<const uint32_t*>(Sm + e0);
+          cv = *reinterpret_cast<const uint32_t*>(Sv + e0);
+        }
+        r.g[4 * k + 0] = a[0], r.g[4 * k + 1] = a[1], r.g[4 * k + 2] = a[2], r.g[4 * k + 3] = a[3];
+        r.p[4 * k + 0] = pv.x, r.p[4 * k + 1] = pv.y, r.p[4 * k + 2] = pv.z, r.p[4 * k + 3] = pv.w;
+        dq4_m(cm, sm, &r.mt[4 * k]);
+        dq4_v(cv, sv, &r.vt[4 * k]);
+      }
+      if (blk.len == ADAM_TILE)
+        adam_block_tail<RSA_NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
+      else
+        adam_block_tail<RSA_NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill);
+    } else {
+      // generic: gradients summed straight from the peers' memory, masked & strided
+#pragma unroll
+      for (int e = 0; e < G::EPT; ++e) {
+        const int i = G::idx(e);
+        float acc = 0.f;
+        if (i < blk.len && blk.len <= ADAM_TILE) {
+          const int64_t o = blk_off(blk, i);
+#pragma unroll
+          for (int q = 0; q < M; ++q)
+            acc += __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16) * scale;
+          r.p[e] = P.master[blk.state_off + o];
+          r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.state_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
+          r.vt[e] = (byte_f(uint32_t(P.vq[blk.state_off + o]), 0) - 8388608.0f) * sv;
+        } else {
+          r.p[e] = r.mt[e] = r.vt[e] = 0.f;
+        }
+        r.g[e] = acc;
+      }
+      adam_block_tail<RSA_NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, refill);
+    }
+  }
+  if constexpr (SYNC) p2p_done(sg, rank, M, epoch);
+}
+
+template <int M, bool BF, bool SYNC>
+static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, float scale,
+                               const AdamPtrs& P, const AdamScalars& s, const P2PSignals& sg, int rank,
+                               uint64_t epoch, cudaStream_t st) {
+  const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * RsaGeom<M>::STAGES;
+  static const int grid = [&] {
+    cudaFuncSetAttribute(rs_adam_tma_kernel<M, BF, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, BF, SYNC>, RSA_NT, smem);
+    return num_sms() * (b < 1 ? 1 : b);
+  }();
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, grid));
+  rs_adam_tma_kernel<M, BF, SYNC><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, scale, P, s, sg,
+                                                                rank, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
+                               float scale, const AdamPtrs& P, const AdamScalars& s,
+                               const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st) {
+  const bool bf = P.param_bf16;
+  if (m == 1) {
+    P2PSignals none{};
+    return bf ? rs_adam_mbs<1, true, false>(tbl, nblocks, grads, scale, P, s, none, rank, epoch, st)
+              : rs_adam_mbs<1, false, false>(tbl, nblocks, grads, scale, P, s, none, rank, epoch, st);
+  }
+  if (!sg) return cudaErrorInvalidValue;
+  switch (m) {
+#define RSA_CASE(MM)                                                                                 \
+  case MM:                                                                                           \
+    return bf ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, scale, P, s, *sg, rank, epoch, st)  \
+              : rs_adam_mbs<MM, false, true>(tbl, nblocks, grads, scale, P, s, *sg, rank, epoch, st);
+    RSA_CASE(2) RSA_CASE(3) RSA_CASE(4) RSA_CASE(5) RSA_CASE(6) RSA_CASE(7) RSA_CASE(8)
+#undef RSA_CASE
     default:
       return cudaErrorInvalidValue;
   }

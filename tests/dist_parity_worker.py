@@ -118,7 +118,19 @@ def main():
         vq = torch.zeros(S, dtype=torch.uint8, device="cuda")
         ma = torch.zeros(nb, dtype=torch.float32, device="cuda")
         va = torch.zeros(nb, dtype=torch.float32, device="cuda")
+        fused_in = [t.clone() for t in (master, mq, vq, ma, va)]
         R.step_8bit_adam(u, master, mq, vq, ma, va, R.AdamConfig(), 1)
+        if eb == 2:
+            # a6 + a7 + a8 in one kernel over NVLink: bit-identical to RS -> Adam
+            p2p = R.P2P(comm, [param_full, grad_full])
+            R.reduce_scatter_adam_p2p(u, p2p, R.AdamConfig(), 1, state=fused_in)
+            torch.cuda.synchronize()
+            for a, b in zip(fused_in, (master, mq, vq, ma, va)):
+                if not torch.equal(a.view(torch.uint8), b.view(torch.uint8)):
+                    ok = False
+                    msgs.append(f"{name}: fused RS+Adam differs from RS then Adam")
+                    break
+            p2p.close()
         R.all_gather(u)
         torch.cuda.synchronize()
         ref_full = []

@@ -243,6 +243,40 @@ def test_adam8_tiles_parity(shapes, specs, rows, m, rank):
     _check_adam(o, rank, tiles_o, (master, mq, vq, ma, va, param_full), ref, ins, 2, cfg.lr)
 
 
+@pytest.mark.parametrize("es", [[5000 * 4, 2048 * 3, 256, 4096 + 16], [256 * 128, 256] * 3,
+                                [77, 5000, 2048 * 2 + 3]])
+def test_fused_rs_adam_world1(es):
+    """a6 + a7 + a8 in one kernel at world 1 (= cast + 8-bit Adam), vs the
+    oracle's group op followed by its Adam step; grad_f32 is not written."""
+    q = 2048
+    gs = [min(q, e) for e in es]
+    o, c = _plans(es, gs, 1, 2)
+    S, E = c.S, sum(es)
+    comm = R.Comm(R.Comm.unique_id(), 1, 0, 0)
+    p_log, g_log = logical_params(8, E), logical_grads(8, 0, E)
+    grad_full = place_gpu(c, g_log, torch.bfloat16)
+    grad_f32 = torch.full((S,), float("nan"), dtype=torch.float32, device="cuda")
+    param_full = torch.zeros(S, dtype=torch.bfloat16, device="cuda")
+    master = place_gpu(c, p_log, torch.float32).clone()
+    u = R.Unit(c, 0, param_full, grad_full, grad_f32, qblock=q, comm=comm)
+    nb = u.num_blocks
+    mq = H.codes_torch(8, H.STREAM_MCODE, 0, S, True, device="cuda")
+    vq = H.codes_torch(8, H.STREAM_VCODE, 0, S, False, device="cuda")
+    ma = H.absmax_torch(8, H.STREAM_ABSM, 0, nb, 14, device="cuda")
+    va = H.absmax_torch(8, H.STREAM_ABSV, 0, nb, 22, device="cuda")
+    ins = [t.cpu().numpy().copy() for t in (master, mq, vq, ma, va)]
+    cfg = R.AdamConfig()
+    R.reduce_scatter_adam_p2p(u, None, cfg, 3, state=(master, mq, vq, ma, va))
+    torch.cuda.synchronize()
+    assert torch.isnan(grad_f32).all()
+    g_or = OD.grouped_cast_scale(o, OD.to_bf16_rne(OD.place_logical(o, g_log.numpy())), True)
+    blocks = OP.rank_blocks(o, 0, q)
+    ref = OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], blocks, OA.AdamCfg(), 3)
+    _check_adam(o, 0, blocks, (master, mq, vq, ma, va, param_full), ref, ins, 2, cfg.lr)
+    del u
+    comm.close()
+
+
 def test_adam8_zero_gradient_block():
     """Zero state + zero gradient: m = v = 0 -> absmax 0 -> codes 0."""
     _adam_case([4096, 2048, 300], 2048, 1, 2, 0, 1, False, zero_grad_tensor=1)
