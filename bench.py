@@ -14,14 +14,21 @@ Synthetic, seeded inputs (synth/), random-init weights.
 One step (all per-step rows of SURVEY §8(a); a1-a3 planning is one-time at
 init, P:491, reported as plan_ms):
     for unit in units:            a4  AllGather (in place, zero-copy views a5)
-    for unit in reversed(units):  a6  fused cast bf16->fp32 x 1/m, padding 0
-                                  a7  ReduceScatter fp32 (in place)
-    one launch over every shard:  a8  block-wise 8-bit Adam (+ bf16 shard)
+    for unit in reversed(units):  a6  cast bf16->fp32 x 1/m, padding 0
+                                  a7  ReduceScatter
+                                  a8  block-wise 8-bit Adam (+ bf16 shard)
+  --collectives p2p (default): per unit ONE kernel over NVLink peer memory does
+      a6+a7+a8 (rsdb_reduce_scatter_adam_p2p; --no-fuse-adam: a6+a7 kernel per
+      unit, then one a8 launch over every shard); AllGather = rsdb_all_gather_p2p.
+  --collectives nccl: ncclAllGather; cast kernel + ncclReduceScatter (fp32) per
+      unit; one a8 launch over every shard.
 
-value = whole-job algorithmic GB/s of the step = sum over ranks of
-        [AG bus bytes + RS bus bytes + cast bytes + Adam bytes] / max-rank time
-        (per-rank bytes: AG (m-1) S 2, RS (m-1) S 4, cast m S 6, Adam 18 per
-        owned element + 16 per block), per unit.
+value = whole-job algorithmic GB/s of the step, with the workload's bytes fixed
+        by SURVEY §8(d) independent of the implementation = sum over ranks of
+        [AG (m-1) S 2 + RS (m-1) S 4 + cast m S 6 + Adam 18 per owned element
+        + 16 per block] (summed over units) / max-rank step time.  The fused
+        path moves fewer physical bytes for the same work; per_op and
+        roofline report physical rates.
 """
 from __future__ import annotations
 
@@ -57,6 +64,9 @@ def parse():
     ap.add_argument("--no-fuse-adam", action="store_true",
                     help="p2p path: separate ReduceScatter kernel + one 8-bit Adam launch instead "
                          "of the fused ReduceScatter+Adam kernel")
+    ap.add_argument("--fused-scope", choices=["unit", "dbuffer"], default=None,
+                    help="fused RS+Adam per unit (FSDP backward order) or one launch over the "
+                         "whole DBuffer; default: dbuffer at world 1, unit otherwise")
     ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
                     help="p2p: fused single-kernel collectives over NVLink peer memory "
                          "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
@@ -278,7 +288,11 @@ def step(R, db, cfg, t, stream, timers=None, p2p=None, fuse=False):
     else:
         for u in units:
             timed("ag", lambda u=u: R.all_gather_p2p(u, p2p, stream))
-        if fuse:  # a6 + a7 + a8: one kernel per unit, no separate optimizer launch
+        if fuse == "dbuffer":  # a6 + a7 + a8 for every unit in ONE launch
+            timed("rs", lambda: db.reduce_scatter_adam(cfg, t, p2p if db.units[0].layout.m > 1
+                                                       else None, stream))
+            return
+        if fuse:  # a6 + a7 + a8: one kernel per unit (FSDP backward order), no optimizer launch
             for u in reversed(units):
                 timed("rs", lambda u=u: R.reduce_scatter_adam_p2p(u, p2p, cfg, t, stream=stream))
             return
@@ -433,6 +447,9 @@ def run_ours(args):
     if args.collectives == "p2p":
         p2p = R.P2P(comm, [arenas[0], arenas[1]])  # PARAM_FULL, GRAD_FULL arenas
     fuse = p2p is not None and not args.no_fuse_adam
+    if fuse:
+        scope = args.fused_scope or ("dbuffer" if world == 1 else "unit")
+        fuse = "dbuffer" if scope == "dbuffer" else True
     ab = algorithmic_bytes(lays, rank)
     per_rank_bytes = ab["ag"] + ab["rs"] + ab["cast"] + ab["adam"]
     job_bytes = sum_over_ranks(per_rank_bytes, world)
@@ -597,13 +614,16 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2
                 R.all_gather(u, stream)
             else:
                 R.all_gather_p2p(u, p2p, stream)
-        for u in reversed(db.units):
-            if p2p is None:
-                R.reduce_scatter(u, stream)
-            elif fuse:
-                R.reduce_scatter_adam_p2p(u, p2p, cfg, tt, stream=stream)
-            else:
-                R.reduce_scatter_p2p(u, p2p, stream)
+        if fuse == "dbuffer":
+            db.reduce_scatter_adam(cfg, tt, p2p if world > 1 else None, stream)
+        else:
+            for u in reversed(db.units):
+                if p2p is None:
+                    R.reduce_scatter(u, stream)
+                elif fuse:
+                    R.reduce_scatter_adam_p2p(u, p2p, cfg, tt, stream=stream)
+                else:
+                    R.reduce_scatter_p2p(u, p2p, stream)
         if not fuse:
             db.step_8bit_adam(cfg, tt, stream)
         for v, h, lay in zip(views, host_p, lays):

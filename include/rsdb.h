@@ -334,6 +334,12 @@ int64_t rsdb_dbuffer_num_blocks(const rsdb_dbuffer*);
 /* a8 over every unit's shard in one kernel launch. */
 rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer*, const rsdb_adam_cfg*, int64_t step,
                                         void* stream);
+/* a6 + a7 + a8 for EVERY unit of the DBuffer in ONE kernel launch (the fused
+ * ReduceScatter + 8-bit Adam of rsdb_reduce_scatter_adam_p2p over all units'
+ * blocks; at world 1 the cast + Adam over the whole model).  Requires bf16
+ * units; p2p (NULL iff world 1) must map this DBuffer's GRAD_FULL arena. */
+rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer*, rsdb_p2p* p2p_or_null,
+                                             const rsdb_adam_cfg*, int64_t step, void* stream);
 /* Grouped zero of every unit's gradient buffer ("zero"). */
 rsdb_status rsdb_dbuffer_zero_grads(rsdb_dbuffer*, void* stream);
 void rsdb_dbuffer_free(rsdb_dbuffer*);

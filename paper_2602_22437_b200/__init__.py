@@ -459,6 +459,12 @@ class DBuffer:
     def step_8bit_adam(self, cfg: AdamConfig, step: int, stream=None) -> None:
         check(lib.rsdb_dbuffer_step_8bit_adam(self._h, C.byref(cfg), step, _stream(stream)))
 
+    def reduce_scatter_adam(self, cfg: AdamConfig, step: int, p2p: Optional["P2P"] = None,
+                            stream=None) -> None:
+        """a6 + a7 + a8 for every unit in one launch (p2p None iff world 1)."""
+        check(lib.rsdb_dbuffer_reduce_scatter_adam(self._h, p2p.handle if p2p is not None else None,
+                                                   C.byref(cfg), step, _stream(stream)))
+
     def zero_grads(self, stream=None) -> None:
         check(lib.rsdb_dbuffer_zero_grads(self._h, _stream(stream)))
 

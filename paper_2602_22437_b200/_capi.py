@@ -101,6 +101,7 @@ _SIGS = {
     "rsdb_dbuffer_num_blocks": (i64, [vp]),
     "rsdb_dbuffer_step_8bit_adam": (i32, [vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_zero_grads": (i32, [vp, vp]),
+    "rsdb_dbuffer_reduce_scatter_adam": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_free": (None, [vp]),
     "rsdb_copy_plan_create": (i32, [C.POINTER(Segment), i64, i32, i32, C.c_float,
                                     C.POINTER(vp)]),

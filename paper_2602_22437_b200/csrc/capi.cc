@@ -89,7 +89,9 @@ struct rsdb_dbuffer {
   std::vector<std::unique_ptr<rsdb_unit>> units;
   void* base[RSDB_NKINDS]{};
   int64_t nblocks = 0;
-  DevTable blocks;  // arena-relative table over all units
+  DevTable blocks;        // arena-relative table over all units (grad in GRAD_F32 elements)
+  DevTable blocks_fused;  // the same with grad in GRAD_FULL (bf16) elements, for the fused RS+Adam
+  int32_t m = 1, rank = 0;
   int32_t param_bf16 = 1;
   std::vector<int64_t> grad_bytes;  // per unit, for grouped zero
 };
@@ -829,7 +831,7 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
       return fail(RSDB_EMISMATCH, "arena %d not aligned to %lld bytes", k, (long long)align_bytes);
   }
   int32_t pbf = -1;
-  std::vector<rsdb::AdamBlock> tbl;
+  std::vector<rsdb::AdamBlock> tbl, tbl_fused;
   for (int32_t u = 0; u < n_units; ++u) {
     const rsdb::Layout& L = units[u]->L;
     const int32_t bf = L.elem_bytes == 2;
@@ -853,17 +855,66 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
     const int64_t pbase = offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_PARAM_FULL] / L.elem_bytes +
                           int64_t(rank) * L.S;
     if (bk_off[u] + int64_t(qb.size()) > INT32_MAX) return fail(RSDB_EINVAL, "too many blocks");
-    for (size_t i = 0; i < qb.size(); ++i)
+    const int64_t gbase16 = bf ? offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_GRAD_FULL] / 2 +
+                                     int64_t(rank) * L.S
+                               : 0;
+    for (size_t i = 0; i < qb.size(); ++i) {
       tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off,
                      qb[i].rows * qb[i].cols, int32_t(bk_off[u] + int64_t(i)), qb[i].cols,
                      int32_t(qb[i].pitch)});
+      tbl_fused.push_back(tbl.back());
+      tbl_fused.back().grad_off = gbase16 + qb[i].off;
+    }
+    db->m = L.m;
+    db->rank = rank;
     db->grad_bytes.push_back(int64_t(L.m) * L.S * L.elem_bytes);
     db->units.push_back(std::move(unit));
   }
   db->param_bf16 = pbf < 0 ? 1 : pbf;
   db->nblocks = int64_t(tbl.size());
   if (rsdb_status st = db->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
+  if (db->param_bf16)
+    if (rsdb_status st = db->blocks_fused.upload(tbl_fused.data(),
+                                                 tbl_fused.size() * sizeof(rsdb::AdamBlock)))
+      return st;
   *out = db.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg,
+                                             int64_t step, void* stream) {
+  if (!d) return fail(RSDB_EINVAL, "null dbuffer");
+  if (!d->param_bf16) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs bf16 units");
+  rsdb::AdamScalars s;
+  if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
+  if (d->nblocks == 0) return OK_CLEAR();
+  const int m = d->m;
+  rsdb::P2PPtrs g{};
+  rsdb::P2PSignals sg{};
+  if (m > 1) {
+    if (!p) return fail(RSDB_EINVAL, "world > 1 needs a p2p object");
+    if (!d->units.empty())
+      if (rsdb_status e = p2p_common(d->units[0].get(), p, &sg)) return e;
+    int32_t bi = 0;
+    int64_t off = 0;
+    if (rsdb_status e = p2p_find(p, d->base[RSDB_KIND_GRAD_FULL], 1, &bi, &off)) return e;
+    if (off != 0) return fail(RSDB_EMISMATCH, "p2p must map the GRAD_FULL arena from its base");
+    for (int r = 0; r < m; ++r) g.p[r] = p->peer[size_t(bi)][size_t(r)];
+    ++p->epoch;
+  } else {
+    g.p[0] = d->base[RSDB_KIND_GRAD_FULL];
+  }
+  rsdb::AdamPtrs ap{static_cast<float*>(d->base[RSDB_KIND_MASTER]),
+                    static_cast<int8_t*>(d->base[RSDB_KIND_MQ]),
+                    static_cast<uint8_t*>(d->base[RSDB_KIND_VQ]),
+                    static_cast<float*>(d->base[RSDB_KIND_MABS]),
+                    static_cast<float*>(d->base[RSDB_KIND_VABS]),
+                    nullptr,
+                    d->base[RSDB_KIND_PARAM_FULL],
+                    1};
+  CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(d->blocks_fused.p), d->nblocks, g,
+                                    m, float(1.0 / double(m)), ap, s, m > 1 ? &sg : nullptr, d->rank,
+                                    m > 1 ? p->epoch : 0, S_(stream)));
   return OK_CLEAR();
 }
 
