@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--fused-scope", choices=["unit", "dbuffer"], default=None,
                     help="fused RS+Adam per unit (FSDP backward order) or one launch over the "
                          "whole DBuffer; default: dbuffer at world 1, unit otherwise")
+    ap.add_argument("--fuse-ag", action="store_true",
+                    help="p2p + fused Adam: the AllGather is fused into the RS+Adam kernel too "
+                         "(each rank pushes its updated bf16 shard into every peer's gathered "
+                         "buffer); the step's AllGather is the one the previous step's kernel did")
     ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
                     help="p2p: fused single-kernel collectives over NVLink peer memory "
                          "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
@@ -286,11 +290,21 @@ def step(R, db, cfg, t, stream, timers=None, p2p=None, fuse=False):
             timed("cast", lambda u=u: R.unit_cast_scale(u, stream))
             timed("rs", lambda u=u: R.unit_reduce_scatter_f32(u, stream))
     else:
-        for u in units:
-            timed("ag", lambda u=u: R.all_gather_p2p(u, p2p, stream))
+        if fuse not in ("dbuffer+ag", "unit+ag"):  # else fused into the previous step
+            for u in units:
+                timed("ag", lambda u=u: R.all_gather_p2p(u, p2p, stream))
         if fuse == "dbuffer":  # a6 + a7 + a8 for every unit in ONE launch
             timed("rs", lambda: db.reduce_scatter_adam(cfg, t, p2p if db.units[0].layout.m > 1
                                                        else None, stream))
+            return
+        if fuse == "dbuffer+ag":  # a6 + a7 + a8 + (next) a4, every unit, ONE launch
+            timed("rs", lambda: db.reduce_scatter_adam_gather(
+                cfg, t, p2p if db.units[0].layout.m > 1 else None, stream))
+            return
+        if fuse == "unit+ag":  # a6 + a7 + a8 + (next) a4, one kernel per unit
+            for u in reversed(units):
+                timed("rs", lambda u=u: R.reduce_scatter_adam_gather_p2p(u, p2p, cfg, t,
+                                                                           stream=stream))
             return
         if fuse:  # a6 + a7 + a8: one kernel per unit (FSDP backward order), no optimizer launch
             for u in reversed(units):
@@ -450,6 +464,11 @@ def run_ours(args):
     if fuse:
         scope = args.fused_scope or ("dbuffer" if world == 1 else "unit")
         fuse = "dbuffer" if scope == "dbuffer" else True
+        if args.fuse_ag:
+            fuse = "dbuffer+ag" if scope == "dbuffer" else "unit+ag"
+            for u in db.units:  # the first step's AllGather (steady state: the previous step's)
+                R.all_gather_p2p(u, p2p)
+            torch.cuda.synchronize()
     ab = algorithmic_bytes(lays, rank)
     per_rank_bytes = ab["ag"] + ab["rs"] + ab["cast"] + ab["adam"]
     job_bytes = sum_over_ranks(per_rank_bytes, world)
@@ -490,13 +509,14 @@ def run_ours(args):
     adam_ms = tot["adam"] / max(1, cnt["adam"])
     cast_ms = tot["cast"] / K
     ag_ms, rs_ms = tot["ag"] / K, tot["rs"] / K
+    fuse_ag = fuse in ("dbuffer+ag", "unit+ag")
     adam_gbs = ab["adam"] / (adam_ms * 1e-3) / 1e9 if adam_ms > 0 else None  # fused: inside RS
     cast_gbs = ab["cast"] / (cast_ms * 1e-3) / 1e9 if cast_ms > 0 else None  # p2p: fused into RS
     # physical bytes crossing NVLink into each rank per step: AG (m-1) S 2;
     # RS (m-1) S 4 on the NCCL fp32 path, (m-1) S 2 on the fused p2p path
     wire_ag = ab["ag"]
     wire_rs = ab["rs"] if p2p is None else ab["rs"] // 2
-    ag_bus = wire_ag / (ag_ms * 1e-3) / 1e9 if world > 1 else None
+    ag_bus = wire_ag / (ag_ms * 1e-3) / 1e9 if world > 1 and ag_ms > 0 else None
     rs_bus = wire_rs / (rs_ms * 1e-3) / 1e9 if world > 1 else None
     hbm_peak, peak_src = load_peaks()
     # fused kernel (a6+a7+a8): HBM bytes per rank per step = every element of
@@ -526,7 +546,9 @@ def run_ours(args):
         else:
             roof = {"kernel": dom, "bound": "nvlink", "achieved": rs_bus, "peak": NVLINK_PEAK_GBS,
                     "unit": "GB/s", "frac": rs_bus / NVLINK_PEAK_GBS, "traffic": None,
-                    "bytes": "physical wire bytes into each rank per launch ((m-1) S 2)",
+                    "bytes": "physical wire bytes into each rank per launch ((m-1) S 2)"
+                             + ("; the fused AllGather pushes the same (m-1) S 2 out of each rank "
+                                "on the other link direction" if fuse_ag else ""),
                     "hbm_achieved": fused_gbs, "hbm_frac": fused_gbs / hbm_peak,
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
     elif dom in (adam_name, "cast_scale_kernel") or world == 1:
@@ -565,6 +587,11 @@ def run_ours(args):
                        "units": len(lays), "params": E, "qblock": QBLOCK,
                        "parallelism": f"fsdp{world}",
                        "collectives": args.collectives,
+                       "fused": {"dbuffer": "rs+adam, one launch per step",
+                                 True: "rs+adam, one launch per unit",
+                                 "dbuffer+ag": "rs+adam+allgather, one launch per step",
+                                 "unit+ag": "rs+adam+allgather, one launch per unit",
+                                 False: "none"}[fuse],
                        "l2": f"no flush: per-step working set {sum(sizes) / 2 ** 30:.1f} GiB "
                              f"per rank >> L2 ({L2_BYTES >> 20} MiB)",
                        "plan_ms": plan_ms},
@@ -612,10 +639,15 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2
         for u in db.units:
             if p2p is None:
                 R.all_gather(u, stream)
-            else:
+            elif fuse not in ("dbuffer+ag", "unit+ag"):
                 R.all_gather_p2p(u, p2p, stream)
         if fuse == "dbuffer":
             db.reduce_scatter_adam(cfg, tt, p2p if world > 1 else None, stream)
+        elif fuse == "dbuffer+ag":
+            db.reduce_scatter_adam_gather(cfg, tt, p2p if world > 1 else None, stream)
+        elif fuse == "unit+ag":
+            for u in reversed(db.units):
+                R.reduce_scatter_adam_gather_p2p(u, p2p, cfg, tt, stream=stream)
         else:
             for u in reversed(db.units):
                 if p2p is None:

@@ -292,6 +292,16 @@ rsdb_status rsdb_all_gather_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
  * pointers: `st`, or NULL for a unit of a DBuffer (its arenas). */
 rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit*, rsdb_p2p* p2p_or_null, const rsdb_adam_state* st,
                                          const rsdb_adam_cfg*, int64_t step, void* stream);
+/* The same step with the NEXT AllGather (a4) fused in: every updated bf16
+ * parameter of this rank's shard is also stored over NVLink into every peer's
+ * param_full at the same offset, so on return (stream order) every rank holds
+ * the full updated parameters -- the result of rsdb_reduce_scatter_adam_p2p
+ * followed by rsdb_all_gather_p2p.  p2p must also map param_full.  Peers must
+ * not read their param_full while the call runs (its start barrier orders it
+ * after every rank's prior work).  world 1: identical to the call above. */
+rsdb_status rsdb_reduce_scatter_adam_gather_p2p(rsdb_unit*, rsdb_p2p* p2p_or_null,
+                                                const rsdb_adam_state* st, const rsdb_adam_cfg*,
+                                                int64_t step, void* stream);
 
 /* ======================================================================== */
 /* DBuffer batched allocation: one allocation per    */
@@ -340,6 +350,12 @@ rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer*, const rsdb_adam_cfg*, int
  * units; p2p (NULL iff world 1) must map this DBuffer's GRAD_FULL arena. */
 rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer*, rsdb_p2p* p2p_or_null,
                                              const rsdb_adam_cfg*, int64_t step, void* stream);
+/* rsdb_dbuffer_reduce_scatter_adam with the AllGather fused in (as
+ * rsdb_reduce_scatter_adam_gather_p2p): the whole step a6+a7+a8+a4 over every
+ * unit in ONE kernel launch.  p2p must map GRAD_FULL and PARAM_FULL arenas
+ * from their bases. */
+rsdb_status rsdb_dbuffer_reduce_scatter_adam_gather(rsdb_dbuffer*, rsdb_p2p* p2p_or_null,
+                                                    const rsdb_adam_cfg*, int64_t step, void* stream);
 /* Grouped zero of every unit's gradient buffer ("zero"). */
 rsdb_status rsdb_dbuffer_zero_grads(rsdb_dbuffer*, void* stream);
 void rsdb_dbuffer_free(rsdb_dbuffer*);

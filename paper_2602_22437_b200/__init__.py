@@ -391,6 +391,18 @@ def reduce_scatter_adam_p2p(unit: Unit, p2p: Optional[P2P], cfg: AdamConfig, ste
                                            st, C.byref(cfg), step, _stream(stream)))
 
 
+def reduce_scatter_adam_gather_p2p(unit: Unit, p2p: Optional[P2P], cfg: AdamConfig, step: int,
+                                   state=None, stream=None) -> None:
+    """reduce_scatter_adam_p2p with the next AllGather fused in: the updated
+    bf16 shard is also stored into every peer's param_full (p2p must map it)."""
+    st = None
+    if state is not None:
+        st = C.byref(_c.AdamState(*[_ptr(t) for t in state]))
+    check(lib.rsdb_reduce_scatter_adam_gather_p2p(unit.handle,
+                                                  p2p.handle if p2p is not None else None,
+                                                  st, C.byref(cfg), step, _stream(stream)))
+
+
 def all_gather_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
     """a4 as one kernel pulling every peer's shard over NVLink."""
     check(lib.rsdb_all_gather_p2p(unit.handle, p2p.handle, _stream(stream)))
@@ -464,6 +476,13 @@ class DBuffer:
         """a6 + a7 + a8 for every unit in one launch (p2p None iff world 1)."""
         check(lib.rsdb_dbuffer_reduce_scatter_adam(self._h, p2p.handle if p2p is not None else None,
                                                    C.byref(cfg), step, _stream(stream)))
+
+    def reduce_scatter_adam_gather(self, cfg: AdamConfig, step: int, p2p: Optional["P2P"] = None,
+                                   stream=None) -> None:
+        """a6 + a7 + a8 + a4 for every unit in one launch: on return every rank
+        holds the full updated parameters (p2p maps GRAD_FULL and PARAM_FULL)."""
+        check(lib.rsdb_dbuffer_reduce_scatter_adam_gather(
+            self._h, p2p.handle if p2p is not None else None, C.byref(cfg), step, _stream(stream)))
 
     def zero_grads(self, stream=None) -> None:
         check(lib.rsdb_dbuffer_zero_grads(self._h, _stream(stream)))

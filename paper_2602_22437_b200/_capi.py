@@ -94,6 +94,8 @@ _SIGS = {
     "rsdb_all_gather_p2p": (i32, [vp, vp, vp]),
     "rsdb_reduce_scatter_adam_p2p": (i32, [vp, vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64,
                                            vp]),
+    "rsdb_reduce_scatter_adam_gather_p2p": (i32, [vp, vp, C.POINTER(AdamState), C.POINTER(AdamCfg),
+                                                  i64, vp]),
     "rsdb_arena_sizes": (i32, [C.POINTER(vp), i32, i32, i64, i64, P_i64, P_i64]),
     "rsdb_dbuffer_create": (i32, [C.POINTER(vp), i32, vp, i32, i64, i64, C.POINTER(vp),
                                   C.POINTER(vp)]),
@@ -102,6 +104,7 @@ _SIGS = {
     "rsdb_dbuffer_step_8bit_adam": (i32, [vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_zero_grads": (i32, [vp, vp]),
     "rsdb_dbuffer_reduce_scatter_adam": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),
+    "rsdb_dbuffer_reduce_scatter_adam_gather": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_free": (None, [vp]),
     "rsdb_copy_plan_create": (i32, [C.POINTER(Segment), i64, i32, i32, C.c_float,
                                     C.POINTER(vp)]),

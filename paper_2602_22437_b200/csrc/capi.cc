@@ -666,8 +666,8 @@ rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   return OK_CLEAR();
 }
 
-rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state* st,
-                                         const rsdb_adam_cfg* cfg, int64_t step, void* stream) {
+static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state* st,
+                                const rsdb_adam_cfg* cfg, int64_t step, void* stream, bool gather) {
   if (!u) return fail(RSDB_EINVAL, "null unit");
   if (u->L.elem_bytes != 2) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs a bf16 unit");
   rsdb::AdamScalars s;
@@ -680,8 +680,9 @@ rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_a
     return fail(RSDB_EINVAL, "null state pointer");
   const int m = u->L.m;
   if (u->L.S == 0 || u->nblocks == 0) return OK_CLEAR();
-  rsdb::P2PPtrs g{};
+  rsdb::P2PPtrs g{}, q{};
   rsdb::P2PSignals sg{};
+  const bool push = gather && m > 1;
   if (m > 1) {
     if (!p) return fail(RSDB_EINVAL, "world > 1 needs a p2p object");
     if (rsdb_status e = p2p_common(u, p, &sg)) return e;
@@ -689,6 +690,10 @@ rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_a
     int64_t off = 0;
     if (rsdb_status e = p2p_find(p, u->bufs.grad_full, int64_t(m) * u->L.S * 2, &bi, &off)) return e;
     for (int r = 0; r < m; ++r) g.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+    if (push) {
+      if (rsdb_status e = p2p_find(p, u->bufs.param_full, int64_t(m) * u->L.S * 2, &bi, &off)) return e;
+      for (int r = 0; r < m; ++r) q.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+    }
     ++p->epoch;
   } else {
     g.p[0] = u->bufs.grad_full;
@@ -700,8 +705,18 @@ rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_a
   const float scale = float(1.0 / double(m));
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, g, m,
                                     scale, ap, s, m > 1 ? &sg : nullptr, u->rank,
-                                    m > 1 ? p->epoch : 0, S_(stream)));
+                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr));
   return OK_CLEAR();
+}
+
+rsdb_status rsdb_reduce_scatter_adam_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state* st,
+                                         const rsdb_adam_cfg* cfg, int64_t step, void* stream) {
+  return rs_adam_unit(u, p, st, cfg, step, stream, false);
+}
+
+rsdb_status rsdb_reduce_scatter_adam_gather_p2p(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state* st,
+                                                const rsdb_adam_cfg* cfg, int64_t step, void* stream) {
+  return rs_adam_unit(u, p, st, cfg, step, stream, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -881,16 +896,17 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
   return OK_CLEAR();
 }
 
-rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg,
-                                             int64_t step, void* stream) {
+static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg, int64_t step,
+                                   void* stream, bool gather) {
   if (!d) return fail(RSDB_EINVAL, "null dbuffer");
   if (!d->param_bf16) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs bf16 units");
   rsdb::AdamScalars s;
   if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
   if (d->nblocks == 0) return OK_CLEAR();
   const int m = d->m;
-  rsdb::P2PPtrs g{};
+  rsdb::P2PPtrs g{}, q{};
   rsdb::P2PSignals sg{};
+  const bool push = gather && m > 1;
   if (m > 1) {
     if (!p) return fail(RSDB_EINVAL, "world > 1 needs a p2p object");
     if (!d->units.empty())
@@ -900,6 +916,11 @@ rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer* d, rsdb_p2p* p, const
     if (rsdb_status e = p2p_find(p, d->base[RSDB_KIND_GRAD_FULL], 1, &bi, &off)) return e;
     if (off != 0) return fail(RSDB_EMISMATCH, "p2p must map the GRAD_FULL arena from its base");
     for (int r = 0; r < m; ++r) g.p[r] = p->peer[size_t(bi)][size_t(r)];
+    if (push) {
+      if (rsdb_status e = p2p_find(p, d->base[RSDB_KIND_PARAM_FULL], 1, &bi, &off)) return e;
+      if (off != 0) return fail(RSDB_EMISMATCH, "p2p must map the PARAM_FULL arena from its base");
+      for (int r = 0; r < m; ++r) q.p[r] = p->peer[size_t(bi)][size_t(r)];
+    }
     ++p->epoch;
   } else {
     g.p[0] = d->base[RSDB_KIND_GRAD_FULL];
@@ -914,8 +935,18 @@ rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer* d, rsdb_p2p* p, const
                     1};
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(d->blocks_fused.p), d->nblocks, g,
                                     m, float(1.0 / double(m)), ap, s, m > 1 ? &sg : nullptr, d->rank,
-                                    m > 1 ? p->epoch : 0, S_(stream)));
+                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr));
   return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg,
+                                             int64_t step, void* stream) {
+  return rs_adam_dbuffer(d, p, cfg, step, stream, false);
+}
+
+rsdb_status rsdb_dbuffer_reduce_scatter_adam_gather(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg,
+                                                    int64_t step, void* stream) {
+  return rs_adam_dbuffer(d, p, cfg, step, stream, true);
 }
 
 rsdb_status rsdb_dbuffer_create(const rsdb_layout* const* units, int32_t n_units, rsdb_comm* comm,

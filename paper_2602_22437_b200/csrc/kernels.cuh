@@ -74,9 +74,12 @@ cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank,
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
 // a6 + a7 + a8 fused: ReduceScatter of the bf16 gradients over NVLink and the
-// 8-bit Adam update of the local shard in one kernel (sg may be null iff m == 1).
+// 8-bit Adam update of the local shard in one kernel (sg may be null iff m == 1);
+// push_params non-null: also a4 -- every updated bf16 parameter is stored into
+// every peer's parameter array (AllGather fused into the step).
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
-                               const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st);
+                               const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
+                               const P2PPtrs* push_params = nullptr);
 
 }  // namespace rsdb

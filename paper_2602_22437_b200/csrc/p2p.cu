@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 #include <cstring>
 
 #include "adam_dev.cuh"
@@ -629,13 +630,40 @@ __device__ __forceinline__ bool rsa_fits(const AdamBlock& b) {
          (b.grad_off & 7) == 0 && (b.param_off & 3) == 0;
 }
 
-template <int M, bool PARAM_BF16, bool SYNC>
+// AllGather fused into the step: every bf16 parameter the Adam tail writes is
+// also stored into every peer's parameter array at the same index (NVLink
+// stores, made visible by the system fence of the done barrier).
+template <int M>
+struct PeerPush {
+  uint16_t* peer[M];
+  int rank;
+  __device__ void quad(int64_t i, uint2 bits) const {
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      if (r != rank) *reinterpret_cast<uint2*>(peer[r] + i) = bits;
+  }
+  __device__ void one(int64_t i, __nv_bfloat16 h) const {
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      if (r != rank) reinterpret_cast<__nv_bfloat16*>(peer[r])[i] = h;
+  }
+};
+
+template <int M, bool PARAM_BF16, bool SYNC, bool PUSH>
 __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __restrict__ tbl,
                                                             int64_t nblocks, P2PPtrs grads,
-                                                            float scale, AdamPtrs P, AdamScalars s,
-                                                            P2PSignals sg, int rank, uint64_t epoch) {
+                                                            P2PPtrs params, float scale, AdamPtrs P,
+                                                            AdamScalars s, P2PSignals sg, int rank,
+                                                            uint64_t epoch) {
   using Gm = RsaGeom<M>;
   using G = AdamGeom<RSA_NT>;
+  using PushT = std::conditional_t<PUSH, PeerPush<M>, NoPush>;
+  PushT push{};
+  if constexpr (PUSH) {
+#pragma unroll
+    for (int r = 0; r < M; ++r) push.peer[r] = static_cast<uint16_t*>(const_cast<void*>(params.p[r]));
+    push.rank = rank;
+  }
   extern __shared__ __align__(128) uint8_t rsa_smem[];
   __shared__ __align__(8) uint64_t full[Gm::STAGES];
   __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
@@ -716,9 +744,9 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
         dq4_v(cv, sv, &r.vt[4 * k]);
       }
       if (blk.len == ADAM_TILE)
-        adam_block_tail<RSA_NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
+        adam_block_tail<RSA_NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill, push);
       else
-        adam_block_tail<RSA_NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill);
+        adam_block_tail<RSA_NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill, push);
     } else {
       // generic: gradients summed straight from the peers' memory, masked & strided
 #pragma unroll
@@ -738,45 +766,50 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
         }
         r.g[e] = acc;
       }
-      adam_block_tail<RSA_NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, refill);
+      adam_block_tail<RSA_NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, refill, push);
     }
   }
   if constexpr (SYNC) p2p_done(sg, rank, M, epoch);
 }
 
-template <int M, bool BF, bool SYNC>
-static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, float scale,
-                               const AdamPtrs& P, const AdamScalars& s, const P2PSignals& sg, int rank,
-                               uint64_t epoch, cudaStream_t st) {
+template <int M, bool SYNC, bool PUSH>
+static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads,
+                               const P2PPtrs& params, float scale, const AdamPtrs& P,
+                               const AdamScalars& s, const P2PSignals& sg, int rank, uint64_t epoch,
+                               cudaStream_t st) {
   const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * RsaGeom<M>::STAGES;
   static const int grid = [&] {
-    cudaFuncSetAttribute(rs_adam_tma_kernel<M, BF, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
+    cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, BF, SYNC>, RSA_NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, true, SYNC, PUSH>, RSA_NT,
+                                                  smem);
     return num_sms() * (b < 1 ? 1 : b);
   }();
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, grid));
-  rs_adam_tma_kernel<M, BF, SYNC><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, scale, P, s, sg,
-                                                                rank, epoch);
+  rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, params,
+                                                                        scale, P, s, sg, rank, epoch);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
-                               const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st) {
-  const bool bf = P.param_bf16;
+                               const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
+                               const P2PPtrs* push_params) {
+  if (!P.param_bf16) return cudaErrorInvalidValue;  // the fused path is for bf16 units
+  const P2PPtrs none_p{};
   if (m == 1) {
     P2PSignals none{};
-    return bf ? rs_adam_mbs<1, true, false>(tbl, nblocks, grads, scale, P, s, none, rank, epoch, st)
-              : rs_adam_mbs<1, false, false>(tbl, nblocks, grads, scale, P, s, none, rank, epoch, st);
+    return rs_adam_mbs<1, false, false>(tbl, nblocks, grads, none_p, scale, P, s, none, rank, epoch, st);
   }
   if (!sg) return cudaErrorInvalidValue;
   switch (m) {
-#define RSA_CASE(MM)                                                                                 \
-  case MM:                                                                                           \
-    return bf ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, scale, P, s, *sg, rank, epoch, st)  \
-              : rs_adam_mbs<MM, false, true>(tbl, nblocks, grads, scale, P, s, *sg, rank, epoch, st);
+#define RSA_CASE(MM)                                                                                  \
+  case MM:                                                                                            \
+    return push_params ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, *push_params, scale, P, s,  \
+                                                     *sg, rank, epoch, st)                            \
+                       : rs_adam_mbs<MM, true, false>(tbl, nblocks, grads, none_p, scale, P, s, *sg,  \
+                                                      rank, epoch, st);
     RSA_CASE(2) RSA_CASE(3) RSA_CASE(4) RSA_CASE(5) RSA_CASE(6) RSA_CASE(7) RSA_CASE(8)
 #undef RSA_CASE
     default:

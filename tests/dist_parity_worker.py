@@ -119,6 +119,7 @@ def main():
         ma = torch.zeros(nb, dtype=torch.float32, device="cuda")
         va = torch.zeros(nb, dtype=torch.float32, device="cuda")
         fused_in = [t.clone() for t in (master, mq, vq, ma, va)]
+        gather_in = [t.clone() for t in (master, mq, vq, ma, va)]
         R.step_8bit_adam(u, master, mq, vq, ma, va, R.AdamConfig(), 1)
         if eb == 2:
             # a6 + a7 + a8 in one kernel over NVLink: bit-identical to RS -> Adam
@@ -169,6 +170,37 @@ def main():
         if np.any((np.abs(got - exp) > tol)[full_mask]):
             ok = False
             msgs.append(f"{name}: post-Adam AllGather mismatch {np.abs(got - exp)[full_mask].max()}")
+        if eb == 2:
+            # a6 + a7 + a8 + a4 in one kernel: the pushed parameters equal the
+            # unfused RS -> Adam -> AllGather result bit for bit on every tensor
+            # element, and the optimizer state equals the unfused state
+            pf_ref = param_full.clone()
+            param_full.fill_(float("nan"))
+            dist.barrier()
+            p2p = R.P2P(comm, [param_full, grad_full])
+            R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 1, state=gather_in)
+            torch.cuda.synchronize()
+            fm = torch.from_numpy(full_mask).cuda()
+            if not torch.equal(param_full.view(torch.int16)[fm], pf_ref.view(torch.int16)[fm]):
+                ok = False
+                msgs.append(f"{name}: fused RS+Adam+AG parameters differ from RS -> Adam -> AG")
+            for a, b in zip(gather_in, (master, mq, vq, ma, va)):
+                if not torch.equal(a.view(torch.uint8), b.view(torch.uint8)):
+                    ok = False
+                    msgs.append(f"{name}: fused RS+Adam+AG state differs from RS then Adam")
+                    break
+            # repeated steps re-arm the barriers; peers' params keep agreeing
+            for t in range(2, 5):
+                R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), t, state=gather_in)
+            torch.cuda.synchronize()
+            h = torch.tensor([float(param_full.view(torch.int16)[fm].to(torch.int64).sum().item())],
+                             dtype=torch.float64)
+            hs = [torch.zeros_like(h) for _ in range(world)]
+            dist.all_gather(hs, h)
+            if len(set(x.item() for x in hs)) != 1:
+                ok = False
+                msgs.append(f"{name}: ranks disagree on the parameters after repeated fused steps")
+            p2p.close()
         del u
     # ---- random-normal bf16 grads: fp32 RS tolerance (non-exact sums)
     es = [300001, 4097]

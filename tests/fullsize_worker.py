@@ -9,8 +9,9 @@ every unit are checked against the oracle, block by block:
                   step_8bit_adam on the block
   check         = codes +-1, params 1e-5 (|p|+lr), absmax 1e-6, bf16 shard
 
-Plus, after a second AllGather, every rank holds the identical full
-parameter buffers (checksum all-reduce).  Runs standalone (world 1) or under
+Plus, after a second AllGather (or the one fused into the step for the "+ag"
+scopes), every rank holds the identical full parameter buffers (checksum
+all-gather).  FULLSIZE_SCOPE = unit | dbuffer | unit+ag | dbuffer+ag.  Runs standalone (world 1) or under
 torchrun.  Exit 0 iff all checks pass on every rank.
 """
 import os
@@ -71,7 +72,7 @@ def main():
     st = torch.cuda.Stream()
     scope = os.environ.get("FULLSIZE_SCOPE", "unit")
     with torch.cuda.stream(st):
-        bench.step(R, db, cfg, 1, st, p2p=p2p, fuse="dbuffer" if scope == "dbuffer" else True)
+        bench.step(R, db, cfg, 1, st, p2p=p2p, fuse={"unit": True}.get(scope, scope))
     st.synchronize()
     ok, msgs = True, []
     ocfg = OA.AdamCfg()
@@ -104,10 +105,12 @@ def main():
         if not good:
             ok = False
             msgs.append(f"unit {ui} block {b}: err {err.max():.2e} dm {dm.max()} dv {dv.max()}")
-    # AllGather: every rank ends with the same full parameter buffers
-    with torch.cuda.stream(st):
-        for u in db.units:
-            R.all_gather_p2p(u, p2p, st)
+    # AllGather: every rank ends with the same full parameter buffers (the
+    # "+ag" scopes already did it inside the fused kernel)
+    if not scope.endswith("+ag"):
+        with torch.cuda.stream(st):
+            for u in db.units:
+                R.all_gather_p2p(u, p2p, st)
     st.synchronize()
     h = torch.tensor([float(arenas[0].view(torch.int32).to(torch.int64).sum().item() % (1 << 40))],
                      dtype=torch.float64)

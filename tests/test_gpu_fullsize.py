@@ -23,7 +23,8 @@ def _port():
 
 
 @pytest.mark.parametrize("n,scope", [(1, "dbuffer"), (1, "unit"), (2, "unit"), (2, "dbuffer"),
-                                     (4, "unit")])
+                                     (2, "dbuffer+ag"), (4, "unit"), (4, "dbuffer+ag"),
+                                     (4, "unit+ag")])
 def test_fullsize_parity(n, scope):
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
