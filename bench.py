@@ -17,9 +17,15 @@ init, P:491, reported as plan_ms):
     for unit in reversed(units):  a6  cast bf16->fp32 x 1/m, padding 0
                                   a7  ReduceScatter
                                   a8  block-wise 8-bit Adam (+ bf16 shard)
-  --collectives p2p (default): per unit ONE kernel over NVLink peer memory does
-      a6+a7+a8 (rsdb_reduce_scatter_adam_p2p; --no-fuse-adam: a6+a7 kernel per
-      unit, then one a8 launch over every shard); AllGather = rsdb_all_gather_p2p.
+  --collectives p2p (default): the step is ONE kernel over NVLink peer memory
+      for the whole DBuffer (rsdb_dbuffer_reduce_scatter_adam_gather): a6+a7
+      (rank-order sum of every rank's bf16 gradient slice), a8 (8-bit Adam of
+      the owned blocks) and a4 (each updated bf16 parameter stored into every
+      peer's gathered buffer -- the AllGather the next step's forward needs;
+      the first step's AllGather runs once at setup).  Variants:
+      --no-fuse-ag: rsdb_all_gather_p2p per unit + the fused RS+Adam kernel;
+      --fused-scope unit: one fused kernel per unit (FSDP backward order);
+      --no-fuse-adam: a6+a7 kernel per unit, then one a8 launch.
   --collectives nccl: ncclAllGather; cast kernel + ncclReduceScatter (fp32) per
       unit; one a8 launch over every shard.
 
@@ -64,13 +70,14 @@ def parse():
     ap.add_argument("--no-fuse-adam", action="store_true",
                     help="p2p path: separate ReduceScatter kernel + one 8-bit Adam launch instead "
                          "of the fused ReduceScatter+Adam kernel")
-    ap.add_argument("--fused-scope", choices=["unit", "dbuffer"], default=None,
-                    help="fused RS+Adam per unit (FSDP backward order) or one launch over the "
-                         "whole DBuffer; default: dbuffer at world 1, unit otherwise")
-    ap.add_argument("--fuse-ag", action="store_true",
+    ap.add_argument("--fused-scope", choices=["unit", "dbuffer"], default="dbuffer",
+                    help="fused kernel per unit (FSDP backward order, 17 launches) or one launch "
+                         "over the whole DBuffer (default)")
+    ap.add_argument("--fuse-ag", action=argparse.BooleanOptionalAction, default=True,
                     help="p2p + fused Adam: the AllGather is fused into the RS+Adam kernel too "
                          "(each rank pushes its updated bf16 shard into every peer's gathered "
-                         "buffer); the step's AllGather is the one the previous step's kernel did")
+                         "buffer); the step's AllGather is the one the previous step's kernel "
+                         "did (default on)")
     ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
                     help="p2p: fused single-kernel collectives over NVLink peer memory "
                          "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
@@ -462,7 +469,7 @@ def run_ours(args):
         p2p = R.P2P(comm, [arenas[0], arenas[1]])  # PARAM_FULL, GRAD_FULL arenas
     fuse = p2p is not None and not args.no_fuse_adam
     if fuse:
-        scope = args.fused_scope or ("dbuffer" if world == 1 else "unit")
+        scope = args.fused_scope
         fuse = "dbuffer" if scope == "dbuffer" else True
         if args.fuse_ag:
             fuse = "dbuffer+ag" if scope == "dbuffer" else "unit+ag"
@@ -544,11 +551,18 @@ def run_ours(args):
                     "bytes": "16 B per owned element (bf16 grad 2, master 8, codes 4, bf16 out 2) "
                              "+ 16 B absmax per block"}
         else:
-            roof = {"kernel": dom, "bound": "nvlink", "achieved": rs_bus, "peak": NVLINK_PEAK_GBS,
-                    "unit": "GB/s", "frac": rs_bus / NVLINK_PEAK_GBS, "traffic": None,
-                    "bytes": "physical wire bytes into each rank per launch ((m-1) S 2)"
-                             + ("; the fused AllGather pushes the same (m-1) S 2 out of each rank "
-                                "on the other link direction" if fuse_ag else ""),
+            # bytes entering each rank over NVLink per launch: the peers' gradient
+            # slices it reads ((m-1) S 2); with the AllGather fused in, also the
+            # peers' updated parameter shards pushed into it ((m-1) S 2 more).
+            # The outbound direction carries the same amount (its slices read by
+            # the peers + its own pushes), so this is the per-direction load.
+            wire_in = wire_rs + (wire_ag if fuse_ag else 0)
+            ach = wire_in / (rs_ms * 1e-3) / 1e9
+            roof = {"kernel": dom, "bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK_GBS,
+                    "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "traffic": None,
+                    "bytes": "physical wire bytes into each rank per launch: (m-1) S 2 gradient "
+                             "reads" + (" + (m-1) S 2 parameter pushes from the peers (the fused "
+                                        "AllGather)" if fuse_ag else ""),
                     "hbm_achieved": fused_gbs, "hbm_frac": fused_gbs / hbm_peak,
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
     elif dom in (adam_name, "cast_scale_kernel") or world == 1:

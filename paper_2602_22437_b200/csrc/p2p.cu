@@ -65,10 +65,20 @@ __device__ __forceinline__ int4 ld_peer_v4(const void* p) {
   return r;
 }
 
+// sg.peer is indexed with compile-time indices only (a runtime index into a
+// kernel-parameter array would copy the struct to the local-memory stack)
+__device__ __forceinline__ uint64_t* sg_peer(const P2PSignals& sg, int i) {
+  uint64_t* q = nullptr;
+#pragma unroll
+  for (int r = 0; r < P2P_MAX_RANKS; ++r)
+    if (r == i) q = sg.peer[r];
+  return q;
+}
+
 __device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < m && int(threadIdx.x) != rank) {
     __threadfence_system();
-    st_release_sys(sg.peer[threadIdx.x] + rank, epoch);
+    st_release_sys(sg_peer(sg, int(threadIdx.x)) + rank, epoch);
   }
   if (threadIdx.x == 0) {
     for (int r = 0; r < m; ++r) {
@@ -89,8 +99,9 @@ __device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, 
     if (old == gridDim.x - 1) {
       atomicExch(ctr, 0u);
       __threadfence_system();
-      for (int r = 0; r < m; ++r)
-        if (r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);
+#pragma unroll
+      for (int r = 0; r < P2P_MAX_RANKS; ++r)
+        if (r < m && r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);
       for (int r = 0; r < m; ++r) {
         if (r == rank) continue;
         while (ld_acquire_sys(sg.local + 8 + r) < epoch) {
