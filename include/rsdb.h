@@ -379,6 +379,36 @@ rsdb_status rsdb_copy_plan_create(const rsdb_segment* segs_host, int64_t n, int3
 rsdb_status rsdb_copy_run(const rsdb_copy_plan*, void* stream);
 void rsdb_copy_plan_free(rsdb_copy_plan*);
 
+/* ======================================================================== */
+/* N2: FP8 (E4M3) 128x128 block quantization of the parameters fused with   */
+/* the AllGather ("Block-wise Quantization", "DeepSeek's 128x128 */
+/* tiling"; readings R18-R20 in DESIGN.md): 1 byte per element on the wire. */
+/* ======================================================================== */
+typedef struct rsdb_fp8_unit rsdb_fp8_unit;
+/* layout: a unit of 2-D weights planned with elem_bytes 1 (g_coll = 16
+ * elements) at 128-row granularity (block = 128 * row_len), so every tile lies
+ * on one rank.  specs[n_tensors]: the tile cut of each tensor (row_len,
+ * tile_rows, tile_cols; normally 128 x 128), as for rsdb_layout_rank_tiles.
+ * Device buffers (caller-owned): master_shard = this rank's S fp32 master
+ * weights (16-B aligned); codes_full = m*S bytes (the gathered E4M3 codes at
+ * the layout's offsets; padding is never written); scales_full =
+ * rsdb_fp8_unit_num_tiles() floats, one per tile in buffer order (tensors in
+ * order, tiles row-major): the dequantization factor fl(A / 448), A = tile
+ * absmax (0 for an all-zero tile, whose codes are 0).  A tile straddling a
+ * shard boundary is EMISMATCH; EINVAL on null pointers or bad specs. */
+rsdb_status rsdb_fp8_unit_create(const rsdb_layout*, const rsdb_qspec* specs, rsdb_comm* comm_or_null,
+                                 int32_t rank, const float* master_shard, uint8_t* codes_full,
+                                 float* scales_full, rsdb_fp8_unit** out);
+int64_t rsdb_fp8_unit_num_tiles(const rsdb_fp8_unit*);   /* all ranks */
+int64_t rsdb_fp8_unit_first_slot(const rsdb_fp8_unit*);  /* this rank's first tile slot */
+/* ONE kernel: quantize every tile of this rank's shard (cvt.rn.satfinite
+ * E4M3 of fl(x * fl(448 / A))) and store the codes and the tile scales into
+ * every rank's codes_full / scales_full (NVLink stores; p2p must map both
+ * buffers of every rank at the same offsets, NULL iff world 1).  On return
+ * (stream order) every rank holds the full gathered codes and scales. */
+rsdb_status rsdb_fp8_quantize_all_gather(rsdb_fp8_unit*, rsdb_p2p* p2p_or_null, void* stream);
+void rsdb_fp8_unit_free(rsdb_fp8_unit*);
+
 #ifdef __cplusplus
 }
 #endif

@@ -521,3 +521,48 @@ class CopyPlan:
         if getattr(self, "_h", None) is not None and self._h.value:
             lib.rsdb_copy_plan_free(self._h)
             self._h = None
+
+
+# ---------------------------------------------------------------- N2: FP8 AllGather
+class Fp8Unit:
+    """FP8 (E4M3) 128x128 block quantization of a unit's fp32 master shard
+    fused with the AllGather of the codes (1 B/element) and per-tile scales
+    (rsdb_fp8_*, R18-R20).  `layout` is planned with elem_bytes=1
+    at 128-row granularity; `specs` = [("tile", row_len, 128, 128), ...]."""
+
+    def __init__(self, layout: Layout, specs, rank: int, master_shard, codes_full, scales_full,
+                 comm: Optional[Comm] = None):
+        self._keep = (layout, master_shard, codes_full, scales_full)
+        self._specs = qspecs(specs)
+        h = C.c_void_p()
+        check(lib.rsdb_fp8_unit_create(layout.handle, self._specs, comm.handle if comm else None,
+                                       rank, _ptr(master_shard), _ptr(codes_full),
+                                       _ptr(scales_full), C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def num_tiles(self) -> int:
+        return lib.rsdb_fp8_unit_num_tiles(self._h)
+
+    @property
+    def first_slot(self) -> int:
+        return lib.rsdb_fp8_unit_first_slot(self._h)
+
+    def quantize_all_gather(self, p2p: Optional["P2P"] = None, stream=None) -> None:
+        check(lib.rsdb_fp8_quantize_all_gather(self._h, p2p.handle if p2p is not None else None,
+                                               _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.rsdb_fp8_unit_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -110,6 +110,11 @@ _SIGS = {
                                     C.POINTER(vp)]),
     "rsdb_copy_run": (i32, [vp, vp]),
     "rsdb_copy_plan_free": (None, [vp]),
+    "rsdb_fp8_unit_create": (i32, [vp, C.POINTER(QSpec), vp, i32, vp, vp, vp, C.POINTER(vp)]),
+    "rsdb_fp8_unit_num_tiles": (i64, [vp]),
+    "rsdb_fp8_unit_first_slot": (i64, [vp]),
+    "rsdb_fp8_quantize_all_gather": (i32, [vp, vp, vp]),
+    "rsdb_fp8_unit_free": (None, [vp]),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -1040,4 +1040,100 @@ rsdb_status rsdb_copy_run(const rsdb_copy_plan* cp, void* stream) {
 
 void rsdb_copy_plan_free(rsdb_copy_plan* cp) { delete cp; }
 
+// ---------------------------------------------------------------------------
+// N2: FP8 block quantization fused with the AllGather
+// ---------------------------------------------------------------------------
+struct rsdb_fp8_unit {
+  rsdb::Layout L;
+  rsdb_comm* comm = nullptr;
+  int32_t rank = 0;
+  const float* master = nullptr;
+  uint8_t* codes = nullptr;
+  float* scales = nullptr;
+  int64_t ntiles_rank = 0, ntiles_total = 0, first_slot = 0;
+  DevTable tiles;  // rsdb::Fp8Tile[ntiles_rank]
+};
+
+rsdb_status rsdb_fp8_unit_create(const rsdb_layout* l, const rsdb_qspec* specs, rsdb_comm* comm,
+                                 int32_t rank, const float* master_shard, uint8_t* codes_full,
+                                 float* scales_full, rsdb_fp8_unit** out) {
+  if (!l || !specs || !out) return fail(RSDB_EINVAL, "null argument");
+  *out = nullptr;
+  const rsdb::Layout& L = l->L;
+  if (L.elem_bytes != 1) return fail(RSDB_EMISMATCH, "FP8 units are planned with elem_bytes 1");
+  if (rank < 0 || rank >= L.m) return fail(RSDB_EINVAL, "rank %d out of [0,%d)", rank, L.m);
+  if (comm && (comm->world != L.m || comm->rank != rank))
+    return fail(RSDB_EMISMATCH, "comm does not match the layout's world / rank");
+  for (size_t t = 0; t < L.e.size(); ++t)
+    if (specs[t].row_len <= 0 || specs[t].tile_rows <= 0 || specs[t].tile_cols <= 0)
+      return fail(RSDB_EINVAL, "tensor %zu: FP8 units need a tile spec (row_len, rows, cols)", t);
+  const auto sp = make_specs(L, 0, specs);
+  auto u = std::make_unique<rsdb_fp8_unit>();
+  u->L = L;
+  u->comm = comm;
+  u->rank = rank;
+  std::vector<rsdb::Fp8Tile> mine;
+  for (int32_t r = 0; r < L.m; ++r) {
+    std::vector<rsdb::QTile> t;
+    if (rsdb_status st = tiles_of(L, r, sp, &t)) return st;
+    if (r == rank) {
+      u->first_slot = u->ntiles_total;
+      for (size_t i = 0; i < t.size(); ++i)
+        mine.push_back({t[i].off, t[i].rows, t[i].cols, int32_t(t[i].pitch),
+                        int32_t(u->ntiles_total + int64_t(i))});
+    }
+    u->ntiles_total += int64_t(t.size());
+  }
+  if (u->ntiles_total > INT32_MAX) return fail(RSDB_EINVAL, "too many tiles");
+  u->ntiles_rank = int64_t(mine.size());
+  if (u->ntiles_rank > 0 && (!master_shard || !codes_full || !scales_full))
+    return fail(RSDB_EINVAL, "null buffer");
+  if (master_shard && !aligned16(master_shard)) return fail(RSDB_EINVAL, "master_shard must be 16-B aligned");
+  u->master = master_shard;
+  u->codes = codes_full;
+  u->scales = scales_full;
+  if (!mine.empty()) {
+    if (rsdb_status st = require_device()) return st;
+    if (rsdb_status st = u->tiles.upload(mine.data(), mine.size() * sizeof(rsdb::Fp8Tile))) return st;
+  }
+  *out = u.release();
+  return OK_CLEAR();
+}
+
+int64_t rsdb_fp8_unit_num_tiles(const rsdb_fp8_unit* u) { return u ? u->ntiles_total : -1; }
+int64_t rsdb_fp8_unit_first_slot(const rsdb_fp8_unit* u) { return u ? u->first_slot : -1; }
+
+rsdb_status rsdb_fp8_quantize_all_gather(rsdb_fp8_unit* u, rsdb_p2p* p, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  const int m = u->L.m;
+  const int64_t S = u->L.S;
+  rsdb::P2PPtrs codes{}, scales{};
+  rsdb::P2PSignals sg{};
+  if (m > 1) {
+    if (!p) return fail(RSDB_EINVAL, "world > 1 needs a p2p object");
+    if (!u->comm || u->comm != p->comm) return fail(RSDB_EMISMATCH, "unit and p2p use different comms");
+    int32_t bi = 0;
+    int64_t off = 0;
+    if (rsdb_status e = p2p_find(p, u->codes, int64_t(m) * S, &bi, &off)) return e;
+    for (int r = 0; r < m; ++r) codes.p[r] = p->peer[size_t(bi)][size_t(r)] + off + int64_t(u->rank) * S;
+    if (rsdb_status e = p2p_find(p, u->scales, u->ntiles_total * 4, &bi, &off)) return e;
+    for (int r = 0; r < m; ++r) scales.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+    sg.local = reinterpret_cast<uint64_t*>(p->local[0]);
+    for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
+      sg.peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+    ++p->epoch;
+  } else {
+    codes.p[0] = u->codes;
+    scales.p[0] = u->scales;
+  }
+  if (u->ntiles_rank == 0 && m == 1) return OK_CLEAR();
+  // every rank launches (the barriers count all ranks), even with no tiles
+  CUDA_TRY(rsdb::launch_fp8_quant_ag(static_cast<const rsdb::Fp8Tile*>(u->tiles.p), u->ntiles_rank,
+                                     u->master, codes, scales, m, u->rank, m > 1 ? &sg : nullptr,
+                                     m > 1 ? p->epoch : 0, S_(stream)));
+  return OK_CLEAR();
+}
+
+void rsdb_fp8_unit_free(rsdb_fp8_unit* u) { delete u; }
+
 }  // extern "C"

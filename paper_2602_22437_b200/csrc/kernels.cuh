@@ -82,4 +82,16 @@ cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PP
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
                                const P2PPtrs* push_params = nullptr);
 
+// ---- N2: FP8 E4M3 block quantization fused with the AllGather (fp8.cu) ----
+struct Fp8Tile {
+  int64_t off;                     // first element, offset inside the rank's shard
+  int32_t rows, cols, pitch, slot; // tile shape, row pitch (elements), global scale slot
+};
+static_assert(sizeof(Fp8Tile) == 24, "Fp8Tile is 24 bytes");
+// codes.p[r] / scales.p[r]: rank r's gathered code buffer (already offset by
+// this rank's rank*S) / scale array; r == rank is local.  sg may be null iff m == 1.
+cudaError_t launch_fp8_quant_ag(const Fp8Tile* tiles, int64_t ntiles, const float* master,
+                                const P2PPtrs& codes, const P2PPtrs& scales, int m, int rank,
+                                const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
+
 }  // namespace rsdb

@@ -24,19 +24,12 @@
 
 #include "adam_dev.cuh"
 #include "kernels.cuh"
+#include "p2p_dev.cuh"
 
 namespace rsdb {
 
 constexpr int P2P_THREADS = 512;
 
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 // peer loads; FL = 0: ld.global.cv (uncached), 1: ld.global.nc (read-only
 // path; the peer does not write its buffer between the barriers), 2: weak ld.global
 template <int FL>
@@ -63,52 +56,6 @@ __device__ __forceinline__ int4 ld_peer_v4(const void* p) {
     asm volatile("ld.global.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
-}
-
-// sg.peer is indexed with compile-time indices only (a runtime index into a
-// kernel-parameter array would copy the struct to the local-memory stack)
-__device__ __forceinline__ uint64_t* sg_peer(const P2PSignals& sg, int i) {
-  uint64_t* q = nullptr;
-#pragma unroll
-  for (int r = 0; r < P2P_MAX_RANKS; ++r)
-    if (r == i) q = sg.peer[r];
-  return q;
-}
-
-__device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
-  if (blockIdx.x == 0 && threadIdx.x < m && int(threadIdx.x) != rank) {
-    __threadfence_system();
-    st_release_sys(sg_peer(sg, int(threadIdx.x)) + rank, epoch);
-  }
-  if (threadIdx.x == 0) {
-    for (int r = 0; r < m; ++r) {
-      if (r == rank) continue;
-      while (ld_acquire_sys(sg.local + r) < epoch) {
-      }
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
-  __syncthreads();  // this CTA's peer reads are complete (values consumed)
-  if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's (possibly remote, push variant) stores
-    unsigned int* ctr = reinterpret_cast<unsigned int*>(sg.local + 16);
-    const unsigned int old = atomicAdd(ctr, 1u);
-    if (old == gridDim.x - 1) {
-      atomicExch(ctr, 0u);
-      __threadfence_system();
-#pragma unroll
-      for (int r = 0; r < P2P_MAX_RANKS; ++r)
-        if (r < m && r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);
-      for (int r = 0; r < m; ++r) {
-        if (r == rank) continue;
-        while (ld_acquire_sys(sg.local + 8 + r) < epoch) {
-        }
-      }
-    }
-  }
 }
 
 __device__ __forceinline__ int first_pad_after_p(const int64_t* pad, int npad, int64_t x) {
@@ -629,9 +576,10 @@ cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int 
 // overlaps the NVLink-bound reduction.  M = 1 (world 1): the cast + Adam.
 constexpr int RSA_NT = 128;
 
+constexpr int RSA_MAX_STAGES = 4;
 template <int M>
 struct RsaGeom {
-  static constexpr int STAGES = M <= 4 ? 3 : 2;
+  static constexpr int STAGES = M <= 4 ? 3 : 2;  // default ring depth (RSDB_RSA_STAGES overrides)
   static constexpr int G_BYTES = M * ADAM_TILE * 2;
   static constexpr int STAGE_BYTES = G_BYTES + ADAM_TILE * 4 + ADAM_TILE * 2;
 };
@@ -665,7 +613,7 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
                                                             int64_t nblocks, P2PPtrs grads,
                                                             P2PPtrs params, float scale, AdamPtrs P,
                                                             AdamScalars s, P2PSignals sg, int rank,
-                                                            uint64_t epoch) {
+                                                            uint64_t epoch, int nst) {
   using Gm = RsaGeom<M>;
   using G = AdamGeom<RSA_NT>;
   using PushT = std::conditional_t<PUSH, PeerPush<M>, NoPush>;
@@ -676,7 +624,7 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
     push.rank = rank;
   }
   extern __shared__ __align__(128) uint8_t rsa_smem[];
-  __shared__ __align__(8) uint64_t full[Gm::STAGES];
+  __shared__ __align__(8) uint64_t full[RSA_MAX_STAGES];
   __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
   if constexpr (SYNC) p2p_start(sg, rank, M, epoch);
   auto issue = [&](int64_t b, int st) {
@@ -697,17 +645,17 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
     }
   };
   if (threadIdx.x == 0) {
-    for (int st = 0; st < Gm::STAGES; ++st) tbar_init(&full[st]);
+    for (int st = 0; st < nst; ++st) tbar_init(&full[st]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int st = 0; st < Gm::STAGES; ++st) {
+    for (int st = 0; st < nst; ++st) {
       const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
       if (b < nblocks) issue(b, st);
     }
   }
   __syncthreads();
-  int it = 0;
+  int it = 0, st = 0;
+  uint32_t phase = 0;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
-    const int st = it % Gm::STAGES;
     const AdamBlock blk = tbl[b];
     const float sm = P.mabs[blk.slot] / 127.0f;
     const float sv = P.vabs[blk.slot] / 255.0f;
@@ -715,14 +663,14 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
     float* rv = red_v[it & 1];
     auto refill = [&]() {
       if (threadIdx.x == 0) {
-        const int64_t nb = b + int64_t(Gm::STAGES) * gridDim.x;
+        const int64_t nb = b + int64_t(nst) * gridDim.x;
         if (nb < nblocks) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue(nb, st);
         }
       }
     };
-    tbar_wait(&full[st], uint32_t(it / Gm::STAGES) & 1u);
+    tbar_wait(&full[st], phase);
     BlockRegs<RSA_NT> r;
     if (rsa_fits(blk)) {
       const uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
@@ -779,8 +727,20 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
       }
       adam_block_tail<RSA_NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, refill, push);
     }
+    if (++st == nst) {  // ring position and mbarrier phase of the next block
+      st = 0;
+      phase ^= 1u;
+    }
   }
   if constexpr (SYNC) p2p_done(sg, rank, M, epoch);
+}
+
+static int rsa_stages(int def) {
+  static const int env = [] {
+    const char* e = std::getenv("RSDB_RSA_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  return env >= 2 && env <= RSA_MAX_STAGES ? env : def;
 }
 
 template <int M, bool SYNC, bool PUSH>
@@ -788,7 +748,8 @@ static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PP
                                const P2PPtrs& params, float scale, const AdamPtrs& P,
                                const AdamScalars& s, const P2PSignals& sg, int rank, uint64_t epoch,
                                cudaStream_t st) {
-  const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * RsaGeom<M>::STAGES;
+  static const int nst = rsa_stages(RsaGeom<M>::STAGES);
+  const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * nst;
   static const int grid = [&] {
     cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -799,7 +760,7 @@ static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PP
   }();
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, grid));
   rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, params,
-                                                                        scale, P, s, sg, rank, epoch);
+                                                                        scale, P, s, sg, rank, epoch, nst);
   return cudaGetLastError();
 }
 

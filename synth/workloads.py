@@ -166,6 +166,16 @@ def dsv3_moe_unit(n_local_experts: int = 8, rows: int = 128) -> Unit:
     return Unit("moe_layer", ts)
 
 
+def dsv3_ffn_fp8_unit(n_local_experts: int = 8) -> Unit:
+    """The FFN weights of the config-4 MoE unit (shared + routed expert
+    gate/up/down projections, 27 matrices, 396,361,728 params) -- the tensors a
+    DeepSeek-style scheme quantizes to FP8 in 128x128 tiles -- as a
+    1-byte-element unit at 128-row granularity (DESIGN R20)."""
+    ts = [t for t in dsv3_moe_unit(n_local_experts, 128).tensors
+          if t.name.startswith("mlp.") and t.name.endswith("_proj.weight")]
+    return Unit("ffn_fp8", ts, elem_bytes=1)
+
+
 def dsv3_moe(rows: int = 128) -> Workload:
     return Workload(f"dsv3-moe-unit-{rows}rows", [dsv3_moe_unit(8, rows)])
 

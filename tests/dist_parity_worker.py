@@ -7,7 +7,9 @@ simulated ranks.  Launched by tests/test_gpu_multi.py:
 Per unit: AllGather (bit exact), fused cast/scale + ReduceScatter (bit exact
 on dyadic synth grads; error bound on random-normal bf16 grads), 8-bit Adam
 (codes +-1, params 1e-5), then a second AllGather that must equal the
-concatenation of every rank's oracle parameter shard (bf16, within 1 ulp).
+concatenation of every rank's oracle parameter shard (bf16, within 1 ulp);
+the fused RS+Adam(+AG) kernels vs the unfused sequence (bit exact); and the
+N2 FP8 block quantization + AllGather vs oracle/fp8.py (bit exact).
 Exit code 0 iff every check passed on every rank.
 """
 import os
@@ -24,6 +26,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_2602_22437_b200 as R  # noqa: E402
 from oracle import adam8 as OA  # noqa: E402
 from oracle import dbuffer as OD  # noqa: E402
+from oracle import fp8 as F  # noqa: E402
 from oracle import planner as OP  # noqa: E402
 from synth import workloads as W  # noqa: E402
 
@@ -239,6 +242,39 @@ def main():
     p2p.close()
     del u
     del rng
+    # ---- N2: FP8 block quantization fused with the AllGather over NVLink
+    shapes = [(256, 384), (512, 128), (128, 200), (130, 128), (384, 64), (1024, 256)]
+    es = [r * c for r, c in shapes]
+    gs = [min(128, r) * c for r, c in shapes]
+    c = R.plan(es, gs, world, elem_bytes=1)
+    o = OP.plan(es, gs, world, OP.gcoll_elems(1))
+    specs = F.tile_specs([cc for _, cc in shapes])
+    logical = np.random.default_rng(7).normal(0, 0.02, sum(es)).astype(np.float32)
+    full = np.zeros(world * c.S, np.float32)
+    off = 0
+    for l, e in zip(c.starts, es):
+        full[l:l + e] = logical[off:off + e]
+        off += e
+    exp_codes, exp_scales = F.quantize_all_gather(o, full, specs)
+    master = torch.from_numpy(full[rank * c.S:(rank + 1) * c.S].copy()).cuda()
+    codes = torch.full((world * c.S,), 0xAB, dtype=torch.uint8, device="cuda")
+    scales = torch.full((len(exp_scales),), float("nan"), device="cuda")
+    p2p = R.P2P(comm, [codes, scales])
+    fu = R.Fp8Unit(c, specs, rank, master, codes, scales, comm=comm)
+    mask = np.zeros(world * c.S, bool)
+    for l, e in zip(c.starts, es):
+        mask[l:l + e] = True
+    for it in range(3):  # repeated calls: epochs advance, barriers re-arm
+        fu.quantize_all_gather(p2p)
+        torch.cuda.synchronize()
+        got = codes.cpu().numpy()
+        if not (np.array_equal(got[mask], exp_codes[mask]) and np.all(got[~mask] == 0xAB)
+                and np.array_equal(scales.cpu().numpy().view(np.uint32), exp_scales.view(np.uint32))):
+            ok = False
+            msgs.append(f"FP8 quantize+AllGather mismatch (call {it})")
+            break
+    fu.close()
+    p2p.close()
     comm.close()
     flag = torch.tensor([0 if ok else 1])
     dist.all_reduce(flag)
