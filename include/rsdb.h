@@ -409,6 +409,51 @@ int64_t rsdb_fp8_unit_first_slot(const rsdb_fp8_unit*);  /* this rank's first ti
 rsdb_status rsdb_fp8_quantize_all_gather(rsdb_fp8_unit*, rsdb_p2p* p2p_or_null, void* stream);
 void rsdb_fp8_unit_free(rsdb_fp8_unit*);
 
+/* ======================================================================== */
+/* N3: distributed Muon over RaggedShard (Algorithm 2;  */
+/* readings R21-R24 in DESIGN.md).                                          */
+/* ======================================================================== */
+typedef struct rsdb_muon rsdb_muon;
+typedef struct {
+  double lr;         /* eta (default 0.02) */
+  double momentum;   /* mu (0.95), Nesterov form: buf = mu buf + g; u = g + mu buf */
+  double eps;        /* Newton-Schulz normalisation X = U / (||U||_F + eps) (1e-7) */
+  int32_t ns_steps;  /* quintic iterations (5), coefficients (3.4445, -4.7750, 2.0315) */
+} rsdb_muon_cfg;
+typedef struct {
+  float* master;       /* S fp32: this rank's master shard (updated in place) */
+  float* momentum;     /* S fp32: momentum buffer shard (updated in place) */
+  const float* grad;   /* S fp32: the reduced gradient shard (e.g. GRAD_F32 + rank*S) */
+  float* u;            /* S fp32 scratch: the momentum output, read by the roots (p2p-registered) */
+  void* param_bf16;    /* S bf16 shard written with the update, or NULL */
+  void* workspace;     /* rsdb_muon_workspace_bytes(): the root matrices + NS scratch (p2p-registered) */
+} rsdb_muon_bufs;
+/* rows[t], cols[t]: the matrix shape of tensor t (rows*cols == numel), or
+ * 0, 0 for tensors Muon skips (norms, biases: left untouched).  SelectRoot
+ * (R24): matrices by decreasing rows*cols*min(rows,cols), each to the least
+ * loaded rank (ties: the rank owning most of it, then the lowest rank) --
+ * identical on every rank.  precision RSDB_F32: Newton-Schulz in fp32
+ * (cuBLAS SGEMM); RSDB_BF16: bf16 operands, fp32 accumulation (tensor cores,
+ * Muon's reference precision).  comm NULL iff world 1. */
+rsdb_status rsdb_muon_create(const rsdb_layout*, const int64_t* rows, const int64_t* cols,
+                             rsdb_comm* comm_or_null, int32_t rank, int32_t precision,
+                             rsdb_muon** out);
+/* Host only (no CUDA): SelectRoot (R24) for every tensor -> roots[n] (-1 for
+ * non-matrices); the assignment rsdb_muon_create uses.  EINVAL on bad shapes. */
+rsdb_status rsdb_muon_select_roots(const rsdb_layout*, const int64_t* rows, const int64_t* cols,
+                                   int32_t* roots);
+int32_t rsdb_muon_root(const rsdb_muon*, int32_t tensor);    /* -1: not a matrix */
+int64_t rsdb_muon_workspace_bytes(const rsdb_muon*);         /* this rank's */
+rsdb_status rsdb_muon_bind(rsdb_muon*, const rsdb_muon_bufs*);
+/* One Muon step of every matrix of the unit (Algorithm 2): momentum on the
+ * shard; ONE kernel gathers every matrix onto its root over NVLink
+ * (Redistribute(u, RaggedShard(r))); Newton-Schulz on the root; ONE kernel
+ * returns each owner its piece and applies w -= eta sqrt(max(1,rows/cols)) o
+ * (Redistribute(o, p) + update, bf16 shard written).  p2p (NULL iff world 1)
+ * must map every rank's `u` and `workspace`. */
+rsdb_status rsdb_muon_step(rsdb_muon*, rsdb_p2p* p2p_or_null, const rsdb_muon_cfg*, void* stream);
+void rsdb_muon_free(rsdb_muon*);
+
 #ifdef __cplusplus
 }
 #endif

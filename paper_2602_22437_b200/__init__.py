@@ -566,3 +566,67 @@ class Fp8Unit:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- N3: distributed Muon
+class MuonConfig(_c.MuonCfg):
+    """R21-R23 defaults: eta 0.02, Nesterov momentum 0.95, NS eps 1e-7, 5 steps."""
+
+    def __init__(self, lr=0.02, momentum=0.95, eps=1e-7, ns_steps=5):
+        super().__init__(lr, momentum, eps, ns_steps)
+
+
+def muon_select_roots(layout: Layout, shapes) -> List[int]:
+    """SelectRoot (R24) on the host: the root rank of every matrix (-1: skipped)."""
+    rows = _c.i64_array([s[0] if s else 0 for s in shapes])
+    cols = _c.i64_array([s[1] if s else 0 for s in shapes])
+    out = (C.c_int32 * max(1, len(shapes)))()
+    check(lib.rsdb_muon_select_roots(layout.handle, rows, cols, out))
+    return list(out[:len(shapes)])
+
+
+class Muon:
+    """Distributed Muon over a RaggedShard unit (Algorithm 2; rsdb_muon_*).
+    shapes[t] = (rows, cols) for the matrices Muon updates, None otherwise.
+    precision "f32" (SGEMM Newton-Schulz) or "bf16" (tensor cores)."""
+
+    def __init__(self, layout: Layout, shapes, rank: int, comm: Optional[Comm] = None,
+                 precision: str = "f32"):
+        rows = _c.i64_array([s[0] if s else 0 for s in shapes])
+        cols = _c.i64_array([s[1] if s else 0 for s in shapes])
+        prec = {"f32": RSDB_F32, "bf16": RSDB_BF16}[precision]
+        h = C.c_void_p()
+        check(lib.rsdb_muon_create(layout.handle, rows, cols, comm.handle if comm else None, rank, prec,
+                                   C.byref(h)))
+        self._h = h
+        self._keep = (layout,)
+        self.n = len(shapes)
+
+    @property
+    def workspace_bytes(self) -> int:
+        return lib.rsdb_muon_workspace_bytes(self._h)
+
+    def root(self, t: int) -> int:
+        return lib.rsdb_muon_root(self._h, t)
+
+    def bind(self, master, momentum, grad, u, workspace, param_bf16=None) -> None:
+        self._bufs = (master, momentum, grad, u, workspace, param_bf16)
+        b = _c.MuonBufs(_ptr(master), _ptr(momentum), _ptr(grad), _ptr(u), _ptr(param_bf16),
+                        _ptr(workspace))
+        check(lib.rsdb_muon_bind(self._h, C.byref(b)))
+
+    def step(self, cfg: Optional[MuonConfig] = None, p2p: Optional["P2P"] = None, stream=None) -> None:
+        cfg = cfg or MuonConfig()
+        check(lib.rsdb_muon_step(self._h, p2p.handle if p2p is not None else None, C.byref(cfg),
+                                 _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.rsdb_muon_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

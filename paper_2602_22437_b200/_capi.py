@@ -46,6 +46,16 @@ class Segment(C.Structure):
     _fields_ = [("src", vp), ("dst", vp), ("numel", i64)]
 
 
+class MuonCfg(C.Structure):
+    _fields_ = [("lr", C.c_double), ("momentum", C.c_double), ("eps", C.c_double),
+                ("ns_steps", i32)]
+
+
+class MuonBufs(C.Structure):
+    _fields_ = [("master", vp), ("momentum", vp), ("grad", vp), ("u", vp), ("param_bf16", vp),
+                ("workspace", vp)]
+
+
 # name: (restype, argtypes)
 _SIGS = {
     "rsdb_last_error": (C.c_char_p, []),
@@ -115,6 +125,13 @@ _SIGS = {
     "rsdb_fp8_unit_first_slot": (i64, [vp]),
     "rsdb_fp8_quantize_all_gather": (i32, [vp, vp, vp]),
     "rsdb_fp8_unit_free": (None, [vp]),
+    "rsdb_muon_create": (i32, [vp, P_i64, P_i64, vp, i32, i32, C.POINTER(vp)]),
+    "rsdb_muon_select_roots": (i32, [vp, P_i64, P_i64, P_i32]),
+    "rsdb_muon_root": (i32, [vp, i32]),
+    "rsdb_muon_workspace_bytes": (i64, [vp]),
+    "rsdb_muon_bind": (i32, [vp, C.POINTER(MuonBufs)]),
+    "rsdb_muon_step": (i32, [vp, vp, C.POINTER(MuonCfg), vp]),
+    "rsdb_muon_free": (None, [vp]),
 }
 EXPORTED = tuple(_SIGS)
 

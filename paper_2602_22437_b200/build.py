@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "librsdb.so")
-SOURCES = ["planner.cc", "capi.cc", "kernels.cu", "p2p.cu", "fp8.cu"]
+SOURCES = ["planner.cc", "capi.cc", "kernels.cu", "p2p.cu", "fp8.cu", "muon.cu"]
 HEADERS = ["planner.hpp", "kernels.cuh", "adam_dev.cuh", "p2p_dev.cuh"]
 
 
@@ -36,6 +36,15 @@ def nccl_dir() -> str:
         if os.path.exists(os.path.join(c, "include", "nccl.h")):
             return c
     raise RuntimeError("NCCL headers not found (expected site-packages/nvidia/nccl)")
+
+
+def cublas_dir() -> str:
+    """The torch-bundled cuBLAS (the same library torch loads: one cuBLAS in
+    the process); used for the Muon Newton-Schulz GEMMs (N3)."""
+    c = os.path.join(os.path.dirname(nccl_dir()), "cublas")
+    if os.path.exists(os.path.join(c, "lib", "libcublas.so.12")):
+        return c
+    raise RuntimeError("cuBLAS not found (expected site-packages/nvidia/cublas)")
 
 
 def nvcc() -> str:
@@ -59,6 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
     nd = nccl_dir()
+    cd = cublas_dir()
     bdir = os.path.join(ROOT, "build")
     os.makedirs(bdir, exist_ok=True)
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
@@ -67,6 +77,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
+           "-L", os.path.join(cd, "lib"), "-l:libcublas.so.12",
+           "-Xlinker", "-rpath," + os.path.join(cd, "lib"),
            "-o", OUT + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(bdir, "ptxas.log"), "w") as f:

@@ -94,4 +94,24 @@ cudaError_t launch_fp8_quant_ag(const Fp8Tile* tiles, int64_t ntiles, const floa
                                 const P2PPtrs& codes, const P2PPtrs& scales, int m, int rank,
                                 const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
 
+// ---- N3: distributed Muon (muon.cu) ----
+struct MuonSeg {
+  int64_t src_off;      // element offset in the source (peer's u shard / root's workspace)
+  int64_t dst_off;      // element offset in the destination (root workspace / local master)
+  int64_t n;            // elements
+  int64_t chunk_begin;  // prefix sum of 8192-element chunks
+  int32_t peer;         // rank owning the source
+  float coef;           // apply: eta * sqrt(max(1, rows/cols))
+};
+static_assert(sizeof(MuonSeg) == 40, "MuonSeg is 40 bytes");
+cudaError_t launch_muon_momentum(const int64_t* segs, int64_t nseg, int64_t max_n, float* buf,
+                                 const float* grad, float* u, float mu, cudaStream_t st);
+cudaError_t launch_muon_gather(const MuonSeg* segs, int64_t nseg, int64_t nchunks, const P2PPtrs& u,
+                               void* ws, int bf16, int m, int rank, const P2PSignals* sg, uint64_t epoch,
+                               cudaStream_t st);
+cudaError_t launch_muon_apply(const MuonSeg* segs, int64_t nseg, int64_t nchunks, const P2PPtrs& ws,
+                              int bf16, float* master, void* param_bf16, int m, int rank,
+                              const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
+cudaError_t launch_muon_normalize(void* x, int64_t n, int bf16, double* ss, double eps, cudaStream_t st);
+
 }  // namespace rsdb

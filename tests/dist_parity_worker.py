@@ -8,8 +8,9 @@ Per unit: AllGather (bit exact), fused cast/scale + ReduceScatter (bit exact
 on dyadic synth grads; error bound on random-normal bf16 grads), 8-bit Adam
 (codes +-1, params 1e-5), then a second AllGather that must equal the
 concatenation of every rank's oracle parameter shard (bf16, within 1 ulp);
-the fused RS+Adam(+AG) kernels vs the unfused sequence (bit exact); and the
-N2 FP8 block quantization + AllGather vs oracle/fp8.py (bit exact).
+the fused RS+Adam(+AG) kernels vs the unfused sequence (bit exact); the
+N2 FP8 block quantization + AllGather vs oracle/fp8.py (bit exact); and N3
+distributed Muon vs oracle/muon.py (fp32 and bf16 Newton-Schulz tolerances).
 Exit code 0 iff every check passed on every rank.
 """
 import os
@@ -275,6 +276,14 @@ def main():
             break
     fu.close()
     p2p.close()
+    # ---- N3: distributed Muon (Algorithm 2): gather to roots, NS, scatter + apply
+    from test_gpu_muon import SHAPES as MUON_SHAPES, muon_case
+    for prec in ("f32", "bf16"):
+        good, why = muon_case(world, rank, MUON_SHAPES, 5, 2, prec, comm=comm,
+                              p2p_factory=lambda uu, ww: R.P2P(comm, [uu, ww]))
+        if not good:
+            ok = False
+            msgs.append(f"Muon {prec}: " + "; ".join(why[:4]))
     comm.close()
     flag = torch.tensor([0 if ok else 1])
     dist.all_reduce(flag)

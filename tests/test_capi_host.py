@@ -263,3 +263,28 @@ def test_device_calls_fail_loudly_without_gpu():
     with pytest.raises(R.RsdbError) as e:
         R.Comm(b"\0" * 128, 1, 0, 0)
     assert e.value.status == _capi.RSDB_ECUDA
+
+
+def test_muon_select_roots_matches_oracle():
+    """N3 SelectRoot (R24): the C++ assignment equals the oracle's on random
+    layouts (matrices straddling ranks, skipped 1-D tensors) and on the
+    Llama-3-8B layer unit at element granularity."""
+    from oracle import muon as MU
+    rng = random.Random(11)
+    for _ in range(300):
+        m = rng.randint(1, 8)
+        shapes = [None if rng.random() < 0.25 else (rng.randint(1, 40), rng.randint(1, 40))
+                  for _ in range(rng.randint(1, 12))]
+        es = [s[0] * s[1] if s else rng.randint(1, 50) for s in shapes]
+        o = P.plan(es, [1] * len(es), m, 8)
+        c = R.plan(es, [1] * len(es), m, elem_bytes=2)
+        assert R.muon_select_roots(c, shapes) == MU.select_roots(o, shapes)
+    u = W.llama3_8b_layer(0)
+    shapes = [t.shape if len(t.shape) == 2 else None for t in u.tensors]
+    es = [t.numel for t in u.tensors]
+    for m in (2, 4, 8):
+        o = P.plan(es, [1] * len(es), m, 8)
+        c = R.plan(es, [1] * len(es), m, elem_bytes=2)
+        assert R.muon_select_roots(c, shapes) == MU.select_roots(o, shapes)
+    with pytest.raises(R.RsdbError):
+        R.muon_select_roots(R.plan([12], [1], 1), [(5, 3)])  # rows * cols != numel
