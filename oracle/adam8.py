@@ -36,6 +36,7 @@ from typing import Sequence, Tuple
 
 import numpy as np
 
+from . import codemap as CM
 from .dbuffer import to_bf16_rne
 
 f32 = np.float32
@@ -100,7 +101,7 @@ def adam_block_update(p, g, mt, vt, sc):
 
 def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: np.ndarray,
                    m_abs: np.ndarray, v_abs: np.ndarray, blocks: Sequence[Tuple[int, int]],
-                   cfg: AdamCfg, step: int, out_bf16: bool = True):
+                   cfg: AdamCfg, step: int, out_bf16: bool = True, codec: str = "linear"):
     """One 8-bit Adam step on a rank's local shard, block by block.
 
     master/grad: fp32 [S]; m_q int8 [S]; v_q uint8 [S]; m_abs/v_abs fp32
@@ -109,7 +110,11 @@ def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: n
     pitch) -- a block is the set of its elements, the update is the same.
     Returns new copies (master, m_q, v_q, m_abs, v_abs, param_shard) where
     param_shard is bf16 bit patterns (uint16) or fp32; positions outside any
-    block are left unchanged (param shard: 0)."""
+    block are left unchanged (param shard: 0).  codec "dynamic": both moments
+    use the dynamic tree maps of oracle/codemap.py (R25; m_q holds uint8 map
+    indices) instead of the linear absmax codes (R9)."""
+    if codec not in ("linear", "dynamic"):
+        raise ValueError(codec)
     sc = host_scalars(cfg, step)
     master = np.array(master, dtype=np.float32, copy=True)
     m_q, v_q = np.array(m_q, copy=True), np.array(v_q, copy=True)
@@ -122,12 +127,20 @@ def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: n
         else:  # 2-D tile: element (a, c) at off + a * pitch + c
             off, rows, cols, pitch = blk
             s = (off + np.arange(rows)[:, None] * pitch + np.arange(cols)[None, :]).ravel()
-        mt = dequantize(m_q[s], m_abs[b], signed=True)
-        vt = dequantize(v_q[s], v_abs[b], signed=False)
+        if codec == "linear":
+            mt = dequantize(m_q[s], m_abs[b], signed=True)
+            vt = dequantize(v_q[s], v_abs[b], signed=False)
+        else:
+            mt = CM.dyn_dequantize(m_q[s], m_abs[b], signed=True)
+            vt = CM.dyn_dequantize(v_q[s], v_abs[b], signed=False)
         p, m, v = adam_block_update(master[s], grad[s], mt, vt, sc)
         master[s] = p
-        m_q[s], m_abs[b] = quantize(m, signed=True)
-        v_q[s], v_abs[b] = quantize(v, signed=False)
+        if codec == "linear":
+            m_q[s], m_abs[b] = quantize(m, signed=True)
+            v_q[s], v_abs[b] = quantize(v, signed=False)
+        else:
+            m_q[s], m_abs[b] = CM.dyn_quantize(m, signed=True)
+            v_q[s], v_abs[b] = CM.dyn_quantize(v, signed=False)
         param[s] = to_bf16_rne(p) if out_bf16 else p
     return master, m_q, v_q, m_abs, v_abs, param
 
