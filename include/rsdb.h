@@ -244,6 +244,12 @@ typedef struct {
  * step >= 1 (EINVAL otherwise). */
 rsdb_status rsdb_step_8bit_adam(rsdb_unit*, const rsdb_adam_state*, const rsdb_adam_cfg*,
                                 int64_t step, void* stream);
+/* The same step with the dynamic code map (see
+ * rsdb_dbuffer_step_8bit_adam_dynamic); m_q is read and written as uint8. */
+rsdb_status rsdb_step_8bit_adam_dynamic(rsdb_unit*, const rsdb_adam_state*, const rsdb_adam_cfg*,
+                                        int64_t step, void* stream);
+/* Host only: the two 256-value maps (ascending fp32) the dynamic codec uses. */
+rsdb_status rsdb_dynamic_code_maps(float* m_map, float* v_map);
 
 /* ======================================================================== */
 /* Fused collectives over NVLink peer memory.              */
@@ -356,6 +362,14 @@ rsdb_status rsdb_dbuffer_reduce_scatter_adam(rsdb_dbuffer*, rsdb_p2p* p2p_or_nul
  * from their bases. */
 rsdb_status rsdb_dbuffer_reduce_scatter_adam_gather(rsdb_dbuffer*, rsdb_p2p* p2p_or_null,
                                                     const rsdb_adam_cfg*, int64_t step, void* stream);
+/* N2: the same one-launch 8-bit Adam with the DYNAMIC (tree) code map of
+ * Dettmers et al. (P:419 [dettmers8]; reading R25 in DESIGN.md) instead of
+ * the linear absmax code: m_q / v_q hold uint8 indices into the 256-value
+ * signed / unsigned maps (the code of 0 is 127 / 0), dequantisation
+ * map[code] * absmax, requantisation to the nearest map value of x / absmax
+ * (fp32, ties to the lower code). */
+rsdb_status rsdb_dbuffer_step_8bit_adam_dynamic(rsdb_dbuffer*, const rsdb_adam_cfg*, int64_t step,
+                                                void* stream);
 /* Grouped zero of every unit's gradient buffer ("zero"). */
 rsdb_status rsdb_dbuffer_zero_grads(rsdb_dbuffer*, void* stream);
 void rsdb_dbuffer_free(rsdb_dbuffer*);

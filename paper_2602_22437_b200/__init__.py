@@ -324,6 +324,22 @@ def step_8bit_adam(unit: Unit, master, m_q, v_q, m_absmax, v_absmax, cfg: AdamCo
     check(lib.rsdb_step_8bit_adam(unit.handle, C.byref(st), C.byref(cfg), step, _stream(stream)))
 
 
+def step_8bit_adam_dynamic(unit: Unit, master, m_q, v_q, m_absmax, v_absmax, cfg: AdamConfig,
+                           step: int, stream=None) -> None:
+    """a8 with the dynamic (tree) code map (N2, R25): m_q / v_q are uint8 map indices."""
+    st = _c.AdamState(_ptr(master), _ptr(m_q), _ptr(v_q), _ptr(m_absmax), _ptr(v_absmax))
+    check(lib.rsdb_step_8bit_adam_dynamic(unit.handle, C.byref(st), C.byref(cfg), step,
+                                          _stream(stream)))
+
+
+def dynamic_code_maps():
+    """The two 256-value maps (signed for m, unsigned for v) of the dynamic codec."""
+    m = (C.c_float * 256)()
+    v = (C.c_float * 256)()
+    check(lib.rsdb_dynamic_code_maps(m, v))
+    return list(m), list(v)
+
+
 # ---------------------------------------------------------------- N1: NVLink peer memory
 def ipc_handle(t) -> bytes:
     buf = C.create_string_buffer(_c.RSDB_IPC_BYTES)
@@ -483,6 +499,10 @@ class DBuffer:
         holds the full updated parameters (p2p maps GRAD_FULL and PARAM_FULL)."""
         check(lib.rsdb_dbuffer_reduce_scatter_adam_gather(
             self._h, p2p.handle if p2p is not None else None, C.byref(cfg), step, _stream(stream)))
+
+    def step_8bit_adam_dynamic(self, cfg: AdamConfig, step: int, stream=None) -> None:
+        """One launch of 8-bit Adam with the dynamic code map over every unit."""
+        check(lib.rsdb_dbuffer_step_8bit_adam_dynamic(self._h, C.byref(cfg), step, _stream(stream)))
 
     def zero_grads(self, stream=None) -> None:
         check(lib.rsdb_dbuffer_zero_grads(self._h, _stream(stream)))

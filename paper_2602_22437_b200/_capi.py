@@ -112,6 +112,9 @@ _SIGS = {
     "rsdb_dbuffer_unit": (vp, [vp, i32]),
     "rsdb_dbuffer_num_blocks": (i64, [vp]),
     "rsdb_dbuffer_step_8bit_adam": (i32, [vp, C.POINTER(AdamCfg), i64, vp]),
+    "rsdb_dbuffer_step_8bit_adam_dynamic": (i32, [vp, C.POINTER(AdamCfg), i64, vp]),
+    "rsdb_step_8bit_adam_dynamic": (i32, [vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64, vp]),
+    "rsdb_dynamic_code_maps": (i32, [C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rsdb_dbuffer_zero_grads": (i32, [vp, vp]),
     "rsdb_dbuffer_reduce_scatter_adam": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_reduce_scatter_adam_gather": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),

@@ -502,6 +502,29 @@ rsdb_status rsdb_step_8bit_adam(rsdb_unit* u, const rsdb_adam_state* st, const r
   return OK_CLEAR();
 }
 
+rsdb_status rsdb_step_8bit_adam_dynamic(rsdb_unit* u, const rsdb_adam_state* st, const rsdb_adam_cfg* cfg,
+                                        int64_t step, void* stream) {
+  if (!u || !st) return fail(RSDB_EINVAL, "null argument");
+  rsdb::AdamScalars s;
+  if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
+  if (u->nblocks == 0) return OK_CLEAR();
+  if (!st->master_f32 || !st->m_q || !st->v_q || !st->m_absmax || !st->v_absmax)
+    return fail(RSDB_EINVAL, "null state pointer");
+  rsdb::AdamPtrs p{static_cast<float*>(st->master_f32), static_cast<int8_t*>(st->m_q),
+                   static_cast<uint8_t*>(st->v_q),       static_cast<float*>(st->m_absmax),
+                   static_cast<float*>(st->v_absmax),    static_cast<const float*>(u->bufs.grad_f32),
+                   u->bufs.param_full,                   u->L.elem_bytes == 2};
+  CUDA_TRY(rsdb::launch_adam8_dyn(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
+                                  S_(stream)));
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_dynamic_code_maps(float* m_map, float* v_map) {
+  if (!m_map || !v_map) return fail(RSDB_EINVAL, "null argument");
+  rsdb::dyn_maps(m_map, v_map);
+  return OK_CLEAR();
+}
+
 // ---------------------------------------------------------------------------
 // fused collectives over NVLink peer memory (N1)
 // ---------------------------------------------------------------------------
@@ -986,6 +1009,25 @@ rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer* d, const rsdb_adam_cfg* cf
                    d->param_bf16};
   CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(d->blocks.p), d->nblocks, p, s, 0,
                               S_(stream)));
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_step_8bit_adam_dynamic(rsdb_dbuffer* d, const rsdb_adam_cfg* cfg, int64_t step,
+                                                void* stream) {
+  if (!d) return fail(RSDB_EINVAL, "null dbuffer");
+  rsdb::AdamScalars s;
+  if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
+  if (d->nblocks == 0) return OK_CLEAR();
+  rsdb::AdamPtrs p{static_cast<float*>(d->base[RSDB_KIND_MASTER]),
+                   static_cast<int8_t*>(d->base[RSDB_KIND_MQ]),
+                   static_cast<uint8_t*>(d->base[RSDB_KIND_VQ]),
+                   static_cast<float*>(d->base[RSDB_KIND_MABS]),
+                   static_cast<float*>(d->base[RSDB_KIND_VABS]),
+                   static_cast<const float*>(d->base[RSDB_KIND_GRAD_F32]),
+                   d->base[RSDB_KIND_PARAM_FULL],
+                   d->param_bf16};
+  CUDA_TRY(rsdb::launch_adam8_dyn(static_cast<const rsdb::AdamBlock*>(d->blocks.p), d->nblocks, p, s,
+                                  S_(stream)));
   return OK_CLEAR();
 }
 

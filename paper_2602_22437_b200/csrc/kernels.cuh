@@ -94,6 +94,12 @@ cudaError_t launch_fp8_quant_ag(const Fp8Tile* tiles, int64_t ntiles, const floa
                                 const P2PPtrs& codes, const P2PPtrs& scales, int m, int rank,
                                 const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
 
+// ---- N2: 8-bit Adam with the dynamic (tree) code map (adam_dyn.cu) ----
+// m_q / v_q hold uint8 indices into the signed / unsigned maps of R25.
+cudaError_t launch_adam8_dyn(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p, const AdamScalars& s,
+                             cudaStream_t st);
+void dyn_maps(float m_map[256], float v_map[256]);  // host: the two maps (R25)
+
 // ---- N3: distributed Muon (muon.cu) ----
 struct MuonSeg {
   int64_t src_off;      // element offset in the source (peer's u shard / root's workspace)

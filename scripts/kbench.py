@@ -45,12 +45,25 @@ def main():
     e1.record(st)
     st.synchronize()
     cast_ms = e0.elapsed_time(e1) / reps
+    # 8-bit Adam with the dynamic (tree) code map (N2, R25) on the same DBuffer
+    # (the warm linear codes are valid uint8 map indices too)
+    for t in range(1, 3):
+        db.step_8bit_adam_dynamic(cfg, t, st)
+    st.synchronize()
+    e0.record(st)
+    for t in range(3, 3 + reps):
+        db.step_8bit_adam_dynamic(cfg, t, st)
+    e1.record(st)
+    st.synchronize()
+    dyn_ms = e0.elapsed_time(e1) / reps
     peak, _ = bench.load_peaks()
     out = {"variant": os.environ.get("RSDB_ADAM_KERNEL", "default"),
            "adam_ms": adam_ms, "adam_gbs": ab["adam"] / adam_ms / 1e6,
            "adam_frac": ab["adam"] / adam_ms / 1e6 / peak,
            "cast_ms": cast_ms, "cast_gbs": ab["cast"] / cast_ms / 1e6,
-           "cast_frac": ab["cast"] / cast_ms / 1e6 / peak}
+           "cast_frac": ab["cast"] / cast_ms / 1e6 / peak,
+           "adam_dynamic_ms": dyn_ms, "adam_dynamic_gbs": ab["adam"] / dyn_ms / 1e6,
+           "adam_dynamic_frac": ab["adam"] / dyn_ms / 1e6 / peak}
     print(json.dumps(out), flush=True)
     db.close()
     comm.close()

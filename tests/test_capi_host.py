@@ -288,3 +288,12 @@ def test_muon_select_roots_matches_oracle():
         assert R.muon_select_roots(c, shapes) == MU.select_roots(o, shapes)
     with pytest.raises(R.RsdbError):
         R.muon_select_roots(R.plan([12], [1], 1), [(5, 3)])  # rows * cols != numel
+
+
+def test_dynamic_code_maps_match_oracle():
+    """N2 dynamic codec (R25): the C++ maps (built independently in double) are
+    bit-identical to the oracle's."""
+    from oracle import codemap as CM
+    m, v = R.dynamic_code_maps()
+    assert np.array_equal(np.array(m, np.float32).view(np.uint32), CM.dynamic_map(True).view(np.uint32))
+    assert np.array_equal(np.array(v, np.float32).view(np.uint32), CM.dynamic_map(False).view(np.uint32))

@@ -16,6 +16,7 @@ import torch
 
 import paper_2602_22437_b200 as R
 from oracle import adam8 as OA
+from oracle import codemap as CM
 from oracle import dbuffer as OD
 from oracle import planner as OP
 from synth import hashgen as H
@@ -98,7 +99,7 @@ def test_unit_rejects_misaligned_buffers():
 
 
 # ------------------------------------------------------------------ a8
-def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None):
+def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None, codec="linear"):
     gs = [min(q, e) for e in es]
     o, c = _plans(es, gs, m, eb)
     E = sum(es)
@@ -119,7 +120,18 @@ def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None):
     nb = u.num_blocks
     blocks_c = c.rank_blocks(rank, q)
     assert len(blocks_c) == nb
-    if warm:
+    if codec == "dynamic":  # uint8 indices into the dynamic maps (R25); zero state = code of 0
+        if warm:
+            mq = H.codes_torch(seed, H.STREAM_MCODE, rank * S, S, False, device="cuda")
+            vq = H.codes_torch(seed, H.STREAM_VCODE, rank * S, S, False, device="cuda")
+            ma = H.absmax_torch(seed, H.STREAM_ABSM, rank * 100000, nb, 14, device="cuda")
+            va = H.absmax_torch(seed, H.STREAM_ABSV, rank * 100000, nb, 22, device="cuda")
+        else:
+            mq = torch.full((S,), CM.zero_code(True), dtype=torch.uint8, device="cuda")
+            vq = torch.full((S,), CM.zero_code(False), dtype=torch.uint8, device="cuda")
+            ma = torch.zeros(nb, dtype=torch.float32, device="cuda")
+            va = torch.zeros(nb, dtype=torch.float32, device="cuda")
+    elif warm:
         mq = H.codes_torch(seed, H.STREAM_MCODE, rank * S, S, True, device="cuda")
         vq = H.codes_torch(seed, H.STREAM_VCODE, rank * S, S, False, device="cuda")
         ma = H.absmax_torch(seed, H.STREAM_ABSM, rank * 100000, nb, 14, device="cuda")
@@ -131,14 +143,15 @@ def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None):
         va = torch.zeros(nb, dtype=torch.float32, device="cuda")
     ins = [t.cpu().numpy().copy() for t in (master, mq, vq, ma, va)]
     cfg = R.AdamConfig()
-    R.step_8bit_adam(u, master, mq, vq, ma, va, cfg, step)
+    (R.step_8bit_adam_dynamic if codec == "dynamic" else R.step_8bit_adam)(
+        u, master, mq, vq, ma, va, cfg, step)
     torch.cuda.synchronize()
     # ----- oracle side (oracle layout) -----
     blocks_o = OP.rank_blocks(o, rank, q)
     assert [tuple(b) for b in blocks_o] == blocks_c
     g_or = OD.shard(o, OD.place_logical(o, g_log.numpy()), rank)
     ref = OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], blocks_o,
-                            OA.AdamCfg(), step, out_bf16=(eb == 2))
+                            OA.AdamCfg(), step, out_bf16=(eb == 2), codec=codec)
     _check_adam(o, rank, blocks_o, (master, mq, vq, ma, va, param_full), ref, ins, eb, cfg.lr)
     return u
 
@@ -200,6 +213,13 @@ ADAM_CASES = [
 @pytest.mark.parametrize("es,q,m,eb,rank,step,warm", ADAM_CASES)
 def test_adam8_parity(es, q, m, eb, rank, step, warm):
     _adam_case(es, q, m, eb, rank, step, warm)
+
+
+@pytest.mark.parametrize("es,q,m,eb,rank,step,warm", [ADAM_CASES[i] for i in (0, 1, 3, 4, 5, 7)])
+def test_adam8_dynamic_codec_parity(es, q, m, eb, rank, step, warm):
+    """N2: the dynamic (tree) code map codec (R25) against the oracle: codes
+    (map indices) +-1, params 1e-5 (|p| + lr), absmax 1e-6."""
+    _adam_case(es, q, m, eb, rank, step, warm, codec="dynamic")
 
 
 TILE_CASES = [
