@@ -1,0 +1,130 @@
+#!/usr/bin/env python
+"""FSDP-size sweep and DBuffer memory accounting (P:369, P:372-373,
+P:493).  For a workload and a list of FSDP sizes m, per rank 0:
+
+  plan      S, padding % and planner time of every unit (C++ planner)
+  wire      AllGather / ReduceScatter bytes into the rank per step (bf16)
+  dbuffer   bytes of the batched DBuffer arenas (rsdb_arena_sizes: one
+            allocation per buffer kind, 256-B aligned units)
+  fsdp2     the same buffers allocated per parameter in FSDP2's per-parameter
+            layout: Shard(0) pads dim 0 to a multiple of m, and every kind of
+            every tensor is its own allocation, rounded to the caching
+            allocator's 512 B (the request; reserved segments come on top)
+
+With --measure (one GPU) both allocation patterns are replayed through
+PyTorch's caching allocator and torch.cuda.memory_reserved() is reported --
+the paper's "peak reserved" comparison (batched DBuffer -12 % vs
+FSDP2's per-parameter eager allocation).  One JSON line per m.
+
+  python scripts/fsdp_sweep.py --workload llama1b --ms 2,4,8,16,64 [--measure]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2602_22437_b200 as R  # noqa: E402
+from synth import workloads as W  # noqa: E402
+
+QBLOCK = 2048
+KINDS = ("param_full", "grad_full", "grad_f32", "master", "m_q", "v_q", "m_absmax", "v_absmax")
+
+
+def workload(name):
+    return {"llama1b": lambda: W.llama32_1b(),
+            "llama8b": lambda: W.llama3_8b_muon(),
+            "dsv3": lambda: W.dsv3_moe()}[name]()
+
+
+def ceil_div(a, b):
+    return -(-a // b)
+
+
+def fsdp2_requests(unit, m):
+    """Per-parameter allocations of FSDP2's layout (rank 0): every tensor is
+    Shard(0) with dim 0 padded to a multiple of m; per kind, the same buffers
+    as one DBuffer unit holds (gathered bf16 param and grad, fp32 RS buffer,
+    fp32 master, 8-bit states, per-2048-block absmax)."""
+    reqs = []
+    for t in unit.tensors:
+        rows = t.shape[0]
+        rest = t.numel // rows
+        s = ceil_div(rows, m) * rest  # shard elements
+        nb = ceil_div(s, QBLOCK)
+        reqs += [m * s * 2, m * s * 2, m * s * 4, s * 4, s, s, nb * 4, nb * 4]
+    return reqs
+
+
+def round512(n):
+    return max(512, ceil_div(n, 512) * 512) if n > 0 else 0
+
+
+def sweep_one(w, m, measure):
+    units = list(W.all_units(w))
+    t0 = time.perf_counter()
+    lays, qspec = [], []
+    for u in units:
+        es = [t.numel for t in u.tensors]
+        gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+        lays.append(R.plan(es, gs, m, elem_bytes=2))
+        qspec.append([("flat", min(QBLOCK, g)) for g in gs])  # 8-bit state blocks stay intact
+    plan_s = time.perf_counter() - t0
+    E = sum(l.E for l in lays)
+    padded = sum(l.m * l.S for l in lays)
+    sizes, _ = R.arena_sizes(lays, 0, QBLOCK, 256, qspec=qspec)
+    reqs = [r for u in units for r in fsdp2_requests(u, m)]
+    fsdp2_pad_elems = sum(ceil_div(t.shape[0], m) * m * (t.numel // t.shape[0]) for u in units
+                          for t in u.tensors)
+    # FSDP2 Shard(0) that keeps the declared row blocks intact: rows per rank
+    # rounded up to a multiple of the block's rows (SURVEY config 4 "row-wise-128")
+    blk_pad_elems = 0
+    for u in units:
+        for t in u.tensors:
+            rows, rest = t.shape[0], t.numel // t.shape[0]
+            br = max(1, R.block_elems(t.shape, t.gran) // rest) if len(t.shape) > 1 else 1
+            blk_pad_elems += ceil_div(ceil_div(rows, m), br) * br * m * rest
+    line = {"workload": w.name, "m": m, "units": len(units), "params": E,
+            "plan_s_total": plan_s,
+            "ragged_padding_pct": 100.0 * (padded - E) / E,
+            "fsdp2_dim0_padding_pct": 100.0 * (fsdp2_pad_elems - E) / E,
+            "fsdp2_rowwise_block_padding_pct": 100.0 * (blk_pad_elems - E) / E,
+            "ag_wire_bytes_per_rank": sum((l.m - 1) * l.S * 2 for l in lays),
+            "rs_wire_bytes_per_rank_bf16": sum((l.m - 1) * l.S * 2 for l in lays),
+            "dbuffer_bytes": sum(sizes), "dbuffer_bytes_by_kind": dict(zip(KINDS, sizes)),
+            "fsdp2_requested_bytes": sum(reqs), "fsdp2_allocations": len(reqs),
+            "fsdp2_rounded_bytes": sum(round512(r) for r in reqs)}
+    line["fsdp2_over_dbuffer"] = line["fsdp2_rounded_bytes"] / max(1, line["dbuffer_bytes"])
+    if measure:
+        import torch
+        torch.cuda.empty_cache()
+        base = torch.cuda.memory_reserved()
+        arenas = [torch.empty(max(1, s), dtype=torch.uint8, device="cuda") for s in sizes]
+        line["dbuffer_reserved"] = torch.cuda.memory_reserved() - base
+        del arenas
+        torch.cuda.empty_cache()
+        base = torch.cuda.memory_reserved()
+        bufs = [torch.empty(r, dtype=torch.uint8, device="cuda") for r in reqs if r > 0]
+        line["fsdp2_reserved"] = torch.cuda.memory_reserved() - base
+        del bufs
+        torch.cuda.empty_cache()
+        line["reserved_fsdp2_over_dbuffer"] = line["fsdp2_reserved"] / max(1, line["dbuffer_reserved"])
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="llama1b", choices=["llama1b", "llama8b", "dsv3"])
+    ap.add_argument("--ms", default="2,4,8,16,32,64")
+    ap.add_argument("--measure", action="store_true")
+    args = ap.parse_args()
+    w = workload(args.workload)
+    for m in [int(x) for x in args.ms.split(",")]:
+        print(json.dumps(sweep_one(w, m, args.measure)), flush=True)
+
+
+if __name__ == "__main__":
+    main()

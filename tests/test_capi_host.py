@@ -297,3 +297,27 @@ def test_dynamic_code_maps_match_oracle():
     m, v = R.dynamic_code_maps()
     assert np.array_equal(np.array(m, np.float32).view(np.uint32), CM.dynamic_map(True).view(np.uint32))
     assert np.array_equal(np.array(v, np.float32).view(np.uint32), CM.dynamic_map(False).view(np.uint32))
+
+
+def test_fsdp_sweep_tool_accounting():
+    """N4 sweep tool (scripts/fsdp_sweep.py, analytic mode): the DBuffer bytes
+    are the exact sum of rsdb_arena_sizes, padding and wire bytes follow the
+    layouts, and FSDP2's dim-0 padding appears where rows % m != 0."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fsdp_sweep", os.path.join(ROOT, "scripts", "fsdp_sweep.py"))
+    fs = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fs)
+    w = W.dsv3_moe()
+    line = fs.sweep_one(w, 7, measure=False)
+    u = w.units[0]
+    gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+    lay = R.plan([t.numel for t in u.tensors], gs, 7)
+    sizes, _ = R.arena_sizes([lay], 0, 2048, 256, qspec=[[("flat", min(2048, g)) for g in gs]])
+    assert line["dbuffer_bytes"] == sum(sizes)
+    assert line["ag_wire_bytes_per_rank"] == 6 * lay.S * 2
+    assert abs(line["ragged_padding_pct"] - 100.0 * (7 * lay.S - lay.E) / lay.E) < 1e-9
+    assert line["fsdp2_dim0_padding_pct"] > 0  # rows not divisible by 7 pad dim 0
+    assert line["fsdp2_allocations"] == 8 * len(u.tensors)
+    # SURVEY §8(d) config 4: row-wise-128 padding 0.24 / 0.86 / 2.12 % at m = 2 / 4 / 8
+    for m, pct in ((2, 0.24), (4, 0.86), (8, 2.12)):
+        assert abs(fs.sweep_one(w, m, measure=False)["fsdp2_rowwise_block_padding_pct"] - pct) < 0.006
