@@ -728,9 +728,12 @@ static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state
                     static_cast<float*>(st->v_absmax),    nullptr,
                     u->bufs.param_full,                   1};
   const float scale = float(1.0 / double(m));
+  // absmax chunks by TMA: arena-backed state (padded to 16 blocks) or whole 16-B chunks
+  const int abs_tma = aligned16(st->m_absmax) && aligned16(st->v_absmax) &&
+                      (st == &u->bound_state || u->nblocks % 4 == 0);
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, g, m,
                                     scale, ap, s, m > 1 ? &sg : nullptr, u->rank,
-                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr));
+                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr, abs_tma));
   return OK_CLEAR();
 }
 
@@ -960,7 +963,8 @@ static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
                     1};
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(d->blocks_fused.p), d->nblocks, g,
                                     m, float(1.0 / double(m)), ap, s, m > 1 ? &sg : nullptr, d->rank,
-                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr));
+                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr,
+                                    aligned16(d->base[RSDB_KIND_MABS]) && aligned16(d->base[RSDB_KIND_VABS])));
   return OK_CLEAR();
 }
 

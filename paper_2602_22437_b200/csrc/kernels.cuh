@@ -76,11 +76,13 @@ cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int 
 // a6 + a7 + a8 fused: ReduceScatter of the bf16 gradients over NVLink and the
 // 8-bit Adam update of the local shard in one kernel (sg may be null iff m == 1);
 // push_params non-null: also a4 -- every updated bf16 parameter is stored into
-// every peer's parameter array (AllGather fused into the step).
+// every peer's parameter array (AllGather fused into the step).  abs_tma: the
+// absmax arrays are 16-B aligned and readable in whole 16-B chunks around
+// every slot (DBuffer arenas), so they are fetched with the block's TMA.
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
-                               const P2PPtrs* push_params = nullptr);
+                               const P2PPtrs* push_params = nullptr, int abs_tma = 0);
 
 // ---- N2: FP8 E4M3 block quantization fused with the AllGather (fp8.cu) ----
 struct Fp8Tile {

@@ -581,7 +581,8 @@ template <int M>
 struct RsaGeom {
   static constexpr int STAGES = M <= 4 ? 3 : 2;  // default ring depth (RSDB_RSA_STAGES overrides)
   static constexpr int G_BYTES = M * ADAM_TILE * 2;
-  static constexpr int STAGE_BYTES = G_BYTES + ADAM_TILE * 4 + ADAM_TILE * 2;
+  static constexpr int ABS_OFF = G_BYTES + ADAM_TILE * 6;  // 16-B chunks holding the block's absmax
+  static constexpr int STAGE_BYTES = ABS_OFF + 32;
 };
 
 __device__ __forceinline__ bool rsa_fits(const AdamBlock& b) {
@@ -608,6 +609,8 @@ struct PeerPush {
   }
 };
 
+// Single-role variant: all 128 threads compute; thread 0 also issues the
+// refill of the stage it just consumed, from the after-reduce hook.
 template <int M, bool PARAM_BF16, bool SYNC, bool PUSH>
 __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __restrict__ tbl,
                                                             int64_t nblocks, P2PPtrs grads,
@@ -735,6 +738,178 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
   if constexpr (SYNC) p2p_done(sg, rank, M, epoch);
 }
 
+
+// Warp-specialised: warps 0..3 compute (128 threads, the shared Adam tail),
+// warp 4 is the producer -- it reads the block table, writes each stage's
+// descriptor to shared memory and issues the stage's bulk copies (peers'
+// gradients, master, codes, absmax chunks), waiting on the stage's "empty"
+// mbarrier, which the compute warps arrive on as soon as the block is in
+// registers (after the absmax reduction).  So no compute warp ever waits on
+// a global load of the table or on issuing copies.
+constexpr int RSA_THREADS = RSA_NT + 32;
+
+template <int M, bool PARAM_BF16, bool SYNC, bool PUSH>
+__global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBlock* __restrict__ tbl,
+                                                                    int64_t nblocks, P2PPtrs grads,
+                                                                    P2PPtrs params, float scale, AdamPtrs P,
+                                                                    AdamScalars s, P2PSignals sg, int rank,
+                                                                    uint64_t epoch, int nst, int abs_tma) {
+  using Gm = RsaGeom<M>;
+  using G = AdamGeom<RSA_NT>;
+  using PushT = std::conditional_t<PUSH, PeerPush<M>, NoPush>;
+  extern __shared__ __align__(128) uint8_t rsa_smem[];
+  __shared__ __align__(8) uint64_t full[RSA_MAX_STAGES];
+  __shared__ __align__(8) uint64_t empty[RSA_MAX_STAGES];
+  __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
+  __shared__ AdamBlock sdesc[RSA_MAX_STAGES];
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < nst; ++st) {
+      tbar_init(&full[st]);   // one arrival: the producer's arrive.expect_tx
+      tbar_init(&empty[st]);  // one arrival: compute thread 0 after the block is in registers
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (SYNC) p2p_start(sg, rank, M, epoch);  // (contains a CTA-wide barrier)
+  else __syncthreads();
+
+  if (threadIdx.x >= RSA_NT) {  // ---------------- producer warp
+    if (threadIdx.x == RSA_NT) {
+      int it = 0, st = 0;
+      AdamBlock nb = blockIdx.x < nblocks ? tbl[blockIdx.x] : AdamBlock{};
+      for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+        const AdamBlock cur = nb;
+        if (b + gridDim.x < nblocks) nb = tbl[b + gridDim.x];  // prefetch the next entry
+        // reuse of stage st: wait for the compute warps' release of its previous
+        // block, i.e. completion number it/nst - 1 of empty[st]
+        if (it >= nst) tbar_wait(&empty[st], uint32_t((it / nst - 1) & 1));
+        uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
+        sdesc[st] = cur;
+        const bool fits = rsa_fits(cur);
+        const uint32_t L = uint32_t(cur.len);
+        const uint32_t tx = (fits ? L * (2 * M + 6) : 0u) + (abs_tma ? 32u : 0u);
+        if (tx == 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[st])) : "memory");
+        } else {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tbar_expect(&full[st], tx);
+          if (fits) {
+#pragma unroll
+            for (int r = 0; r < M; ++r)
+              tma_g2s(S + r * ADAM_TILE * 2, static_cast<const uint16_t*>(grads.p[r]) + cur.grad_off, L * 2,
+                      &full[st]);
+            tma_g2s(S + Gm::G_BYTES, P.master + cur.state_off, L * 4, &full[st]);
+            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + cur.state_off, L, &full[st]);
+            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + cur.state_off, L, &full[st]);
+          }
+          if (abs_tma) {  // the 16-B chunks holding the block's two absmax values
+            tma_g2s(S + Gm::ABS_OFF, P.mabs + (cur.slot & ~3), 16, &full[st]);
+            tma_g2s(S + Gm::ABS_OFF + 16, P.vabs + (cur.slot & ~3), 16, &full[st]);
+          }
+        }
+        if (++st == nst) st = 0;
+      }
+    }
+  } else {  // ---------------------------------------- compute warps
+    PushT push{};
+    if constexpr (PUSH) {
+#pragma unroll
+      for (int r = 0; r < M; ++r) push.peer[r] = static_cast<uint16_t*>(const_cast<void*>(params.p[r]));
+      push.rank = rank;
+    }
+    int it = 0, st = 0;
+    uint32_t phase = 0;
+    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+      float* rm = red_m[it & 1];
+      float* rv = red_v[it & 1];
+      auto release = [&]() {  // the whole stage is in registers: hand it back to the producer
+        if (threadIdx.x == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
+      };
+      tbar_wait(&full[st], phase);
+      const AdamBlock blk = sdesc[st];
+      float am0, av0;
+      if (abs_tma) {
+        const float* Sa = reinterpret_cast<const float*>(rsa_smem + st * Gm::STAGE_BYTES + Gm::ABS_OFF);
+        am0 = Sa[blk.slot & 3];
+        av0 = Sa[4 + (blk.slot & 3)];
+      } else {
+        am0 = P.mabs[blk.slot];
+        av0 = P.vabs[blk.slot];
+      }
+      const float sm = am0 / 127.0f;
+      const float sv = av0 / 255.0f;
+      BlockRegs<RSA_NT> r;
+      if (rsa_fits(blk)) {
+        const uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
+        const uint16_t* Sg = reinterpret_cast<const uint16_t*>(S);
+        const float* Sp = reinterpret_cast<const float*>(S + Gm::G_BYTES);
+        const uint8_t* Sm = S + Gm::G_BYTES + ADAM_TILE * 4;
+        const uint8_t* Sv = S + Gm::G_BYTES + ADAM_TILE * 5;
+#pragma unroll
+        for (int k = 0; k < G::Q; ++k) {
+          const int e0 = G::quad(k);
+          float a[4] = {0.f, 0.f, 0.f, 0.f};
+          float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+          uint32_t cm = 0x80808080u, cv = 0u;  // decode to m = v = 0 for masked quads
+          if (e0 < blk.len) {
+#pragma unroll
+            for (int q = 0; q < M; ++q) {  // rank order
+              const uint2 w = *reinterpret_cast<const uint2*>(Sg + q * ADAM_TILE + e0);
+              a[0] += __uint_as_float(w.x << 16) * scale;
+              a[1] += __uint_as_float(w.x & 0xffff0000u) * scale;
+              a[2] += __uint_as_float(w.y << 16) * scale;
+              a[3] += __uint_as_float(w.y & 0xffff0000u) * scale;
+            }
+            pv = *reinterpret_cast<const float4*>(Sp + e0);
+            cm = *reinterpret_cast<const uint32_t*>(Sm + e0);
+            cv = *reinterpret_cast<const uint32_t*>(Sv + e0);
+          }
+          r.g[4 * k + 0] = a[0], r.g[4 * k + 1] = a[1], r.g[4 * k + 2] = a[2], r.g[4 * k + 3] = a[3];
+          r.p[4 * k + 0] = pv.x, r.p[4 * k + 1] = pv.y, r.p[4 * k + 2] = pv.z, r.p[4 * k + 3] = pv.w;
+          dq4_m(cm, sm, &r.mt[4 * k]);
+          dq4_v(cv, sv, &r.vt[4 * k]);
+        }
+        if (blk.len == ADAM_TILE)
+          adam_block_tail<RSA_NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, release, push);
+        else
+          adam_block_tail<RSA_NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, release, push);
+      } else {
+        // generic: gradients summed straight from the peers' memory, masked & strided
+#pragma unroll
+        for (int e = 0; e < G::EPT; ++e) {
+          const int i = G::idx(e);
+          float acc = 0.f;
+          if (i < blk.len && blk.len <= ADAM_TILE) {
+            const int64_t o = blk_off(blk, i);
+#pragma unroll
+            for (int q = 0; q < M; ++q)
+              acc += __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16) * scale;
+            r.p[e] = P.master[blk.state_off + o];
+            r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.state_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
+            r.vt[e] = (byte_f(uint32_t(P.vq[blk.state_off + o]), 0) - 8388608.0f) * sv;
+          } else {
+            r.p[e] = r.mt[e] = r.vt[e] = 0.f;
+          }
+          r.g[e] = acc;
+        }
+        adam_block_tail<RSA_NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, release, push);
+      }
+      if (++st == nst) {  // ring position and mbarrier phase of the next block
+        st = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+  if constexpr (SYNC) p2p_done(sg, rank, M, epoch);  // (contains a CTA-wide barrier)
+}
+
+// RSDB_RSA_KERNEL=ws: the warp-specialised kernel (producer warp); default:
+// the single-role kernel (measured faster at N=1)
+static bool rsa_warp_specialised() {
+  const char* e = std::getenv("RSDB_RSA_KERNEL");
+  return e && std::strcmp(e, "ws") == 0;
+}
+
 static int rsa_stages(int def) {
   static const int env = [] {
     const char* e = std::getenv("RSDB_RSA_STAGES");
@@ -747,41 +922,54 @@ template <int M, bool SYNC, bool PUSH>
 static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads,
                                const P2PPtrs& params, float scale, const AdamPtrs& P,
                                const AdamScalars& s, const P2PSignals& sg, int rank, uint64_t epoch,
-                               cudaStream_t st) {
+                               cudaStream_t st, int abs_tma) {
   static const int nst = rsa_stages(RsaGeom<M>::STAGES);
+  static const bool ws = rsa_warp_specialised();
   const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * nst;
   static const int grid = [&] {
-    cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, true, SYNC, PUSH>, RSA_NT,
-                                                  smem);
+    if (ws) {
+      cudaFuncSetAttribute(rs_adam_ws_kernel<M, true, SYNC, PUSH>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_ws_kernel<M, true, SYNC, PUSH>, RSA_THREADS,
+                                                    smem);
+    } else {
+      cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, true, SYNC, PUSH>, RSA_NT,
+                                                    smem);
+    }
     return num_sms() * (b < 1 ? 1 : b);
   }();
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, grid));
-  rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, params,
-                                                                        scale, P, s, sg, rank, epoch, nst);
+  if (ws)
+    rs_adam_ws_kernel<M, true, SYNC, PUSH><<<blocks, RSA_THREADS, smem, st>>>(
+        tbl, nblocks, grads, params, scale, P, s, sg, rank, epoch, nst, abs_tma);
+  else
+    rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, params, scale, P,
+                                                                         s, sg, rank, epoch, nst);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
-                               const P2PPtrs* push_params) {
+                               const P2PPtrs* push_params, int abs_tma) {
   if (!P.param_bf16) return cudaErrorInvalidValue;  // the fused path is for bf16 units
   const P2PPtrs none_p{};
   if (m == 1) {
     P2PSignals none{};
-    return rs_adam_mbs<1, false, false>(tbl, nblocks, grads, none_p, scale, P, s, none, rank, epoch, st);
+    return rs_adam_mbs<1, false, false>(tbl, nblocks, grads, none_p, scale, P, s, none, rank, epoch, st,
+                                        abs_tma);
   }
   if (!sg) return cudaErrorInvalidValue;
   switch (m) {
 #define RSA_CASE(MM)                                                                                  \
   case MM:                                                                                            \
     return push_params ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, *push_params, scale, P, s,  \
-                                                     *sg, rank, epoch, st)                            \
+                                                     *sg, rank, epoch, st, abs_tma)                   \
                        : rs_adam_mbs<MM, true, false>(tbl, nblocks, grads, none_p, scale, P, s, *sg,  \
-                                                      rank, epoch, st);
+                                                      rank, epoch, st, abs_tma);
     RSA_CASE(2) RSA_CASE(3) RSA_CASE(4) RSA_CASE(5) RSA_CASE(6) RSA_CASE(7) RSA_CASE(8)
 #undef RSA_CASE
     default:
