@@ -112,15 +112,31 @@ class Clocks:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpus):
+        import threading
         self.gpus = set(gpus)
         self.p = None
         self.t0 = self.t1 = None
+        self.lines = []
+        self.live = threading.Event()
         try:
             self.p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS,
                                        "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line)
+            self.live.set()
+
+    def ready(self):
+        """Blocks until the sampler produces lines (nvidia-smi takes 0.1-1 s to
+        start; a short N=1 timed region could otherwise end first).  Called
+        before the pre-timing barrier so no rank's timing includes the wait."""
+        if self.p is not None:
+            self.live.wait(timeout=10.0)
 
     def begin(self):
         self.t0 = time.time()
@@ -135,10 +151,11 @@ class Clocks:
         time.sleep(0.12)
         self.p.terminate()
         try:
-            out, _ = self.p.communicate(timeout=5)
+            self.p.wait(timeout=5)
         except Exception:
             self.p.kill()
-            out = ""
+        time.sleep(0.05)
+        out = "".join(self.lines)
         sm, mx, reasons, n = [], 0.0, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.splitlines():
@@ -490,6 +507,8 @@ def run_ours(args):
     stream.synchronize()
     # ---------------- timed region: inputs resident in HBM
     timers = Timers()
+    if clocks:
+        clocks.ready()
     barrier(world)
     torch.cuda.synchronize()
     if clocks:
