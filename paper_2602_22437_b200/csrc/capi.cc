@@ -701,10 +701,10 @@ static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state
     if (!u->has_bound_state) return fail(RSDB_EINVAL, "null state and the unit is not part of a DBuffer");
     st = &u->bound_state;
   }
-  if (!st->master_f32 || !st->m_q || !st->v_q || !st->m_absmax || !st->v_absmax)
+  if (!st->master_f32 || !st->m_q || !st->v_q || (u->nblocks > 0 && (!st->m_absmax || !st->v_absmax)))
     return fail(RSDB_EINVAL, "null state pointer");
   const int m = u->L.m;
-  if (u->L.S == 0 || u->nblocks == 0) return OK_CLEAR();
+  if (u->L.S == 0 || (u->nblocks == 0 && m == 1)) return OK_CLEAR();  // world > 1: barriers count every rank
   rsdb::P2PPtrs g{}, q{};
   rsdb::P2PSignals sg{};
   const bool push = gather && m > 1;
@@ -930,8 +930,10 @@ static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
   if (!d->param_bf16) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs bf16 units");
   rsdb::AdamScalars s;
   if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
-  if (d->nblocks == 0) return OK_CLEAR();
   const int m = d->m;
+  // a rank may own no block (e.g. whole-matrix granularity at large m) but at
+  // world > 1 it still launches: the kernel's barriers count every rank
+  if (d->nblocks == 0 && m == 1) return OK_CLEAR();
   rsdb::P2PPtrs g{}, q{};
   rsdb::P2PSignals sg{};
   const bool push = gather && m > 1;

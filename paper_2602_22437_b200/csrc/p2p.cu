@@ -593,19 +593,29 @@ __device__ __forceinline__ bool rsa_fits(const AdamBlock& b) {
 // AllGather fused into the step: every bf16 parameter the Adam tail writes is
 // also stored into every peer's parameter array at the same index (NVLink
 // stores, made visible by the system fence of the done barrier).
+// Peers are visited in rank-rotated order (rank+1, rank+2, ...) so that the
+// ranks do not all store into the same GPU at the same moment.
 template <int M>
 struct PeerPush {
-  uint16_t* peer[M];
-  int rank;
+  uint16_t* peer[M > 1 ? M - 1 : 1];  // peer[j] = rank (rank + 1 + j) mod M
+  __device__ void init(const P2PPtrs& params, int rank) {
+#pragma unroll
+    for (int j = 0; j < M - 1; ++j) {
+      const int r = (rank + 1 + j) % M;
+      uint16_t* q = nullptr;
+#pragma unroll
+      for (int k = 0; k < M; ++k)  // compile-time indices into params.p
+        if (k == r) q = static_cast<uint16_t*>(const_cast<void*>(params.p[k]));
+      peer[j] = q;
+    }
+  }
   __device__ void quad(int64_t i, uint2 bits) const {
 #pragma unroll
-    for (int r = 0; r < M; ++r)
-      if (r != rank) *reinterpret_cast<uint2*>(peer[r] + i) = bits;
+    for (int j = 0; j < M - 1; ++j) *reinterpret_cast<uint2*>(peer[j] + i) = bits;
   }
   __device__ void one(int64_t i, __nv_bfloat16 h) const {
 #pragma unroll
-    for (int r = 0; r < M; ++r)
-      if (r != rank) reinterpret_cast<__nv_bfloat16*>(peer[r])[i] = h;
+    for (int j = 0; j < M - 1; ++j) reinterpret_cast<__nv_bfloat16*>(peer[j])[i] = h;
   }
 };
 
@@ -621,11 +631,7 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
   using G = AdamGeom<RSA_NT>;
   using PushT = std::conditional_t<PUSH, PeerPush<M>, NoPush>;
   PushT push{};
-  if constexpr (PUSH) {
-#pragma unroll
-    for (int r = 0; r < M; ++r) push.peer[r] = static_cast<uint16_t*>(const_cast<void*>(params.p[r]));
-    push.rank = rank;
-  }
+  if constexpr (PUSH) push.init(params, rank);
   extern __shared__ __align__(128) uint8_t rsa_smem[];
   __shared__ __align__(8) uint64_t full[RSA_MAX_STAGES];
   __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
@@ -811,11 +817,7 @@ __global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBl
     }
   } else {  // ---------------------------------------- compute warps
     PushT push{};
-    if constexpr (PUSH) {
-#pragma unroll
-      for (int r = 0; r < M; ++r) push.peer[r] = static_cast<uint16_t*>(const_cast<void*>(params.p[r]));
-      push.rank = rank;
-    }
+    if constexpr (PUSH) push.init(params, rank);
     int it = 0, st = 0;
     uint32_t phase = 0;
     for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {

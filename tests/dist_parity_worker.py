@@ -243,6 +243,53 @@ def main():
     p2p.close()
     del u
     del rng
+    # ---- ranks owning no quantization block (one whole-tensor block on rank 0):
+    # the fused RS+Adam+AG kernel still launches on every rank (its barriers
+    # count every rank) and equals RS -> Adam -> AG
+    es = [4096 * 8]
+    c = R.plan(es, es, world, elem_bytes=2)
+    o = OP.plan(es, es, world, OP.gcoll_elems(2))
+    S = c.S
+    p_log = logical_params(9, es[0])
+    pf0 = place_gpu(c, p_log, torch.bfloat16)
+    param_full = pf0.clone()
+    grad_full = place_gpu(c, logical_grads(9, rank, es[0]), torch.bfloat16)
+    grad_f32 = torch.zeros(world * S, dtype=torch.float32, device="cuda")
+    u = R.Unit(c, rank, param_full, grad_full, grad_f32, qblock=2048, comm=comm)
+    nb = u.num_blocks
+    master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
+    st_a = [master, torch.zeros(S, dtype=torch.int8, device="cuda"),
+            torch.zeros(S, dtype=torch.uint8, device="cuda"),
+            torch.zeros(max(nb, 1), device="cuda"), torch.zeros(max(nb, 1), device="cuda")]
+    st_b = [t.clone() for t in st_a]
+    p2p = R.P2P(comm, [param_full, grad_full])
+    R.reduce_scatter_p2p(u, p2p)
+    R.step_8bit_adam(u, *st_a, R.AdamConfig(), 1)
+    R.all_gather_p2p(u, p2p)
+    torch.cuda.synchronize()
+    pf_ref = param_full.clone()
+    param_full.copy_(pf0)
+    dist.barrier()
+    for _ in range(2):  # twice: the epochs of every rank stay in step
+        R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 1, state=[t.clone() for t in st_b])
+    st_c = [t.clone() for t in st_b]
+    param_full.copy_(pf0)
+    dist.barrier()
+    R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 1, state=st_c)
+    torch.cuda.synchronize()
+    if nb == 0 and rank == 0:
+        ok = False
+        msgs.append("owner-less case: rank 0 should own the block")
+    if not torch.equal(param_full.view(torch.int16)[:es[0]], pf_ref.view(torch.int16)[:es[0]]):
+        ok = False
+        msgs.append(f"owner-less ranks: fused RS+Adam+AG differs (rank {rank}, {nb} blocks)")
+    for a_, b_ in zip(st_c, st_a):
+        if not torch.equal(a_.view(torch.uint8), b_.view(torch.uint8)):
+            ok = False
+            msgs.append(f"owner-less ranks: fused state differs (rank {rank})")
+            break
+    p2p.close()
+    del u
     # ---- N2: FP8 block quantization fused with the AllGather over NVLink
     shapes = [(256, 384), (512, 128), (128, 200), (130, 128), (384, 64), (1024, 256)]
     es = [r * c for r, c in shapes]
