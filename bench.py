@@ -431,7 +431,25 @@ def cpu_baseline(world, target_s=10.0):
     return {"value": nb / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{E} params ({blocks} x 2048-elem blocks of the layer unit), "
                       f"{world} simulated rank(s), AG+cast+RS+8-bit Adam, numpy single thread, "
-                      f"{dt:.1f} s"}
+                      f"{dt:.1f} s", "host": host_info()}
+
+
+def host_info():
+    """CPU model and the cores this process may use (SURVEY §8(d) 'oracle beside it')."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = os.cpu_count()
+    return {"cpu_model": model, "affinity_cores": aff}
 
 
 def run_reference(args):
@@ -459,7 +477,8 @@ def run_reference(args):
                        "qblock": QBLOCK, "parallelism": f"fsdp{world} (simulated ranks)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{E} params per step ({blocks} blocks), {world} "
-                                       "simulated rank(s), numpy single thread"},
+                                       "simulated rank(s), numpy single thread",
+                             "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -515,9 +534,12 @@ def run_ours(args):
         clocks.begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev0.record(stream)
     with torch.cuda.stream(stream):
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            if i:
+                step_ev[i - 1].record(stream)  # step boundaries: per-step distribution
             step(R, db, cfg, t, stream, timers, p2p=p2p, fuse=fuse)
             t += 1
     ev1.record(stream)
@@ -528,6 +550,11 @@ def run_ours(args):
     clk = clocks.stop() if clocks else None
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
+    bounds = [ev0] + step_ev[:args.steps - 1] + [ev1]
+    per_step = sorted(bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps))
+    pct = lambda q: per_step[min(len(per_step) - 1, int(q * (len(per_step) - 1) + 0.5))]  # noqa: E731
+    step_dist = {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9), "rank": rank,
+                 "note": "rank 0's per-step CUDA-event times inside the timed region"}
     tot = timers.totals_ms()
     cnt = timers.counts()
     K = args.steps
@@ -629,6 +656,7 @@ def run_ours(args):
                        "l2": f"no flush: per-step working set {sum(sizes) / 2 ** 30:.1f} GiB "
                              f"per rank >> L2 ({L2_BYTES >> 20} MiB)",
                        "plan_ms": plan_ms},
+            "step_ms": step_dist,
             "per_op": {"adam_hbm_gbs": adam_gbs, "adam_ms_per_launch": adam_ms,
                        "cast_hbm_gbs": cast_gbs, "cast_ms_per_step": cast_ms,
                        "ag_wire_gbs": ag_bus, "rs_wire_gbs": rs_bus,

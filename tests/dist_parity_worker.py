@@ -290,6 +290,51 @@ def main():
             break
     p2p.close()
     del u
+    # ---- N2 tiles through the fused kernel: 32x32 quantization tiles (the
+    # paper's 8-bit Adam setup) at 32-row granularity take the fused
+    # kernel's strided peer-load path; it must equal RS -> tiled Adam -> AG
+    shapes = [(96, 64), (64, 40), (130,), (256, 96)]
+    es = [int(np.prod(sh)) for sh in shapes]
+    gs = [32 * sh[1] if len(sh) == 2 else e for sh, e in zip(shapes, es)]
+    specs = [("tile", sh[1], 32, 32) if len(sh) == 2 else ("flat", e) for sh, e in zip(shapes, es)]
+    c = R.plan(es, gs, world, elem_bytes=2)
+    o = OP.plan(es, gs, world, OP.gcoll_elems(2))
+    S = c.S
+    p_log = logical_params(11, sum(es))
+    pf0 = place_gpu(c, p_log, torch.bfloat16)
+    param_full = pf0.clone()
+    grad_full = place_gpu(c, logical_grads(11, rank, sum(es)), torch.bfloat16)
+    grad_f32 = torch.zeros(world * S, dtype=torch.float32, device="cuda")
+    u = R.Unit(c, rank, param_full, grad_full, grad_f32, comm=comm, qspec=specs)
+    nb = u.num_blocks
+    master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
+    st_a = [master, torch.zeros(S, dtype=torch.int8, device="cuda"),
+            torch.zeros(S, dtype=torch.uint8, device="cuda"),
+            torch.zeros(max(nb, 1), device="cuda"), torch.zeros(max(nb, 1), device="cuda")]
+    st_b = [t.clone() for t in st_a]
+    p2p = R.P2P(comm, [param_full, grad_full])
+    R.reduce_scatter_p2p(u, p2p)
+    R.step_8bit_adam(u, *st_a, R.AdamConfig(), 2)
+    R.all_gather_p2p(u, p2p)
+    torch.cuda.synchronize()
+    pf_ref = param_full.clone()
+    param_full.copy_(pf0)
+    dist.barrier()
+    R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 2, state=st_b)
+    torch.cuda.synchronize()
+    mask = torch.zeros(world * S, dtype=torch.bool, device="cuda")
+    for l, e in zip(c.starts, es):
+        mask[l:l + e] = True
+    if not torch.equal(param_full.view(torch.int16)[mask], pf_ref.view(torch.int16)[mask]):
+        ok = False
+        msgs.append("tiles: fused RS+Adam+AG parameters differ from RS -> Adam -> AG")
+    for a_, b_ in zip(st_b, st_a):
+        if not torch.equal(a_.view(torch.uint8), b_.view(torch.uint8)):
+            ok = False
+            msgs.append("tiles: fused state differs from RS then tiled Adam")
+            break
+    p2p.close()
+    del u
     # ---- N2: FP8 block quantization fused with the AllGather over NVLink
     shapes = [(256, 384), (512, 128), (128, 200), (130, 128), (384, 64), (1024, 256)]
     es = [r * c for r, c in shapes]
