@@ -1,21 +1,19 @@
-// Fused collectives over NVLink peer memory.
+// Fused collectives over NVLink peer memory, one process
+// per GPU, peers' buffers mapped with CUDA IPC (rsdb_p2p_create).
 //
-//  rs_p2p_kernel  a6+a7: rank k pulls G_r[kS + i] (bf16) from every rank r
-//                 over NVLink, y = sum_{r=0..m-1} fp32(G_r) * scale in rank
-//                 order (fp32), padding -> 0, writes its fp32 shard.  Bytes on
-//                 the wire per rank: (m-1) S 2 (bf16), vs (m-1) S 4 for the
-//                 fp32 NCCL ReduceScatter, and no separate m*S cast pass.
-//  ag_p2p_kernel  a4: rank k pulls every peer's shard into its own buffer.
+//  rs_p2p_kernel / rs_tma_kernel   a6+a7: rank k pulls G_r[kS + i] (bf16) from
+//        every rank r, y = sum_{r=0..m-1} fp32(G_r) * scale in rank order
+//        (fp32), padding -> 0, writes its fp32 shard.  Wire bytes per rank
+//        (m-1) S 2, vs (m-1) S 4 for the fp32 NCCL ReduceScatter, and no
+//        separate m*S cast pass.
+//  ag_p2p_kernel / ag_tma_kernel / copy-engine AG   a4: rank k pulls every
+//        peer's shard into its own buffer (rotated peer order).
+//  rs_adam_tma_kernel (default) / rs_adam_ws_kernel   a6+a7+a8 (+ a4 with
+//        PUSH): the ReduceScatter feeds the 8-bit Adam update of the shard;
+//        with PUSH every updated bf16 parameter is also stored into every
+//        peer's gathered buffer -- the whole step in one kernel.
 //
-// Synchronisation through a per-rank signal buffer (uint64 words):
-//   [0, 8)   start[r] = epoch written by rank r when it enters the call
-//   [8, 16)  done[r]  = epoch written by rank r when all its CTAs finished
-//                       reading its peers
-//   [16]     CTA completion counter of this rank's running kernel
-// Start: block 0 publishes `epoch` to every peer (after a system fence), every
-// CTA waits until all peers have published.  Done: the last CTA of the rank
-// publishes to every peer and waits for all peers, so the kernel -- and the
-// stream -- only moves on once nobody reads this rank's buffers any more.
+// Start/done barriers between the ranks: p2p_dev.cuh.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
