@@ -666,7 +666,10 @@ def run_ours(args):
                        "bytes_per_rank": ab},
             "roofline": roof,
             "clocks": clk,
-            "gpu_launches": (cnt["cast"] + cnt["adam"] + (0 if p2p is None else cnt["ag"] + cnt["rs"])),
+            # this library's kernels in the timed region (world 1: the p2p
+            # AllGather is the identity and launches nothing)
+            "gpu_launches": (cnt["cast"] + cnt["adam"] +
+                             (0 if p2p is None else (cnt["ag"] if world > 1 else 0) + cnt["rs"])),
             "nccl_calls": 0 if p2p is not None else cnt["ag"] + cnt["rs"],
             "cpu_baseline": cpu,
             "e2e": e2e,
