@@ -468,6 +468,33 @@ rsdb_status rsdb_muon_bind(rsdb_muon*, const rsdb_muon_bufs*);
 rsdb_status rsdb_muon_step(rsdb_muon*, rsdb_p2p* p2p_or_null, const rsdb_muon_cfg*, void* stream);
 void rsdb_muon_free(rsdb_muon*);
 
+/* ======================================================================== */
+/* K-slot unsharded ring: only K units' gathered         */
+/* parameters / gradients are resident; each unit keeps a persistent        */
+/* parameter shard, slots are reused in stream (event) order.               */
+/* ======================================================================== */
+/* Ring mode for a (non-DBuffer) unit: the persistent S-element parameter
+ * shard (caller-owned, 16-B aligned, same element type as the unit).  The
+ * 8-bit Adam calls then write the updated shard there instead of into
+ * param_full + rank*S; NULL turns ring mode off.  EMISMATCH for DBuffer units. */
+rsdb_status rsdb_unit_set_shard(rsdb_unit*, void* param_shard);
+/* Points the unit at other gathered buffers (a ring slot): the same rules as
+ * rsdb_unit_create (non-null, 16-B aligned, grad_full != grad_f32 for bf16). */
+rsdb_status rsdb_unit_rebind(rsdb_unit*, const rsdb_unit_bufs*);
+/* AllGather from the persistent shards: param_full[r*S ...] = shard of rank r
+ * for every r (the local one by a local copy, the peers' over NVLink by the
+ * copy engines, between the p2p start/done barriers).  p2p (NULL iff world
+ * 1) must map every rank's shard buffer at the same offset. */
+rsdb_status rsdb_all_gather_shards_p2p(rsdb_unit*, rsdb_p2p* p2p_or_null, void* stream);
+typedef struct rsdb_ring rsdb_ring;
+/* A ring of k slots handed out round robin: acquisition i gets slot i mod k
+ * on every rank (so peers agree on slot addresses); the stream waits until
+ * the slot's previous holder released it. */
+rsdb_status rsdb_ring_create(int32_t k_slots, rsdb_ring** out);
+rsdb_status rsdb_ring_acquire(rsdb_ring*, void* stream, int32_t* slot);
+rsdb_status rsdb_ring_release(rsdb_ring*, int32_t slot, void* stream);  /* records the slot's event */
+void rsdb_ring_free(rsdb_ring*);
+
 #ifdef __cplusplus
 }
 #endif

@@ -280,6 +280,18 @@ class Unit:
     def num_blocks(self) -> int:
         return lib.rsdb_unit_num_blocks(self._h)
 
+    def set_shard(self, shard) -> None:
+        """K-slot ring mode: the persistent parameter shard (S elements) the
+        optimizer writes; None turns ring mode off."""
+        self._shard = shard
+        check(lib.rsdb_unit_set_shard(self._h, _ptr(shard) if shard is not None else None))
+
+    def rebind(self, param_full, grad_full, grad_f32) -> None:
+        """Point the unit at other gathered buffers (e.g. a ring slot)."""
+        self._keep = (param_full, grad_full, grad_f32)
+        bufs = _c.UnitBufs(_ptr(param_full), _ptr(grad_full), _ptr(grad_f32))
+        check(lib.rsdb_unit_rebind(self._h, C.byref(bufs)))
+
     def close(self):
         if self._owned and self._h is not None and self._h.value:
             lib.rsdb_unit_free(self._h)
@@ -643,6 +655,43 @@ class Muon:
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             lib.rsdb_muon_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- K-slot unsharded ring
+def all_gather_shards_p2p(unit: Unit, p2p: Optional["P2P"] = None, stream=None) -> None:
+    """AllGather of every rank's persistent shard into the unit's param_full."""
+    check(lib.rsdb_all_gather_shards_p2p(unit.handle, p2p.handle if p2p is not None else None,
+                                         _stream(stream)))
+
+
+class Ring:
+    """K slots handed out round robin (same slot sequence on every rank); the
+    stream waits for the slot's previous release."""
+
+    def __init__(self, k: int):
+        h = C.c_void_p()
+        check(lib.rsdb_ring_create(k, C.byref(h)))
+        self._h = h
+        self.k = k
+
+    def acquire(self, stream=None) -> int:
+        out = C.c_int32()
+        check(lib.rsdb_ring_acquire(self._h, _stream(stream), C.byref(out)))
+        return out.value
+
+    def release(self, slot: int, stream=None) -> None:
+        check(lib.rsdb_ring_release(self._h, slot, _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.rsdb_ring_free(self._h)
         self._h = None
 
     def __del__(self):

@@ -135,6 +135,13 @@ _SIGS = {
     "rsdb_muon_bind": (i32, [vp, C.POINTER(MuonBufs)]),
     "rsdb_muon_step": (i32, [vp, vp, C.POINTER(MuonCfg), vp]),
     "rsdb_muon_free": (None, [vp]),
+    "rsdb_unit_set_shard": (i32, [vp, vp]),
+    "rsdb_unit_rebind": (i32, [vp, C.POINTER(UnitBufs)]),
+    "rsdb_all_gather_shards_p2p": (i32, [vp, vp, vp]),
+    "rsdb_ring_create": (i32, [i32, C.POINTER(vp)]),
+    "rsdb_ring_acquire": (i32, [vp, vp, P_i32]),
+    "rsdb_ring_release": (i32, [vp, i32, vp]),
+    "rsdb_ring_free": (None, [vp]),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -85,7 +85,15 @@ struct rsdb_unit {
   DevTable blocks;  // rsdb::AdamBlock, unit-relative (state = shard, grad/param = +rank*S)
   bool has_bound_state = false;  // unit of a DBuffer: optimizer state in its arenas
   rsdb_adam_state bound_state{};
+  void* shard = nullptr;  // K-slot ring mode: persistent bf16/f32 parameter shard (S elements)
 };
+
+// where the optimizer writes the unit's parameter shard: param_full + rank*S,
+// or the persistent shard (ring mode; the table's param offsets carry +rank*S)
+static void* param_target(const rsdb_unit* u) {
+  if (!u->shard) return u->bufs.param_full;
+  return static_cast<char*>(u->shard) - int64_t(u->rank) * u->L.S * u->L.elem_bytes;
+}
 
 struct rsdb_dbuffer {
   std::vector<std::unique_ptr<rsdb_unit>> units;
@@ -496,7 +504,7 @@ rsdb_status rsdb_step_8bit_adam(rsdb_unit* u, const rsdb_adam_state* st, const r
   rsdb::AdamPtrs p{static_cast<float*>(st->master_f32), static_cast<int8_t*>(st->m_q),
                    static_cast<uint8_t*>(st->v_q),       static_cast<float*>(st->m_absmax),
                    static_cast<float*>(st->v_absmax),    static_cast<const float*>(u->bufs.grad_f32),
-                   u->bufs.param_full,                   u->L.elem_bytes == 2};
+                   param_target(u),                      u->L.elem_bytes == 2};
   CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
                               0, S_(stream)));
   return OK_CLEAR();
@@ -513,7 +521,7 @@ rsdb_status rsdb_step_8bit_adam_dynamic(rsdb_unit* u, const rsdb_adam_state* st,
   rsdb::AdamPtrs p{static_cast<float*>(st->master_f32), static_cast<int8_t*>(st->m_q),
                    static_cast<uint8_t*>(st->v_q),       static_cast<float*>(st->m_absmax),
                    static_cast<float*>(st->v_absmax),    static_cast<const float*>(u->bufs.grad_f32),
-                   u->bufs.param_full,                   u->L.elem_bytes == 2};
+                   param_target(u),                      u->L.elem_bytes == 2};
   CUDA_TRY(rsdb::launch_adam8_dyn(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
                                   S_(stream)));
   return OK_CLEAR();
@@ -704,6 +712,8 @@ static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state
   if (!st->master_f32 || !st->m_q || !st->v_q || (u->nblocks > 0 && (!st->m_absmax || !st->v_absmax)))
     return fail(RSDB_EINVAL, "null state pointer");
   const int m = u->L.m;
+  if (gather && u->shard)
+    return fail(RSDB_EINVAL, "ring mode (persistent shard): gather with rsdb_all_gather_shards_p2p instead");
   if (u->L.S == 0 || (u->nblocks == 0 && m == 1)) return OK_CLEAR();  // world > 1: barriers count every rank
   rsdb::P2PPtrs g{}, q{};
   rsdb::P2PSignals sg{};
@@ -726,7 +736,7 @@ static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state
   rsdb::AdamPtrs ap{static_cast<float*>(st->master_f32), static_cast<int8_t*>(st->m_q),
                     static_cast<uint8_t*>(st->v_q),       static_cast<float*>(st->m_absmax),
                     static_cast<float*>(st->v_absmax),    nullptr,
-                    u->bufs.param_full,                   1};
+                    param_target(u),                      1};
   const float scale = float(1.0 / double(m));
   // absmax chunks by TMA: arena-backed state (padded to 16 blocks) or whole 16-B chunks
   const int abs_tma = aligned16(st->m_absmax) && aligned16(st->v_absmax) &&
@@ -1476,5 +1486,92 @@ rsdb_status rsdb_muon_step(rsdb_muon* u, rsdb_p2p* p, const rsdb_muon_cfg* cfg, 
 }
 
 void rsdb_muon_free(rsdb_muon* u) { delete u; }
+
+// ---------------------------------------------------------------------------
+// K-slot unsharded ring
+// ---------------------------------------------------------------------------
+rsdb_status rsdb_unit_set_shard(rsdb_unit* u, void* shard) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (u->has_bound_state) return fail(RSDB_EMISMATCH, "DBuffer units keep their shard in PARAM_FULL");
+  if (shard && !aligned16(shard)) return fail(RSDB_EINVAL, "shard must be 16-byte aligned");
+  u->shard = shard;
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_unit_rebind(rsdb_unit* u, const rsdb_unit_bufs* b) {
+  if (!u || !b) return fail(RSDB_EINVAL, "null argument");
+  if (u->has_bound_state) return fail(RSDB_EMISMATCH, "DBuffer units cannot be rebound");
+  if (!b->param_full || !b->grad_full || !b->grad_f32) return fail(RSDB_EINVAL, "unit buffers must be non-null");
+  if (!aligned16(b->param_full) || !aligned16(b->grad_full) || !aligned16(b->grad_f32))
+    return fail(RSDB_EMISMATCH, "unit buffers must be 16-byte aligned (P:199, P:369)");
+  if (u->L.elem_bytes == 2 && b->grad_full == b->grad_f32)
+    return fail(RSDB_EMISMATCH, "bf16 unit: grad_full must not alias grad_f32");
+  u->bufs = *b;
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_all_gather_shards_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (!u->shard) return fail(RSDB_EINVAL, "no persistent shard (rsdb_unit_set_shard)");
+  const int m = u->L.m;
+  const int64_t bytes_S = u->L.S * u->L.elem_bytes;
+  if (u->L.S == 0) return OK_CLEAR();
+  rsdb::P2PPtrs sh{};
+  rsdb::P2PSignals sg{};
+  if (m > 1) {
+    if (rsdb_status e = p2p_common(u, p, &sg)) return e;
+    int32_t bi = 0;
+    int64_t off = 0;
+    if (rsdb_status e = p2p_find(p, u->shard, bytes_S, &bi, &off)) return e;
+    for (int r = 0; r < m; ++r) sh.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+    ++p->epoch;
+  } else {
+    sh.p[0] = u->shard;
+  }
+  CUDA_TRY(rsdb::launch_ag_shards(sh, u->bufs.param_full, bytes_S, u->rank, m, m > 1 ? &sg : nullptr,
+                                  m > 1 ? p->epoch : 0, S_(stream)));
+  return OK_CLEAR();
+}
+
+struct rsdb_ring {
+  int32_t k = 0, next = 0;
+  std::vector<cudaEvent_t> ev;
+  std::vector<bool> held;  // released at least once (has an event to wait on)
+  ~rsdb_ring() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+rsdb_status rsdb_ring_create(int32_t k, rsdb_ring** out) {
+  if (!out || k < 1) return fail(RSDB_EINVAL, "k_slots must be >= 1");
+  *out = nullptr;
+  if (rsdb_status st = require_device()) return st;
+  auto r = std::make_unique<rsdb_ring>();
+  r->k = k;
+  r->ev.assign(size_t(k), nullptr);
+  r->held.assign(size_t(k), false);
+  for (auto& e : r->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *out = r.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_ring_acquire(rsdb_ring* r, void* stream, int32_t* slot) {
+  if (!r || !slot) return fail(RSDB_EINVAL, "null argument");
+  const int32_t s = r->next;
+  r->next = (r->next + 1) % r->k;
+  if (r->held[size_t(s)]) CUDA_TRY(cudaStreamWaitEvent(S_(stream), r->ev[size_t(s)], 0));
+  *slot = s;
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_ring_release(rsdb_ring* r, int32_t slot, void* stream) {
+  if (!r || slot < 0 || slot >= r->k) return fail(RSDB_EINVAL, "bad slot");
+  CUDA_TRY(cudaEventRecord(r->ev[size_t(slot)], S_(stream)));
+  r->held[size_t(slot)] = true;
+  return OK_CLEAR();
+}
+
+void rsdb_ring_free(rsdb_ring* r) { delete r; }
 
 }  // extern "C"

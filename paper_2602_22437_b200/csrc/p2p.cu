@@ -459,6 +459,40 @@ static cudaError_t ag_ce_m(const P2PPtrs& params, int64_t bytes_S, int rank, con
   return cudaGetLastError();
 }
 
+// AllGather from persistent shards (K-slot ring mode):
+// dst[r*bytes_S ...] = shard_r for every rank r, the local shard by a local
+// copy and the peers' over NVLink by the copy engines (rotated peer order),
+// between the start/done barriers.
+template <int M>
+static cudaError_t ag_shards_ce_m(const P2PPtrs& shards, char* dst, int64_t bytes_S, int rank,
+                                  const P2PSignals& sg, uint64_t epoch, cudaStream_t st) {
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
+  for (int p = 0; p < M; ++p) {
+    const int r = (rank + p) % M;
+    cudaError_t e = cudaMemcpyAsync(dst + int64_t(r) * bytes_S, shards.p[r], size_t(bytes_S),
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, int rank, int m,
+                             const P2PSignals* sg, uint64_t epoch, cudaStream_t st) {
+  char* d = static_cast<char*>(dst);
+  if (m == 1) return cudaMemcpyAsync(d, shards.p[0], size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
+  if (!sg) return cudaErrorInvalidValue;
+  switch (m) {
+#define AGS_CASE(MM) \
+  case MM:           \
+    return ag_shards_ce_m<MM>(shards, d, bytes_S, rank, *sg, epoch, st);
+    AGS_CASE(2) AGS_CASE(3) AGS_CASE(4) AGS_CASE(5) AGS_CASE(6) AGS_CASE(7) AGS_CASE(8)
+#undef AGS_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 template <typename K>
 static int p2p_grid(K kernel) {
   int b = 0;

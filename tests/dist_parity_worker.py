@@ -368,6 +368,13 @@ def main():
             break
     fu.close()
     p2p.close()
+    # ---- K-slot unsharded ring: shards gathered into
+    # reused slots, fused RS+Adam writing the persistent shards
+    from test_gpu_ring import ring_case
+    good, why = ring_case(world, rank, comm=comm, p2p_factory=lambda bufs: R.P2P(comm, bufs))
+    if not good:
+        ok = False
+        msgs.append("ring: " + "; ".join(why[:4]))
     # ---- N3: distributed Muon (Algorithm 2): gather to roots, NS, scatter + apply
     from test_gpu_muon import SHAPES as MUON_SHAPES, muon_case
     for prec in ("f32", "bf16"):
