@@ -114,6 +114,15 @@ struct rsdb_p2p {
   std::vector<std::vector<char*>> peer;  // [n][world], own rank = local
   std::vector<void*> opened;         // IPC mappings to close
   uint64_t epoch = 0;
+  // copy-engine ReduceScatter (RSDB_P2P_RS=ce): auxiliary stream + chunk events
+  static constexpr int CE_CHUNKS = 8;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev[CE_CHUNKS + 1]{};
+  ~rsdb_p2p() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (aux) cudaStreamDestroy(aux);
+  }
 };
 
 struct rsdb_copy_plan {
@@ -677,8 +686,21 @@ rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   for (int r = 0; r < m; ++r) g.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
   const float scale = float(1.0 / double(m));
   ++p->epoch;
-  CUDA_TRY(rsdb::launch_rs_p2p(g, static_cast<float*>(u->bufs.grad_f32) + int64_t(u->rank) * u->L.S,
-                               u->L.S, u->rank, m, scale, static_cast<const int64_t*>(u->pad.p),
+  float* out = static_cast<float*>(u->bufs.grad_f32) + int64_t(u->rank) * u->L.S;
+  if (rsdb::rs_use_ce()) {
+    if (!p->aux) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+      for (auto& e : p->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // staging for the (m-1) peers' bf16 slices: the side of grad_f32 not holding
+    // this rank's fp32 output ((m-1) S 2 bytes fit on the larger side)
+    float* gf = static_cast<float*>(u->bufs.grad_f32);
+    uint16_t* stage = reinterpret_cast<uint16_t*>(2 * u->rank >= m - 1 ? gf : gf + int64_t(u->rank + 1) * u->L.S);
+    CUDA_TRY(rsdb::launch_rs_ce(g, out, stage, u->L.S, u->rank, m, scale, static_cast<const int64_t*>(u->pad.p),
+                                int32_t(u->npad), sg, p->epoch, S_(stream), p->aux, p->ev, rsdb_p2p::CE_CHUNKS));
+    return OK_CLEAR();
+  }
+  CUDA_TRY(rsdb::launch_rs_p2p(g, out, u->L.S, u->rank, m, scale, static_cast<const int64_t*>(u->pad.p),
                                int32_t(u->npad), sg, p->epoch, S_(stream)));
   return OK_CLEAR();
 }

@@ -73,6 +73,13 @@ cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank,
                           cudaStream_t st);
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
+// ReduceScatter through the copy engines + a local rank-order reduction,
+// chunked so copies (aux stream) and reductions (st) overlap; stage holds
+// (m-1)*S bf16; ev has nchunk + 1 events.  rs_use_ce(): RSDB_P2P_RS=ce.
+cudaError_t launch_rs_ce(const P2PPtrs& grads, float* out, uint16_t* stage, int64_t S, int rank, int m, float scale,
+                         const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch, cudaStream_t st,
+                         cudaStream_t aux, cudaEvent_t* ev, int nchunk);
+bool rs_use_ce();
 // K-slot ring: gather every rank's persistent shard (shards.p[r], bytes_S) into dst
 cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, int rank, int m,
                              const P2PSignals* sg, uint64_t epoch, cudaStream_t st);

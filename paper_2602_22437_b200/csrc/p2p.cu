@@ -493,6 +493,94 @@ cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, 
   }
 }
 
+// ---- ReduceScatter through the copy engines (RSDB_P2P_RS=ce) ----
+// The peers' bf16 slices of this rank's shard are copied over NVLink by the
+// copy engines (cudaMemcpyAsync over the IPC mappings, rotated peer order,
+// on an auxiliary stream) into a local staging area, chunk by chunk; a local
+// kernel reduces each chunk in rank order (fp32, x scale, padding -> 0) as
+// soon as its copies have landed, so copies and reduction overlap.
+template <int M>
+__global__ void __launch_bounds__(256) rs_local_reduce_kernel(const uint16_t* __restrict__ own,
+                                                             const uint16_t* __restrict__ stage,
+                                                             float* __restrict__ out, int64_t c0,
+                                                             int64_t len, int64_t S, int rank, float scale,
+                                                             const int64_t* __restrict__ pad, int npad) {
+  const uint16_t* src[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    const int p = (r - rank + M) % M;  // 0: own slice; p >= 1: staging slot p - 1
+    src[r] = p == 0 ? own : stage + int64_t(p - 1) * S;
+  }
+  const int64_t nv = len / 4;  // chunks are multiples of 8 elements
+  for (int64_t v = int64_t(blockIdx.x) * 256 + threadIdx.x; v < nv; v += int64_t(gridDim.x) * 256) {
+    const int64_t i = c0 + 4 * v;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < M; ++r) {  // rank order, as the oracle
+      const uint2 w = ld_nc_v2(src[r] + i);
+      a[0] += __uint_as_float(w.x << 16) * scale;
+      a[1] += __uint_as_float(w.x & 0xffff0000u) * scale;
+      a[2] += __uint_as_float(w.y << 16) * scale;
+      a[3] += __uint_as_float(w.y & 0xffff0000u) * scale;
+    }
+    pad_zero4(pad, npad, int64_t(rank) * S + i, a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<float4*>(out + i) = make_float4(a[0], a[1], a[2], a[3]);
+  }
+}
+
+template <int M>
+static cudaError_t rs_ce_m(const P2PPtrs& grads, float* out, uint16_t* stage, int64_t S, int rank, float scale,
+                           const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch, cudaStream_t st,
+                           cudaStream_t aux, cudaEvent_t* ev, int nchunk) {
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
+  cudaError_t e = cudaEventRecord(ev[nchunk], st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(aux, ev[nchunk], 0);
+  if (e != cudaSuccess) return e;
+  const int64_t chunk = ((S + nchunk - 1) / nchunk + 7) / 8 * 8;
+  const uint16_t* own = static_cast<const uint16_t*>(grads.p[rank]) + int64_t(rank) * S;
+  for (int c = 0; c < nchunk; ++c) {
+    const int64_t c0 = int64_t(c) * chunk;
+    if (c0 >= S) break;
+    const int64_t len = std::min<int64_t>(chunk, S - c0);
+    for (int p = 1; p < M; ++p) {
+      const int r = (rank + p) % M;
+      e = cudaMemcpyAsync(stage + int64_t(p - 1) * S + c0,
+                          static_cast<const uint16_t*>(grads.p[r]) + int64_t(rank) * S + c0, size_t(len) * 2,
+                          cudaMemcpyDeviceToDevice, aux);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaEventRecord(ev[c], aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[c], 0);
+    if (e != cudaSuccess) return e;
+    const int grid = int(std::min<int64_t>(int64_t(num_sms()) * 8, std::max<int64_t>(1, (len / 4 + 255) / 256)));
+    rs_local_reduce_kernel<M><<<grid, 256, 0, st>>>(own, stage, out, c0, len, S, rank, scale, pad, npad);
+  }
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_ce(const P2PPtrs& grads, float* out, uint16_t* stage, int64_t S, int rank, int m, float scale,
+                         const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch, cudaStream_t st,
+                         cudaStream_t aux, cudaEvent_t* ev, int nchunk) {
+  switch (m) {
+#define RSCE_CASE(MM) \
+  case MM:            \
+    return rs_ce_m<MM>(grads, out, stage, S, rank, scale, pad, npad, sg, epoch, st, aux, ev, nchunk);
+    RSCE_CASE(2) RSCE_CASE(3) RSCE_CASE(4) RSCE_CASE(5) RSCE_CASE(6) RSCE_CASE(7) RSCE_CASE(8)
+#undef RSCE_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+bool rs_use_ce() {
+  static const bool v = [] {
+    const char* e = getenv("RSDB_P2P_RS");
+    return e && !strcmp(e, "ce");
+  }();
+  return v;
+}
+
 template <typename K>
 static int p2p_grid(K kernel) {
   int b = 0;
