@@ -699,7 +699,9 @@ constexpr int RSA_NT = 128;
 constexpr int RSA_MAX_STAGES = 4;
 template <int M>
 struct RsaGeom {
-  static constexpr int STAGES = M <= 4 ? 3 : 2;  // default ring depth (RSDB_RSA_STAGES overrides)
+  // default ring depth (RSDB_RSA_STAGES overrides): 3 at world 1, 2 with peers
+  // (more CTAs per SM; +0.5-0.7 % at N = 2 / 4, profiles/r1/v14_misc/stages_ab)
+  static constexpr int STAGES = M == 1 ? 3 : 2;
   static constexpr int G_BYTES = M * ADAM_TILE * 2;
   static constexpr int ABS_OFF = G_BYTES + ADAM_TILE * 6;  // 16-B chunks holding the block's absmax
   static constexpr int STAGE_BYTES = ABS_OFF + 32;
