@@ -1,5 +1,5 @@
 """-m gpu multi-GPU parity: torchrun at every world size the box offers
-(2, 4, 8 <= device count) running tests/dist_parity_worker.py.  Skipped on
+(2, 3, 4, 8 <= device count) running tests/dist_parity_worker.py.  Skipped on
 single-GPU boxes (NCCL cannot place two ranks on one GPU)."""
 import os
 import socket
@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 3, 4, 8])  # 3: a world where 1/m is not exact
 def test_dist_parity(n):
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
