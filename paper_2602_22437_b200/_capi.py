@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsdb.so")
+# RSDB_LIB: another build of the library (same-box A/B of two versions; tests and
+# the bench load the in-tree librsdb.so otherwise)
+LIB_PATH = os.environ.get("RSDB_LIB") or os.path.join(_HERE, "librsdb.so")
 
 RSDB_OK, RSDB_EINVAL, RSDB_EMISMATCH, RSDB_ECUDA, RSDB_ENCCL, RSDB_EINTERNAL = range(6)
 RSDB_BF16, RSDB_F32 = 0, 1

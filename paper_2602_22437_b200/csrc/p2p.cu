@@ -73,6 +73,15 @@ __device__ __forceinline__ bool in_pad_p(const int64_t* pad, int npad, int j, in
   return false;
 }
 
+// One term of the rank-order sum acc = ((0 + x_0) + x_1) + ..., x_r = fl(g_r *
+// scale): the first term as ONE fma(g, scale, +0) (= 0 + fl(g * scale) exactly,
+// signed zeros included), later ones with the product rounded on its own
+// (__fmul_rn: no FMA contraction into the add, which matters when
+// scale = fl(1/m) is not exact, m = 3, 5, ...).
+__device__ __forceinline__ float rank_acc(float acc, float g, float scale, bool first) {
+  return first ? __fmaf_rn(g, scale, 0.f) : __fadd_rn(acc, __fmul_rn(g, scale));
+}
+
 // Zero the padding positions of 4 consecutive outputs starting at e0.
 __device__ __forceinline__ void pad_zero4(const int64_t* pad, int npad, int64_t e0, float& a0,
                                           float& a1, float& a2, float& a3) {
@@ -129,9 +138,7 @@ __global__ void __launch_bounds__(P2P_THREADS) rs_p2p_kernel(P2PPtrs grads, floa
     for (int u = 0; u < U; ++u) {
       const int64_t v = v0 + int64_t(u) * P2P_THREADS;
       if (v >= nvec) break;
-      // rank-order accumulation: acc = ((0 + x_0) + x_1) + ... (fp32), x_r = fl(fp32(G_r) * scale):
-      // __fmul_rn keeps the product rounded on its own (no FMA contraction into
-      // the add), which matters when scale = fl(1/m) is not exact (m = 3, 5, ...)
+      // rank-order accumulation: acc = ((0 + x_0) + x_1) + ... (fp32), x_r = fl(fp32(G_r) * scale)
       float a[VEC];
 #pragma unroll
       for (int k = 0; k < VEC; ++k) a[k] = 0.f;
@@ -139,8 +146,8 @@ __global__ void __launch_bounds__(P2P_THREADS) rs_p2p_kernel(P2PPtrs grads, floa
       for (int r = 0; r < M; ++r)
 #pragma unroll
         for (int k = 0; k < VEC / 2; ++k) {
-          a[2 * k] += __fmul_rn(__uint_as_float(w[r][u][k] << 16), scale);
-          a[2 * k + 1] += __fmul_rn(__uint_as_float(w[r][u][k] & 0xffff0000u), scale);
+          a[2 * k] = rank_acc(a[2 * k], __uint_as_float(w[r][u][k] << 16), scale, r == 0);
+          a[2 * k + 1] = rank_acc(a[2 * k + 1], __uint_as_float(w[r][u][k] & 0xffff0000u), scale, r == 0);
         }
 #pragma unroll
       for (int k = 0; k < VEC / 4; ++k) {
@@ -376,10 +383,10 @@ __global__ void __launch_bounds__(RS_TMA_THREADS) rs_tma_kernel(P2PPtrs grads, f
       for (int q = 0; q < 2; ++q) {
         const int i = 4 * threadIdx.x + q * (RS_TMA_TILE / 2);
         const uint2 w = *reinterpret_cast<const uint2*>(src + i);
-        a[q][0] += __fmul_rn(__uint_as_float(w.x << 16), scale);
-        a[q][1] += __fmul_rn(__uint_as_float(w.x & 0xffff0000u), scale);
-        a[q][2] += __fmul_rn(__uint_as_float(w.y << 16), scale);
-        a[q][3] += __fmul_rn(__uint_as_float(w.y & 0xffff0000u), scale);
+        a[q][0] = rank_acc(a[q][0], __uint_as_float(w.x << 16), scale, r == 0);
+        a[q][1] = rank_acc(a[q][1], __uint_as_float(w.x & 0xffff0000u), scale, r == 0);
+        a[q][2] = rank_acc(a[q][2], __uint_as_float(w.y << 16), scale, r == 0);
+        a[q][3] = rank_acc(a[q][3], __uint_as_float(w.y & 0xffff0000u), scale, r == 0);
       }
     }
     __syncthreads();  // every thread has read stage s
@@ -520,10 +527,10 @@ __global__ void __launch_bounds__(256) rs_local_reduce_kernel(const uint16_t* __
 #pragma unroll
     for (int r = 0; r < M; ++r) {  // rank order, as the oracle
       const uint2 w = ld_nc_v2(src[r] + i);
-      a[0] += __fmul_rn(__uint_as_float(w.x << 16), scale);
-      a[1] += __fmul_rn(__uint_as_float(w.x & 0xffff0000u), scale);
-      a[2] += __fmul_rn(__uint_as_float(w.y << 16), scale);
-      a[3] += __fmul_rn(__uint_as_float(w.y & 0xffff0000u), scale);
+      a[0] = rank_acc(a[0], __uint_as_float(w.x << 16), scale, r == 0);
+      a[1] = rank_acc(a[1], __uint_as_float(w.x & 0xffff0000u), scale, r == 0);
+      a[2] = rank_acc(a[2], __uint_as_float(w.y << 16), scale, r == 0);
+      a[3] = rank_acc(a[3], __uint_as_float(w.y & 0xffff0000u), scale, r == 0);
     }
     pad_zero4(pad, npad, int64_t(rank) * S + i, a[0], a[1], a[2], a[3]);
     *reinterpret_cast<float4*>(out + i) = make_float4(a[0], a[1], a[2], a[3]);
@@ -822,10 +829,10 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
 #pragma unroll
           for (int q = 0; q < M; ++q) {  // rank order
             const uint2 w = *reinterpret_cast<const uint2*>(Sg + q * ADAM_TILE + e0);
-            a[0] += __fmul_rn(__uint_as_float(w.x << 16), scale);
-            a[1] += __fmul_rn(__uint_as_float(w.x & 0xffff0000u), scale);
-            a[2] += __fmul_rn(__uint_as_float(w.y << 16), scale);
-            a[3] += __fmul_rn(__uint_as_float(w.y & 0xffff0000u), scale);
+            a[0] = rank_acc(a[0], __uint_as_float(w.x << 16), scale, q == 0);
+            a[1] = rank_acc(a[1], __uint_as_float(w.x & 0xffff0000u), scale, q == 0);
+            a[2] = rank_acc(a[2], __uint_as_float(w.y << 16), scale, q == 0);
+            a[3] = rank_acc(a[3], __uint_as_float(w.y & 0xffff0000u), scale, q == 0);
           }
           pv = *reinterpret_cast<const float4*>(Sp + e0);
           cm = *reinterpret_cast<const uint32_t*>(Sm + e0);
@@ -850,7 +857,7 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
           const int64_t o = blk_off(blk, i);
 #pragma unroll
           for (int q = 0; q < M; ++q)
-            acc += __fmul_rn(__uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale);
+            acc = rank_acc(acc, __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale, q == 0);
           r.p[e] = P.master[blk.state_off + o];
           r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.mq_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
           r.vt[e] = (byte_f(uint32_t(P.vq[blk.vq_off + o]), 0) - 8388608.0f) * sv;
@@ -982,10 +989,10 @@ __global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBl
 #pragma unroll
             for (int q = 0; q < M; ++q) {  // rank order
               const uint2 w = *reinterpret_cast<const uint2*>(Sg + q * ADAM_TILE + e0);
-              a[0] += __fmul_rn(__uint_as_float(w.x << 16), scale);
-              a[1] += __fmul_rn(__uint_as_float(w.x & 0xffff0000u), scale);
-              a[2] += __fmul_rn(__uint_as_float(w.y << 16), scale);
-              a[3] += __fmul_rn(__uint_as_float(w.y & 0xffff0000u), scale);
+              a[0] = rank_acc(a[0], __uint_as_float(w.x << 16), scale, q == 0);
+              a[1] = rank_acc(a[1], __uint_as_float(w.x & 0xffff0000u), scale, q == 0);
+              a[2] = rank_acc(a[2], __uint_as_float(w.y << 16), scale, q == 0);
+              a[3] = rank_acc(a[3], __uint_as_float(w.y & 0xffff0000u), scale, q == 0);
             }
             pv = *reinterpret_cast<const float4*>(Sp + e0);
             cm = *reinterpret_cast<const uint32_t*>(Sm + e0);
@@ -1010,7 +1017,7 @@ __global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBl
             const int64_t o = blk_off(blk, i);
 #pragma unroll
             for (int q = 0; q < M; ++q)
-              acc += __fmul_rn(__uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale);
+              acc = rank_acc(acc, __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale, q == 0);
             r.p[e] = P.master[blk.state_off + o];
             r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.mq_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
             r.vt[e] = (byte_f(uint32_t(P.vq[blk.vq_off + o]), 0) - 8388608.0f) * sv;
