@@ -55,8 +55,6 @@ WORKLOAD = "llama-3.2-1b"
 QBLOCK = 2048
 ALIGN = 256
 L2_BYTES = 126 * 2 ** 20
-# experimental interleaved optimizer-state layout (library env switch)
-INTERLEAVED = os.environ.get("RSDB_STATE_LAYOUT") == "interleaved"
 
 
 def parse():
@@ -236,17 +234,14 @@ def setup(rank, world, local, units, comm):
             v["grad_full"][l:l + e] = g[o:o + e].to(torch.bfloat16)
             o += e
         v["param_full"].copy_(full_p.to(torch.bfloat16))
-        if not INTERLEAVED:
-            v["master"].copy_(full_p[rank * S:(rank + 1) * S])
-            # warm synthetic 8-bit Adam state (codes + per-block absmax)
-            v["mq"].copy_(H.codes_torch(ui, H.STREAM_MCODE, rank * S, S, True, device=dev))
-            v["vq"].copy_(H.codes_torch(ui, H.STREAM_VCODE, rank * S, S, False, device=dev))
+        v["master"].copy_(full_p[rank * S:(rank + 1) * S])
+        # warm synthetic 8-bit Adam state (codes + per-block absmax)
+        v["mq"].copy_(H.codes_torch(ui, H.STREAM_MCODE, rank * S, S, True, device=dev))
+        v["vq"].copy_(H.codes_torch(ui, H.STREAM_VCODE, rank * S, S, False, device=dev))
         v["ma"].copy_(H.absmax_torch(ui, H.STREAM_ABSM, rank * 10 ** 7, nb, 14, device=dev))
         v["va"].copy_(H.absmax_torch(ui, H.STREAM_ABSV, rank * 10 ** 7, nb, 22, device=dev))
         del p, g, full_p
         views.append(v)
-    if INTERLEAVED:  # experimental layout (timing only): every state run holds valid fp32 / codes
-        arenas[3].view(torch.float32).fill_(0.0123)
     torch.cuda.synchronize()
     return lays, db, arenas, views, plan_ms, sizes
 

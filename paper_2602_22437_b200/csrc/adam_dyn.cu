@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
       return av > 0.f ? dyn_code(mapv, T.lb[2], T.lb[2], __fdiv_rn(v, av)) : zero_v;
     };
     float am = 0.f, av = 0.f;
-    const bool fast = blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 && ((blk.mq_off | blk.vq_off) & 3) == 0 &&
+    const bool fast = blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
                       (blk.grad_off & 3) == 0 && (blk.param_off & 3) == 0;
     if (fast) {
       float p[G::EPT], m[G::EPT], v[G::EPT];
@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
         const int a = G::quad(k);
         const int4 pv = ld_na_v4(P.master + blk.state_off + a);
         const int4 gv = ld_nc_v4(P.grad + blk.grad_off + a);
-        const uint32_t cm = ld_na_u32(mq + blk.mq_off + a);
-        const uint32_t cv = ld_na_u32(P.vq + blk.vq_off + a);
+        const uint32_t cm = ld_na_u32(mq + blk.state_off + a);
+        const uint32_t cv = ld_na_u32(P.vq + blk.state_off + a);
         const float pp[4] = {__int_as_float(pv.x), __int_as_float(pv.y), __int_as_float(pv.z),
                              __int_as_float(pv.w)};
         const float gg[4] = {__int_as_float(gv.x), __int_as_float(gv.y), __int_as_float(gv.z),
@@ -175,9 +175,9 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
         const int a = G::quad(k);
         const float* pk = &p[4 * k];
         st_f4(P.master + blk.state_off + a, make_float4(pk[0], pk[1], pk[2], pk[3]));
-        st_u32(mq + blk.mq_off + a, qm(m[4 * k], am) | (qm(m[4 * k + 1], am) << 8) |
+        st_u32(mq + blk.state_off + a, qm(m[4 * k], am) | (qm(m[4 * k + 1], am) << 8) |
                                            (qm(m[4 * k + 2], am) << 16) | (qm(m[4 * k + 3], am) << 24));
-        st_u32(P.vq + blk.vq_off + a, qv(v[4 * k], av) | (qv(v[4 * k + 1], av) << 8) |
+        st_u32(P.vq + blk.state_off + a, qv(v[4 * k], av) | (qv(v[4 * k + 1], av) << 8) |
                                              (qv(v[4 * k + 2], av) << 16) | (qv(v[4 * k + 3], av) << 24));
         if constexpr (PARAM_BF16)
           st_u2(static_cast<uint16_t*>(P.param) + blk.param_off + a,
@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
     } else {
       auto elem = [&](int i, float& m, float& v) -> float {  // update element i, returns new p
         const int64_t o = blk_off(blk, i);
-        const float mt = __fmul_rn(mapm[mq[blk.mq_off + o]], Am);
-        const float vt = __fmul_rn(mapv[P.vq[blk.vq_off + o]], Av);
+        const float mt = __fmul_rn(mapm[mq[blk.state_off + o]], Am);
+        const float vt = __fmul_rn(mapv[P.vq[blk.state_off + o]], Av);
         const ElemOut r = adam_elem(P.master[blk.state_off + o], P.grad[blk.grad_off + o], mt, vt, s);
         m = r.m;
         v = r.v;
@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
       auto store = [&](int i, float p, float m, float v) {
         const int64_t o = blk_off(blk, i);
         P.master[blk.state_off + o] = p;
-        mq[blk.mq_off + o] = uint8_t(qm(m, am));
-        P.vq[blk.vq_off + o] = uint8_t(qv(v, av));
+        mq[blk.state_off + o] = uint8_t(qm(m, am));
+        P.vq[blk.state_off + o] = uint8_t(qv(v, av));
         if constexpr (PARAM_BF16)
           static_cast<__nv_bfloat16*>(P.param)[blk.param_off + o] = __float2bfloat16_rn(p);
         else

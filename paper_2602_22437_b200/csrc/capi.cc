@@ -272,8 +272,8 @@ static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t ra
   std::vector<rsdb::AdamBlock> tbl(qb.size());
   const int64_t base = int64_t(rank) * L.S;
   for (size_t i = 0; i < qb.size(); ++i)
-    tbl[i] = {qb[i].off, base + qb[i].off, base + qb[i].off, qb[i].off, qb[i].off, qb[i].rows * qb[i].cols,
-              int32_t(i), qb[i].cols, int32_t(qb[i].pitch)};
+    tbl[i] = {qb[i].off, base + qb[i].off, base + qb[i].off, qb[i].rows * qb[i].cols, int32_t(i),
+              qb[i].cols, int32_t(qb[i].pitch)};
   if (rsdb_status st = u->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
   if (blocks_out) *blocks_out = std::move(qb);
   return RSDB_OK;
@@ -668,20 +668,6 @@ rsdb_status rsdb_reduce_scatter_adam_gather_p2p(rsdb_unit* u, rsdb_p2p* p, const
 // ---------------------------------------------------------------------------
 static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-// Experimental interleaved optimizer-state layout (RSDB_STATE_LAYOUT=interleaved;
-// flat blocks only): every block's state is one contiguous run in the MASTER
-// arena -- fp32 master, then the m codes, then the v codes, 16-B aligned --
-// and the MQ / VQ arenas are empty.  Fewer concurrent DRAM streams per block;
-// the DBuffer-level calls only (unit-level Adam calls need the split layout).
-static bool state_interleaved() {
-  static const bool v = [] {
-    const char* e = std::getenv("RSDB_STATE_LAYOUT");
-    return e && std::strcmp(e, "interleaved") == 0;
-  }();
-  return v;
-}
-static int64_t interleaved_block_bytes(int64_t len) { return (6 * len + 15) / 16 * 16; }
-
 static rsdb_status kind_sizes(const rsdb::Layout& L, int32_t rank, const std::vector<rsdb::QSpec>& specs,
                               int64_t sz[RSDB_NKINDS]) {
   std::vector<rsdb::QTile> qb;
@@ -693,15 +679,6 @@ static rsdb_status kind_sizes(const rsdb::Layout& L, int32_t rank, const std::ve
   sz[RSDB_KIND_MASTER] = L.S * 4;
   sz[RSDB_KIND_MQ] = L.S;
   sz[RSDB_KIND_VQ] = L.S;
-  if (state_interleaved()) {
-    int64_t b = 0;
-    for (auto& t : qb) {
-      if (t.rows != 1) return fail(RSDB_EINVAL, "interleaved state layout: flat blocks only");
-      b += interleaved_block_bytes(int64_t(t.rows) * t.cols);
-    }
-    sz[RSDB_KIND_MASTER] = b;
-    sz[RSDB_KIND_MQ] = sz[RSDB_KIND_VQ] = 0;
-  }
   sz[RSDB_KIND_MABS] = int64_t(qb.size()) * 4;
   sz[RSDB_KIND_VABS] = int64_t(qb.size()) * 4;
   return RSDB_OK;
@@ -742,39 +719,26 @@ static rsdb_status arena_layout(const rsdb_layout* const* units, int32_t n_units
       if (offs) offs[int64_t(u) * RSDB_NKINDS + k] = acc[k];
       acc[k] += sz[k];
     }
+    state_e = round_up(state_e, align);  // align elements => align bytes for 1- and 4-byte kinds
     blk_e = round_up(blk_e, align);
+    if (state_elem_off) state_elem_off->push_back(state_e);
     if (blk_idx_off) blk_idx_off->push_back(blk_e);
-    if (state_interleaved()) {  // state_e counts BYTES of the MASTER arena
-      state_e = round_up(state_e, align);
-      if (state_elem_off) state_elem_off->push_back(state_e / 4);
-      if (offs) {
-        offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MASTER] = state_e;
-        offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MQ] = 0;
-        offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_VQ] = 0;
-      }
-      state_e += sz[RSDB_KIND_MASTER];
-    } else {
-      state_e = round_up(state_e, align);  // align elements => align bytes for 1- and 4-byte kinds
-      if (state_elem_off) state_elem_off->push_back(state_e);
-      if (offs) {
-        offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MASTER] = state_e * 4;
-        offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MQ] = state_e;
-        offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_VQ] = state_e;
-      }
-      state_e += L.S;
-    }
     if (offs) {
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MASTER] = state_e * 4;
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MQ] = state_e;
+      offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_VQ] = state_e;
       offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_MABS] = blk_e * 4;
       offs[int64_t(u) * RSDB_NKINDS + RSDB_KIND_VABS] = blk_e * 4;
     }
+    state_e += L.S;
     blk_e += sz[RSDB_KIND_MABS] / 4;
   }
   for (int k : {RSDB_KIND_PARAM_FULL, RSDB_KIND_GRAD_FULL, RSDB_KIND_GRAD_F32}) bytes[k] = round_up(acc[k], align);
   state_e = round_up(state_e, align);
   blk_e = round_up(blk_e, align);
-  bytes[RSDB_KIND_MASTER] = state_interleaved() ? state_e : state_e * 4;
-  bytes[RSDB_KIND_MQ] = state_interleaved() ? 0 : state_e;
-  bytes[RSDB_KIND_VQ] = state_interleaved() ? 0 : state_e;
+  bytes[RSDB_KIND_MASTER] = state_e * 4;
+  bytes[RSDB_KIND_MQ] = state_e;
+  bytes[RSDB_KIND_VQ] = state_e;
   bytes[RSDB_KIND_MABS] = blk_e * 4;
   bytes[RSDB_KIND_VABS] = blk_e * 4;
   return RSDB_OK;
@@ -841,7 +805,7 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
     auto unit = std::make_unique<rsdb_unit>();
     std::vector<rsdb::QTile> qb;
     if (rsdb_status st = build_unit(L, comm, rank, b, sp[size_t(u)], unit.get(), &qb)) return st;
-    unit->has_bound_state = !state_interleaved();  // interleaved: DBuffer-level calls only
+    unit->has_bound_state = true;
     unit->bound_state = {at(RSDB_KIND_MASTER), at(RSDB_KIND_MQ), at(RSDB_KIND_VQ), at(RSDB_KIND_MABS),
                          at(RSDB_KIND_VABS)};
     // arena-relative combined table: state in MASTER/MQ/VQ elements, grad in
@@ -853,18 +817,10 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
     const int64_t gbase16 = bf ? offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_GRAD_FULL] / 2 +
                                      int64_t(rank) * L.S
                                : 0;
-    int64_t ib = st_off[u] * 4;  // interleaved: byte offset of the block's state run
     for (size_t i = 0; i < qb.size(); ++i) {
-      const int64_t len = int64_t(qb[i].rows) * qb[i].cols;
-      if (state_interleaved()) {
-        tbl.push_back({ib / 4, gbase + qb[i].off, pbase + qb[i].off, ib + 4 * len, ib + 5 * len, int32_t(len),
-                       int32_t(bk_off[u] + int64_t(i)), qb[i].cols, int32_t(qb[i].pitch)});
-        ib += interleaved_block_bytes(len);
-      } else {
-        tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off, st_off[u] + qb[i].off,
-                       st_off[u] + qb[i].off, int32_t(len), int32_t(bk_off[u] + int64_t(i)), qb[i].cols,
-                       int32_t(qb[i].pitch)});
-      }
+      tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off,
+                     qb[i].rows * qb[i].cols, int32_t(bk_off[u] + int64_t(i)), qb[i].cols,
+                     int32_t(qb[i].pitch)});
       tbl_fused.push_back(tbl.back());
       tbl_fused.back().grad_off = gbase16 + qb[i].off;
     }
@@ -916,8 +872,8 @@ static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
     g.p[0] = d->base[RSDB_KIND_GRAD_FULL];
   }
   rsdb::AdamPtrs ap{static_cast<float*>(d->base[RSDB_KIND_MASTER]),
-                    static_cast<int8_t*>(d->base[state_interleaved() ? RSDB_KIND_MASTER : RSDB_KIND_MQ]),
-                    static_cast<uint8_t*>(d->base[state_interleaved() ? RSDB_KIND_MASTER : RSDB_KIND_VQ]),
+                    static_cast<int8_t*>(d->base[RSDB_KIND_MQ]),
+                    static_cast<uint8_t*>(d->base[RSDB_KIND_VQ]),
                     static_cast<float*>(d->base[RSDB_KIND_MABS]),
                     static_cast<float*>(d->base[RSDB_KIND_VABS]),
                     nullptr,
@@ -966,8 +922,8 @@ rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer* d, const rsdb_adam_cfg* cf
   if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
   if (d->nblocks == 0) return OK_CLEAR();
   rsdb::AdamPtrs p{static_cast<float*>(d->base[RSDB_KIND_MASTER]),
-                   static_cast<int8_t*>(d->base[state_interleaved() ? RSDB_KIND_MASTER : RSDB_KIND_MQ]),
-                   static_cast<uint8_t*>(d->base[state_interleaved() ? RSDB_KIND_MASTER : RSDB_KIND_VQ]),
+                   static_cast<int8_t*>(d->base[RSDB_KIND_MQ]),
+                   static_cast<uint8_t*>(d->base[RSDB_KIND_VQ]),
                    static_cast<float*>(d->base[RSDB_KIND_MABS]),
                    static_cast<float*>(d->base[RSDB_KIND_VABS]),
                    static_cast<const float*>(d->base[RSDB_KIND_GRAD_F32]),
@@ -985,8 +941,8 @@ rsdb_status rsdb_dbuffer_step_8bit_adam_dynamic(rsdb_dbuffer* d, const rsdb_adam
   if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
   if (d->nblocks == 0) return OK_CLEAR();
   rsdb::AdamPtrs p{static_cast<float*>(d->base[RSDB_KIND_MASTER]),
-                   static_cast<int8_t*>(d->base[state_interleaved() ? RSDB_KIND_MASTER : RSDB_KIND_MQ]),
-                   static_cast<uint8_t*>(d->base[state_interleaved() ? RSDB_KIND_MASTER : RSDB_KIND_VQ]),
+                   static_cast<int8_t*>(d->base[RSDB_KIND_MQ]),
+                   static_cast<uint8_t*>(d->base[RSDB_KIND_VQ]),
                    static_cast<float*>(d->base[RSDB_KIND_MABS]),
                    static_cast<float*>(d->base[RSDB_KIND_VABS]),
                    static_cast<const float*>(d->base[RSDB_KIND_GRAD_F32]),

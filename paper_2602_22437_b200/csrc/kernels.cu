@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(NT) adam8_kernel(const AdamBlock* __restrict__
 
 // bulk copies need 16-B aligned global addresses: codes at state_off % 16
 __device__ __forceinline__ bool adam_tma_ok(const AdamBlock& b) {
-  return b.len == ADAM_TILE && b.cols == b.len && (b.state_off & 3) == 0 && ((b.mq_off | b.vq_off) & 15) == 0 &&
+  return b.len == ADAM_TILE && b.cols == b.len && (b.state_off & 15) == 0 &&
          ((b.grad_off | b.param_off) & 3) == 0;
 }
 
@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
       mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
       bulk_g2s(stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
       bulk_g2s(stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
-      bulk_g2s(stage[st].mq, P.mq + nb.mq_off, ADAM_TILE, &full[st]);
-      bulk_g2s(stage[st].vq, P.vq + nb.vq_off, ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
     } else {
       mbar_arrive(&full[st]);
     }
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
       BlockRegs<NT> r;
       if (adam_fast(blk)) {
         load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off,
-                            P.mq + blk.mq_off, P.vq + blk.vq_off, sm, sv);
+                            P.mq + blk.state_off, P.vq + blk.state_off, sm, sv);
         adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
       } else if (adam_tile_fast(blk)) {
         load_tile<NT>(r, blk, P, sm, sv);

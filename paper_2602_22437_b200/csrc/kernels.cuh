@@ -13,17 +13,17 @@ namespace rsdb {
 // elements apart (contiguous block: cols == pitch == len; 2-D tile, N2:
 // cols = tile width, pitch = row length of the tensor).
 struct AdamBlock {
-  int64_t state_off;  // master (fp32 elements)
+  int64_t state_off;
   int64_t grad_off;
   int64_t param_off;
-  int64_t mq_off;     // m codes (bytes); == state_off in the split state layout
-  int64_t vq_off;     // v codes (bytes); == state_off in the split state layout
   int32_t len;
   int32_t slot;
   int32_t cols;
   int32_t pitch;
 };
-static_assert(sizeof(AdamBlock) == 56, "AdamBlock is 56 bytes");
+// 40 B: every thread of a CTA loads its block's entry on the critical path of
+// the block; a 56-B entry (separate m / v code offsets) cost 3.5 % at N = 1
+static_assert(sizeof(AdamBlock) == 40, "AdamBlock is 40 bytes");
 
 struct AdamScalars {
   float w1, b2, w2, eps, c_wd, step_size, inv_bc2s;

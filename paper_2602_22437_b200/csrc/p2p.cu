@@ -717,8 +717,7 @@ struct RsaGeom {
 };
 
 __device__ __forceinline__ bool rsa_fits(const AdamBlock& b) {
-  return b.cols == b.len && b.len <= ADAM_TILE && (b.len & 15) == 0 && (b.state_off & 3) == 0 &&
-         ((b.mq_off | b.vq_off) & 15) == 0 &&
+  return b.cols == b.len && b.len <= ADAM_TILE && (b.len & 15) == 0 && (b.state_off & 15) == 0 &&
          (b.grad_off & 7) == 0 && (b.param_off & 3) == 0;
 }
 
@@ -779,8 +778,8 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
         tma_g2s(S + r * ADAM_TILE * 2, static_cast<const uint16_t*>(grads.p[r]) + nb.grad_off, L * 2,
                 &full[st]);
       tma_g2s(S + Gm::G_BYTES, P.master + nb.state_off, L * 4, &full[st]);
-      tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + nb.mq_off, L, &full[st]);
-      tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + nb.vq_off, L, &full[st]);
+      tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + nb.state_off, L, &full[st]);
+      tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + nb.state_off, L, &full[st]);
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[st])) : "memory");
     }
@@ -859,8 +858,8 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
           for (int q = 0; q < M; ++q)
             acc = rank_acc(acc, __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale, q == 0);
           r.p[e] = P.master[blk.state_off + o];
-          r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.mq_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
-          r.vt[e] = (byte_f(uint32_t(P.vq[blk.vq_off + o]), 0) - 8388608.0f) * sv;
+          r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.state_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
+          r.vt[e] = (byte_f(uint32_t(P.vq[blk.state_off + o]), 0) - 8388608.0f) * sv;
         } else {
           r.p[e] = r.mt[e] = r.vt[e] = 0.f;
         }
@@ -936,8 +935,8 @@ __global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBl
               tma_g2s(S + r * ADAM_TILE * 2, static_cast<const uint16_t*>(grads.p[r]) + cur.grad_off, L * 2,
                       &full[st]);
             tma_g2s(S + Gm::G_BYTES, P.master + cur.state_off, L * 4, &full[st]);
-            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + cur.mq_off, L, &full[st]);
-            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + cur.vq_off, L, &full[st]);
+            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + cur.state_off, L, &full[st]);
+            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + cur.state_off, L, &full[st]);
           }
           if (abs_tma) {  // the 16-B chunks holding the block's two absmax values
             tma_g2s(S + Gm::ABS_OFF, P.mabs + (cur.slot & ~3), 16, &full[st]);
@@ -1019,8 +1018,8 @@ __global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBl
             for (int q = 0; q < M; ++q)
               acc = rank_acc(acc, __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale, q == 0);
             r.p[e] = P.master[blk.state_off + o];
-            r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.mq_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
-            r.vt[e] = (byte_f(uint32_t(P.vq[blk.vq_off + o]), 0) - 8388608.0f) * sv;
+            r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.state_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
+            r.vt[e] = (byte_f(uint32_t(P.vq[blk.state_off + o]), 0) - 8388608.0f) * sv;
           } else {
             r.p[e] = r.mt[e] = r.vt[e] = 0.f;
           }
