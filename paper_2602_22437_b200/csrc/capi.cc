@@ -791,6 +791,9 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
   }
   int32_t pbf = -1;
   std::vector<rsdb::AdamBlock> tbl, tbl_fused;
+  std::vector<rsdb::AdamBlockC> tbl_c;
+  std::vector<rsdb::UnitBase> ubases;
+  bool compact_ok = n_units <= rsdb::RSA_MAX_UNITS;
   for (int32_t u = 0; u < n_units; ++u) {
     const rsdb::Layout& L = units[u]->L;
     const int32_t bf = L.elem_bytes == 2;
@@ -817,12 +820,17 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
     const int64_t gbase16 = bf ? offs[size_t(u) * RSDB_NKINDS + RSDB_KIND_GRAD_FULL] / 2 +
                                      int64_t(rank) * L.S
                                : 0;
+    ubases.push_back({st_off[u], gbase16, pbase});
     for (size_t i = 0; i < qb.size(); ++i) {
       tbl.push_back({st_off[u] + qb[i].off, gbase + qb[i].off, pbase + qb[i].off,
                      qb[i].rows * qb[i].cols, int32_t(bk_off[u] + int64_t(i)), qb[i].cols,
                      int32_t(qb[i].pitch)});
       tbl_fused.push_back(tbl.back());
       tbl_fused.back().grad_off = gbase16 + qb[i].off;
+      const int64_t len = int64_t(qb[i].rows) * qb[i].cols;
+      compact_ok = compact_ok && qb[i].rows == 1 && qb[i].off <= INT32_MAX;
+      if (compact_ok)
+        tbl_c.push_back({uint32_t(u), uint32_t(qb[i].off), int32_t(len), int32_t(bk_off[u] + int64_t(i))});
     }
     db->m = L.m;
     db->rank = rank;
@@ -832,17 +840,35 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
   db->param_bf16 = pbf < 0 ? 1 : pbf;
   db->nblocks = int64_t(tbl.size());
   if (rsdb_status st = db->blocks.upload(tbl.data(), tbl.size() * sizeof(rsdb::AdamBlock))) return st;
-  if (db->param_bf16)
+  if (db->param_bf16) {
     if (rsdb_status st = db->blocks_fused.upload(tbl_fused.data(),
                                                  tbl_fused.size() * sizeof(rsdb::AdamBlock)))
       return st;
+    if (compact_ok && !tbl_c.empty()) {
+      if (rsdb_status st = db->blocks_compact.upload(tbl_c.data(), tbl_c.size() * sizeof(rsdb::AdamBlockC)))
+        return st;
+      if (rsdb_status st = db->unit_bases.upload(ubases.data(), ubases.size() * sizeof(rsdb::UnitBase)))
+        return st;
+      db->n_units = n_units;
+    }
+  }
   *out = db.release();
   return OK_CLEAR();
+}
+
+// RSDB_RSA_COMPACT=0: the fused DBuffer step reads the full 40-B table (A/B)
+static bool rsa_compact_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("RSDB_RSA_COMPACT");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return v;
 }
 
 static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg, int64_t step,
                                    void* stream, bool gather) {
   if (!d) return fail(RSDB_EINVAL, "null dbuffer");
+  const bool use_compact = d->blocks_compact.p && rsa_compact_enabled();
   if (!d->param_bf16) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs bf16 units");
   rsdb::AdamScalars s;
   if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
@@ -882,7 +908,10 @@ static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(d->blocks_fused.p), d->nblocks, g,
                                     m, float(1.0 / double(m)), ap, s, m > 1 ? &sg : nullptr, d->rank,
                                     m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr,
-                                    aligned16(d->base[RSDB_KIND_MABS]) && aligned16(d->base[RSDB_KIND_VABS])));
+                                    aligned16(d->base[RSDB_KIND_MABS]) && aligned16(d->base[RSDB_KIND_VABS]),
+                                    use_compact ? static_cast<const rsdb::AdamBlockC*>(d->blocks_compact.p) : nullptr,
+                                    use_compact ? static_cast<const rsdb::UnitBase*>(d->unit_bases.p) : nullptr,
+                                    use_compact ? d->n_units : 0));
   return OK_CLEAR();
 }
 

@@ -96,6 +96,9 @@ struct rsdb_dbuffer {
   int64_t nblocks = 0;
   DevTable blocks;        // arena-relative table over all units (grad in GRAD_F32 elements)
   DevTable blocks_fused;  // the same with grad in GRAD_FULL (bf16) elements, for the fused RS+Adam
+  DevTable blocks_compact;  // rsdb::AdamBlockC over the fused table (flat blocks only), or empty
+  DevTable unit_bases;      // rsdb::UnitBase per unit for the compact table
+  int32_t n_units = 0;
   int32_t m = 1, rank = 0;
   int32_t param_bf16 = 1;
   std::vector<int64_t> grad_bytes;  // per unit, for grouped zero

@@ -91,10 +91,27 @@ cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, 
 // every peer's parameter array (AllGather fused into the step).  abs_tma: the
 // absmax arrays are 16-B aligned and readable in whole 16-B chunks around
 // every slot (DBuffer arenas), so they are fetched with the block's TMA.
+// Compact block table for the fused DBuffer step (flat blocks): 16 B per
+// block -- the block's unit, its offset inside the unit's shard, length and
+// absmax slot -- plus per-unit bases (kept in shared memory), so each CTA
+// loads 16 B per block instead of the 40-B AdamBlock on the critical path.
+struct AdamBlockC {
+  uint32_t unit;
+  uint32_t off;
+  int32_t len;
+  int32_t slot;
+};
+static_assert(sizeof(AdamBlockC) == 16, "AdamBlockC is 16 bytes");
+struct UnitBase {
+  int64_t state, grad, param;  // element offsets of the unit's shard in MASTER, GRAD_FULL, PARAM_FULL
+};
+constexpr int RSA_MAX_UNITS = 64;
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
-                               const P2PPtrs* push_params = nullptr, int abs_tma = 0);
+                               const P2PPtrs* push_params = nullptr, int abs_tma = 0,
+                               const AdamBlockC* ctbl = nullptr, const UnitBase* ubase = nullptr,
+                               int n_units = 0);
 
 // ---- N2: FP8 E4M3 block quantization fused with the AllGather (fp8.cu) ----
 struct Fp8Tile {

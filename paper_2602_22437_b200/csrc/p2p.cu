@@ -757,7 +757,10 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
                                                             int64_t nblocks, P2PPtrs grads,
                                                             P2PPtrs params, float scale, AdamPtrs P,
                                                             AdamScalars s, P2PSignals sg, int rank,
-                                                            uint64_t epoch, int nst) {
+                                                            uint64_t epoch, int nst,
+                                                            const AdamBlockC* __restrict__ ctbl,
+                                                            const UnitBase* __restrict__ ubase,
+                                                            int n_units) {
   using Gm = RsaGeom<M>;
   using G = AdamGeom<RSA_NT>;
   using PushT = std::conditional_t<PUSH, PeerPush<M>, NoPush>;
@@ -766,9 +769,22 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
   extern __shared__ __align__(128) uint8_t rsa_smem[];
   __shared__ __align__(8) uint64_t full[RSA_MAX_STAGES];
   __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
-  if constexpr (SYNC) p2p_start(sg, rank, M, epoch);
+  __shared__ UnitBase s_ub[RSA_MAX_UNITS];
+  if (ctbl)
+    for (int i = threadIdx.x; i < n_units; i += RSA_NT) s_ub[i] = ubase[i];
+  if constexpr (SYNC) p2p_start(sg, rank, M, epoch);  // (contains a CTA barrier)
+  else __syncthreads();
+  // block b's descriptor: the compact 16-B entry + its unit's bases, or the full entry
+  auto desc = [&](int64_t b) -> AdamBlock {
+    if (ctbl) {
+      const AdamBlockC c = ctbl[b];
+      const UnitBase& u = s_ub[c.unit];
+      return AdamBlock{u.state + c.off, u.grad + c.off, u.param + c.off, c.len, c.slot, c.len, c.len};
+    }
+    return tbl[b];
+  };
   auto issue = [&](int64_t b, int st) {
-    const AdamBlock nb = tbl[b];
+    const AdamBlock nb = desc(b);
     uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
     if (rsa_fits(nb)) {
       const uint32_t L = uint32_t(nb.len);
@@ -796,7 +812,7 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
   int it = 0, st = 0;
   uint32_t phase = 0;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
-    const AdamBlock blk = tbl[b];
+    const AdamBlock blk = desc(b);
     const float sm = P.mabs[blk.slot] / 127.0f;
     const float sv = P.vabs[blk.slot] / 255.0f;
     float* rm = red_m[it & 1];
@@ -1055,7 +1071,8 @@ template <int M, bool SYNC, bool PUSH>
 static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads,
                                const P2PPtrs& params, float scale, const AdamPtrs& P,
                                const AdamScalars& s, const P2PSignals& sg, int rank, uint64_t epoch,
-                               cudaStream_t st, int abs_tma) {
+                               cudaStream_t st, int abs_tma, const AdamBlockC* ctbl, const UnitBase* ubase,
+                               int n_units) {
   static const int nst = rsa_stages(RsaGeom<M>::STAGES);
   static const bool ws = rsa_warp_specialised();
   const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * nst;
@@ -1079,30 +1096,33 @@ static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PP
     rs_adam_ws_kernel<M, true, SYNC, PUSH><<<blocks, RSA_THREADS, smem, st>>>(
         tbl, nblocks, grads, params, scale, P, s, sg, rank, epoch, nst, abs_tma);
   else
-    rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(tbl, nblocks, grads, params, scale, P,
-                                                                         s, sg, rank, epoch, nst);
+    rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(
+        tbl, nblocks, grads, params, scale, P, s, sg, rank, epoch, nst, ctbl, ubase, n_units);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
-                               const P2PPtrs* push_params, int abs_tma) {
+                               const P2PPtrs* push_params, int abs_tma, const AdamBlockC* ctbl,
+                               const UnitBase* ubase, int n_units) {
+  if (rsa_warp_specialised()) ctbl = nullptr;  // the warp-specialised variant reads the full table
   if (!P.param_bf16) return cudaErrorInvalidValue;  // the fused path is for bf16 units
   const P2PPtrs none_p{};
   if (m == 1) {
     P2PSignals none{};
     return rs_adam_mbs<1, false, false>(tbl, nblocks, grads, none_p, scale, P, s, none, rank, epoch, st,
-                                        abs_tma);
+                                        abs_tma, ctbl, ubase, n_units);
   }
   if (!sg) return cudaErrorInvalidValue;
   switch (m) {
 #define RSA_CASE(MM)                                                                                  \
   case MM:                                                                                            \
     return push_params ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, *push_params, scale, P, s,  \
-                                                     *sg, rank, epoch, st, abs_tma)                   \
+                                                     *sg, rank, epoch, st, abs_tma, ctbl, ubase,      \
+                                                     n_units)                                         \
                        : rs_adam_mbs<MM, true, false>(tbl, nblocks, grads, none_p, scale, P, s, *sg,  \
-                                                      rank, epoch, st, abs_tma);
+                                                      rank, epoch, st, abs_tma, ctbl, ubase, n_units);
     RSA_CASE(2) RSA_CASE(3) RSA_CASE(4) RSA_CASE(5) RSA_CASE(6) RSA_CASE(7) RSA_CASE(8)
 #undef RSA_CASE
     default:
