@@ -103,3 +103,18 @@ def test_sharded_step_equals_per_matrix_muon(m):
         assert np.allclose(buf[l:l + e], b1, rtol=0, atol=1e-15)
         assert np.allclose(master[l:l + e], w0 - 0.02 * np.sqrt(max(1, r / c)) * o, atol=1e-14)
         assert roots[t] in range(m)
+
+
+@pytest.mark.parametrize("shape", [(96, 24), (24, 96), (64, 64), (200, 40)])
+def test_shape_scale_makes_update_rms_about_one_over_sqrt_cols(shape):
+    """R23's sqrt(max(1, rows/cols)) is Muon's scale: NS output has singular
+    values in Muon's ~[0.68, 1.13] band, so its RMS is about
+    1/sqrt(max(rows, cols)), and the scaled update's RMS * sqrt(cols) lands in
+    that band for both orientations (a transposed ratio would put tall
+    matrices at sqrt(cols/rows) < 0.68)."""
+    rng = np.random.default_rng(sum(shape))
+    G = rng.normal(size=shape)
+    o = MU.newton_schulz(G)
+    r, c = shape
+    rms = np.sqrt(np.mean((MU.shape_scale(r, c) * o) ** 2)) * np.sqrt(c)
+    assert 0.6 < rms < 1.2
