@@ -15,7 +15,10 @@ Modules
   planner  -- a1 granularity, a2 Alg. 1 planner (O1), validator, brute force,
               a3 per-rank segment / quantization-block tables
   dbuffer  -- a4/a5 AllGather + views, a6 grouped cast/scale, a7 ReduceScatter (O2, O3)
-  adam8    -- a8 block-wise 8-bit Adam (O4)
+  adam8    -- a8 block-wise 8-bit Adam (O4; linear codes, or the dynamic map)
+  codemap  -- N2 dynamic (tree) code map of the 8-bit states (R25)
+  fp8      -- N2 FP8 E4M3 128x128 block quantization before the AllGather (R18-R20)
+  muon     -- N3 distributed Muon, Algorithm 2 (R21-R24)
 
 Parity status of every function is stated in its docstring; all are pinned
 (tests/test_oracle_*.py) -- there is no "parity unpinned" function.
