@@ -321,3 +321,32 @@ def test_fsdp_sweep_tool_accounting():
     # row-wise-128 padding 0.24 / 0.86 / 2.12 % at m = 2 / 4 / 8
     for m, pct in ((2, 0.24), (4, 0.86), (8, 2.12)):
         assert abs(fs.sweep_one(w, m, measure=False)["fsdp2_rowwise_block_padding_pct"] - pct) < 0.006
+
+
+def test_extension_entry_points_error_behaviour():
+    """The §8(f) / §7 extensions validate their arguments before touching a
+    device (header: EINVAL / EMISMATCH), and fail loudly (ECUDA) without one."""
+    from oracle import fp8 as F
+    lay2 = R.plan([256 * 128], [128 * 128], 1, elem_bytes=2)
+    lay1 = R.plan([256 * 128], [128 * 128], 1, elem_bytes=1)
+    with pytest.raises(R.RsdbError) as e:          # FP8 units are 1-byte layouts
+        R.Fp8Unit(lay2, F.tile_specs([128]), 0, None, None, None)
+    assert e.value.status == _capi.RSDB_EMISMATCH
+    with pytest.raises(R.RsdbError) as e:          # tile specs required
+        R.Fp8Unit(lay1, [("flat", 2048)], 0, None, None, None)
+    assert e.value.status == _capi.RSDB_EINVAL
+    with pytest.raises(R.RsdbError) as e:          # rows * cols must equal numel
+        R.Muon(lay2, [(100, 100)], 0)
+    assert e.value.status == _capi.RSDB_EINVAL
+    with pytest.raises(R.RsdbError) as e:          # world > 1 needs a comm
+        R.Muon(R.plan([64], [1], 2), [(8, 8)], 0)
+    assert e.value.status == _capi.RSDB_EINVAL
+    with pytest.raises(R.RsdbError) as e:          # valid arguments, no GPU here
+        R.Muon(lay2, [(256, 128)], 0)
+    assert e.value.status == _capi.RSDB_ECUDA
+    with pytest.raises(R.RsdbError) as e:
+        R.Ring(0)
+    assert e.value.status == _capi.RSDB_EINVAL
+    with pytest.raises(R.RsdbError) as e:
+        R.Ring(2)
+    assert e.value.status == _capi.RSDB_ECUDA
