@@ -1,0 +1,51 @@
+#!/usr/bin/env python
+"""Fig. 9 of the paper: RaggedShard padding of DeepSeek-V3-671B
+and GPT-OSS-120B per-layer FSDP units when the expert FFN weights are sharded
+at 1 / 16 / 128-row granularity, over FSDP sizes m, with the C++ planner
+(Algorithm 1).  Padding ratio of a model = sum over units of (m*S - E) /
+sum of E.  Also the planner time ("< 0.3 s").  One JSON line per
+(model, rows, m); host only.
+
+  python scripts/fig9_padding.py > profiles/r1/fig9_padding.jsonl
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2602_22437_b200 as R  # noqa: E402
+from synth import workloads as W  # noqa: E402
+
+MS = (8, 16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024)
+
+
+def main():
+    for name, mk in (("deepseek-v3-671b", W.deepseek_v3_671b), ("gpt-oss-120b", W.gpt_oss_120b)):
+        for rows in (1, 16, 128):
+            wl = mk(rows)
+            # identical layer units plan identically: plan each distinct unit once
+            kinds = {}
+            for u in wl.units:
+                key = tuple((t.numel, R.block_elems(t.shape, t.gran)) for t in u.tensors)
+                kinds[key] = kinds.get(key, 0) + 1
+            for m in MS:
+                pad = tot = 0
+                t_max = 0.0
+                for key, count in kinds.items():
+                    es = [k[0] for k in key]
+                    gs = [k[1] for k in key]
+                    t0 = time.perf_counter()
+                    lay = R.plan(es, gs, m, elem_bytes=2)
+                    t_max = max(t_max, time.perf_counter() - t0)
+                    pad += count * (m * lay.S - lay.E)
+                    tot += count * lay.E
+                print(json.dumps({"model": name, "rows": rows, "m": m, "units": len(wl.units),
+                                  "params": tot, "padding_pct": 100.0 * pad / tot,
+                                  "max_plan_s_per_unit": t_max}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
