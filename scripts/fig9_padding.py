@@ -3,7 +3,8 @@
 and GPT-OSS-120B per-layer FSDP units when the expert FFN weights are sharded
 at 1 / 16 / 128-row granularity, over FSDP sizes m, with the C++ planner
 (Algorithm 1).  Padding ratio of a model = sum over units of (m*S - E) /
-sum of E.  Also the planner time ("< 0.3 s").  One JSON line per
+sum of E; also the ratio of each distinct unit kind (root, dense layer, MoE
+layer), since a whole-model figure mixes them.  Also the planner time ("< 0.3 s").  One JSON line per
 (model, rows, m); host only.
 
   python scripts/fig9_padding.py > profiles/r1/fig9_padding.jsonl
@@ -27,14 +28,15 @@ def main():
         for rows in (1, 16, 128):
             wl = mk(rows)
             # identical layer units plan identically: plan each distinct unit once
-            kinds = {}
+            kinds = {}  # key -> [first unit name, count]
             for u in wl.units:
                 key = tuple((t.numel, R.block_elems(t.shape, t.gran)) for t in u.tensors)
-                kinds[key] = kinds.get(key, 0) + 1
+                kinds.setdefault(key, [u.name, 0])[1] += 1
             for m in MS:
                 pad = tot = 0
                 t_max = 0.0
-                for key, count in kinds.items():
+                per_kind = {}
+                for key, (uname, count) in kinds.items():
                     es = [k[0] for k in key]
                     gs = [k[1] for k in key]
                     t0 = time.perf_counter()
@@ -42,8 +44,10 @@ def main():
                     t_max = max(t_max, time.perf_counter() - t0)
                     pad += count * (m * lay.S - lay.E)
                     tot += count * lay.E
+                    per_kind[f"{uname} (x{count})"] = round(100.0 * (m * lay.S - lay.E) / lay.E, 3)
                 print(json.dumps({"model": name, "rows": rows, "m": m, "units": len(wl.units),
                                   "params": tot, "padding_pct": 100.0 * pad / tot,
+                                  "unit_padding_pct": per_kind,
                                   "max_plan_s_per_unit": t_max}), flush=True)
 
 
