@@ -109,10 +109,6 @@ def quantize_tile(x: np.ndarray) -> Tuple[np.ndarray, np.float32]:
     return codes, f32(A / f32(E4M3_MAX))
 
 
-def dequantize_tile(codes: np.ndarray, scale) -> np.ndarray:
-    return (e4m3_decode(codes) * f32(scale)).astype(f32)
-
-
 def tile_specs(row_len: Sequence[int], tile: int = 128) -> List[Tuple]:
     """("tile", C, tile, tile) for every tensor of row length C (R20)."""
     return [("tile", int(c), tile, tile) for c in row_len]

@@ -305,17 +305,6 @@ def validate(lay: Layout) -> List[str]:
 # ----------------------------------------------------------------------------
 
 
-def _start_ok(l: int, e: int, g: int, S: int, m: int) -> bool:
-    r = l + e
-    if r > m * S:
-        return False
-    for k in range(1, m):
-        b = k * S
-        if l < b < r and (b - l) % g != 0:
-            return False
-    return True
-
-
 def exists_layout(es: Sequence[int], gs: Sequence[int], m: int, S: int) -> bool:
     """Exhaustive: is there ANY choice of starts (fixed order) satisfying
     P:226-229 at this S?  Tracks the set of every reachable end position

@@ -261,18 +261,5 @@ def gpt_oss_120b(rows: int) -> Workload:
     return Workload(f"gpt-oss-120b-{rows}rows", units)
 
 
-def unit_numels(unit: Unit) -> List[int]:
-    return [t.numel for t in unit.tensors]
-
-
-def flat_offsets(unit: Unit) -> List[int]:
-    """Logical (padding-free) flat start index of each tensor in a unit."""
-    out, acc = [], 0
-    for t in unit.tensors:
-        out.append(acc)
-        acc += t.numel
-    return out
-
-
 def all_units(w: Workload) -> Sequence[Unit]:
     return w.units

@@ -22,7 +22,7 @@ from oracle import planner as OP
 from synth import hashgen as H
 from synth import workloads as W
 
-from gpu_helpers import bf16_bits, f32, logical_grads, logical_params, numels, place_gpu
+from gpu_helpers import bf16_bits, f32, logical_grads, logical_params, place_gpu
 
 pytestmark = pytest.mark.gpu
 

@@ -8,7 +8,6 @@ order): acquire, gather again, write the gradients into the slot, run the
 fused ReduceScatter + 8-bit Adam writing the persistent shard, release.  The
 shards and optimizer states must equal, bit for bit, the same step on
 dedicated (non-ring) buffers.  World 1 here; N = 2/4 in the parity worker."""
-import numpy as np
 import pytest
 import torch
 
