@@ -458,7 +458,8 @@ def arena_sizes(layouts: Sequence[Layout], rank: int, qblock: int = 2048, align:
     else:
         ptrs, _keep = _spec_ptrs(qspec)
         check(lib.rsdb_arena_sizes_q(arr, len(layouts), rank, ptrs, align, sizes, offs))
-    return list(sizes), [list(offs[u * 8:(u + 1) * 8]) for u in range(len(layouts))]
+    K = _c.RSDB_NKINDS
+    return list(sizes), [list(offs[u * K:(u + 1) * K]) for u in range(len(layouts))]
 
 
 class DBuffer:

@@ -350,3 +350,56 @@ def test_extension_entry_points_error_behaviour():
     with pytest.raises(R.RsdbError) as e:
         R.Ring(2)
     assert e.value.status == _capi.RSDB_ECUDA
+
+
+# ------------------------------------------------ header <-> binding agreement
+_STRUCTS = {  # C typedef -> ctypes class in the binding
+    "rsdb_qspec": "QSpec", "rsdb_unit_bufs": "UnitBufs", "rsdb_adam_cfg": "AdamCfg",
+    "rsdb_adam_state": "AdamState", "rsdb_segment": "Segment", "rsdb_muon_cfg": "MuonCfg",
+    "rsdb_muon_bufs": "MuonBufs",
+}
+
+
+def test_header_defines_match_the_binding():
+    import re
+    from paper_2602_22437_b200 import _capi as CB
+    import paper_2602_22437_b200 as R
+    hdr = open(os.path.join(ROOT, "include", "rsdb.h")).read()
+    defines = {k: int(v) for k, v in re.findall(r"^#define (RSDB_\w+) (\d+)", hdr, re.M)}
+    assert len(defines) >= 25
+    for name, val in defines.items():
+        if name.startswith("RSDB_ORDER_"):
+            assert R.ORDER[name[len("RSDB_ORDER_"):].lower()] == val, name
+        else:
+            assert getattr(CB, name) == val, name
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """sizeof / offsetof of every public struct, compiled from include/rsdb.h
+    with gcc, equals the ctypes declaration the binding marshals with."""
+    import shutil
+    import subprocess
+    from paper_2602_22437_b200 import _capi as CB
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rsdb.h"', "int main(void) {"]
+    for cname, pyname in _STRUCTS.items():
+        cls = getattr(CB, pyname)
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        c, f, v = ln.split()
+        got[(c, f)] = int(v)
+    for cname, pyname in _STRUCTS.items():
+        cls = getattr(CB, pyname)
+        assert got[(cname, "size")] == C.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)
