@@ -403,3 +403,29 @@ def test_struct_layouts_match_the_header(tmp_path):
         assert got[(cname, "size")] == C.sizeof(cls), cname
         for f, _ in cls._fields_:
             assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)
+
+
+def test_plain_c_client(tmp_path):
+    """The boundary is usable from plain C: tests/c_client/plan_toy.c, linked
+    against librsdb.so, plans BJ config 1 and must reproduce the hand-derived
+    layout of tests/golden/toy_config_plan.json."""
+    import json
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    lib = os.path.dirname(_capi.LIB_PATH)
+    exe = tmp_path / "plan_toy"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_client", "plan_toy.c"), "-o", str(exe),
+                    "-L", lib, "-lrsdb", f"-Wl,-rpath,{lib}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    tok = out.stdout.split()
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "toy_config_plan.json")))
+    assert int(tok[tok.index("S") + 1]) == g["S"]
+    assert int(tok[tok.index("padding") + 1]) == g["padding"]
+    i = tok.index("starts") + 1
+    assert [int(x) for x in tok[i:i + len(g["starts"])]] == g["starts"]
+    j = tok.index("blocks") + 1
+    assert [int(x) for x in tok[j:j + 2]] == [g["rank_blocks_per_rank"]] * 2
