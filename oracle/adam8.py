@@ -10,22 +10,27 @@ AdamW order, host fp64 scalars rounded to fp32, the update uses the fresh
 fp32 m, v before requantization).
 
 Per quant block (block = contiguous elements of one tensor, tail shorter),
-every op below is one IEEE fp32 operation, in this order:
+every op below is one IEEE fp32 operation (RN = round to nearest even once;
+steps 3 and 4 round once per fused multiply-add, as torch's lerp_ and
+addcmul_ do -- reading R26), in this order:
   1. mt = q_m * fl(A_m / 127)                 dequantize first moment (signed)
   2. vt = q_v * fl(A_v / 255)                 dequantize second moment (unsigned)
-  3. m  = mt + w1 * (g - mt)                  w1 = fl(1 - beta1)   (torch lerp, weight < 0.5)
-  4. v  = b2 * vt + w2 * (g * g)              b2 = fl(beta2), w2 = fl(1 - beta2)
+  3. m  = RN(mt + w1 * fl(g - mt))            w1 = fl(1 - beta1)   (torch lerp_, weight < 0.5)
+  4. v  = RN(fl(w2 * g) * g + fl(b2 * vt))    b2 = fl(beta2), w2 = fl(1 - beta2)
+                                              (torch mul_(beta2).addcmul_(g, g, 1 - beta2))
   5. p  = p * c_wd                            c_wd = fl(1 - lr * wd)   (decoupled decay)
   6. p  = p - step_size * (m / (sqrt(v) / bc2s + eps))
                                               step_size = fl(lr / (1 - beta1^t)),
                                               bc2s = fl(sqrt(1 - beta2^t))
   7. A_m' = max |m|,  A_v' = max v            over the block
-  8. q_m = clamp(rint(m / fl(A_m'/127)), -127, 127)   (int8)
-     q_v = clamp(rint(v / fl(A_v'/255)),    0, 255)   (uint8); A' = 0 -> codes 0
+  8. q_m = clamp(rint(m * fl(127 / A_m')), -127, 127)   (int8)
+     q_v = clamp(rint(v * fl(255 / A_v')),    0, 255)   (uint8); A' = 0 -> codes 0
+     (the code is decided in the kernel's arithmetic, reading R26)
   9. param shard for the next AllGather = bf16_RNE(p)  (or p itself for fp32 units)
 
 Parity pins (tests/test_oracle_adam8.py): step-1 closed form from the zero
-state, the identity-codec variant equals torch.optim.AdamW (library routine),
+state, the identity-codec variant equals torch.optim.AdamW (library routine:
+m and v bit for bit, p within 1e-6), fma32 against exact rational arithmetic,
 codec round trip / error bound / zero block, shard-local = unsharded result
 (containment, P:419/P:433).
 """
@@ -66,6 +71,25 @@ def host_scalars(cfg: AdamCfg, step: int) -> dict:
     }
 
 
+def fma32(a, b, c) -> np.ndarray:
+    """RN32(a*b + c) for fp32 a, b, c: the exact value rounded once to fp32
+    (a fused multiply-add).  a*b is exact in fp64 (24 + 24 <= 53 bits); the
+    fp64 sum s and its exact error e (TwoSum) give exact = s + e.  RN32(s)
+    equals RN32(exact) unless s lies exactly on a midpoint between two fp32
+    values while e != 0 -- then the sign of e picks the side."""
+    a, b, c = (np.asarray(x, np.float32).astype(np.float64) for x in (a, b, c))
+    ab = a * b
+    s = ab + c
+    bv = s - ab
+    e = (ab - (s - bv)) + (c - bv)
+    r = s.astype(np.float32)
+    r64 = r.astype(np.float64)
+    other = np.nextafter(r, np.where(s > r64, np.inf, -np.inf).astype(np.float32)).astype(np.float64)
+    on_mid = (s != r64) & (s == (r64 + other) / 2) & (e != 0)
+    fix = np.where(e > 0, np.maximum(r64, other), np.minimum(r64, other)).astype(np.float32)
+    return np.where(on_mid, fix, r).astype(np.float32)
+
+
 def dequantize(codes: np.ndarray, absmax: f32, signed: bool) -> np.ndarray:
     levels = f32(127.0) if signed else f32(255.0)
     scale = f32(f32(absmax) / levels)
@@ -79,11 +103,11 @@ def quantize(x: np.ndarray, signed: bool) -> Tuple[np.ndarray, f32]:
     if a == 0:
         return np.zeros(x.shape, np.int8 if signed else np.uint8), f32(0)
     if signed:
-        scale = f32(a / f32(127.0))
-        q = np.clip(np.rint((x / scale).astype(np.float32)), -127, 127).astype(np.int8)
+        inv = f32(f32(127.0) / a)
+        q = np.clip(np.rint((x * inv).astype(np.float32)), -127, 127).astype(np.int8)
     else:
-        scale = f32(a / f32(255.0))
-        q = np.clip(np.rint((x / scale).astype(np.float32)), 0, 255).astype(np.uint8)
+        inv = f32(f32(255.0) / a)
+        q = np.clip(np.rint((x * inv).astype(np.float32)), 0, 255).astype(np.uint8)
     return q, a
 
 
@@ -91,8 +115,8 @@ def adam_block_update(p, g, mt, vt, sc):
     """Steps 3-6 on fp32 arrays (shared by the 8-bit and identity-codec
     variants); returns (p_new, m, v)."""
     g = np.asarray(g, dtype=np.float32)
-    m = (mt + sc["w1"] * (g - mt).astype(np.float32)).astype(np.float32)
-    v = (sc["b2"] * vt + sc["w2"] * (g * g).astype(np.float32)).astype(np.float32)
+    m = fma32(sc["w1"], (g - mt).astype(np.float32), mt)
+    v = fma32((sc["w2"] * g).astype(np.float32), g, (sc["b2"] * vt).astype(np.float32))
     p = (p * sc["c_wd"]).astype(np.float32)
     denom = (np.sqrt(v).astype(np.float32) / sc["bc2s"] + sc["eps"]).astype(np.float32)
     p = (p - sc["step_size"] * (m / denom).astype(np.float32)).astype(np.float32)
