@@ -99,7 +99,8 @@ def test_unit_rejects_misaligned_buffers():
 
 
 # ------------------------------------------------------------------ a8
-def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None, codec="linear"):
+def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None, codec="linear",
+               exact_codes=False):
     gs = [min(q, e) for e in es]
     o, c = _plans(es, gs, m, eb)
     E = sum(es)
@@ -152,11 +153,12 @@ def _adam_case(es, q, m, eb, rank, step, warm, seed=0, zero_grad_tensor=None, co
     g_or = OD.shard(o, OD.place_logical(o, g_log.numpy()), rank)
     ref = OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], blocks_o,
                             OA.AdamCfg(), step, out_bf16=(eb == 2), codec=codec)
-    _check_adam(o, rank, blocks_o, (master, mq, vq, ma, va, param_full), ref, ins, eb, cfg.lr)
+    _check_adam(o, rank, blocks_o, (master, mq, vq, ma, va, param_full), ref, ins, eb, cfg.lr,
+                exact_codes=exact_codes)
     return u
 
 
-def _check_adam(o, rank, blocks, gpu, ref, ins, eb, lr):
+def _check_adam(o, rank, blocks, gpu, ref, ins, eb, lr, exact_codes=False):
     master, mq, vq, ma, va, param_full = gpu
     S = o.S
     mask = np.zeros(S, bool)
@@ -176,6 +178,9 @@ def _check_adam(o, rank, blocks, gpu, ref, ins, eb, lr):
     dv = np.abs(vq.cpu().numpy().astype(np.int32) - ref[2].astype(np.int32))
     assert dm[mask].max(initial=0) <= 1 and dv[mask].max(initial=0) <= 1
     assert np.mean(dm[mask] != 0) < 1e-3 and np.mean(dv[mask] != 0) < 1e-3
+    if exact_codes:  # R26: moments and code decision are the same IEEE ops on both sides
+        assert not dm[mask].any() and not dv[mask].any(), (int(dm[mask].sum()), int(dv[mask].sum()))
+        assert np.array_equal(f32(ma), ref[3]) and np.array_equal(f32(va), ref[4])
     # absmax
     for a, r in ((f32(ma), ref[3]), (f32(va), ref[4])):
         assert np.all(np.abs(a - r) <= 1e-6 * np.abs(r) + 1e-30)
@@ -213,6 +218,13 @@ ADAM_CASES = [
 @pytest.mark.parametrize("es,q,m,eb,rank,step,warm", ADAM_CASES)
 def test_adam8_parity(es, q, m, eb, rank, step, warm):
     _adam_case(es, q, m, eb, rank, step, warm)
+
+
+@pytest.mark.xfail(strict=False, reason="R26 makes the codes and absmax bit exact by construction "
+                   "(CPU emulation); kept non-fatal until a GPU run of the R26 kernel confirms it")
+@pytest.mark.parametrize("es,q,m,eb,rank,step,warm", ADAM_CASES)
+def test_adam8_codes_exact_r26(es, q, m, eb, rank, step, warm):
+    _adam_case(es, q, m, eb, rank, step, warm, exact_codes=True)
 
 
 @pytest.mark.parametrize("es,q,m,eb,rank,step,warm", [ADAM_CASES[i] for i in (0, 1, 3, 4, 5, 7)])
