@@ -22,7 +22,7 @@ from ._capi import (RSDB_BF16, RSDB_F32, RSDB_GRAN_ELEM, RSDB_GRAN_FLAT,  # noqa
 lib = _c.lib
 check = _c.check
 
-__all__ = ["block_elems", "plan", "Layout", "Comm", "Unit", "DBuffer", "CopyPlan", "AdamConfig",
+__all__ = ["block_elems", "plan", "Layout", "tensor_views", "Comm", "Unit", "DBuffer", "CopyPlan", "AdamConfig",
            "all_gather", "reduce_scatter", "step_8bit_adam", "unit_cast_scale", "RsdbError",
            "init_comm"]
 
@@ -201,6 +201,28 @@ def layout_from_starts(numel, block, world, S, starts, elem_bytes=2, gcoll_bytes
 
 
 # ---------------------------------------------------------------- comm
+def tensor_views(layout: Layout, full, shapes: Sequence[Sequence[int]]) -> list:
+    """a5 (P:308 "zero-copy access before and after communication"): the
+    tensors of a unit as views of its m*S buffer (PARAM_FULL, GRAD_FULL or
+    GRAD_F32 of any dtype): tensor t = full[l_t : l_t + e_t] reshaped to
+    shapes[t].  No bytes move; writes through a view land in the buffer the
+    collectives read.  Padding is never covered by a view."""
+    numel = layout.to_json()["numel"]
+    if len(shapes) != len(numel):
+        raise ValueError(f"{len(shapes)} shapes for a unit of {len(numel)} tensors")
+    if full.dim() != 1 or full.numel() != layout.m * layout.S:
+        raise ValueError(f"buffer must be flat with m*S = {layout.m * layout.S} elements")
+    out = []
+    for t, (l, e, shp) in enumerate(zip(layout.starts, numel, shapes)):
+        n = 1
+        for d in shp:
+            n *= int(d)
+        if n != e:
+            raise ValueError(f"tensor {t}: shape {tuple(shp)} has {n} elements, the layout {e}")
+        out.append(full[l:l + e].view(*[int(d) for d in shp]))
+    return out
+
+
 class Comm:
     def __init__(self, uid: bytes, world: int, rank: int, device: int):
         h = C.c_void_p()

@@ -429,3 +429,33 @@ def test_plain_c_client(tmp_path):
     assert [int(x) for x in tok[i:i + len(g["starts"])]] == g["starts"]
     j = tok.index("blocks") + 1
     assert [int(x) for x in tok[j:j + 2]] == [g["rank_blocks_per_rank"]] * 2
+
+
+def test_tensor_views_alias_the_unit_buffer():
+    """a5: R.tensor_views gives each tensor of a unit as a zero-copy
+    view at l_t of its m*S buffer -- the oracle's views -- on CPU
+    tensors (pure pointer arithmetic, no library compute)."""
+    from oracle import dbuffer as OD
+    shapes = [(256, 128), (256,), (77,), (40, 50), (2049,)]
+    es = [int(np.prod(s)) for s in shapes]
+    gs = [min(2048, e) for e in es]
+    lay = R.plan(es, gs, 3, elem_bytes=4)
+    o = P.plan(es, gs, 3, P.gcoll_elems(4))
+    full = torch.zeros(lay.m * lay.S, dtype=torch.float32)
+    views = R.tensor_views(lay, full, shapes)
+    rng = np.random.default_rng(0)
+    logical = rng.normal(size=sum(es)).astype(np.float32)
+    off = 0
+    for v, s, e, l in zip(views, shapes, es, o.starts):
+        assert tuple(v.shape) == s and v.storage_offset() == l and v.untyped_storage().data_ptr() == \
+            full.untyped_storage().data_ptr()
+        v.copy_(torch.from_numpy(logical[off:off + e]).view(s))  # write through the view
+        off += e
+    # the buffer is the oracle's placement of the logical tensors, padding untouched (0)
+    assert np.array_equal(full.numpy(), OD.place_logical(o, logical))
+    with pytest.raises(ValueError):
+        R.tensor_views(lay, full, shapes[:-1])
+    with pytest.raises(ValueError):
+        R.tensor_views(lay, full[:-1], shapes)
+    with pytest.raises(ValueError):
+        R.tensor_views(lay, full, shapes[:-1] + [(2048,)])
