@@ -68,6 +68,8 @@ def test_select_roots_lpt_bound_and_rules():
             load[r] += c
         opt = MU.brute_force_makespan(costs, m)
         assert max(load) <= (4 / 3 - 1 / (3 * m)) * opt + 1e-9
+        # greedy balance (SPEC S:428 invariant): spread <= the largest single cost
+        assert max(load) - min(load) <= max(costs)
     # rules: biggest first; ties in load -> the rank owning most of the matrix
     shapes = [(4, 4), (8, 8), None]
     lay = OP.plan([16, 64, 3], [1, 1, 1], 2, 1)  # S = 42: (8,8) spans ranks 0 (26) and 1 (38)
