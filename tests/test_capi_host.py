@@ -459,3 +459,28 @@ def test_tensor_views_alias_the_unit_buffer():
         R.tensor_views(lay, full[:-1], shapes)
     with pytest.raises(ValueError):
         R.tensor_views(lay, full, shapes[:-1] + [(2048,)])
+
+
+def test_tensor_views_random_plans():
+    """SPEC S:511 acceptance: DBuffer aliasing on 200 randomized plans --
+    writing every tensor through R.tensor_views reproduces the oracle's
+    placement exactly and leaves padding untouched."""
+    from oracle import dbuffer as OD
+    rng = random.Random(11)
+    for _ in range(200):
+        n = rng.randint(1, 6)
+        shapes = [(rng.randint(1, 9),) if rng.random() < 0.3 else (rng.randint(1, 9), rng.randint(1, 9))
+                  for _ in range(n)]
+        es = [int(np.prod(s)) for s in shapes]
+        gs = [s[-1] * rng.randint(1, 2) if len(s) == 2 and rng.random() < 0.5 else 1 for s in shapes]
+        gs = [min(g, e) for g, e in zip(gs, es)]
+        m = rng.randint(1, 4)
+        lay = R.plan(es, gs, m, elem_bytes=4)
+        o = P.plan(es, gs, m, P.gcoll_elems(4))
+        full = torch.full((m * lay.S,), -1.0)
+        logical = np.arange(1, sum(es) + 1, dtype=np.float32)
+        off = 0
+        for v, s, e in zip(R.tensor_views(lay, full, shapes), shapes, es):
+            v.copy_(torch.from_numpy(logical[off:off + e]).view(s))
+            off += e
+        assert np.array_equal(full.numpy(), OD.place_logical(o, logical, fill=-1))
