@@ -234,6 +234,13 @@ def test_adam8_dynamic_codec_parity(es, q, m, eb, rank, step, warm):
     _adam_case(es, q, m, eb, rank, step, warm, codec="dynamic")
 
 
+@pytest.mark.xfail(strict=False, reason="R26 + R25: identical moments and the same fp32 nearest-code "
+                   "decision; kept non-fatal until a GPU run confirms it")
+@pytest.mark.parametrize("es,q,m,eb,rank,step,warm", [ADAM_CASES[i] for i in (0, 1, 3, 4, 5, 7)])
+def test_adam8_dynamic_codes_exact_r26(es, q, m, eb, rank, step, warm):
+    _adam_case(es, q, m, eb, rank, step, warm, codec="dynamic", exact_codes=True)
+
+
 TILE_CASES = [
     # shapes, specs (per tensor), row granularity, m, rank
     ([(96, 64), (64, 40), (130,)], [("tile", 64, 32, 32), ("tile", 40, 32, 32), ("flat", 130)], 32, 2, 1),
