@@ -324,7 +324,9 @@ rsdb_status rsdb_reduce_scatter_adam_gather_p2p(rsdb_unit*, rsdb_p2p* p2p_or_nul
 #define RSDB_NKINDS 8
 /* Byte size of each kind's arena for `rank` and each unit's byte offset in it
  * (unit_offsets[u*RSDB_NKINDS + kind]); every offset is a multiple of
- * align_bytes (>= 16, power of two).  MASTER/MQ/VQ share element offsets. */
+ * align_bytes (>= 16, power of two).  MASTER/MQ/VQ share element offsets.
+ * All units belong to one FSDP group: EMISMATCH if their worlds m differ;
+ * EINVAL for a null layout, rank outside [0, m) or a bad align_bytes. */
 rsdb_status rsdb_arena_sizes(const rsdb_layout* const* units, int32_t n_units, int32_t rank,
                              int64_t qblock, int64_t align_bytes, int64_t* bytes_per_kind,
                              int64_t* unit_offsets);

@@ -712,6 +712,9 @@ static rsdb_status arena_layout(const rsdb_layout* const* units, int32_t n_units
     if (!units[u]) return fail(RSDB_EINVAL, "null layout %d", u);
     const rsdb::Layout& L = units[u]->L;
     if (rank < 0 || rank >= L.m) return fail(RSDB_EINVAL, "rank out of range for unit %d", u);
+    if (L.m != units[0]->L.m)
+      return fail(RSDB_EMISMATCH, "unit %d is planned for world %d, unit 0 for %d (one DBuffer = one FSDP group)",
+                  u, L.m, units[0]->L.m);
     int64_t sz[RSDB_NKINDS] = {0};
     if (rsdb_status st = kind_sizes(L, rank, specs[size_t(u)], sz)) return st;
     for (int k : {RSDB_KIND_PARAM_FULL, RSDB_KIND_GRAD_FULL, RSDB_KIND_GRAD_F32}) {

@@ -484,3 +484,14 @@ def test_tensor_views_random_plans():
             v.copy_(torch.from_numpy(logical[off:off + e]).view(s))
             off += e
         assert np.array_equal(full.numpy(), OD.place_logical(o, logical, fill=-1))
+
+
+def test_arena_sizes_rejects_mixed_worlds():
+    """One DBuffer is one FSDP group: units planned for different world sizes
+    are refused (EMISMATCH), before any device work."""
+    a = R.plan([4096, 100], [2048, 100], 2)
+    b = R.plan([4096, 100], [2048, 100], 4)
+    R.arena_sizes([a, a], 1)
+    with pytest.raises(R.RsdbError) as ei:
+        R.arena_sizes([a, b], 1)
+    assert ei.value.status == _capi.RSDB_EMISMATCH and "world" in str(ei.value)
