@@ -11,12 +11,19 @@ P:493).  For a workload and a list of FSDP sizes m, per rank 0:
             every tensor is its own allocation, rounded to the caching
             allocator's 512 B (the request; reserved segments come on top)
 
+--select N (host): P:493's offline choice of the FSDP group size -- among
+the divisors m of N GPUs with m >= --min-fsdp (the smallest group whose
+shards fit in memory; the rest of the N goes to replication, HSDP), the m
+with the least LCM-induced padding; ties go to the larger m (less memory per
+GPU).  One JSON line with every candidate and the choice.
+
 With --measure (one GPU) both allocation patterns are replayed through
 PyTorch's caching allocator and torch.cuda.memory_reserved() is reported --
 the paper's "peak reserved" comparison (batched DBuffer -12 % vs
 FSDP2's per-parameter eager allocation).  One JSON line per m.
 
   python scripts/fsdp_sweep.py --workload llama1b --ms 2,4,8,16,64 [--measure]
+  python scripts/fsdp_sweep.py --workload gptoss128 --select 1024 --min-fsdp 256
 """
 import argparse
 import json
@@ -37,7 +44,36 @@ KINDS = ("param_full", "grad_full", "grad_f32", "master", "m_q", "v_q", "m_absma
 def workload(name):
     return {"llama1b": lambda: W.llama32_1b(),
             "llama8b": lambda: W.llama3_8b_muon(),
-            "dsv3": lambda: W.dsv3_moe()}[name]()
+            "dsv3": lambda: W.dsv3_moe(),
+            "dsv3_671b_128": lambda: W.deepseek_v3_671b(128),
+            "gptoss128": lambda: W.gpt_oss_120b(128)}[name]()
+
+
+def padding_ratio(w, m):
+    """Σ(m·S − E) / ΣE over the workload's units (C++ planner); identical
+    units are planned once."""
+    pad = tot = 0
+    seen = {}
+    for u in W.all_units(w):
+        key = tuple((t.numel, R.block_elems(t.shape, t.gran)) for t in u.tensors)
+        if key not in seen:
+            lay = R.plan([k[0] for k in key], [k[1] for k in key], m, elem_bytes=2)
+            seen[key] = (lay.m * lay.S - lay.E, lay.E)
+        pad += seen[key][0]
+        tot += seen[key][1]
+    return pad / tot
+
+
+def select_group_size(w, n_gpus, min_fsdp=2):
+    """"we select the FSDP group size by offline simulation to minimize
+    LCM-induced rounding".  Candidates: the divisors m >= min_fsdp of n_gpus;
+    the one with the least padding wins, ties to the larger group."""
+    ms = [m for m in range(max(2, min_fsdp), n_gpus + 1) if n_gpus % m == 0]
+    if not ms:
+        raise ValueError(f"no divisor of {n_gpus} is >= {min_fsdp}")
+    table = {m: padding_ratio(w, m) for m in ms}
+    best = min(ms, key=lambda m: (round(table[m], 12), -m))
+    return best, table
 
 
 def ceil_div(a, b):
@@ -117,11 +153,20 @@ def sweep_one(w, m, measure):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="llama1b", choices=["llama1b", "llama8b", "dsv3"])
+    ap.add_argument("--workload", default="llama1b",
+                    choices=["llama1b", "llama8b", "dsv3", "dsv3_671b_128", "gptoss128"])
+    ap.add_argument("--select", type=int, default=0, help="choose the FSDP size for N GPUs (P:493)")
+    ap.add_argument("--min-fsdp", type=int, default=8, help="smallest FSDP group that fits in memory")
     ap.add_argument("--ms", default="2,4,8,16,32,64")
     ap.add_argument("--measure", action="store_true")
     args = ap.parse_args()
     w = workload(args.workload)
+    if args.select:
+        best, table = select_group_size(w, args.select, args.min_fsdp)
+        print(json.dumps({"workload": w.name, "gpus": args.select, "fsdp_size": best,
+                          "hsdp_replicas": args.select // best,
+                          "padding_pct": {m: round(100 * r, 4) for m, r in table.items()}}), flush=True)
+        return
     for m in [int(x) for x in args.ms.split(",")]:
         print(json.dumps(sweep_one(w, m, args.measure)), flush=True)
 

@@ -495,3 +495,30 @@ def test_arena_sizes_rejects_mixed_worlds():
     with pytest.raises(R.RsdbError) as ei:
         R.arena_sizes([a, b], 1)
     assert ei.value.status == _capi.RSDB_EMISMATCH and "world" in str(ei.value)
+
+
+def test_fsdp_group_size_selection():
+    """P:493 offline FSDP-size choice (scripts/fsdp_sweep.py --select): the
+    padding of every candidate equals the oracle planner's, and the choice is
+    the least-padding divisor >= min_fsdp, ties to the larger group -- for
+    GPT-OSS-120B at 128 rows on 1024 GPUs that is the 5.7 % plateau (m = 512),
+    not the 17 % spike at m = 1024."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fsdp_sweep", os.path.join(ROOT, "scripts", "fsdp_sweep.py"))
+    fs = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fs)
+    w = W.gpt_oss_120b(128)
+    best, table = fs.select_group_size(w, 1024, 256)
+    assert sorted(table) == [256, 512, 1024] and best == 512
+    for m, r in table.items():
+        pad = tot = 0
+        for u in w.units[:2]:  # root + one layer (all layers are identical)
+            lay = P.plan([t.numel for t in u.tensors], [P.block_elems(t.shape, t.gran) for t in u.tensors],
+                         m, P.gcoll_elems(2))
+            k = 1 if u is w.units[0] else len(w.units) - 1
+            pad += k * lay.padding
+            tot += k * lay.E
+        assert r == pytest.approx(pad / tot, rel=1e-12)
+    assert table[1024] > 3 * table[512]
+    with pytest.raises(ValueError):
+        fs.select_group_size(w, 6, 7)
