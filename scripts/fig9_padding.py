@@ -4,7 +4,8 @@ and GPT-OSS-120B per-layer FSDP units when the expert FFN weights are sharded
 at 1 / 16 / 128-row granularity, over FSDP sizes m, with the C++ planner
 (Algorithm 1).  Padding ratio of a model = sum over units of (m*S - E) /
 sum of E; also the ratio of each distinct unit kind (root, dense layer, MoE
-layer), since a whole-model figure mixes them.  Also the planner time ("< 0.3 s").  One JSON line per
+layer), since a whole-model figure mixes them, and the padding with the best
+of P:279's tensor orders (the paper adopts the default order).  Also the planner time ("< 0.3 s").  One JSON line per
 (model, rows, m); host only.
 
   python scripts/fig9_padding.py > profiles/r1/fig9_padding.jsonl
@@ -33,7 +34,7 @@ def main():
                 key = tuple((t.numel, R.block_elems(t.shape, t.gran)) for t in u.tensors)
                 kinds.setdefault(key, [u.name, 0])[1] += 1
             for m in MS:
-                pad = tot = 0
+                pad = tot = pad_best = 0
                 t_max = 0.0
                 per_kind = {}
                 for key, (uname, count) in kinds.items():
@@ -44,9 +45,12 @@ def main():
                     t_max = max(t_max, time.perf_counter() - t0)
                     pad += count * (m * lay.S - lay.E)
                     tot += count * lay.E
+                    best = R.plan_ordered(es, gs, m, "best", elem_bytes=2)  # P:279 orders (N4)
+                    pad_best += count * (m * best.S - best.E)
                     per_kind[f"{uname} (x{count})"] = round(100.0 * (m * lay.S - lay.E) / lay.E, 3)
                 print(json.dumps({"model": name, "rows": rows, "m": m, "units": len(wl.units),
                                   "params": tot, "padding_pct": 100.0 * pad / tot,
+                                  "padding_pct_best_order": 100.0 * pad_best / tot,
                                   "unit_padding_pct": per_kind,
                                   "max_plan_s_per_unit": t_max}), flush=True)
 
