@@ -4,7 +4,8 @@
   * the per-rank quantization-block tables of all ranks partition exactly the
     tensor intervals (so the 8-bit Adam needs no communication, P:419);
   * the NCCL unique-id bootstrap over torch.distributed delivers rank 0's id;
-  * the bench's per-rank algorithmic byte accounting and DBuffer arena sizes.
+  * the bench's per-rank algorithmic byte accounting, its max-over-ranks
+    timing reduction, and DBuffer arena sizes.
 """
 import os
 import socket
@@ -87,6 +88,8 @@ def _worker(rank, world, port, q):
         res["adam_elems_total"] = tot == sum(l.E for l in lays[:3])
         sizes, offs = R.arena_sizes(lays[:3], rank, 2048, 256)
         res["arena_master"] = sizes[3] >= sum(l.S * 4 for l in lays[:3])
+        # the bench's timing rule: step time = MAX over ranks (each rank passes its own)
+        res["max_rule"] = bench.max_over_ranks(1.0 + rank, world) == float(world)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -108,6 +111,7 @@ def test_world2_host_logic():
         assert res["blocks_partition"], res
         assert res["adam_elems_total"], res
         assert res["arena_master"], res
+        assert res["max_rule"], res
         if isinstance(res["uid_ok"], str):
             pytest.skip(res["uid_ok"])
         assert res["uid_ok"] is True
