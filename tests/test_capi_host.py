@@ -416,7 +416,7 @@ def test_plain_c_client(tmp_path):
         pytest.skip("no gcc")
     lib = os.path.dirname(_capi.LIB_PATH)
     exe = tmp_path / "plan_toy"
-    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "c_client", "plan_toy.c"), "-o", str(exe),
                     "-L", lib, "-lrsdb", f"-Wl,-rpath,{lib}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
