@@ -14,3 +14,4 @@ d = json.loads(open("gpurun_out/r2_bench_n1.json").read().strip().splitlines()[-
 r = d["roofline"]
 print(round(d["value"], 1), round(d["ms_per_step"], 3), r["kernel"], round(r["frac"], 3), d["clocks"])
 PY
+timeout 600 python scripts/bench_tiles.py --reps 20 > gpurun_out/r2_tiles.json 2> gpurun_out/r2_tiles.err; echo tiles_rc=$?; cat gpurun_out/r2_tiles.json
