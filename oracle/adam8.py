@@ -19,9 +19,10 @@ addcmul_ do -- reading R26), in this order:
   4. v  = RN(fl(w2 * g) * g + fl(b2 * vt))    b2 = fl(beta2), w2 = fl(1 - beta2)
                                               (torch mul_(beta2).addcmul_(g, g, 1 - beta2))
   5. p  = p * c_wd                            c_wd = fl(1 - lr * wd)   (decoupled decay)
-  6. p  = p - step_size * (m / (sqrt(v) / bc2s + eps))
+  6. p  = p + (-step_size * m) / (sqrt(v) / bc2s + eps)
                                               step_size = fl(lr / (1 - beta1^t)),
                                               bc2s = fl(sqrt(1 - beta2^t))
+                                              (torch addcdiv_(m, denom, -step_size), R11)
   7. A_m' = max |m|,  A_v' = max v            over the block
   8. q_m = clamp(rint(m * fl(127 / A_m')), -127, 127)   (int8)
      q_v = clamp(rint(v * fl(255 / A_v')),    0, 255)   (uint8); A' = 0 -> codes 0
@@ -30,7 +31,8 @@ addcmul_ do -- reading R26), in this order:
 
 Parity pins (tests/test_oracle_adam8.py): step-1 closed form from the zero
 state, the identity-codec variant equals torch.optim.AdamW (library routine:
-m and v bit for bit, p within 1e-6), fma32 against exact rational arithmetic,
+m and v bit for bit, p bit for bit wherever torch's CPU sqrt is correctly
+rounded), fma32 against exact rational arithmetic,
 codec round trip / error bound / zero block, shard-local = unsharded result
 (containment, P:419/P:433).
 """
@@ -118,8 +120,8 @@ def adam_block_update(p, g, mt, vt, sc):
     m = fma32(sc["w1"], (g - mt).astype(np.float32), mt)
     v = fma32((sc["w2"] * g).astype(np.float32), g, (sc["b2"] * vt).astype(np.float32))
     p = (p * sc["c_wd"]).astype(np.float32)
-    denom = (np.sqrt(v).astype(np.float32) / sc["bc2s"] + sc["eps"]).astype(np.float32)
-    p = (p - sc["step_size"] * (m / denom).astype(np.float32)).astype(np.float32)
+    denom = ((np.sqrt(v).astype(np.float32) / sc["bc2s"]).astype(np.float32) + sc["eps"]).astype(np.float32)
+    p = (p + ((-sc["step_size"] * m).astype(np.float32) / denom).astype(np.float32)).astype(np.float32)
     return p, m, v
 
 

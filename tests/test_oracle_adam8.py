@@ -34,28 +34,35 @@ def test_step1_closed_form():
 def test_identity_codec_matches_torch_adamw():
     """torch.optim.AdamW (single-tensor path) is the library routine the
     identity codec reduces to (R11).  Its moments are bit for bit the
-    oracle's steps 3-4 (lerp_ and addcmul_ round once, R26); the parameter
-    within 1e-6 (torch's CPU sqrt is not correctly rounded on every element,
-    the oracle's is)."""
+    oracle's steps 3-4 (lerp_ and addcmul_ round once, R26), and its
+    parameter is bit for bit the oracle's step 5-6 (mul_, then addcdiv_)
+    wherever torch's CPU sqrt returns the correctly rounded root -- it does
+    not on ~0.6 % of elements; there the two agree within 1e-6.  Each step
+    starts from torch's parameter, so a sqrt difference does not propagate."""
     cfg = A.AdamCfg(lr=3e-3, weight_decay=0.05)
     n = 1 << 16
     rng = np.random.default_rng(0)
-    p = rng.normal(0, 0.02, n).astype(np.float32)
     m = np.zeros(n, np.float32)
     v = np.zeros(n, np.float32)
-    tp = torch.nn.Parameter(torch.from_numpy(p.copy()))
+    tp = torch.nn.Parameter(torch.from_numpy(rng.normal(0, 0.02, n).astype(np.float32)))
     opt = torch.optim.AdamW([tp], lr=cfg.lr, betas=(cfg.beta1, cfg.beta2), eps=cfg.eps,
                             weight_decay=cfg.weight_decay, foreach=False, fused=False)
+    exact = 0
     for step in range(1, 6):
         g = rng.normal(0, 1e-3, n).astype(np.float32)
-        p, m, v = A.step_adam_fp32_states(p, g, m, v, cfg, step)
+        p_in = tp.detach().numpy().copy()
+        p, m, v = A.step_adam_fp32_states(p_in, g, m, v, cfg, step)
         tp.grad = torch.from_numpy(g.copy())
         opt.step()
         ref = tp.detach().numpy()
-        assert np.max(np.abs(p - ref) / (np.abs(ref) + cfg.lr)) < 1e-6
         st = opt.state[tp]
         assert np.array_equal(m, st["exp_avg"].numpy())
         assert np.array_equal(v, st["exp_avg_sq"].numpy())
+        ieee = np.sqrt(v) == torch.from_numpy(v).sqrt().numpy()
+        assert np.array_equal(p[ieee], ref[ieee])
+        assert np.max(np.abs(p - ref) / (np.abs(ref) + cfg.lr)) < 1e-6
+        exact += int(ieee.sum())
+    assert exact > 0.95 * 5 * n
 
 
 def _fma_exact(a, b, c):
