@@ -1,7 +1,7 @@
 """Static checks of the oracle / product separation (task rule ③): the oracle
 and the CUDA path share no code and neither imports the other; `synth/` (the
-only shared module) imports neither; nothing on the product path reads
-/root/reference at run time."""
+only shared module) imports neither; the measurement scripts never run the
+oracle; nothing on the product path reads /root/reference at run time."""
 import ast
 import os
 
@@ -34,6 +34,7 @@ def _imports(path):
     ("oracle", {PKG}),
     (PKG, {"oracle"}),
     ("synth", {PKG, "oracle"}),
+    ("scripts", {"oracle"}),  # measurement scripts: only tests/, smoke() and bench.py's baseline run the oracle
 ])
 def test_no_cross_imports(sub, forbidden):
     files = list(_py_files(sub))
