@@ -82,7 +82,8 @@ def main():
             src = OD.place_logical(o, logical_grads(5, r, E).numpy(), fill=np.nan)
             bufs.append(OD.grouped_cast_scale(o, OD.to_bf16_rne(src) if eb == 2 else src,
                                               eb == 2))
-        y_ref = OD.reduce_scatter(o, bufs)[rank]
+        y_all = OD.reduce_scatter(o, bufs)  # the oracle's reduced shard of every rank
+        y_ref = y_all[rank]
         y = f32(grad_f32[rank * S:(rank + 1) * S])
         if world & (world - 1) == 0:
             # m a power of two: x * fl(1/m) is exact on the dyadic inputs, so
@@ -134,7 +135,6 @@ def main():
         fused_in = [t.clone() for t in (master, mq, vq, ma, va)]
         gather_in = [t.clone() for t in (master, mq, vq, ma, va)]
         torch.cuda.synchronize()
-        g_red = f32(grad_f32[rank * S:(rank + 1) * S]).copy()  # the gradient Adam consumes
         R.step_8bit_adam(u, master, mq, vq, ma, va, R.AdamConfig(), 1)
         if eb == 2:
             # a6 + a7 + a8 in one kernel over NVLink: bit-identical to RS -> Adam
@@ -149,15 +149,16 @@ def main():
             p2p.close()
         R.all_gather(u)
         torch.cuda.synchronize()
-        # the oracle's Adam runs on the GPU's reduced gradients (every rank's,
-        # gathered): the ReduceScatter numerics are checked above on their own
-        g_all = [torch.zeros(S, dtype=torch.float32) for _ in range(world)]
-        dist.all_gather(g_all, torch.from_numpy(g_red))
+        # the oracle's Adam runs on the oracle's reduced gradients (no oracle
+        # input comes from the GPU).  They equal the GPU's bit for bit except
+        # for the fp32 toy unit at m = 3, where NCCL's summation order differs
+        # (within the bound checked above): a few-ulp gradient difference moves
+        # codes only at rounding ties and params far below the tolerance.
         ref_full = []
         for r in range(world):
             blocks = OP.rank_blocks(o, r, q)
             p0 = OD.shard(o, OD.place_logical(o, p_log.numpy()), r)
-            st = OA.step_8bit_adam(p0, g_all[r].numpy(), np.zeros(S, np.int8),
+            st = OA.step_8bit_adam(p0, y_all[r], np.zeros(S, np.int8),
                                    np.zeros(S, np.uint8), np.zeros(len(blocks), np.float32),
                                    np.zeros(len(blocks), np.float32), blocks, OA.AdamCfg(), 1,
                                    out_bf16=(eb == 2))

@@ -3,8 +3,9 @@ the launch configuration bench.py times: bench.setup builds the DBuffer,
 bench.step runs ONE step (default path), and sampled quantization blocks of
 every unit are checked against the oracle, block by block:
 
-  oracle input  = the block's pre-step master / codes / absmax (read before the
-                  step) and every rank's bf16 gradient regenerated from synth
+  oracle input  = the block's pre-step master / codes / absmax and every
+                  rank's bf16 gradient, regenerated from synth (the values
+                  bench.setup placed; nothing is read back from the device)
   oracle        = grouped_cast_scale -> reduce_scatter (rank order) ->
                   step_8bit_adam on the block
   check         = codes +-1, params 1e-5 (|p|+lr), absmax 1e-6, bf16 shard
@@ -62,11 +63,13 @@ def main():
             pos = rank * lay.S + off
             t = max(i for i in range(len(starts)) if starts[i] <= pos)
             logical = int(flat0[t] + pos - starts[t])
-            pre = (v["master"][off:off + n].cpu().numpy().copy(),
-                   v["mq"][off:off + n].cpu().numpy().copy(),
-                   v["vq"][off:off + n].cpu().numpy().copy(),
-                   v["ma"][b:b + 1].cpu().numpy().copy(),
-                   v["va"][b:b + 1].cpu().numpy().copy())
+            # the oracle's inputs regenerated from synth (what bench.setup placed
+            # in the arenas), never read back from the device
+            pre = (H.params_np(ui, logical, n),
+                   H.codes_np(ui, H.STREAM_MCODE, rank * lay.S + off, n, True),
+                   H.codes_np(ui, H.STREAM_VCODE, rank * lay.S + off, n, False),
+                   H.absmax_np(ui, H.STREAM_ABSM, rank * 10 ** 7 + b, 1, 14),
+                   H.absmax_np(ui, H.STREAM_ABSV, rank * 10 ** 7 + b, 1, 22))
             picks.append((ui, b, off, n, logical, pre))
     cfg = R.AdamConfig()
     st = torch.cuda.Stream()
