@@ -522,3 +522,31 @@ def test_fsdp_group_size_selection():
     assert table[1024] > 3 * table[512]
     with pytest.raises(ValueError):
         fs.select_group_size(w, 6, 7)
+
+
+def test_last_error_is_thread_local():
+    """Header convention: the error message lives in thread-local storage
+    until the next rsdb_* call on the same thread."""
+    import threading
+    lib = _capi.lib
+    one, zero = (C.c_int64 * 1)(4), (C.c_int64 * 1)(0)
+    h = C.c_void_p()
+    assert lib.rsdb_plan(1, one, zero, 2, 4, 16, C.byref(h)) == _capi.RSDB_EINVAL
+    main_msg = lib.rsdb_last_error()
+    assert main_msg
+    seen = {}
+
+    def other():
+        seen["before"] = lib.rsdb_last_error()
+        seen["st"] = lib.rsdb_plan(1, one, one, 0, 4, 16, C.byref(C.c_void_p()))
+        seen["after"] = lib.rsdb_last_error()
+
+    t = threading.Thread(target=other)
+    t.start()
+    t.join()
+    assert seen["before"] in (b"", None)  # a fresh thread has no error
+    assert seen["st"] == _capi.RSDB_EINVAL and seen["after"] and seen["after"] != main_msg
+    assert lib.rsdb_last_error() == main_msg  # untouched by the other thread
+    assert lib.rsdb_plan(1, one, one, 2, 4, 16, C.byref(h)) == _capi.RSDB_OK
+    assert lib.rsdb_last_error() in (b"", None)  # success clears it
+    lib.rsdb_layout_free(h)
