@@ -550,3 +550,33 @@ def test_last_error_is_thread_local():
     assert lib.rsdb_plan(1, one, one, 2, 4, 16, C.byref(h)) == _capi.RSDB_OK
     assert lib.rsdb_last_error() in (b"", None)  # success clears it
     lib.rsdb_layout_free(h)
+
+
+def test_planner_is_thread_safe_and_deterministic():
+    """Header: planning is pure host, deterministic and thread-safe -- eight
+    threads planning concurrently (ctypes drops the GIL) reproduce the serial
+    layouts exactly."""
+    import threading
+    u = W.dsv3_moe_unit()
+    es = [t.numel for t in u.tensors]
+    gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+    ms = [2, 3, 4, 5, 6, 7, 8, 16]
+    serial = {m: (R.plan(es, gs, m).S, R.plan(es, gs, m).starts) for m in ms}
+    out, errs = {}, []
+
+    def work(m):
+        try:
+            for _ in range(20):
+                lay = R.plan(es, gs, m)
+                out.setdefault(m, set()).add((lay.S, tuple(lay.starts)))
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(m,)) for m in ms]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for m in ms:
+        assert out[m] == {(serial[m][0], tuple(serial[m][1]))}
