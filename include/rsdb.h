@@ -23,7 +23,8 @@
  *    library.  DEVICE MEMORY FOR DATA IS OWNED BY THE CALLER (e.g. torch
  *    tensors' data_ptr()); the library never frees it.  The library allocates
  *    only its own small metadata tables (block / padding tables, < 0.02 B per
- *    element) at unit / dbuffer creation and frees them in *_free.
+ *    element) at unit / dbuffer creation and frees them in *_free; every
+ *    *_free accepts NULL (no-op).
  *  - Device calls take a cudaStream_t (passed as void*; NULL = legacy default
  *    stream), are stream-ordered and asynchronous, and return after enqueue.
  *    CUDA launch errors and synchronous NCCL errors come back as status;

@@ -580,3 +580,18 @@ def test_planner_is_thread_safe_and_deterministic():
     assert not errs
     for m in ms:
         assert out[m] == {(serial[m][0], tuple(serial[m][1]))}
+
+
+def test_free_functions_accept_null():
+    """Header convention: every *_free is a no-op on NULL (run in a child
+    process so a crash cannot take the test session down)."""
+    import subprocess
+    import sys
+    frees = [s for s in _header_symbols() if s.endswith("_free")]
+    assert len(frees) >= 9
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2602_22437_b200 import _capi as c\n"
+            "for f in %r: getattr(c.lib, f)(None)\n"
+            "print('ok')\n") % (ROOT, frees)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
