@@ -595,3 +595,22 @@ def test_free_functions_accept_null():
             "print('ok')\n") % (ROOT, frees)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
+
+
+def test_planner_parity_large_random_sweep():
+    """C++ planner == oracle (S and every start) on 120,000 more random
+    instances in two families: tiny (n <= 7, e <= 64, g <= 9, m <= 9) and
+    medium (n <= 30, e <= 5000, g <= 600 or whole-tensor, m <= 64), all three
+    element sizes (g_coll 4 / 8 / 16)."""
+    for seed, (count, nmax, emax, gmax, mmax) in enumerate([(100000, 7, 64, 9, 9),
+                                                            (20000, 30, 5000, 600, 64)]):
+        rng = random.Random(1000 + seed)
+        for _ in range(count):
+            n = rng.randint(0, nmax)
+            es = [rng.randint(1, emax) for _ in range(n)]
+            gs = [min(e, rng.randint(1, gmax)) if rng.random() < 0.7 else e for e in es]
+            m = rng.randint(1, mmax)
+            eb = rng.choice([1, 2, 4])
+            o = P.plan(es, gs, m, P.gcoll_elems(eb))
+            c = R.plan(es, gs, m, elem_bytes=eb)
+            assert (c.S, c.starts) == (o.S, o.starts), (es, gs, m, eb)
