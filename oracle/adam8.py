@@ -23,10 +23,18 @@ addcmul_ do -- reading R26), in this order:
                                               step_size = fl(lr / (1 - beta1^t)),
                                               bc2s = fl(sqrt(1 - beta2^t))
                                               (torch addcdiv_(m, denom, -step_size), R11)
-  7. A_m' = max |m|,  A_v' = max v            over the block
-  8. q_m = clamp(rint(m * fl(127 / A_m')), -127, 127)   (int8)
-     q_v = clamp(rint(v * fl(255 / A_v')),    0, 255)   (uint8); A' = 0 -> codes 0
-     (the code is decided in the kernel's arithmetic, reading R26)
+  7. A_m' = max |m|,  A_v' = max v            over the block (NaN-propagating
+                                              max: one NaN makes A' NaN, reading R27)
+  8. q_m = clamp(rint(fl(m / fl(A_m' / 127))), -127, 127)   (int8)
+     q_v = clamp(rint(fl(v / fl(A_v' / 255))),    0, 255)   (uint8)
+     SURVEY.md §8(c) O4 step 8 as written there (before any kernel existed):
+     one IEEE fp32 division by the dequantization step d = fl(A'/L), then
+     round half to even.  Total for every A' (reading R27): a NaN quotient
+     (0/0 when A' = 0 or d underflows to 0; anything / NaN) gives code 0,
+     +-inf (x/0) saturates -- so A' = 0 gives all-zero codes, and a
+     block whose A' is NaN or +inf (a non-finite gradient) gets all-zero
+     codes and keeps A' (its next dequantization is then NaN: the block's
+     state is visibly poisoned instead of silently wrong).
   9. param shard for the next AllGather = bf16_RNE(p)  (or p itself for fp32 units)
 
 Parity pins (tests/test_oracle_adam8.py): step-1 closed form from the zero
@@ -94,23 +102,23 @@ def fma32(a, b, c) -> np.ndarray:
 
 def dequantize(codes: np.ndarray, absmax: f32, signed: bool) -> np.ndarray:
     levels = f32(127.0) if signed else f32(255.0)
-    scale = f32(f32(absmax) / levels)
-    return (codes.astype(np.float32) * scale).astype(np.float32)
+    with np.errstate(invalid="ignore", under="ignore"):  # 0 * inf = NaN (R27)
+        scale = f32(f32(absmax) / levels)
+        return (codes.astype(np.float32) * scale).astype(np.float32)
 
 
 def quantize(x: np.ndarray, signed: bool) -> Tuple[np.ndarray, f32]:
-    """Linear absmax code of one block (R9); returns (codes, absmax)."""
+    """Linear absmax code of one block (R9; step 8 above, R27); returns
+    (codes, absmax)."""
     x = np.asarray(x, dtype=np.float32)
-    a = f32(np.max(np.abs(x))) if x.size else f32(0)
-    if a == 0:
-        return np.zeros(x.shape, np.int8 if signed else np.uint8), f32(0)
-    if signed:
-        inv = f32(f32(127.0) / a)
-        q = np.clip(np.rint((x * inv).astype(np.float32)), -127, 127).astype(np.int8)
-    else:
-        inv = f32(f32(255.0) / a)
-        q = np.clip(np.rint((x * inv).astype(np.float32)), 0, 255).astype(np.uint8)
-    return q, a
+    a = f32(np.max(np.abs(x))) if x.size else f32(0)  # numpy's max propagates NaN
+    levels = f32(127.0) if signed else f32(255.0)
+    lo, hi = (-127, 127) if signed else (0, 255)
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore", under="ignore"):
+        d = f32(a / levels)
+        y = (x / d).astype(np.float32)  # IEEE fp32 division (correctly rounded)
+    q = np.where(np.isnan(y), f32(0), np.clip(np.rint(y), lo, hi))
+    return q.astype(np.int8 if signed else np.uint8), a
 
 
 def adam_block_update(p, g, mt, vt, sc):
@@ -142,6 +150,11 @@ def step_8bit_adam(master: np.ndarray, grad: np.ndarray, m_q: np.ndarray, v_q: n
     if codec not in ("linear", "dynamic"):
         raise ValueError(codec)
     sc = host_scalars(cfg, step)
+    with np.errstate(all="ignore"):  # non-finite gradients propagate as IEEE says (R27)
+        return _step_8bit_adam(master, grad, m_q, v_q, m_abs, v_abs, blocks, sc, out_bf16, codec)
+
+
+def _step_8bit_adam(master, grad, m_q, v_q, m_abs, v_abs, blocks, sc, out_bf16, codec):
     master = np.array(master, dtype=np.float32, copy=True)
     m_q, v_q = np.array(m_q, copy=True), np.array(v_q, copy=True)
     m_abs = np.array(m_abs, dtype=np.float32, copy=True)

@@ -20,7 +20,10 @@ tree construction with 7 exponent levels:
   quantize:   A = max|x| over the block; y = fl32(x / A); hi = first code with
               map[hi] >= y (clamped to [1, 255]), lo = hi - 1;
               code = hi if fl32(map[hi] - y) < fl32(y - map[lo]) else lo
-              (ties -> the lower code); A = 0 -> the code of 0.
+              (ties -> the lower code); A = 0 -> the code of 0.  A is the
+              NaN-propagating max; a block whose A is NaN or +inf (a
+              non-finite gradient) keeps A and gets the code of 0 everywhere
+              (reading R27, as the linear codec).
   dequantize: x = fl32(map[code] * A).
 Both sides decide the code in fp32 with the same operations, so codes are
 comparable bit for bit.
@@ -82,6 +85,7 @@ def dyn_quantize(x: np.ndarray, signed: bool) -> Tuple[np.ndarray, f32]:
     """One block -> (codes uint8, absmax)."""
     x = np.asarray(x, f32)
     a = f32(np.max(np.abs(x))) if x.size else f32(0)
-    if a == 0:
-        return np.full(x.shape, zero_code(signed), np.uint8), f32(0)
-    return dyn_code((x / a).astype(f32), signed), a
+    if a == 0 or not np.isfinite(a):  # R27: a NaN / infinite block keeps A, codes of 0
+        return np.full(x.shape, zero_code(signed), np.uint8), a
+    with np.errstate(under="ignore"):
+        return dyn_code((x / a).astype(f32), signed), a

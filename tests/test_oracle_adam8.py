@@ -67,8 +67,15 @@ def test_identity_codec_matches_torch_adamw():
 
 def _fma_exact(a, b, c):
     from fractions import Fraction
-    x = Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c))
-    # round the rational x to fp32, nearest-even, by bracketing with nextafter
+    return _rn32(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def _rn32(x):
+    """The rational x rounded to fp32, nearest-even (subnormals included),
+    by bracketing with nextafter."""
+    from fractions import Fraction
+    if abs(x) >= Fraction(2) ** 128 - Fraction(2) ** 103:  # past the overflow midpoint
+        return np.float32(np.inf) if x > 0 else np.float32(-np.inf)
     r = np.float32(float(x))  # float(x) is RN64(x); fix the possible double rounding below
     lo = r if Fraction(float(r)) <= x else np.nextafter(r, np.float32(-np.inf))
     hi = np.nextafter(lo, np.float32(np.inf))
@@ -120,8 +127,8 @@ def test_codec_properties():
     q, a = A.quantize(x, signed=False)
     assert np.array_equal(A.dequantize(q, a, False), x)
     # |x - deq(q(x))| <= A/254 (signed), A/510 (unsigned), up to fp32 rounding:
-    # the code is decided on fl(x * fl(L/A)) (R26), within L * 2^-23 code steps of
-    # the exact x * L / A, so at a tie the error exceeds half a step by at most
+    # the code is decided on fl(x / fl(A/L)) (O4 step 8), within L * 2^-23 code steps
+    # of the exact x * L / A, so at a tie the error exceeds half a step by at most
     # that: the bound is (A / 2L) (1 + 2 L 2^-23) plus the dequantization rounding
     rng = np.random.default_rng(1)
     for _ in range(50):
@@ -132,6 +139,115 @@ def test_codec_properties():
         q, a = A.quantize(np.abs(x), False)
         err = np.abs(np.abs(x).astype(np.float64) - A.dequantize(q, a, False))
         assert np.all(err <= a / 510 * (1 + 2 * 255 * 2.0 ** -23 + 1e-6))
+
+
+def _code_exact(x, a, signed):
+    """O4 step 8 in exact rational arithmetic: d = RN32(A / L), y = RN32(x / d),
+    round half to even, clamp; a NaN quotient (0/0, x/NaN) -> 0 (R27)."""
+    from fractions import Fraction
+    L, lo, hi = (127, -127, 127) if signed else (255, 0, 255)
+    if not np.isfinite(a):  # A = NaN: every quotient NaN; A = inf: x/inf = 0, inf/inf = NaN
+        return 0
+    d = _rn32(Fraction(float(a)) / L)
+    if d == 0:
+        return 0 if x == 0 else (hi if x > 0 else lo)
+    y = _rn32(Fraction(float(x)) / Fraction(float(d)))
+    if not np.isfinite(y):
+        return hi if y > 0 else lo
+    fy = Fraction(float(y))
+    n = int(np.floor(float(y)))  # exact: |y| < 2^24 here or the clamp decides
+    rem = fy - n
+    k = n + 1 if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2) else n
+    return max(lo, min(hi, k))
+
+
+def test_code_is_the_exact_division_rounded_twice():
+    """O4 step 8: the code is rint(RN32(x / RN32(A/L))),
+    checked against exact rational arithmetic on inputs within a few ulps of
+    every rounding tie k + 1/2 and over the whole exponent range of A,
+    subnormal steps d included.  The reciprocal-multiply form
+    rint(RN32(x * RN32(L/A))) disagrees on some of these inputs (asserted),
+    so the pin tells the two apart."""
+    rng = np.random.default_rng(7)
+    n_diff_recip = 0
+    cases = 0
+    for signed in (True, False):
+        L = 127 if signed else 255
+        for e in list(range(-149, -120, 3)) + list(range(-120, 120, 7)):
+            a = np.float32(np.ldexp(1.0 + rng.random(), e))
+            if not np.isfinite(a) or a == 0:
+                continue
+            d = np.float32(a / np.float32(L))
+            ks = rng.integers(0 if not signed else -L, L, 24)
+            xs = []
+            for k in ks:
+                t = np.float32((k + 0.5) * float(d))
+                for u in range(-3, 4):
+                    xs.append(t)
+                    t = np.nextafter(t, np.float32(np.inf))
+            x = np.array([v for v in xs if abs(v) <= a], np.float32)
+            x = np.concatenate([x, np.float32([a, -a if signed else 0, 0])])
+            if not signed:
+                x = np.abs(x)
+            blk = np.concatenate([x, np.float32([a])])  # pin the block's absmax to a
+            q, aa = A.quantize(blk, signed)
+            assert aa == a
+            exp = [_code_exact(v, a, signed) for v in blk]
+            assert q.astype(int).tolist() == exp, (signed, e)
+            with np.errstate(all="ignore"):
+                rq = np.clip(np.rint((blk * np.float32(np.float32(L) / a)).astype(np.float32)),
+                             -L if signed else 0, L)
+            n_diff_recip += int(np.sum(np.isfinite(rq) & (rq != np.array(exp))))
+            cases += blk.size
+    assert cases > 5000 and n_diff_recip > 0
+
+
+def test_codec_total_at_tiny_and_non_finite_absmax():
+    """R27: the codec is defined for every block.  Tiny absmax (d = A/L
+    subnormal, or underflowing to 0 -- the regime a block with a long run of
+    zero gradients reaches, m decaying x0.9 per step) gives in-range codes
+    equal to the exact-arithmetic decision; A = 0 gives zeros; a NaN
+    or infinite element gives all-zero codes and keeps A (NaN / +inf)."""
+    for a in [np.float32(v) for v in (1e-45, 3e-45, 1e-44, 1e-43, 7e-42, 1e-40, 1.2e-38,
+                                      3.7e-37, 7.5e-37, 1e-30, 3e38)]:
+        x = np.float32([a, -a, a / 2, a / 3, -a / 7, 0, np.float32(-0.0)])
+        for signed in (True, False):
+            xx = x if signed else np.abs(x)
+            q, aa = A.quantize(xx, signed)
+            assert aa == a
+            assert q.astype(int).tolist() == [_code_exact(v, a, signed) for v in xx]
+            deq = A.dequantize(q, aa, signed)
+            assert np.all(np.isfinite(deq))
+    for bad, exp_a in ((np.nan, np.nan), (np.inf, np.inf), (-np.inf, np.inf)):
+        x = np.float32([1.0, bad, -2.0, 0.0])
+        for signed in (True, False):
+            q, aa = A.quantize(x if signed else np.abs(x), signed)
+            assert not q.any()
+            assert (np.isnan(aa) and np.isnan(exp_a)) or aa == exp_a
+            assert np.all(np.isnan(A.dequantize(q, aa, signed)))  # the block is poisoned
+
+
+def test_zero_gradient_run_stays_in_range():
+    """A block whose gradient stays 0 decays m by beta1 per step (and v by
+    beta2) until A_m underflows; 900 oracle steps keep every code in range,
+    A_m non-increasing, and m's dequantized value within one step of 0.9x
+    the previous one -- no overflow, no NaN."""
+    rng = np.random.default_rng(3)
+    n = 2048
+    p = rng.normal(0, 0.02, n).astype(np.float32)
+    g0 = rng.normal(0, 1e-3, n).astype(np.float32)
+    mq, vq, ma, va = _zero_state(n, 1)
+    cfg = A.AdamCfg()
+    st = A.step_8bit_adam(p, g0, mq, vq, ma, va, [(0, n)], cfg, 1)
+    zero = np.zeros(n, np.float32)
+    prev = st[3][0]
+    for t in range(2, 902):
+        st = A.step_8bit_adam(st[0], zero, st[1], st[2], st[3], st[4], [(0, n)], cfg, t)
+        assert np.isfinite(st[3][0]) and np.isfinite(st[4][0])
+        assert st[3][0] <= prev
+        prev = st[3][0]
+        assert np.all(np.isfinite(st[0]))
+    assert st[3][0] < np.float32(3.7e-37)  # reached the regime where fl(127/A) overflows
 
 
 @pytest.mark.parametrize("m", [2, 3, 4, 8])
