@@ -99,14 +99,21 @@ def e4m3_encode(x: np.ndarray) -> np.ndarray:
 
 
 def quantize_tile(x: np.ndarray) -> Tuple[np.ndarray, np.float32]:
-    """One tile (any shape) of fp32 weights -> (codes, scale) per R19."""
+    """One tile (any shape) of fp32 weights -> (codes, scale) per R19, made
+    total by R28: A is the NaN-propagating max; inv = min(fl(448 / A),
+    FLT_MAX), so a tile with A < 448 / FLT_MAX (fl(448/A) = inf) still maps
+    every x to a finite fl(x * inv) (|x| <= A); a tile whose A is NaN or +inf
+    gets the NaN code 0x7F everywhere and scale A (poisoned, visible)."""
     x = np.asarray(x, dtype=f32)
-    A = f32(np.max(np.abs(x))) if x.size else f32(0)
+    A = f32(np.max(np.abs(x))) if x.size else f32(0)  # numpy's max propagates NaN
     if A == 0:
         return np.zeros(x.shape, np.uint8), f32(0)
-    inv = f32(f32(E4M3_MAX) / A)
-    codes = e4m3_encode((x * inv).astype(f32))
-    return codes, f32(A / f32(E4M3_MAX))
+    if not np.isfinite(A):
+        return np.full(x.shape, E4M3_NAN, np.uint8), A
+    with np.errstate(over="ignore", under="ignore"):
+        inv = f32(min(f32(f32(E4M3_MAX) / A), np.finfo(f32).max))
+        codes = e4m3_encode((x * inv).astype(f32))
+        return codes, f32(A / f32(E4M3_MAX))
 
 
 def tile_specs(row_len: Sequence[int], tile: int = 128) -> List[Tuple]:

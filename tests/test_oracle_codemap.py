@@ -109,3 +109,25 @@ def test_dynamic_codec_in_adam_step():
     for (off, ln), k in zip(blocks, range(2)):
         q, a = CM.dyn_quantize(m1[off:off + ln], True)
         assert np.array_equal(dyn[1][off:off + ln], q) and dyn[3][k] == a
+
+
+def test_dynamic_codec_total_at_tiny_and_non_finite_absmax():
+    """R27 for the dynamic map: a subnormal absmax still gives the nearest
+    code of the exactly-rounded y = fl(x / A) (brute force over the map);
+    A NaN / +inf gives the code of 0 everywhere and keeps A."""
+    for signed in (True, False):
+        mp = CM.dynamic_map(signed).astype(np.float64)
+        for a in (np.float32(1e-45), np.float32(1e-41), np.float32(3e-39), np.float32(1e-37)):
+            x = np.float32([a, a / 3, a / 7, 0.0, a / 1000])
+            if signed:
+                x = np.concatenate([x, -x])
+            q, aa = CM.dyn_quantize(x, signed)
+            assert aa == a
+            y = (x / a).astype(np.float32).astype(np.float64)
+            for yi, qi in zip(y, q):
+                d = np.abs(mp - yi)
+                assert d[qi] == d.min()
+        for bad in (np.nan, np.inf):
+            q, aa = CM.dyn_quantize(np.float32([0.5, bad, 0.0]), signed)
+            assert np.all(q == CM.zero_code(signed))
+            assert (np.isnan(aa) and np.isnan(bad)) or aa == bad

@@ -134,3 +134,23 @@ def test_sharded_equals_unsharded(m):
     bases = [F.slot_base(lay, r, specs) for r in range(m + 1)]
     assert bases[0] == 0 and bases[m] == len(exp_scales)
     assert all(bases[r] <= bases[r + 1] for r in range(m))
+
+
+def test_quantize_tile_total_at_tiny_and_non_finite_absmax():
+    """R28: for A < 448 / FLT_MAX, fl(448 / A) overflows; inv is clamped to
+    FLT_MAX so every code is still the E4M3 code of the finite fl(x * inv)
+    (no NaN code for zeros, no saturation of non-maximal values); the
+    codes equal torch's float8_e4m3fn cast of x * FLT_MAX (library routine).
+    A NaN / infinite weight poisons the tile (NaN codes, scale = A)."""
+    fmax = np.finfo(np.float32).max
+    for a in (np.float32(1e-38), np.float32(1e-40), np.float32(1.2e-36)):
+        x = np.float32([a, -a, a / 3, 0.0, -a / 5]).reshape(1, 5)
+        q, sc = F.quantize_tile(x)
+        assert sc == np.float32(a / np.float32(448))
+        y = (x * np.float32(fmax)).astype(np.float32)
+        ref = torch.from_numpy(y).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+        assert np.array_equal(q, ref)
+        assert not np.any((q & 0x7F) == 0x7F)
+    for bad in (np.nan, np.inf, -np.inf):
+        q, sc = F.quantize_tile(np.float32([[1.0, bad, 0.0]]))
+        assert np.all(q == 0x7F) and not np.isfinite(sc)
