@@ -580,13 +580,8 @@ def run_ours(args):
     fused_gbs = fused_hbm / (rs_ms * 1e-3) / 1e9 if fuse else None
     # dominant kernel of the step (largest share of device time)
     names = ({"ag": "nccl_all_gather", "rs": "nccl_reduce_scatter"} if p2p is None else
-             {"ag": "ag_p2p (copy engines)" if os.environ.get("RSDB_P2P_AG", "ce") == "ce"
-              else "ag_p2p_kernel",
-              "rs": ("rs_adam_ws_kernel" if os.environ.get("RSDB_RSA_KERNEL") == "ws"
-                     else "rs_adam_tma_kernel") if fuse else "rs_p2p_kernel"})
-    # the default 8-bit Adam kernel is the TMA-pipelined one (RSDB_ADAM_KERNEL overrides)
-    adam_name = ("adam8_tma_kernel" if os.environ.get("RSDB_ADAM_KERNEL", "tma3").startswith("tma")
-                 else "adam8_kernel")
+             {"ag": "ag_p2p (copy engines)", "rs": "rs_adam_tma_kernel" if fuse else "rs_tma_kernel"})
+    adam_name = "adam8_tma_kernel"
     shares = {adam_name: tot["adam"], "cast_scale_kernel": tot["cast"],
               names["rs"]: tot["rs"], names["ag"]: tot["ag"]}
     dom = max(shares, key=shares.get)

@@ -177,6 +177,17 @@ rsdb_status rsdb_comm_init(const uint8_t id[128], int32_t world, int32_t rank,
 int32_t rsdb_comm_rank(const rsdb_comm*);
 int32_t rsdb_comm_world(const rsdb_comm*);
 void rsdb_comm_free(rsdb_comm*);
+/* Single-device multi-rank mode (testing / debugging the p2p path on one
+ * GPU): a communicator for logical rank `rank` of `world` <= 8 ranks that all
+ * live in THIS process on the CURRENT device -- one comm per logical rank.
+ * It has no NCCL communicator: the NCCL entry points (rsdb_all_gather,
+ * rsdb_reduce_scatter, rsdb_unit_reduce_scatter_f32) return EINVAL on its
+ * units; every p2p / fused / FP8 / Muon / ring call works, through a p2p
+ * object from rsdb_p2p_create_local.  The caller issues each logical rank's
+ * calls on its own CUDA stream (the ranks' kernels must run concurrently;
+ * the library splits the device's SMs among them).  EINVAL on bad world /
+ * rank, ECUDA without a device. */
+rsdb_status rsdb_comm_create_local(int32_t world, int32_t rank, rsdb_comm** out);
 
 /* ======================================================================== */
 /* Unit: one planned FSDP unit bound to caller-owned device buffers.         */
@@ -283,11 +294,28 @@ rsdb_status rsdb_ipc_handle(const void* dev_ptr, uint8_t out[RSDB_IPC_BYTES]);
  * ECUDA if a handle cannot be opened (no P2P path). */
 rsdb_status rsdb_p2p_create(rsdb_comm* comm, int32_t n_bufs, void* const* local_bufs,
                             const int64_t* sizes, const uint8_t* all_handles, rsdb_p2p** out);
+/* Local mode (comm from rsdb_comm_create_local): all_bufs holds world *
+ * n_bufs device pointers on the current device, rank-major (all_bufs[r *
+ * n_bufs + i] = logical rank r's buffer i; i = 0 the zero-filled signal
+ * buffers, one per rank); sizes[i] as above, equal for every rank.  Each
+ * logical rank creates its own p2p object over the same table.  EMISMATCH if
+ * comm is not local. */
+rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* all_bufs,
+                                  const int64_t* sizes, rsdb_p2p** out);
+/* Barrier spin limit of the p2p kernels (default 60 s): a kernel whose peer
+ * never arrives stops waiting after `seconds`, sets an error flag in its
+ * rank's signal buffer and returns (its results are then invalid) instead of
+ * hanging the device.  EINVAL if seconds <= 0. */
+rsdb_status rsdb_p2p_set_timeout(rsdb_p2p*, double seconds);
+/* Synchronises the device, reads and clears this rank's error flag into
+ * *flags (0 = every barrier completed); ECUDA if a barrier timed out. */
+rsdb_status rsdb_p2p_check(rsdb_p2p*, int64_t* flags);
 void rsdb_p2p_free(rsdb_p2p*);
 /* The unit's grad_full (bf16 units) / param_full must lie inside one of the
  * registered buffers at the same offset on every rank (true for DBuffer
  * arenas: offsets are rank-independent for PARAM_FULL / GRAD_FULL).
- * EMISMATCH otherwise. */
+ * EMISMATCH otherwise.  The p2p object may be NULL at world 1 (AllGather is
+ * then the identity, ReduceScatter the group op alone). */
 rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
 rsdb_status rsdb_all_gather_p2p(rsdb_unit*, rsdb_p2p*, void* stream);
 /* a6 + a7 + a8 in ONE kernel: the ReduceScatter of the unit's bf16 gradients

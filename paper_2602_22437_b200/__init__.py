@@ -229,6 +229,16 @@ class Comm:
         check(lib.rsdb_comm_init(uid, world, rank, device, C.byref(h)))
         self._h = h
 
+    @classmethod
+    def local(cls, world: int, rank: int) -> "Comm":
+        """Logical rank `rank` of `world` ranks living in this process on the
+        current device (rsdb_comm_create_local; no NCCL)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        check(lib.rsdb_comm_create_local(world, rank, C.byref(h)))
+        self._h = h
+        return self
+
     @staticmethod
     def unique_id() -> bytes:
         buf = C.create_string_buffer(128)
@@ -407,6 +417,41 @@ class P2P:
         self._h = h
         self.comm = comm
 
+    @classmethod
+    def local_group(cls, comms: Sequence[Comm], bufs_per_rank: Sequence[Sequence]) -> List["P2P"]:
+        """Local mode: one P2P per logical rank (comms from Comm.local) over
+        every rank's buffers, all on the current device
+        (rsdb_p2p_create_local).  bufs_per_rank[r] = rank r's tensors."""
+        import torch
+        world = len(comms)
+        tables = []
+        for bufs in bufs_per_rank:
+            sig = torch.zeros(_c.RSDB_P2P_SIGNAL_BYTES, dtype=torch.uint8, device=bufs[0].device)
+            tables.append([sig] + list(bufs))
+        n = len(tables[0])
+        ptrs = (C.c_void_p * (world * n))(*[t.data_ptr() for tb in tables for t in tb])
+        sizes = (C.c_int64 * n)(*[t.numel() * t.element_size() for t in tables[0]])
+        out = []
+        for r in range(world):
+            self = cls.__new__(cls)
+            h = C.c_void_p()
+            check(lib.rsdb_p2p_create_local(comms[r].handle, n, ptrs, sizes, C.byref(h)))
+            self._h = h
+            self.comm = comms[r]
+            self.signal = tables[r][0]
+            self.bufs = tables  # keeps every rank's tensors alive
+            out.append(self)
+        return out
+
+    def set_timeout(self, seconds: float) -> None:
+        check(lib.rsdb_p2p_set_timeout(self._h, float(seconds)))
+
+    def check(self) -> int:
+        """Synchronise; raise if a barrier of this rank timed out."""
+        f = C.c_int64(0)
+        check(lib.rsdb_p2p_check(self._h, C.byref(f)))
+        return f.value
+
     @property
     def handle(self):
         return self._h
@@ -423,9 +468,10 @@ class P2P:
             pass
 
 
-def reduce_scatter_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
+def reduce_scatter_p2p(unit: Unit, p2p: Optional[P2P], stream=None) -> None:
     """a6 + a7 fused in one kernel over NVLink peer memory (bf16 on the wire)."""
-    check(lib.rsdb_reduce_scatter_p2p(unit.handle, p2p.handle, _stream(stream)))
+    check(lib.rsdb_reduce_scatter_p2p(unit.handle, p2p.handle if p2p is not None else None,
+                                      _stream(stream)))
 
 
 def reduce_scatter_adam_p2p(unit: Unit, p2p: Optional[P2P], cfg: AdamConfig, step: int,
@@ -453,9 +499,9 @@ def reduce_scatter_adam_gather_p2p(unit: Unit, p2p: Optional[P2P], cfg: AdamConf
                                                   st, C.byref(cfg), step, _stream(stream)))
 
 
-def all_gather_p2p(unit: Unit, p2p: P2P, stream=None) -> None:
+def all_gather_p2p(unit: Unit, p2p: Optional[P2P], stream=None) -> None:
     """a4 as one kernel pulling every peer's shard over NVLink."""
-    check(lib.rsdb_all_gather_p2p(unit.handle, p2p.handle, _stream(stream)))
+    check(lib.rsdb_all_gather_p2p(unit.handle, p2p.handle if p2p is not None else None, _stream(stream)))
 
 
 # ---------------------------------------------------------------- DBuffer

@@ -10,9 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# RSDB_LIB: another build of the library (same-box A/B of two versions; tests and
-# the bench load the in-tree librsdb.so otherwise)
-LIB_PATH = os.environ.get("RSDB_LIB") or os.path.join(_HERE, "librsdb.so")
+LIB_PATH = os.path.join(_HERE, "librsdb.so")
 
 RSDB_OK, RSDB_EINVAL, RSDB_EMISMATCH, RSDB_ECUDA, RSDB_ENCCL, RSDB_EINTERNAL = range(6)
 RSDB_BF16, RSDB_F32 = 0, 1
@@ -91,6 +89,7 @@ _SIGS = {
     "rsdb_comm_rank": (i32, [vp]),
     "rsdb_comm_world": (i32, [vp]),
     "rsdb_comm_free": (None, [vp]),
+    "rsdb_comm_create_local": (i32, [i32, i32, C.POINTER(vp)]),
     "rsdb_unit_create": (i32, [vp, vp, i32, C.POINTER(UnitBufs), i64, C.POINTER(vp)]),
     "rsdb_unit_num_blocks": (i64, [vp]),
     "rsdb_unit_free": (None, [vp]),
@@ -102,6 +101,9 @@ _SIGS = {
     "rsdb_ipc_handle": (i32, [vp, C.c_char_p]),
     "rsdb_p2p_create": (i32, [vp, i32, C.POINTER(vp), P_i64, C.c_char_p, C.POINTER(vp)]),
     "rsdb_p2p_free": (None, [vp]),
+    "rsdb_p2p_create_local": (i32, [vp, i32, C.POINTER(vp), P_i64, C.POINTER(vp)]),
+    "rsdb_p2p_set_timeout": (i32, [vp, C.c_double]),
+    "rsdb_p2p_check": (i32, [vp, P_i64]),
     "rsdb_reduce_scatter_p2p": (i32, [vp, vp, vp]),
     "rsdb_all_gather_p2p": (i32, [vp, vp, vp]),
     "rsdb_reduce_scatter_adam_p2p": (i32, [vp, vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64,

@@ -135,11 +135,12 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
     const float Am = P.mabs[blk.slot], Av = P.vabs[blk.slot];
     float* rm = red_m[it & 1];
     float* rv = red_v[it & 1];
+    // R27: A = 0, NaN or +inf -> the code of 0 everywhere
     auto qm = [&](float m, float am) {
-      return am > 0.f ? dyn_code(mapm, T.lb[0], T.lb[1], __fdiv_rn(m, am)) : zero_m;
+      return am > 0.f && am <= FLT_MAX_F ? dyn_code(mapm, T.lb[0], T.lb[1], __fdiv_rn(m, am)) : zero_m;
     };
     auto qv = [&](float v, float av) {
-      return av > 0.f ? dyn_code(mapv, T.lb[2], T.lb[2], __fdiv_rn(v, av)) : zero_v;
+      return av > 0.f && av <= FLT_MAX_F ? dyn_code(mapv, T.lb[2], T.lb[2], __fdiv_rn(v, av)) : zero_v;
     };
     float am = 0.f, av = 0.f;
     const bool fast = blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
@@ -165,8 +166,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
           p[4 * k + j] = r.p;
           m[4 * k + j] = r.m;
           v[4 * k + j] = r.v;
-          am = fmaxf(am, fabsf(r.m));
-          av = fmaxf(av, r.v);
+          am = fmax_nan(am, fabsf(r.m));
+          av = fmax_nan(av, r.v);
         }
       }
       block_max2<G::WARPS>(am, av, rm, rv);
@@ -213,8 +214,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
           const int i = int(threadIdx.x) + e * DYN_NT;
           if (i < blk.len) {
             p[e] = elem(i, m[e], v[e]);
-            am = fmaxf(am, fabsf(m[e]));
-            av = fmaxf(av, v[e]);
+            am = fmax_nan(am, fabsf(m[e]));
+            av = fmax_nan(av, v[e]);
           }
         }
         block_max2<G::WARPS>(am, av, rm, rv);
@@ -227,8 +228,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
         for (int i = threadIdx.x; i < blk.len; i += DYN_NT) {
           float m, v;
           elem(i, m, v);
-          am = fmaxf(am, fabsf(m));
-          av = fmaxf(av, v);
+          am = fmax_nan(am, fabsf(m));
+          av = fmax_nan(av, v);
         }
         block_max2<G::WARPS>(am, av, rm, rv);
         for (int i = threadIdx.x; i < blk.len; i += DYN_NT) {

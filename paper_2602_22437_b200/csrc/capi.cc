@@ -213,6 +213,20 @@ void rsdb_comm_free(rsdb_comm* c) {
   delete c;
 }
 
+rsdb_status rsdb_comm_create_local(int32_t world, int32_t rank, rsdb_comm** out) {
+  if (!out || world < 1 || world > rsdb::P2P_MAX_RANKS || rank < 0 || rank >= world)
+    return fail(RSDB_EINVAL, "rsdb_comm_create_local: need 1 <= world <= %d and 0 <= rank < world",
+                rsdb::P2P_MAX_RANKS);
+  if (rsdb_status st = require_device()) return st;
+  auto c = std::make_unique<rsdb_comm>();
+  c->world = world;
+  c->rank = rank;
+  CUDA_TRY(cudaGetDevice(&c->device));
+  c->local = true;
+  *out = c.release();
+  return OK_CLEAR();
+}
+
 // ---------------------------------------------------------------------------
 // unit
 // ---------------------------------------------------------------------------
@@ -322,6 +336,7 @@ void rsdb_unit_free(rsdb_unit* u) { delete u; }
 rsdb_status rsdb_all_gather(rsdb_unit* u, void* stream) {
   if (!u) return fail(RSDB_EINVAL, "null unit");
   if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
+  if (!u->comm->nc) return fail(RSDB_EINVAL, "a local comm has no NCCL communicator (use the p2p calls)");
   if (u->L.S == 0) return OK_CLEAR();
   const ncclDataType_t dt = u->L.elem_bytes == 2 ? ncclBfloat16 : ncclFloat32;
   char* full = static_cast<char*>(u->bufs.param_full);
@@ -356,6 +371,7 @@ static rsdb_status rs_f32(rsdb_unit* u, void* stream) {
 rsdb_status rsdb_reduce_scatter(rsdb_unit* u, void* stream) {
   if (!u) return fail(RSDB_EINVAL, "null unit");
   if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
+  if (!u->comm->nc) return fail(RSDB_EINVAL, "a local comm has no NCCL communicator (use the p2p calls)");
   if (u->L.S == 0) return OK_CLEAR();
   if (rsdb_status st = cast_scale(u, stream)) return st;
   if (rsdb_status st = rs_f32(u, stream)) return st;
@@ -365,6 +381,7 @@ rsdb_status rsdb_reduce_scatter(rsdb_unit* u, void* stream) {
 rsdb_status rsdb_unit_reduce_scatter_f32(rsdb_unit* u, void* stream) {
   if (!u) return fail(RSDB_EINVAL, "null unit");
   if (!u->comm) return fail(RSDB_EINVAL, "unit has no communicator");
+  if (!u->comm->nc) return fail(RSDB_EINVAL, "a local comm has no NCCL communicator (use the p2p calls)");
   if (u->L.S == 0) return OK_CLEAR();
   if (rsdb_status st = rs_f32(u, stream)) return st;
   return OK_CLEAR();
@@ -525,6 +542,52 @@ void rsdb_p2p_free(rsdb_p2p* p) {
   delete p;
 }
 
+rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* all_bufs,
+                                  const int64_t* sizes, rsdb_p2p** out) {
+  if (!comm || n_bufs < 1 || !all_bufs || !sizes || !out)
+    return fail(RSDB_EINVAL, "rsdb_p2p_create_local: null argument or n_bufs < 1");
+  if (!comm->local) return fail(RSDB_EMISMATCH, "rsdb_p2p_create_local needs a local comm");
+  if (sizes[0] < RSDB_P2P_SIGNAL_BYTES) return fail(RSDB_EINVAL, "signal buffer too small");
+  auto p = std::make_unique<rsdb_p2p>();
+  p->comm = comm;
+  p->n = n_bufs;
+  p->grid_div = comm->world;  // every logical rank's kernel must fit on the device at once
+  p->peer.assign(size_t(n_bufs), std::vector<char*>(size_t(comm->world), nullptr));
+  for (int32_t i = 0; i < n_bufs; ++i) {
+    if (sizes[i] < 0) return fail(RSDB_EINVAL, "buffer %d size invalid", i);
+    for (int32_t r = 0; r < comm->world; ++r) {
+      char* b = static_cast<char*>(all_bufs[int64_t(r) * n_bufs + i]);
+      if (!b) return fail(RSDB_EINVAL, "buffer %d of rank %d is null", i, r);
+      p->peer[size_t(i)][size_t(r)] = b;
+    }
+    p->local.push_back(p->peer[size_t(i)][size_t(comm->rank)]);
+    p->size.push_back(sizes[i]);
+  }
+  *out = p.release();
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_p2p_set_timeout(rsdb_p2p* p, double seconds) {
+  if (!p || !(seconds > 0)) return fail(RSDB_EINVAL, "rsdb_p2p_set_timeout: null p2p or seconds <= 0");
+  p->timeout_ns = seconds >= 1.8e10 ? UINT64_MAX : uint64_t(seconds * 1e9);
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_p2p_check(rsdb_p2p* p, int64_t* flags) {
+  if (!p || !flags) return fail(RSDB_EINVAL, "null argument");
+  uint64_t* w = reinterpret_cast<uint64_t*>(p->local[0]) + rsdb::P2P_ERR_WORD;
+  uint64_t v = 0;
+  CUDA_TRY(cudaMemcpy(&v, w, sizeof v, cudaMemcpyDeviceToHost));  // synchronises the device
+  *flags = int64_t(v);
+  if (v) {
+    const uint64_t zero = 0;
+    CUDA_TRY(cudaMemcpy(w, &zero, sizeof zero, cudaMemcpyHostToDevice));
+    return fail(RSDB_ECUDA, "a p2p barrier timed out (flags 0x%llx): a peer never reached the call; "
+                "results of the timed-out calls are invalid", (unsigned long long)v);
+  }
+  return OK_CLEAR();
+}
+
 // locate `ptr` (with `bytes` behind it) inside a registered buffer i (>= 1)
 extern "C++" rsdb_status p2p_find(const rsdb_p2p* p, const void* ptr, int64_t bytes, int32_t* idx,
                             int64_t* off) {
@@ -540,6 +603,14 @@ extern "C++" rsdb_status p2p_find(const rsdb_p2p* p, const void* ptr, int64_t by
   return fail(RSDB_EMISMATCH, "unit buffer is not inside a registered p2p buffer");
 }
 
+extern "C++" void p2p_signals(const rsdb_p2p* p, int m, rsdb::P2PSignals* sg) {
+  sg->local = reinterpret_cast<uint64_t*>(p->local[0]);
+  for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
+    sg->peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+  sg->timeout_ns = p->timeout_ns;
+  sg->grid_div = p->grid_div;
+}
+
 extern "C++" rsdb_status p2p_common(rsdb_unit* u, rsdb_p2p* p, rsdb::P2PSignals* sg) {
   if (!u || !p) return fail(RSDB_EINVAL, "null argument");
   if (!u->comm || u->comm != p->comm) return fail(RSDB_EMISMATCH, "unit and p2p use different comms");
@@ -547,15 +618,15 @@ extern "C++" rsdb_status p2p_common(rsdb_unit* u, rsdb_p2p* p, rsdb::P2PSignals*
   if ((u->L.S * u->L.elem_bytes) % 16 != 0)
     return fail(RSDB_EMISMATCH, "p2p collectives need 16-byte aligned shards (S*elem %% 16 == 0; "
                                 "planner layouts always are, P:199)");
-  sg->local = reinterpret_cast<uint64_t*>(p->local[0]);
-  for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
-    sg->peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+  p2p_signals(p, m, sg);
   return RSDB_OK;
 }
 
 rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   rsdb::P2PSignals sg;
-  if (rsdb_status st = p2p_common(u, p, &sg)) return st;
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (u->L.m > 1 || p)
+    if (rsdb_status st = p2p_common(u, p, &sg)) return st;
   if (u->L.elem_bytes != 2) return fail(RSDB_EMISMATCH, "p2p ReduceScatter needs a bf16 unit");
   if (u->L.S == 0) return OK_CLEAR();
   const int m = u->L.m;
@@ -571,19 +642,6 @@ rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   const float scale = float(1.0 / double(m));
   ++p->epoch;
   float* out = static_cast<float*>(u->bufs.grad_f32) + int64_t(u->rank) * u->L.S;
-  if (rsdb::rs_use_ce()) {
-    if (!p->aux) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
-      for (auto& e : p->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    // staging for the (m-1) peers' bf16 slices: the side of grad_f32 not holding
-    // this rank's fp32 output ((m-1) S 2 bytes fit on the larger side)
-    float* gf = static_cast<float*>(u->bufs.grad_f32);
-    uint16_t* stage = reinterpret_cast<uint16_t*>(2 * u->rank >= m - 1 ? gf : gf + int64_t(u->rank + 1) * u->L.S);
-    CUDA_TRY(rsdb::launch_rs_ce(g, out, stage, u->L.S, u->rank, m, scale, static_cast<const int64_t*>(u->pad.p),
-                                int32_t(u->npad), sg, p->epoch, S_(stream), p->aux, p->ev, rsdb_p2p::CE_CHUNKS));
-    return OK_CLEAR();
-  }
   CUDA_TRY(rsdb::launch_rs_p2p(g, out, u->L.S, u->rank, m, scale, static_cast<const int64_t*>(u->pad.p),
                                int32_t(u->npad), sg, p->epoch, S_(stream)));
   return OK_CLEAR();
@@ -591,7 +649,9 @@ rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
 
 rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   rsdb::P2PSignals sg;
-  if (rsdb_status st = p2p_common(u, p, &sg)) return st;
+  if (!u) return fail(RSDB_EINVAL, "null unit");
+  if (u->L.m > 1 || p)
+    if (rsdb_status st = p2p_common(u, p, &sg)) return st;
   if (u->L.S == 0 || u->L.m == 1) return OK_CLEAR();  // world 1: AllGather is the identity
   const int m = u->L.m;
   const int64_t bytes_S = u->L.S * u->L.elem_bytes;
@@ -644,12 +704,9 @@ static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state
                     static_cast<float*>(st->v_absmax),    nullptr,
                     param_target(u),                      1};
   const float scale = float(1.0 / double(m));
-  // absmax chunks by TMA: arena-backed state (padded to 16 blocks) or whole 16-B chunks
-  const int abs_tma = aligned16(st->m_absmax) && aligned16(st->v_absmax) &&
-                      (st == &u->bound_state || u->nblocks % 4 == 0);
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, g, m,
                                     scale, ap, s, m > 1 ? &sg : nullptr, u->rank,
-                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr, abs_tma));
+                                    m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr));
   return OK_CLEAR();
 }
 
@@ -859,19 +916,11 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
   return OK_CLEAR();
 }
 
-// RSDB_RSA_COMPACT=0: the fused DBuffer step reads the full 40-B table (A/B)
-static bool rsa_compact_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("RSDB_RSA_COMPACT");
-    return !(e && std::strcmp(e, "0") == 0);
-  }();
-  return v;
-}
-
 static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg, int64_t step,
                                    void* stream, bool gather) {
   if (!d) return fail(RSDB_EINVAL, "null dbuffer");
-  const bool use_compact = d->blocks_compact.p && rsa_compact_enabled();
+  // the compact 16-B block table (+4 % at N = 1 over the 40-B one)
+  const bool use_compact = d->blocks_compact.p != nullptr;
   if (!d->param_bf16) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs bf16 units");
   rsdb::AdamScalars s;
   if (rsdb_status e = adam_scalars(cfg, step, &s)) return e;
@@ -911,7 +960,6 @@ static rsdb_status rs_adam_dbuffer(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
   CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(d->blocks_fused.p), d->nblocks, g,
                                     m, float(1.0 / double(m)), ap, s, m > 1 ? &sg : nullptr, d->rank,
                                     m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr,
-                                    aligned16(d->base[RSDB_KIND_MABS]) && aligned16(d->base[RSDB_KIND_VABS]),
                                     use_compact ? static_cast<const rsdb::AdamBlockC*>(d->blocks_compact.p) : nullptr,
                                     use_compact ? static_cast<const rsdb::UnitBase*>(d->unit_bases.p) : nullptr,
                                     use_compact ? d->n_units : 0));

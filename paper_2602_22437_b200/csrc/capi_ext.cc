@@ -83,9 +83,7 @@ rsdb_status rsdb_fp8_quantize_all_gather(rsdb_fp8_unit* u, rsdb_p2p* p, void* st
     for (int r = 0; r < m; ++r) codes.p[r] = p->peer[size_t(bi)][size_t(r)] + off + int64_t(u->rank) * S;
     if (rsdb_status e = p2p_find(p, u->scales, u->ntiles_total * 4, &bi, &off)) return e;
     for (int r = 0; r < m; ++r) scales.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
-    sg.local = reinterpret_cast<uint64_t*>(p->local[0]);
-    for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
-      sg.peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+    p2p_signals(p, m, &sg);
     ++p->epoch;
   } else {
     codes.p[0] = u->codes;
@@ -104,6 +102,8 @@ void rsdb_fp8_unit_free(rsdb_fp8_unit* u) { delete u; }
 // ---------------------------------------------------------------------------
 // N3: distributed Muon (Algorithm 2)
 // ---------------------------------------------------------------------------
+constexpr size_t MUON_CUBLAS_WS = size_t(32) << 20;  // cuBLAS's recommended size on Hopper / Blackwell
+
 struct rsdb_muon {
   rsdb::Layout L;
   rsdb_comm* comm = nullptr;
@@ -115,9 +115,9 @@ struct rsdb_muon {
   std::vector<int32_t> mine;  // matrices this rank is the root of
   int64_t ws_bytes = 0, x2_off = 0, a_off = 0, b_off = 0, ss_off = 0;  // bytes, this rank
   DevTable mom, gat, app;
+  DevTable cublas_ws;  // cuBLAS workspace (MUON_CUBLAS_WS bytes)
   int64_t n_mom = 0, max_mom = 0, n_gat = 0, c_gat = 0, n_app = 0, c_app = 0;
   std::vector<rsdb::MuonSeg> app_host;
-  double app_lr = -1.0;
   rsdb_muon_bufs b{};
   bool bound = false;
   cublasHandle_t h = nullptr;
@@ -247,7 +247,13 @@ rsdb_status rsdb_muon_create(const rsdb_layout* l, const int64_t* rows, const in
   if (rsdb_status st = require_device()) return st;
   if (rsdb_status st = u->mom.upload(mom.data(), mom.size() * sizeof(int64_t))) return st;
   if (rsdb_status st = u->gat.upload(gat.data(), gat.size() * sizeof(rsdb::MuonSeg))) return st;
+  if (rsdb_status st = u->app.upload(u->app_host.data(), u->app_host.size() * sizeof(rsdb::MuonSeg)))
+    return st;
   if (cublasCreate(&u->h) != CUBLAS_STATUS_SUCCESS) return fail(RSDB_ECUDA, "cublasCreate failed");
+  // cuBLAS workspace owned here and set after every cublasSetStream, so a step
+  // never allocates (no implicit synchronisation while peers' kernels wait in
+  // a barrier; graph-capturable)
+  if (rsdb_status st = u->cublas_ws.alloc(MUON_CUBLAS_WS)) return st;
   *out = u.release();
   return OK_CLEAR();
 }
@@ -357,19 +363,10 @@ rsdb_status rsdb_muon_step(rsdb_muon* u, rsdb_p2p* p, const rsdb_muon_cfg* cfg, 
     for (int r = 0; r < m; ++r) up.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
     if (rsdb_status e = p2p_find(p, u->b.workspace, 1, &bi, &off)) return e;
     for (int r = 0; r < m; ++r) wp.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
-    sg.local = reinterpret_cast<uint64_t*>(p->local[0]);
-    for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
-      sg.peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+    p2p_signals(p, m, &sg);
   } else {
     up.p[0] = u->b.u;
     wp.p[0] = u->b.workspace;
-  }
-  if (cfg->lr != u->app_lr) {  // apply coefficients eta * shape scale
-    std::vector<rsdb::MuonSeg> v = u->app_host;
-    for (auto& s : v) s.coef = float(cfg->lr * double(s.coef));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (rsdb_status e = u->app.upload(v.data(), v.size() * sizeof(rsdb::MuonSeg))) return e;
-    u->app_lr = cfg->lr;
   }
   // 1. MomentumUpdate on the shard (R21)
   CUDA_TRY(rsdb::launch_muon_momentum(static_cast<const int64_t*>(u->mom.p), u->n_mom, u->max_mom,
@@ -381,12 +378,13 @@ rsdb_status rsdb_muon_step(rsdb_muon* u, rsdb_p2p* p, const rsdb_muon_cfg* cfg, 
                                     m > 1 ? p->epoch : 0, st));
   // 3. Newton-Schulz on the root's matrices (R22)
   CUBLAS_TRY(cublasSetStream(u->h, st));
+  CUBLAS_TRY(cublasSetWorkspace(u->h, u->cublas_ws.p, u->cublas_ws.bytes));
   for (size_t i = 0; i < u->mine.size(); ++i)
     if (rsdb_status e = muon_newton_schulz(u, u->mine[i], int(i), cfg, st)) return e;
   // 4. Redistribute(o, p) + w -= eta * scale * o (R23): one kernel
   if (m > 1) ++p->epoch;
   CUDA_TRY(rsdb::launch_muon_apply(static_cast<const rsdb::MuonSeg*>(u->app.p), u->n_app, u->c_app, wp,
-                                   u->bf16, u->b.master, u->b.param_bf16, m, u->rank, m > 1 ? &sg : nullptr,
+                                   u->bf16, u->b.master, u->b.param_bf16, cfg->lr, m, u->rank, m > 1 ? &sg : nullptr,
                                    m > 1 ? p->epoch : 0, st));
   return OK_CLEAR();
 }

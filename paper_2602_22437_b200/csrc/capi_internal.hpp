@@ -44,8 +44,9 @@ struct rsdb_layout {
 };
 
 struct rsdb_comm {
-  ncclComm_t nc = nullptr;
+  ncclComm_t nc = nullptr;  // null for a local comm (rsdb_comm_create_local)
   int32_t world = 1, rank = 0, device = 0;
+  bool local = false;       // one of `world` logical ranks sharing this device
 };
 
 // device allocation owned by the library (metadata tables only)
@@ -54,6 +55,13 @@ struct DevTable {
   size_t bytes = 0;
   ~DevTable() {
     if (p) cudaFree(p);
+  }
+  rsdb_status alloc(size_t nbytes) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = nbytes;
+    if (nbytes) CUDA_TRY(cudaMalloc(&p, nbytes));
+    return RSDB_OK;
   }
   rsdb_status upload(const void* host, size_t nbytes) {
     if (p) {
@@ -112,15 +120,8 @@ struct rsdb_p2p {
   std::vector<std::vector<char*>> peer;  // [n][world], own rank = local
   std::vector<void*> opened;         // IPC mappings to close
   uint64_t epoch = 0;
-  // copy-engine ReduceScatter (RSDB_P2P_RS=ce): auxiliary stream + chunk events
-  static constexpr int CE_CHUNKS = 8;
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev[CE_CHUNKS + 1]{};
-  ~rsdb_p2p() {
-    for (auto e : ev)
-      if (e) cudaEventDestroy(e);
-    if (aux) cudaStreamDestroy(aux);
-  }
+  uint64_t timeout_ns = 60ull * 1000000000ull;  // barrier spin limit (rsdb_p2p_set_timeout)
+  int32_t grid_div = 1;  // logical ranks sharing the device (local mode: world)
 };
 
 struct rsdb_copy_plan {
@@ -141,3 +142,4 @@ rsdb_status tiles_of(const rsdb::Layout& L, int32_t rank, const std::vector<rsdb
                      std::vector<rsdb::QTile>* out);
 rsdb_status p2p_find(const rsdb_p2p* p, const void* ptr, int64_t bytes, int32_t* idx, int64_t* off);
 rsdb_status p2p_common(rsdb_unit* u, rsdb_p2p* p, rsdb::P2PSignals* sg);
+void p2p_signals(const rsdb_p2p* p, int m, rsdb::P2PSignals* sg);  // fill from p's signal buffers

@@ -17,6 +17,7 @@
 
 #include <cstdint>
 
+#include "devmath.cuh"
 #include "kernels.cuh"
 #include "p2p_dev.cuh"
 
@@ -38,15 +39,20 @@ __device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
 
 __device__ __forceinline__ float block_absmax(float v, float* red) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int w = threadIdx.x >> 5;
   __syncthreads();  // red[] of the previous tile has been consumed
   if ((threadIdx.x & 31) == 0) red[w] = v;
   __syncthreads();
   float a = red[0];
 #pragma unroll
-  for (int i = 1; i < FP8_WARPS; ++i) a = fmaxf(a, red[i]);
+  for (int i = 1; i < FP8_WARPS; ++i) a = fmax_nan(a, red[i]);
   return a;
+}
+
+// R19 + R28: inv = min(fl(448 / A), FLT_MAX) (finite for every A > 0)
+__device__ __forceinline__ float tile_inv(float A) {
+  return A > 0.f ? fminf(__fdiv_rn(E4M3_MAX, A), FLT_MAX_F) : 0.f;
 }
 
 template <int M>
@@ -88,20 +94,22 @@ __global__ void __launch_bounds__(FP8_NT) fp8_quant_ag_kernel(const Fp8Tile* __r
         const int row = w + FP8_WARPS * k, col = 4 * lane;
         if (row < T.rows && col < T.cols) {
           x[k] = __ldcs(reinterpret_cast<const float4*>(master + T.off + int64_t(row) * T.pitch + col));
-          a = fmaxf(a, fmaxf(fmaxf(fabsf(x[k].x), fabsf(x[k].y)), fmaxf(fabsf(x[k].z), fabsf(x[k].w))));
+          a = fmax_nan(a, fmax_nan(fmax_nan(fabsf(x[k].x), fabsf(x[k].y)), fmax_nan(fabsf(x[k].z), fabsf(x[k].w))));
         } else {
           x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
       A = block_absmax(a, red);
-      const float inv = A > 0.f ? __fdiv_rn(E4M3_MAX, A) : 0.f;
+      const float inv = tile_inv(A);
+      const uint32_t fixed = A > 0.f ? 0x7F7F7F7Fu : 0u;  // zero tile: codes 0 (R19); NaN/inf tile: NaN (R28)
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int row = w + FP8_WARPS * k, col = 4 * lane;
         if (row < T.rows && col < T.cols) {
-          const uint32_t c = A > 0.f ? e4m3x4(__fmul_rn(x[k].x, inv), __fmul_rn(x[k].y, inv),
-                                              __fmul_rn(x[k].z, inv), __fmul_rn(x[k].w, inv))
-                                     : 0u;  // zero tile: every code 0 (R19)
+          const uint32_t c = A > 0.f && A <= FLT_MAX_F
+                                 ? e4m3x4(__fmul_rn(x[k].x, inv), __fmul_rn(x[k].y, inv),
+                                          __fmul_rn(x[k].z, inv), __fmul_rn(x[k].w, inv))
+                                 : fixed;
           put_codes<M>(codes, rank, T.off + int64_t(row) * T.pitch + col, c);
         }
       }
@@ -111,18 +119,21 @@ __global__ void __launch_bounds__(FP8_NT) fp8_quant_ag_kernel(const Fp8Tile* __r
       float a = 0.f;
       for (int e = threadIdx.x; e < n; e += FP8_NT) {
         const int row = e / T.cols, col = e - row * T.cols;
-        a = fmaxf(a, fabsf(master[T.off + int64_t(row) * T.pitch + col]));
+        a = fmax_nan(a, fabsf(master[T.off + int64_t(row) * T.pitch + col]));
       }
       A = block_absmax(a, red);
-      const float inv = A > 0.f ? __fdiv_rn(E4M3_MAX, A) : 0.f;
+      const float inv = tile_inv(A);
+      const uint8_t fixed = A > 0.f ? 0x7F : 0;
       for (int e = threadIdx.x; e < n; e += FP8_NT) {
         const int row = e / T.cols, col = e - row * T.cols;
         const int64_t o = T.off + int64_t(row) * T.pitch + col;
-        put_code<M>(codes, o, A > 0.f ? uint8_t(e4m3x2(__fmul_rn(master[o], inv), 0.f) & 0xffu) : 0);
+        put_code<M>(codes, o, A > 0.f && A <= FLT_MAX_F ? uint8_t(e4m3x2(__fmul_rn(master[o], inv), 0.f) & 0xffu)
+                                                       : fixed);
       }
     }
     if (threadIdx.x == 0) {
-      const float sc = A > 0.f ? __fdiv_rn(A, E4M3_MAX) : 0.f;
+      // scale fl(A / 448); A = 0 -> 0; NaN / +inf kept (R28)
+      const float sc = A <= FLT_MAX_F ? __fdiv_rn(A, E4M3_MAX) : A;
 #pragma unroll
       for (int r = 0; r < M; ++r) static_cast<float*>(const_cast<void*>(scales.p[r]))[T.slot] = sc;
     }
@@ -139,7 +150,7 @@ static cudaError_t fp8_mbs(const Fp8Tile* tiles, int64_t ntiles, const float* ma
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fp8_quant_ag_kernel<M, SYNC>, FP8_NT, 0);
     return num_sms() * (b < 1 ? 1 : b);
   }();
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ntiles, grid));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ntiles, grid_share(grid, sg)));
   fp8_quant_ag_kernel<M, SYNC><<<blocks, FP8_NT, 0, st>>>(tiles, ntiles, master, codes, scales, rank, sg,
                                                           epoch);
   return cudaGetLastError();

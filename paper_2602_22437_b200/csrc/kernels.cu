@@ -2,7 +2,7 @@
 //
 //  cast_scale_kernel  a6  fused DBuffer group op: bf16|f32 -> f32 * 1/m,
 //                         padding written 0.  HBM-bound: 6 B/elem (bf16 src).
-//  adam8_kernel       a8  block-wise 8-bit Adam on the local ragged shard.
+//  adam8_tma_kernel   a8  block-wise 8-bit Adam on the local ragged shard.
 //                         HBM-bound: 18 B/elem (+ 16 B of absmax per block).
 //  copy_seg_kernel        batched ragged copy (FSDP2 Copy-In/Copy-Out baseline).
 //
@@ -11,8 +11,6 @@
 // on a persistent grid of (resident CTAs per SM) x (148 SMs).
 #include <cuda_bf16.h>
 
-#include <cstdlib>
-#include <cstring>
 
 #include "adam_dev.cuh"
 #include "kernels.cuh"
@@ -63,9 +61,11 @@ __device__ __forceinline__ bool in_pad_from(const int64_t* pad, int npad, int j,
   return false;
 }
 
-template <bool SRC_BF16>
-__global__ void __launch_bounds__(CAST_THREADS) cast_scale_kernel(const void* __restrict__ src,
-                                                                  float* __restrict__ dst,
+// ALIAS (src == dst, an f32 unit scaled in place, rsdb.h): coherent loads and
+// no __restrict__ -- each thread still rewrites exactly the vector it read.
+// Otherwise the read-only (non-coherent) path.
+template <bool SRC_BF16, bool ALIAS>
+__global__ void __launch_bounds__(CAST_THREADS) cast_scale_kernel(const void* src, float* dst,
                                                                   int64_t n, float scale,
                                                                   const int64_t* __restrict__ pad_g,
                                                                   int npad) {
@@ -90,13 +90,14 @@ __global__ void __launch_bounds__(CAST_THREADS) cast_scale_kernel(const void* __
       const int64_t c = base + u * CAST_THREADS;
       if (c < nvec) {
         if constexpr (SRC_BF16) {
-          const uint2 w = ld_nc_v2(static_cast<const uint2*>(src) + c);
+          const uint2 w = ld_nc_v2(static_cast<const uint2*>(src) + c);  // bf16 src never aliases dst
           f[u][0] = bf16lo(w.x);
           f[u][1] = bf16hi(w.x);
           f[u][2] = bf16lo(w.y);
           f[u][3] = bf16hi(w.y);
         } else {
-          const int4 w = ld_nc_v4(static_cast<const int4*>(src) + c);
+          const int4 w = ALIAS ? ld_na_v4(static_cast<const int4*>(src) + c)
+                               : ld_nc_v4(static_cast<const int4*>(src) + c);
           f[u][0] = __int_as_float(w.x);
           f[u][1] = __int_as_float(w.y);
           f[u][2] = __int_as_float(w.z);
@@ -134,9 +135,9 @@ __global__ void __launch_bounds__(CAST_THREADS) cast_scale_kernel(const void* __
   }
 }
 
-// misaligned fallback: one element per thread
+// misaligned fallback: one element per thread (src may equal dst)
 template <bool SRC_BF16>
-__global__ void cast_scale_scalar_kernel(const void* __restrict__ src, float* __restrict__ dst,
+__global__ void cast_scale_scalar_kernel(const void* src, float* dst,
                                          int64_t n, float scale, const int64_t* __restrict__ pad,
                                          int npad) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -162,32 +163,19 @@ cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t
       cast_scale_scalar_kernel<false><<<blocks, 256, 0, st>>>(src, dst, n, scale, pad_dev, npad);
     return cudaGetLastError();
   }
-  static int occ_bf16 = resident_blocks(cast_scale_kernel<true>, CAST_THREADS, 0);
-  static int occ_f32 = resident_blocks(cast_scale_kernel<false>, CAST_THREADS, 0);
+  static int occ_bf16 = resident_blocks(cast_scale_kernel<true, false>, CAST_THREADS, 0);
+  static int occ_f32 = resident_blocks(cast_scale_kernel<false, false>, CAST_THREADS, 0);
   const int64_t per_block = int64_t(CAST_THREADS) * CAST_UNROLL;
   const int64_t want = std::max<int64_t>(1, (nvec + per_block - 1) / per_block);
   const int64_t cap = int64_t(num_sms()) * (src_bf16 ? occ_bf16 : occ_f32);
   const int64_t blocks = std::min(want, cap);
   if (src_bf16)
-    cast_scale_kernel<true><<<blocks, CAST_THREADS, 0, st>>>(src, dst, n, scale, pad_dev, npad);
+    cast_scale_kernel<true, false><<<blocks, CAST_THREADS, 0, st>>>(src, dst, n, scale, pad_dev, npad);
+  else if (src == static_cast<const void*>(dst))
+    cast_scale_kernel<false, true><<<blocks, CAST_THREADS, 0, st>>>(src, dst, n, scale, pad_dev, npad);
   else
-    cast_scale_kernel<false><<<blocks, CAST_THREADS, 0, st>>>(src, dst, n, scale, pad_dev, npad);
+    cast_scale_kernel<false, false><<<blocks, CAST_THREADS, 0, st>>>(src, dst, n, scale, pad_dev, npad);
   return cudaGetLastError();
-}
-
-template <int NT, bool PARAM_BF16>
-__global__ void __launch_bounds__(NT) adam8_kernel(const AdamBlock* __restrict__ tbl,
-                                                   int64_t nblocks, AdamPtrs P, AdamScalars s) {
-  __shared__ float red_m[2][AdamGeom<NT>::WARPS], red_v[2][AdamGeom<NT>::WARPS];
-  int it = 0;
-  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
-    const AdamBlock blk = tbl[b];
-    const float sm = P.mabs[blk.slot] / 127.0f;  // dequantization scales (IEEE div)
-    const float sv = P.vabs[blk.slot] / 255.0f;
-    // red_m/red_v are double-buffered: a thread can be at most one block
-    // ahead (every block has a barrier), so no trailing __syncthreads.
-    adam_block_global<NT, PARAM_BF16>(blk, P, s, sm, sv, red_m[it & 1], red_v[it & 1]);
-  }
 }
 
 // bulk copies need 16-B aligned global addresses: codes at state_off % 16
@@ -266,25 +254,9 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
         adam_block_tail<NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, refill);
       }
     } else {
-      adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, refill);
+      adam_block_two_pass<NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, refill, GradF32{P.grad + blk.grad_off});
     }
   }
-}
-
-// Variant switch (experiments; the default is the measured best):
-// RSDB_ADAM_KERNEL = direct128 | direct256 | tma2 | tma3 | tma4  (TMA: 128 threads)
-static int adam_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("RSDB_ADAM_KERNEL");
-    v = 3;  // measured best on B200: TMA ring of 3 stages, 128 threads (profiles/r1)
-    if (e && !strcmp(e, "direct128")) v = 128;
-    if (e && !strcmp(e, "direct256")) v = 256;
-    if (e && !strcmp(e, "tma2")) v = 2;
-    if (e && !strcmp(e, "tma3")) v = 3;
-    if (e && !strcmp(e, "tma4")) v = 4;
-  }
-  return v;
 }
 
 template <int NT, bool BF, int ST>
@@ -301,36 +273,15 @@ static cudaError_t launch_adam8_tma(const AdamBlock* tbl, int64_t nblocks, const
   return cudaGetLastError();
 }
 
-template <int NT, bool BF>
-static cudaError_t launch_adam8_direct(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
-                                       const AdamScalars& s, cudaStream_t st) {
-  static int occ = resident_blocks(adam8_kernel<NT, BF>, NT, 0);
-  const int64_t blocks = std::min<int64_t>(nblocks, int64_t(num_sms()) * occ);
-  adam8_kernel<NT, BF><<<blocks, NT, 0, st>>>(tbl, nblocks, p, s);
-  return cudaGetLastError();
-}
-
+// One kernel: the TMA-fed persistent kernel, 3 stages, 128 threads (measured
+// best of the round-1 variants -- direct loads with 128 / 256 threads, 2-4
+// stages, profiles/r1/).  Blocks it cannot bulk-load (tails,
+// misaligned, 2-D tiles, longer than 2048) take its direct-load paths.
 cudaError_t launch_adam8(const AdamBlock* table_dev, int64_t nblocks, const AdamPtrs& p,
                          const AdamScalars& s, int32_t /*max_len*/, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
-  const bool bf = p.param_bf16;
-  switch (adam_variant()) {
-    case 2:
-      return bf ? launch_adam8_tma<128, true, 2>(table_dev, nblocks, p, s, st)
-                : launch_adam8_tma<128, false, 2>(table_dev, nblocks, p, s, st);
-    case 3:
-      return bf ? launch_adam8_tma<128, true, 3>(table_dev, nblocks, p, s, st)
-                : launch_adam8_tma<128, false, 3>(table_dev, nblocks, p, s, st);
-    case 4:
-      return bf ? launch_adam8_tma<128, true, 4>(table_dev, nblocks, p, s, st)
-                : launch_adam8_tma<128, false, 4>(table_dev, nblocks, p, s, st);
-    case 256:
-      return bf ? launch_adam8_direct<256, true>(table_dev, nblocks, p, s, st)
-                : launch_adam8_direct<256, false>(table_dev, nblocks, p, s, st);
-    default:
-      return bf ? launch_adam8_direct<128, true>(table_dev, nblocks, p, s, st)
-                : launch_adam8_direct<128, false>(table_dev, nblocks, p, s, st);
-  }
+  return p.param_bf16 ? launch_adam8_tma<128, true, 3>(table_dev, nblocks, p, s, st)
+                      : launch_adam8_tma<128, false, 3>(table_dev, nblocks, p, s, st);
 }
 
 // ----------------------------------------------------------------------------

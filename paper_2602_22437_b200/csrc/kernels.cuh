@@ -69,28 +69,28 @@ struct P2PPtrs {
 struct P2PSignals {
   uint64_t* local;                  // this rank's signal buffer
   uint64_t* peer[P2P_MAX_RANKS];    // every rank's signal buffer, mapped here
+  uint64_t timeout_ns;              // barrier spin limit (then the error flag, no hang)
+  int32_t grid_div;                 // host: ranks sharing this device (local mode), >= 1
 };
+// persistent grid of a barrier kernel: every rank's kernel must be resident at
+// once, so ranks sharing one device (rsdb_p2p_create_local) split its SMs
+inline int64_t grid_share(int64_t grid, const P2PSignals& sg) {
+  const int64_t d = sg.grid_div > 1 ? sg.grid_div : 1;
+  return grid / d > 0 ? grid / d : 1;
+}
+constexpr int P2P_ERR_WORD = 17;  // signal-buffer word: barrier timeout flag
 cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,
                           const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
                           cudaStream_t st);
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
-// ReduceScatter through the copy engines + a local rank-order reduction,
-// chunked so copies (aux stream) and reductions (st) overlap; stage holds
-// (m-1)*S bf16; ev has nchunk + 1 events.  rs_use_ce(): RSDB_P2P_RS=ce.
-cudaError_t launch_rs_ce(const P2PPtrs& grads, float* out, uint16_t* stage, int64_t S, int rank, int m, float scale,
-                         const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch, cudaStream_t st,
-                         cudaStream_t aux, cudaEvent_t* ev, int nchunk);
-bool rs_use_ce();
 // K-slot ring: gather every rank's persistent shard (shards.p[r], bytes_S) into dst
 cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, int rank, int m,
                              const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
 // a6 + a7 + a8 fused: ReduceScatter of the bf16 gradients over NVLink and the
 // 8-bit Adam update of the local shard in one kernel (sg may be null iff m == 1);
 // push_params non-null: also a4 -- every updated bf16 parameter is stored into
-// every peer's parameter array (AllGather fused into the step).  abs_tma: the
-// absmax arrays are 16-B aligned and readable in whole 16-B chunks around
-// every slot (DBuffer arenas), so they are fetched with the block's TMA.
+// every peer's parameter array (AllGather fused into the step).
 // Compact block table for the fused DBuffer step (flat blocks): 16 B per
 // block -- the block's unit, its offset inside the unit's shard, length and
 // absmax slot -- plus per-unit bases (kept in shared memory), so each CTA
@@ -109,7 +109,7 @@ constexpr int RSA_MAX_UNITS = 64;
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
-                               const P2PPtrs* push_params = nullptr, int abs_tma = 0,
+                               const P2PPtrs* push_params = nullptr,
                                const AdamBlockC* ctbl = nullptr, const UnitBase* ubase = nullptr,
                                int n_units = 0);
 
@@ -138,7 +138,7 @@ struct MuonSeg {
   int64_t n;            // elements
   int64_t chunk_begin;  // prefix sum of 8192-element chunks
   int32_t peer;         // rank owning the source
-  float coef;           // apply: eta * sqrt(max(1, rows/cols))
+  float coef;           // apply: the shape scale sqrt(max(1, rows/cols)) (x lr in the kernel)
 };
 static_assert(sizeof(MuonSeg) == 40, "MuonSeg is 40 bytes");
 cudaError_t launch_muon_momentum(const int64_t* segs, int64_t nseg, int64_t max_n, float* buf,
@@ -147,7 +147,7 @@ cudaError_t launch_muon_gather(const MuonSeg* segs, int64_t nseg, int64_t nchunk
                                void* ws, int bf16, int m, int rank, const P2PSignals* sg, uint64_t epoch,
                                cudaStream_t st);
 cudaError_t launch_muon_apply(const MuonSeg* segs, int64_t nseg, int64_t nchunks, const P2PPtrs& ws,
-                              int bf16, float* master, void* param_bf16, int m, int rank,
+                              int bf16, float* master, void* param_bf16, double lr, int m, int rank,
                               const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
 cudaError_t launch_muon_normalize(void* x, int64_t n, int bf16, double* ss, double eps, cudaStream_t st);
 

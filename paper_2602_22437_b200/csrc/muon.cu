@@ -86,11 +86,12 @@ __global__ void __launch_bounds__(MUON_NT) muon_gather_kernel(const MuonSeg* __r
   if constexpr (SYNC) p2p_done(sg, rank, m, epoch);
 }
 
-// Redistribute(o, p) fused with w <- w - coef * o and the bf16 shard
+// Redistribute(o, p) fused with w <- w - coef * o and the bf16 shard;
+// coef = fl(lr * shape scale) (the segment's coef holds the shape scale)
 template <bool BF16, bool SYNC>
 __global__ void __launch_bounds__(MUON_NT) muon_apply_kernel(const MuonSeg* __restrict__ segs, int64_t nseg,
                                                             int64_t nchunks, P2PPtrs ws, float* master,
-                                                            __nv_bfloat16* param, int m, int rank,
+                                                            __nv_bfloat16* param, double lr, int m, int rank,
                                                             P2PSignals sg, uint64_t epoch) {
   if constexpr (SYNC) p2p_start(sg, rank, m, epoch);
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(MUON_NT) muon_apply_kernel(const MuonSeg* __re
     const int64_t e0 = (c - S.chunk_begin) * MUON_CHUNK;
     const int64_t n = S.n - e0 < MUON_CHUNK ? S.n - e0 : MUON_CHUNK;
     const void* src = peer_ptr(ws, S.peer);
+    const float coef = float(lr * double(S.coef));
     for (int64_t i = threadIdx.x; i < n; i += MUON_NT) {
       float o;
       if constexpr (BF16)
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(MUON_NT) muon_apply_kernel(const MuonSeg* __re
       else
         o = __ldcv(static_cast<const float*>(src) + S.src_off + e0 + i);
       const int64_t d = S.dst_off + e0 + i;
-      const float w = __fmaf_rn(-S.coef, o, master[d]);
+      const float w = __fmaf_rn(-coef, o, master[d]);
       master[d] = w;
       if (param) param[d] = __float2bfloat16_rn(w);
     }
@@ -154,6 +156,16 @@ static int grid_for(int64_t items) {
   const int64_t cap = int64_t(num_sms()) * 8;
   return int(items < 1 ? 1 : (items < cap ? items : cap));
 }
+// barrier kernels: every CTA resident at once (its share of the device when
+// several logical ranks share it, rsdb_p2p_create_local)
+template <typename K>
+static int grid_sync(K kernel, int64_t items, const P2PSignals& sg) {
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, MUON_NT, 0);
+  const int64_t res = int64_t(num_sms()) * (b < 1 ? 1 : b);
+  const int64_t g = grid_for(items);
+  return int(grid_share(g < res ? g : res, sg));
+}
 
 cudaError_t launch_muon_momentum(const int64_t* segs, int64_t nseg, int64_t max_n, float* buf,
                                  const float* grad, float* u, float mu, cudaStream_t st) {
@@ -166,17 +178,17 @@ cudaError_t launch_muon_momentum(const int64_t* segs, int64_t nseg, int64_t max_
 cudaError_t launch_muon_gather(const MuonSeg* segs, int64_t nseg, int64_t nchunks, const P2PPtrs& u,
                                void* ws, int bf16, int m, int rank, const P2PSignals* sg, uint64_t epoch,
                                cudaStream_t st) {
-  const int g = grid_for(nchunks);
   const P2PSignals none{};
   if (m > 1 && !sg) return cudaErrorInvalidValue;
+  const int g = grid_for(nchunks);
   if (bf16) {
     if (m > 1)
-      muon_gather_kernel<true, true><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, u, ws, m, rank, *sg, epoch);
+      muon_gather_kernel<true, true><<<grid_sync(muon_gather_kernel<true, true>, nchunks, *sg), MUON_NT, 0, st>>>(segs, nseg, nchunks, u, ws, m, rank, *sg, epoch);
     else if (nchunks)
       muon_gather_kernel<true, false><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, u, ws, m, rank, none, 0);
   } else {
     if (m > 1)
-      muon_gather_kernel<false, true><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, u, ws, m, rank, *sg, epoch);
+      muon_gather_kernel<false, true><<<grid_sync(muon_gather_kernel<false, true>, nchunks, *sg), MUON_NT, 0, st>>>(segs, nseg, nchunks, u, ws, m, rank, *sg, epoch);
     else if (nchunks)
       muon_gather_kernel<false, false><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, u, ws, m, rank, none, 0);
   }
@@ -184,25 +196,25 @@ cudaError_t launch_muon_gather(const MuonSeg* segs, int64_t nseg, int64_t nchunk
 }
 
 cudaError_t launch_muon_apply(const MuonSeg* segs, int64_t nseg, int64_t nchunks, const P2PPtrs& ws,
-                              int bf16, float* master, void* param_bf16, int m, int rank,
+                              int bf16, float* master, void* param_bf16, double lr, int m, int rank,
                               const P2PSignals* sg, uint64_t epoch, cudaStream_t st) {
-  const int g = grid_for(nchunks);
   const P2PSignals none{};
   auto* pb = static_cast<__nv_bfloat16*>(param_bf16);
   if (m > 1 && !sg) return cudaErrorInvalidValue;
+  const int g = grid_for(nchunks);
   if (bf16) {
     if (m > 1)
-      muon_apply_kernel<true, true><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, m, rank, *sg,
+      muon_apply_kernel<true, true><<<grid_sync(muon_apply_kernel<true, true>, nchunks, *sg), MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, lr, m, rank, *sg,
                                                            epoch);
     else if (nchunks)
-      muon_apply_kernel<true, false><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, m, rank, none,
+      muon_apply_kernel<true, false><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, lr, m, rank, none,
                                                             0);
   } else {
     if (m > 1)
-      muon_apply_kernel<false, true><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, m, rank, *sg,
+      muon_apply_kernel<false, true><<<grid_sync(muon_apply_kernel<false, true>, nchunks, *sg), MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, lr, m, rank, *sg,
                                                             epoch);
     else if (nchunks)
-      muon_apply_kernel<false, false><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, m, rank,
+      muon_apply_kernel<false, false><<<g, MUON_NT, 0, st>>>(segs, nseg, nchunks, ws, master, pb, lr, m, rank,
                                                              none, 0);
   }
   return cudaGetLastError();

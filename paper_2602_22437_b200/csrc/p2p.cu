@@ -1,24 +1,28 @@
 // Fused collectives over NVLink peer memory, one process
-// per GPU, peers' buffers mapped with CUDA IPC (rsdb_p2p_create).
+// per GPU, peers' buffers mapped with CUDA IPC (rsdb_p2p_create) -- or, for
+// the single-device multi-rank test mode (rsdb_p2p_create_local), several
+// logical ranks on one device sharing it.
 //
-//  rs_p2p_kernel / rs_tma_kernel   a6+a7: rank k pulls G_r[kS + i] (bf16) from
-//        every rank r, y = sum_{r=0..m-1} fp32(G_r) * scale in rank order
-//        (fp32), padding -> 0, writes its fp32 shard.  Wire bytes per rank
-//        (m-1) S 2, vs (m-1) S 4 for the fp32 NCCL ReduceScatter, and no
-//        separate m*S cast pass.
-//  ag_p2p_kernel / ag_tma_kernel / copy-engine AG   a4: rank k pulls every
-//        peer's shard into its own buffer (rotated peer order).
-//  rs_adam_tma_kernel (default) / rs_adam_ws_kernel   a6+a7+a8 (+ a4 with
-//        PUSH): the ReduceScatter feeds the 8-bit Adam update of the shard;
-//        with PUSH every updated bf16 parameter is also stored into every
-//        peer's gathered buffer -- the whole step in one kernel.
+//  rs_tma_kernel        a6+a7: rank k bulk-loads (TMA) G_r[kS + i] (bf16) from
+//        every rank r into shared memory, y = sum_{r=0..m-1} fp32(G_r) * scale
+//        in rank order (fp32), padding -> 0, writes its fp32 shard.  Wire
+//        bytes per rank (m-1) S 2, vs (m-1) S 4 for the fp32 NCCL
+//        ReduceScatter, and no separate m*S cast pass.
+//  copy-engine AG       a4: rank k copies every peer's shard into its own
+//        buffer with cudaMemcpyAsync over the mappings (rotated peer order)
+//        between a start and a done barrier kernel.
+//  rs_adam_tma_kernel   a6+a7+a8 (+ a4 with PUSH): the ReduceScatter feeds
+//        the 8-bit Adam update of the shard; with PUSH every updated bf16
+//        parameter is also stored into every peer's gathered buffer -- the
+//        whole step in one kernel.
+// Round 1 measured the alternatives (8/16-B peer loads and stores, a TMA
+// AllGather, a copy-engine ReduceScatter, a warp-specialised fused kernel;
+// DESIGN.md §7b, profiles/r1/); only the measured best of each is built.
 //
 // Start/done barriers between the ranks: p2p_dev.cuh.
 #include <cuda_bf16.h>
 
-#include <cstdlib>
 #include <type_traits>
-#include <cstring>
 
 #include "adam_dev.cuh"
 #include "kernels.cuh"
@@ -26,35 +30,7 @@
 
 namespace rsdb {
 
-constexpr int P2P_THREADS = 512;
 
-// peer loads; FL = 0: ld.global.cv (uncached), 1: ld.global.nc (read-only
-// path; the peer does not write its buffer between the barriers), 2: weak ld.global
-template <int FL>
-__device__ __forceinline__ uint2 ld_peer_v2(const void* p) {
-  uint2 r;
-  if constexpr (FL == 0)
-    asm volatile("ld.global.cv.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  else if constexpr (FL == 1)
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  else
-    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-template <int FL>
-__device__ __forceinline__ int4 ld_peer_v4(const void* p) {
-  int4 r;
-  if constexpr (FL == 0)
-    asm volatile("ld.global.cv.v4.s32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  else if constexpr (FL == 1)
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  else
-    asm volatile("ld.global.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
 
 __device__ __forceinline__ int first_pad_after_p(const int64_t* pad, int npad, int64_t x) {
   int lo = 0, hi = npad;
@@ -95,128 +71,6 @@ __device__ __forceinline__ void pad_zero4(const int64_t* pad, int npad, int64_t 
   }
 }
 
-// grads: M pointers to each rank's unit grad_full base (bf16).  out = this
-// rank's grad_f32 + rank*S.  pad: padding intervals of the global buffer.
-// Templated on the world size M so the peer loop unrolls with static indices
-// (no local-memory copy of the pointer table) and all M x U peer loads are in
-// flight before the rank-ordered accumulation.  VEC = bf16 elements per load
-// (4: 8-byte loads, one coalesced float4 store; 8: 16-byte loads, two float4
-// stores), FL = peer-load flavour.
-template <int M, int VEC, int FL>
-__global__ void __launch_bounds__(P2P_THREADS) rs_p2p_kernel(P2PPtrs grads, float* __restrict__ out,
-                                                            int64_t S, int rank, float scale,
-                                                            const int64_t* __restrict__ pad, int npad,
-                                                            P2PSignals sg, uint64_t epoch) {
-  constexpr int U = (M <= 2 ? 8 : (M <= 4 ? 4 : 2)) * 4 / VEC;  // vectors per thread per iteration
-  p2p_start(sg, rank, M, epoch);
-  const int64_t base = int64_t(rank) * S;
-  const int64_t nvec = S / VEC;  // S is a multiple of g_coll = 8 for bf16 units
-  const int64_t stride = int64_t(gridDim.x) * P2P_THREADS * U;
-  const uint16_t* g[M];
-#pragma unroll
-  for (int r = 0; r < M; ++r) g[r] = static_cast<const uint16_t*>(grads.p[r]) + base;
-  for (int64_t v0 = int64_t(blockIdx.x) * P2P_THREADS * U + threadIdx.x; v0 < nvec; v0 += stride) {
-    uint32_t w[M][U][VEC / 2];
-#pragma unroll
-    for (int r = 0; r < M; ++r)
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-        if constexpr (VEC == 4) {
-          const uint2 x = v < nvec ? ld_peer_v2<FL>(g[r] + 4 * v) : make_uint2(0u, 0u);
-          w[r][u][0] = x.x;
-          w[r][u][1] = x.y;
-        } else {
-          const int4 x = v < nvec ? ld_peer_v4<FL>(g[r] + 8 * v) : make_int4(0, 0, 0, 0);
-          w[r][u][0] = uint32_t(x.x);
-          w[r][u][1] = uint32_t(x.y);
-          w[r][u][2] = uint32_t(x.z);
-          w[r][u][3] = uint32_t(x.w);
-        }
-      }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-      if (v >= nvec) break;
-      // rank-order accumulation: acc = ((0 + x_0) + x_1) + ... (fp32), x_r = fl(fp32(G_r) * scale)
-      float a[VEC];
-#pragma unroll
-      for (int k = 0; k < VEC; ++k) a[k] = 0.f;
-#pragma unroll
-      for (int r = 0; r < M; ++r)
-#pragma unroll
-        for (int k = 0; k < VEC / 2; ++k) {
-          a[2 * k] = rank_acc(a[2 * k], __uint_as_float(w[r][u][k] << 16), scale, r == 0);
-          a[2 * k + 1] = rank_acc(a[2 * k + 1], __uint_as_float(w[r][u][k] & 0xffff0000u), scale, r == 0);
-        }
-#pragma unroll
-      for (int k = 0; k < VEC / 4; ++k) {
-        const int64_t e0 = base + VEC * v + 4 * k;
-        pad_zero4(pad, npad, e0, a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]);
-        *reinterpret_cast<float4*>(out + VEC * v + 4 * k) =
-            make_float4(a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]);
-      }
-    }
-  }
-  p2p_done(sg, rank, M, epoch);
-}
-
-// params: M pointers to each rank's unit param_full base.  PUSH = false: copy
-// every peer's shard [r*S, (r+1)*S) into this rank's buffer (peer loads);
-// PUSH = true: write this rank's shard into every peer's buffer (peer stores,
-// made visible by the system fence of the done barrier).  bytes_S = S * elem.
-template <int M, bool PUSH, int FL>
-__global__ void __launch_bounds__(P2P_THREADS) ag_p2p_kernel(P2PPtrs params, int64_t bytes_S, int rank,
-                                                            P2PSignals sg, uint64_t epoch) {
-  constexpr int U = 4;
-  p2p_start(sg, rank, M, epoch);
-  char* buf[M];
-#pragma unroll
-  for (int r = 0; r < M; ++r) buf[r] = static_cast<char*>(const_cast<void*>(params.p[r]));
-  char* mine = static_cast<char*>(const_cast<void*>(params.p[0]));
-#pragma unroll
-  for (int r = 0; r < M; ++r)
-    if (r == rank) mine = buf[r];
-  const int64_t nvec = bytes_S / 16;  // S * elem is a multiple of 16 (g_coll)
-  const int64_t stride = int64_t(gridDim.x) * P2P_THREADS * U;
-  for (int64_t v0 = int64_t(blockIdx.x) * P2P_THREADS * U + threadIdx.x; v0 < nvec; v0 += stride) {
-    if constexpr (PUSH) {
-      int4 w[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-        if (v < nvec) w[u] = ld_peer_v4<1>(mine + int64_t(rank) * bytes_S + 16 * v);
-      }
-#pragma unroll
-      for (int r = 0; r < M; ++r) {
-        if (r == rank) continue;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-          if (v < nvec) *reinterpret_cast<int4*>(buf[r] + int64_t(rank) * bytes_S + 16 * v) = w[u];
-        }
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < M; ++r) {
-        if (r == rank) continue;
-        int4 w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-          if (v < nvec) w[u] = ld_peer_v4<FL>(buf[r] + int64_t(r) * bytes_S + 16 * v);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t v = v0 + int64_t(u) * P2P_THREADS;
-          if (v < nvec) *reinterpret_cast<int4*>(mine + int64_t(r) * bytes_S + 16 * v) = w[u];
-        }
-      }
-    }
-  }
-  p2p_done(sg, rank, M, epoch);
-}
-
 // ---------------- TMA (bulk-copy) variants over NVLink ----------------
 // The data movement is issued by ONE thread per CTA as 1-D bulk copies
 // (cp.async.bulk) straight from the peers' mapped memory into a ring of
@@ -250,84 +104,6 @@ __device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t byt
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
-}
-__device__ __forceinline__ void tma_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_addr(src)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void tma_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-constexpr int AG_TMA_CHUNK = 16384;  // bytes per stage
-constexpr int AG_TMA_STAGES = 4;
-
-template <int M>
-__global__ void __launch_bounds__(32) ag_tma_kernel(P2PPtrs params, int64_t bytes_S, int rank,
-                                                   P2PSignals sg, uint64_t epoch) {
-  extern __shared__ __align__(128) uint8_t ag_smem[];
-  __shared__ __align__(8) uint64_t bar[AG_TMA_STAGES];
-  p2p_start(sg, rank, M, epoch);
-  if (threadIdx.x == 0) {
-    char* buf[M];
-#pragma unroll
-    for (int r = 0; r < M; ++r) buf[r] = static_cast<char*>(const_cast<void*>(params.p[r]));
-    char* mine = buf[0];
-#pragma unroll
-    for (int r = 0; r < M; ++r)
-      if (r == rank) mine = buf[r];
-    for (int s = 0; s < AG_TMA_STAGES; ++s) tbar_init(&bar[s]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int64_t per = (bytes_S + AG_TMA_CHUNK - 1) / AG_TMA_CHUNK;  // chunks per peer shard
-    const int64_t total = per * (M - 1);
-    // chunk j -> (peer r, byte offset inside the global buffer, length)
-    // peer slot p = j / per reads from rank (rank + 1 + p) % M: at any moment the
-    // ranks read from distinct peers (a permutation), so no GPU's links are
-    // shared by several readers while others idle
-    auto chunk = [&](int64_t j, int& r, int64_t& off, uint32_t& len) {
-      const int p = int(j / per);
-      const int64_t c = j - int64_t(p) * per;
-      r = (rank + 1 + p) % M;
-      off = int64_t(r) * bytes_S + c * AG_TMA_CHUNK;
-      len = uint32_t(imin64(AG_TMA_CHUNK, bytes_S - c * AG_TMA_CHUNK));
-    };
-    auto issue = [&](int64_t j, int s) {
-      int r;
-      int64_t off;
-      uint32_t len;
-      chunk(j, r, off, len);
-      const char* src = buf[0];
-#pragma unroll
-      for (int q = 0; q < M; ++q)
-        if (q == r) src = buf[q];
-      tbar_expect(&bar[s], len);
-      tma_g2s(ag_smem + s * AG_TMA_CHUNK, src + off, len, &bar[s]);
-    };
-    for (int s = 0; s < AG_TMA_STAGES; ++s) {
-      const int64_t j = blockIdx.x + int64_t(s) * gridDim.x;
-      if (j < total) issue(j, s);
-    }
-    int it = 0;
-    for (int64_t j = blockIdx.x; j < total; j += gridDim.x, ++it) {
-      const int s = it % AG_TMA_STAGES;
-      tbar_wait(&bar[s], uint32_t(it / AG_TMA_STAGES) & 1u);
-      int r;
-      int64_t off;
-      uint32_t len;
-      chunk(j, r, off, len);
-      tma_s2g(mine + off, ag_smem + s * AG_TMA_CHUNK, len);
-      const int64_t jn = j + int64_t(AG_TMA_STAGES) * gridDim.x;
-      if (jn < total) {
-        tma_wait_read_all();  // the store above has read stage s
-        issue(jn, s);
-      }
-    }
-    tma_wait_all();
-  }
-  p2p_done(sg, rank, M, epoch);
 }
 
 constexpr int RS_TMA_THREADS = 256;
@@ -410,22 +186,6 @@ __global__ void __launch_bounds__(RS_TMA_THREADS) rs_tma_kernel(P2PPtrs grads, f
 }
 
 template <int M>
-static cudaError_t ag_tma_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
-                            uint64_t epoch, cudaStream_t st) {
-  const size_t smem = size_t(AG_TMA_CHUNK) * AG_TMA_STAGES;
-  static const int grid = [&] {
-    cudaFuncSetAttribute(ag_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ag_tma_kernel<M>, 32, smem);
-    return num_sms() * (b < 1 ? 1 : b);
-  }();
-  const int64_t chunks = (bytes_S + AG_TMA_CHUNK - 1) / AG_TMA_CHUNK * (M - 1);
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(chunks, grid));
-  ag_tma_kernel<M><<<blocks, 32, smem, st>>>(params, bytes_S, rank, sg, epoch);
-  return cudaGetLastError();
-}
-
-template <int M>
 static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
                             const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
                             cudaStream_t st) {
@@ -437,7 +197,7 @@ static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int ran
     return num_sms() * (b < 1 ? 1 : b);
   }();
   const int64_t tiles = (S + RS_TMA_TILE - 1) / RS_TMA_TILE;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, grid));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, grid_share(grid, sg)));
   rs_tma_kernel<M><<<blocks, RS_TMA_THREADS, smem, st>>>(grads, out, S, rank, scale, pad, npad, sg, epoch);
   return cudaGetLastError();
 }
@@ -502,179 +262,14 @@ cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, 
   }
 }
 
-// ---- ReduceScatter through the copy engines (RSDB_P2P_RS=ce) ----
-// The peers' bf16 slices of this rank's shard are copied over NVLink by the
-// copy engines (cudaMemcpyAsync over the IPC mappings, rotated peer order,
-// on an auxiliary stream) into a local staging area, chunk by chunk; a local
-// kernel reduces each chunk in rank order (fp32, x scale, padding -> 0) as
-// soon as its copies have landed, so copies and reduction overlap.
-template <int M>
-__global__ void __launch_bounds__(256) rs_local_reduce_kernel(const uint16_t* __restrict__ own,
-                                                             const uint16_t* __restrict__ stage,
-                                                             float* __restrict__ out, int64_t c0,
-                                                             int64_t len, int64_t S, int rank, float scale,
-                                                             const int64_t* __restrict__ pad, int npad) {
-  const uint16_t* src[M];
-#pragma unroll
-  for (int r = 0; r < M; ++r) {
-    const int p = (r - rank + M) % M;  // 0: own slice; p >= 1: staging slot p - 1
-    src[r] = p == 0 ? own : stage + int64_t(p - 1) * S;
-  }
-  const int64_t nv = len / 4;  // chunks are multiples of 8 elements
-  for (int64_t v = int64_t(blockIdx.x) * 256 + threadIdx.x; v < nv; v += int64_t(gridDim.x) * 256) {
-    const int64_t i = c0 + 4 * v;
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int r = 0; r < M; ++r) {  // rank order, as the oracle
-      const uint2 w = ld_nc_v2(src[r] + i);
-      a[0] = rank_acc(a[0], __uint_as_float(w.x << 16), scale, r == 0);
-      a[1] = rank_acc(a[1], __uint_as_float(w.x & 0xffff0000u), scale, r == 0);
-      a[2] = rank_acc(a[2], __uint_as_float(w.y << 16), scale, r == 0);
-      a[3] = rank_acc(a[3], __uint_as_float(w.y & 0xffff0000u), scale, r == 0);
-    }
-    pad_zero4(pad, npad, int64_t(rank) * S + i, a[0], a[1], a[2], a[3]);
-    *reinterpret_cast<float4*>(out + i) = make_float4(a[0], a[1], a[2], a[3]);
-  }
-}
-
-template <int M>
-static cudaError_t rs_ce_m(const P2PPtrs& grads, float* out, uint16_t* stage, int64_t S, int rank, float scale,
-                           const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch, cudaStream_t st,
-                           cudaStream_t aux, cudaEvent_t* ev, int nchunk) {
-  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
-  cudaError_t e = cudaEventRecord(ev[nchunk], st);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(aux, ev[nchunk], 0);
-  if (e != cudaSuccess) return e;
-  const int64_t chunk = ((S + nchunk - 1) / nchunk + 7) / 8 * 8;
-  const uint16_t* own = static_cast<const uint16_t*>(grads.p[rank]) + int64_t(rank) * S;
-  for (int c = 0; c < nchunk; ++c) {
-    const int64_t c0 = int64_t(c) * chunk;
-    if (c0 >= S) break;
-    const int64_t len = std::min<int64_t>(chunk, S - c0);
-    for (int p = 1; p < M; ++p) {
-      const int r = (rank + p) % M;
-      e = cudaMemcpyAsync(stage + int64_t(p - 1) * S + c0,
-                          static_cast<const uint16_t*>(grads.p[r]) + int64_t(rank) * S + c0, size_t(len) * 2,
-                          cudaMemcpyDeviceToDevice, aux);
-      if (e != cudaSuccess) return e;
-    }
-    e = cudaEventRecord(ev[c], aux);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[c], 0);
-    if (e != cudaSuccess) return e;
-    const int grid = int(std::min<int64_t>(int64_t(num_sms()) * 8, std::max<int64_t>(1, (len / 4 + 255) / 256)));
-    rs_local_reduce_kernel<M><<<grid, 256, 0, st>>>(own, stage, out, c0, len, S, rank, scale, pad, npad);
-  }
-  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_rs_ce(const P2PPtrs& grads, float* out, uint16_t* stage, int64_t S, int rank, int m, float scale,
-                         const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch, cudaStream_t st,
-                         cudaStream_t aux, cudaEvent_t* ev, int nchunk) {
-  switch (m) {
-#define RSCE_CASE(MM) \
-  case MM:            \
-    return rs_ce_m<MM>(grads, out, stage, S, rank, scale, pad, npad, sg, epoch, st, aux, ev, nchunk);
-    RSCE_CASE(2) RSCE_CASE(3) RSCE_CASE(4) RSCE_CASE(5) RSCE_CASE(6) RSCE_CASE(7) RSCE_CASE(8)
-#undef RSCE_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
-bool rs_use_ce() {
-  static const bool v = [] {
-    const char* e = getenv("RSDB_P2P_RS");
-    return e && !strcmp(e, "ce");
-  }();
-  return v;
-}
-
-template <typename K>
-static int p2p_grid(K kernel) {
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, P2P_THREADS, 0);
-  return num_sms() * (b < 1 ? 1 : b);
-}
-
-// Variant switch (experiments; defaults = measured best):
-// RSDB_P2P_RS = v4cv | v4nc | v4ld | v8cv | v8nc | v8ld | tma ;
-// RSDB_P2P_AG = pullcv | pullnc | push | tma | ce   (defaults: RS tma, AG ce; profiles/r1)
-static int p2p_env(const char* name, const char* const* opts, int n, int dflt) {
-  const char* e = getenv(name);
-  if (!e) return dflt;
-  for (int i = 0; i < n; ++i)
-    if (!strcmp(e, opts[i])) return i;
-  return dflt;
-}
-static int rs_variant() {
-  static const char* o[] = {"v4cv", "v4nc", "v4ld", "v8cv", "v8nc", "v8ld", "tma"};
-  static int v = p2p_env("RSDB_P2P_RS", o, 7, 6);  // tma: 604-614 GB/s wire (profiles/r1)
-  return v;
-}
-static int ag_variant() {
-  static const char* o[] = {"pullcv", "pullnc", "push", "tma", "ce"};
-  static int v = p2p_env("RSDB_P2P_AG", o, 5, 4);  // ce: 701 GB/s at N=2 and 4 (profiles/r1)
-  return v;
-}
-
-template <int M, int VEC, int FL>
-static cudaError_t rs_p2p_mvf(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
-                              const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
-                              cudaStream_t st) {
-  static const int grid = p2p_grid(rs_p2p_kernel<M, VEC, FL>);
-  const int64_t per = int64_t(P2P_THREADS) * VEC * ((M <= 2 ? 8 : (M <= 4 ? 4 : 2)) * 4 / VEC);
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((S + per - 1) / per, grid));
-  rs_p2p_kernel<M, VEC, FL><<<blocks, P2P_THREADS, 0, st>>>(grads, out, S, rank, scale, pad, npad, sg,
-                                                             epoch);
-  return cudaGetLastError();
-}
-
-template <int M>
-static cudaError_t rs_p2p_m(const P2PPtrs& grads, float* out, int64_t S, int rank, float scale,
-                            const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
-                            cudaStream_t st) {
-  switch (rs_variant()) {
-    case 1: return rs_p2p_mvf<M, 4, 1>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    case 2: return rs_p2p_mvf<M, 4, 2>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    case 3: return rs_p2p_mvf<M, 8, 0>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    case 4: return rs_p2p_mvf<M, 8, 1>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    case 5: return rs_p2p_mvf<M, 8, 2>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    case 6: return rs_tma_m<M>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    default: return rs_p2p_mvf<M, 4, 0>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-  }
-}
-
-template <int M, bool PUSH, int FL>
-static cudaError_t ag_p2p_mvf(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
-                              uint64_t epoch, cudaStream_t st) {
-  static const int grid = p2p_grid(ag_p2p_kernel<M, PUSH, FL>);
-  const int64_t per = int64_t(P2P_THREADS) * 4;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((bytes_S / 16 + per - 1) / per, grid));
-  ag_p2p_kernel<M, PUSH, FL><<<blocks, P2P_THREADS, 0, st>>>(params, bytes_S, rank, sg, epoch);
-  return cudaGetLastError();
-}
-
-template <int M>
-static cudaError_t ag_p2p_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
-                            uint64_t epoch, cudaStream_t st) {
-  switch (ag_variant()) {
-    case 1: return ag_p2p_mvf<M, false, 1>(params, bytes_S, rank, sg, epoch, st);
-    case 2: return ag_p2p_mvf<M, true, 1>(params, bytes_S, rank, sg, epoch, st);
-    case 3: return ag_tma_m<M>(params, bytes_S, rank, sg, epoch, st);
-    case 4: return ag_ce_m<M>(params, bytes_S, rank, sg, epoch, st);
-    default: return ag_p2p_mvf<M, false, 0>(params, bytes_S, rank, sg, epoch, st);
-  }
-}
-
 cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,
                           const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
                           cudaStream_t st) {
   switch (m) {
 #define RS_CASE(M) \
   case M:          \
-    return rs_p2p_m<M>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
-    RS_CASE(1) RS_CASE(2) RS_CASE(3) RS_CASE(4) RS_CASE(5) RS_CASE(6) RS_CASE(7) RS_CASE(8)
+    return rs_tma_m<M>(grads, out, S, rank, scale, pad, npad, sg, epoch, st);
+    RS_CASE(2) RS_CASE(3) RS_CASE(4) RS_CASE(5) RS_CASE(6) RS_CASE(7) RS_CASE(8)
 #undef RS_CASE
     default:
       return cudaErrorInvalidValue;
@@ -686,8 +281,8 @@ cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int 
   switch (m) {
 #define AG_CASE(M) \
   case M:          \
-    return ag_p2p_m<M>(params, bytes_S, rank, sg, epoch, st);
-    AG_CASE(1) AG_CASE(2) AG_CASE(3) AG_CASE(4) AG_CASE(5) AG_CASE(6) AG_CASE(7) AG_CASE(8)
+    return ag_ce_m<M>(params, bytes_S, rank, sg, epoch, st);
+    AG_CASE(2) AG_CASE(3) AG_CASE(4) AG_CASE(5) AG_CASE(6) AG_CASE(7) AG_CASE(8)
 #undef AG_CASE
     default:
       return cudaErrorInvalidValue;
@@ -705,11 +300,10 @@ cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int 
 // overlaps the NVLink-bound reduction.  M = 1 (world 1): the cast + Adam.
 constexpr int RSA_NT = 128;
 
-constexpr int RSA_MAX_STAGES = 4;
 template <int M>
 struct RsaGeom {
-  // default ring depth (RSDB_RSA_STAGES overrides): 3 at world 1, 2 with peers
-  // (more CTAs per SM; +0.5-0.7 % at N = 2 / 4, profiles/r1/v14_misc/stages_ab)
+  // ring depth: 3 at world 1, 2 with peers (more CTAs per SM; +0.5-0.7 % at
+  // N = 2 / 4, profiles/r1/v14_misc/stages_ab)
   static constexpr int STAGES = M == 1 ? 3 : 2;
   static constexpr int G_BYTES = M * ADAM_TILE * 2;
   static constexpr int ABS_OFF = G_BYTES + ADAM_TILE * 6;  // 16-B chunks holding the block's absmax
@@ -750,6 +344,23 @@ struct PeerPush {
   }
 };
 
+// Reduced gradient of one element straight from the peers' bf16 buffers
+// (rank-order fp32 sum x scale, as rs_p2p), for the two-pass long blocks.
+template <int M>
+struct PeerGradSum {
+  P2PPtrs grads;
+  int64_t base;
+  float scale;
+  __device__ float operator()(int64_t o) const {
+    float acc = 0.f;
+#pragma unroll
+    for (int q = 0; q < M; ++q)
+      acc = rank_acc(acc, __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[base + o]) << 16),
+                     scale, q == 0);
+    return acc;
+  }
+};
+
 // Single-role variant: all 128 threads compute; thread 0 also issues the
 // refill of the stage it just consumed, from the after-reduce hook.
 template <int M, bool PARAM_BF16, bool SYNC, bool PUSH>
@@ -767,7 +378,7 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
   PushT push{};
   if constexpr (PUSH) push.init(params, rank);
   extern __shared__ __align__(128) uint8_t rsa_smem[];
-  __shared__ __align__(8) uint64_t full[RSA_MAX_STAGES];
+  __shared__ __align__(8) uint64_t full[3];
   __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
   __shared__ UnitBase s_ub[RSA_MAX_UNITS];
   if (ctbl)
@@ -862,13 +473,18 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
         adam_block_tail<RSA_NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill, push);
       else
         adam_block_tail<RSA_NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill, push);
+    } else if (blk.len > ADAM_TILE) {
+      // long block (q > 2048, 2-D tiles such as 128x128): two passes, the
+      // rank-order sum of the peers' gradients recomputed in each
+      adam_block_two_pass<RSA_NT, PARAM_BF16>(blk, sm, sv, P, s, rm, rv, refill,
+                                              PeerGradSum<M>{grads, blk.grad_off, scale}, push);
     } else {
       // generic: gradients summed straight from the peers' memory, masked & strided
 #pragma unroll
       for (int e = 0; e < G::EPT; ++e) {
         const int i = G::idx(e);
         float acc = 0.f;
-        if (i < blk.len && blk.len <= ADAM_TILE) {
+        if (i < blk.len) {
           const int64_t o = blk_off(blk, i);
 #pragma unroll
           for (int q = 0; q < M; ++q)
@@ -891,238 +507,46 @@ __global__ void __launch_bounds__(RSA_NT) rs_adam_tma_kernel(const AdamBlock* __
   if constexpr (SYNC) p2p_done(sg, rank, M, epoch);
 }
 
-
-// Warp-specialised: warps 0..3 compute (128 threads, the shared Adam tail),
-// warp 4 is the producer -- it reads the block table, writes each stage's
-// descriptor to shared memory and issues the stage's bulk copies (peers'
-// gradients, master, codes, absmax chunks), waiting on the stage's "empty"
-// mbarrier, which the compute warps arrive on as soon as the block is in
-// registers (after the absmax reduction).  So no compute warp ever waits on
-// a global load of the table or on issuing copies.
-constexpr int RSA_THREADS = RSA_NT + 32;
-
-template <int M, bool PARAM_BF16, bool SYNC, bool PUSH>
-__global__ void __launch_bounds__(RSA_THREADS, 4) rs_adam_ws_kernel(const AdamBlock* __restrict__ tbl,
-                                                                    int64_t nblocks, P2PPtrs grads,
-                                                                    P2PPtrs params, float scale, AdamPtrs P,
-                                                                    AdamScalars s, P2PSignals sg, int rank,
-                                                                    uint64_t epoch, int nst, int abs_tma) {
-  using Gm = RsaGeom<M>;
-  using G = AdamGeom<RSA_NT>;
-  using PushT = std::conditional_t<PUSH, PeerPush<M>, NoPush>;
-  extern __shared__ __align__(128) uint8_t rsa_smem[];
-  __shared__ __align__(8) uint64_t full[RSA_MAX_STAGES];
-  __shared__ __align__(8) uint64_t empty[RSA_MAX_STAGES];
-  __shared__ float red_m[2][G::WARPS], red_v[2][G::WARPS];
-  __shared__ AdamBlock sdesc[RSA_MAX_STAGES];
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < nst; ++st) {
-      tbar_init(&full[st]);   // one arrival: the producer's arrive.expect_tx
-      tbar_init(&empty[st]);  // one arrival: compute thread 0 after the block is in registers
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if constexpr (SYNC) p2p_start(sg, rank, M, epoch);  // (contains a CTA-wide barrier)
-  else __syncthreads();
-
-  if (threadIdx.x >= RSA_NT) {  // ---------------- producer warp
-    if (threadIdx.x == RSA_NT) {
-      int it = 0, st = 0;
-      AdamBlock nb = blockIdx.x < nblocks ? tbl[blockIdx.x] : AdamBlock{};
-      for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
-        const AdamBlock cur = nb;
-        if (b + gridDim.x < nblocks) nb = tbl[b + gridDim.x];  // prefetch the next entry
-        // reuse of stage st: wait for the compute warps' release of its previous
-        // block, i.e. completion number it/nst - 1 of empty[st]
-        if (it >= nst) tbar_wait(&empty[st], uint32_t((it / nst - 1) & 1));
-        uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
-        sdesc[st] = cur;
-        const bool fits = rsa_fits(cur);
-        const uint32_t L = uint32_t(cur.len);
-        const uint32_t tx = (fits ? L * (2 * M + 6) : 0u) + (abs_tma ? 32u : 0u);
-        if (tx == 0) {
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[st])) : "memory");
-        } else {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tbar_expect(&full[st], tx);
-          if (fits) {
-#pragma unroll
-            for (int r = 0; r < M; ++r)
-              tma_g2s(S + r * ADAM_TILE * 2, static_cast<const uint16_t*>(grads.p[r]) + cur.grad_off, L * 2,
-                      &full[st]);
-            tma_g2s(S + Gm::G_BYTES, P.master + cur.state_off, L * 4, &full[st]);
-            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 4, P.mq + cur.state_off, L, &full[st]);
-            tma_g2s(S + Gm::G_BYTES + ADAM_TILE * 5, P.vq + cur.state_off, L, &full[st]);
-          }
-          if (abs_tma) {  // the 16-B chunks holding the block's two absmax values
-            tma_g2s(S + Gm::ABS_OFF, P.mabs + (cur.slot & ~3), 16, &full[st]);
-            tma_g2s(S + Gm::ABS_OFF + 16, P.vabs + (cur.slot & ~3), 16, &full[st]);
-          }
-        }
-        if (++st == nst) st = 0;
-      }
-    }
-  } else {  // ---------------------------------------- compute warps
-    PushT push{};
-    if constexpr (PUSH) push.init(params, rank);
-    int it = 0, st = 0;
-    uint32_t phase = 0;
-    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
-      float* rm = red_m[it & 1];
-      float* rv = red_v[it & 1];
-      auto release = [&]() {  // the whole stage is in registers: hand it back to the producer
-        if (threadIdx.x == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
-      };
-      tbar_wait(&full[st], phase);
-      const AdamBlock blk = sdesc[st];
-      float am0, av0;
-      if (abs_tma) {
-        const float* Sa = reinterpret_cast<const float*>(rsa_smem + st * Gm::STAGE_BYTES + Gm::ABS_OFF);
-        am0 = Sa[blk.slot & 3];
-        av0 = Sa[4 + (blk.slot & 3)];
-      } else {
-        am0 = P.mabs[blk.slot];
-        av0 = P.vabs[blk.slot];
-      }
-      const float sm = am0 / 127.0f;
-      const float sv = av0 / 255.0f;
-      BlockRegs<RSA_NT> r;
-      if (rsa_fits(blk)) {
-        const uint8_t* S = rsa_smem + st * Gm::STAGE_BYTES;
-        const uint16_t* Sg = reinterpret_cast<const uint16_t*>(S);
-        const float* Sp = reinterpret_cast<const float*>(S + Gm::G_BYTES);
-        const uint8_t* Sm = S + Gm::G_BYTES + ADAM_TILE * 4;
-        const uint8_t* Sv = S + Gm::G_BYTES + ADAM_TILE * 5;
-#pragma unroll
-        for (int k = 0; k < G::Q; ++k) {
-          const int e0 = G::quad(k);
-          float a[4] = {0.f, 0.f, 0.f, 0.f};
-          float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
-          uint32_t cm = 0x80808080u, cv = 0u;  // decode to m = v = 0 for masked quads
-          if (e0 < blk.len) {
-#pragma unroll
-            for (int q = 0; q < M; ++q) {  // rank order
-              const uint2 w = *reinterpret_cast<const uint2*>(Sg + q * ADAM_TILE + e0);
-              a[0] = rank_acc(a[0], __uint_as_float(w.x << 16), scale, q == 0);
-              a[1] = rank_acc(a[1], __uint_as_float(w.x & 0xffff0000u), scale, q == 0);
-              a[2] = rank_acc(a[2], __uint_as_float(w.y << 16), scale, q == 0);
-              a[3] = rank_acc(a[3], __uint_as_float(w.y & 0xffff0000u), scale, q == 0);
-            }
-            pv = *reinterpret_cast<const float4*>(Sp + e0);
-            cm = *reinterpret_cast<const uint32_t*>(Sm + e0);
-            cv = *reinterpret_cast<const uint32_t*>(Sv + e0);
-          }
-          r.g[4 * k + 0] = a[0], r.g[4 * k + 1] = a[1], r.g[4 * k + 2] = a[2], r.g[4 * k + 3] = a[3];
-          r.p[4 * k + 0] = pv.x, r.p[4 * k + 1] = pv.y, r.p[4 * k + 2] = pv.z, r.p[4 * k + 3] = pv.w;
-          dq4_m(cm, sm, &r.mt[4 * k]);
-          dq4_v(cv, sv, &r.vt[4 * k]);
-        }
-        if (blk.len == ADAM_TILE)
-          adam_block_tail<RSA_NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, release, push);
-        else
-          adam_block_tail<RSA_NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, release, push);
-      } else {
-        // generic: gradients summed straight from the peers' memory, masked & strided
-#pragma unroll
-        for (int e = 0; e < G::EPT; ++e) {
-          const int i = G::idx(e);
-          float acc = 0.f;
-          if (i < blk.len && blk.len <= ADAM_TILE) {
-            const int64_t o = blk_off(blk, i);
-#pragma unroll
-            for (int q = 0; q < M; ++q)
-              acc = rank_acc(acc, __uint_as_float(uint32_t(static_cast<const uint16_t*>(grads.p[q])[blk.grad_off + o]) << 16), scale, q == 0);
-            r.p[e] = P.master[blk.state_off + o];
-            r.mt[e] = (byte_f(uint32_t(uint8_t(P.mq[blk.state_off + o])) ^ 0x80u, 0) - 8388736.0f) * sm;
-            r.vt[e] = (byte_f(uint32_t(P.vq[blk.state_off + o]), 0) - 8388608.0f) * sv;
-          } else {
-            r.p[e] = r.mt[e] = r.vt[e] = 0.f;
-          }
-          r.g[e] = acc;
-        }
-        adam_block_tail<RSA_NT, PARAM_BF16, 0>(r, blk, P, s, rm, rv, release, push);
-      }
-      if (++st == nst) {  // ring position and mbarrier phase of the next block
-        st = 0;
-        phase ^= 1u;
-      }
-    }
-  }
-  if constexpr (SYNC) p2p_done(sg, rank, M, epoch);  // (contains a CTA-wide barrier)
-}
-
-// RSDB_RSA_KERNEL=ws: the warp-specialised kernel (producer warp); default:
-// the single-role kernel (measured faster at N=1)
-static bool rsa_warp_specialised() {
-  const char* e = std::getenv("RSDB_RSA_KERNEL");
-  return e && std::strcmp(e, "ws") == 0;
-}
-
-static int rsa_stages(int def) {
-  static const int env = [] {
-    const char* e = std::getenv("RSDB_RSA_STAGES");
-    return e ? std::atoi(e) : 0;
-  }();
-  return env >= 2 && env <= RSA_MAX_STAGES ? env : def;
-}
-
 template <int M, bool SYNC, bool PUSH>
 static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads,
                                const P2PPtrs& params, float scale, const AdamPtrs& P,
                                const AdamScalars& s, const P2PSignals& sg, int rank, uint64_t epoch,
-                               cudaStream_t st, int abs_tma, const AdamBlockC* ctbl, const UnitBase* ubase,
-                               int n_units) {
-  static const int nst = rsa_stages(RsaGeom<M>::STAGES);
-  static const bool ws = rsa_warp_specialised();
+                               cudaStream_t st, const AdamBlockC* ctbl, const UnitBase* ubase, int n_units) {
+  constexpr int nst = RsaGeom<M>::STAGES;
   const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * nst;
   static const int grid = [&] {
     int b = 0;
-    if (ws) {
-      cudaFuncSetAttribute(rs_adam_ws_kernel<M, true, SYNC, PUSH>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_ws_kernel<M, true, SYNC, PUSH>, RSA_THREADS,
-                                                    smem);
-    } else {
-      cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, true, SYNC, PUSH>, RSA_NT,
-                                                    smem);
-    }
+    cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, true, SYNC, PUSH>, RSA_NT, smem);
     return num_sms() * (b < 1 ? 1 : b);
   }();
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, grid));
-  if (ws)
-    rs_adam_ws_kernel<M, true, SYNC, PUSH><<<blocks, RSA_THREADS, smem, st>>>(
-        tbl, nblocks, grads, params, scale, P, s, sg, rank, epoch, nst, abs_tma);
-  else
-    rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(
-        tbl, nblocks, grads, params, scale, P, s, sg, rank, epoch, nst, ctbl, ubase, n_units);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, grid_share(grid, sg)));
+  rs_adam_tma_kernel<M, true, SYNC, PUSH><<<blocks, RSA_NT, smem, st>>>(
+      tbl, nblocks, grads, params, scale, P, s, sg, rank, epoch, nst, ctbl, ubase, n_units);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rs_adam_p2p(const AdamBlock* tbl, int64_t nblocks, const P2PPtrs& grads, int m,
                                float scale, const AdamPtrs& P, const AdamScalars& s,
                                const P2PSignals* sg, int rank, uint64_t epoch, cudaStream_t st,
-                               const P2PPtrs* push_params, int abs_tma, const AdamBlockC* ctbl,
+                               const P2PPtrs* push_params, const AdamBlockC* ctbl,
                                const UnitBase* ubase, int n_units) {
-  if (rsa_warp_specialised()) ctbl = nullptr;  // the warp-specialised variant reads the full table
   if (!P.param_bf16) return cudaErrorInvalidValue;  // the fused path is for bf16 units
   const P2PPtrs none_p{};
   if (m == 1) {
     P2PSignals none{};
-    return rs_adam_mbs<1, false, false>(tbl, nblocks, grads, none_p, scale, P, s, none, rank, epoch, st,
-                                        abs_tma, ctbl, ubase, n_units);
+    return rs_adam_mbs<1, false, false>(tbl, nblocks, grads, none_p, scale, P, s, none, rank, epoch, st, ctbl,
+                                        ubase, n_units);
   }
   if (!sg) return cudaErrorInvalidValue;
   switch (m) {
-#define RSA_CASE(MM)                                                                                  \
-  case MM:                                                                                            \
-    return push_params ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, *push_params, scale, P, s,  \
-                                                     *sg, rank, epoch, st, abs_tma, ctbl, ubase,      \
-                                                     n_units)                                         \
-                       : rs_adam_mbs<MM, true, false>(tbl, nblocks, grads, none_p, scale, P, s, *sg,  \
-                                                      rank, epoch, st, abs_tma, ctbl, ubase, n_units);
+#define RSA_CASE(MM)                                                                                     \
+  case MM:                                                                                               \
+    return push_params ? rs_adam_mbs<MM, true, true>(tbl, nblocks, grads, *push_params, scale, P, s, *sg, \
+                                                     rank, epoch, st, ctbl, ubase, n_units)              \
+                       : rs_adam_mbs<MM, true, false>(tbl, nblocks, grads, none_p, scale, P, s, *sg,     \
+                                                      rank, epoch, st, ctbl, ubase, n_units);
     RSA_CASE(2) RSA_CASE(3) RSA_CASE(4) RSA_CASE(5) RSA_CASE(6) RSA_CASE(7) RSA_CASE(8)
 #undef RSA_CASE
     default:

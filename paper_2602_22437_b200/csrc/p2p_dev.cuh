@@ -5,6 +5,9 @@
 //   [0, 8)   start[r] = epoch written by rank r when it enters the call
 //   [8, 16)  done[r]  = epoch written by rank r when all its CTAs finished
 //   [16]     CTA completion counter of this rank's running kernel
+//   [17]     error flag: bit 0 = a barrier wait exceeded sg.timeout_ns (the
+//            kernel then gives up waiting instead of hanging the device;
+//            rsdb_p2p_check reports and clears it)
 // p2p_start: block 0 publishes `epoch` to every peer (after a system fence),
 // every CTA waits until all peers have published -- every rank's prior stream
 // work is then complete.  p2p_done: the last CTA (atomic counter) fences,
@@ -36,6 +39,23 @@ __device__ __forceinline__ uint64_t* sg_peer(const P2PSignals& sg, int i) {
   return q;
 }
 
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// spin until *p >= epoch, or set the error flag after sg.timeout_ns
+__device__ __forceinline__ void wait_epoch(const P2PSignals& sg, const uint64_t* p, uint64_t epoch) {
+  if (ld_acquire_sys(p) >= epoch) return;
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_sys(p) < epoch) {
+    if (global_ns() - t0 > sg.timeout_ns) {
+      atomicOr(reinterpret_cast<unsigned long long*>(sg.local + P2P_ERR_WORD), 1ull);
+      return;
+    }
+  }
+}
+
 __device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < m && int(threadIdx.x) != rank) {
     __threadfence_system();
@@ -44,8 +64,7 @@ __device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m,
   if (threadIdx.x == 0) {
     for (int r = 0; r < m; ++r) {
       if (r == rank) continue;
-      while (ld_acquire_sys(sg.local + r) < epoch) {
-      }
+      wait_epoch(sg, sg.local + r, epoch);
     }
   }
   __syncthreads();
@@ -65,8 +84,7 @@ __device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, 
         if (r < m && r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);
       for (int r = 0; r < m; ++r) {
         if (r == rank) continue;
-        while (ld_acquire_sys(sg.local + 8 + r) < epoch) {
-        }
+        wait_epoch(sg, sg.local + 8 + r, epoch);
       }
     }
   }

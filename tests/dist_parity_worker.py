@@ -1,22 +1,15 @@
-"""torchrun worker: one FSDP step through the C-ABI on N GPUs vs the oracle's
-simulated ranks.  Launched by tests/test_gpu_multi.py:
+"""torchrun worker: every multi-rank parity case (tests/parity_cases.py) with
+one process per GPU -- the p2p kernels over NVLink peer memory (CUDA IPC)
+plus the NCCL entry points -- against the oracle's simulated ranks.
+Launched by tests/test_gpu_multi.py:
 
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
       --master-port P tests/dist_parity_worker.py
 
-Per unit: AllGather (bit exact), fused cast/scale + ReduceScatter (bit exact
-on dyadic synth grads; error bound on random-normal bf16 grads), 8-bit Adam
-(codes +-1, params 1e-5), then a second AllGather that must equal the
-concatenation of every rank's oracle parameter shard (bf16, within 1 ulp);
-the fused RS+Adam(+AG) kernels vs the unfused sequence (bit exact); the
-N2 FP8 block quantization + AllGather vs oracle/fp8.py (bit exact); and N3
-distributed Muon vs oracle/muon.py (fp32 and bf16 Newton-Schulz tolerances).
-Exit code 0 iff every check passed on every rank.
-"""
+Exit code 0 iff every check passed on every rank."""
 import os
 import sys
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -25,21 +18,8 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import paper_2602_22437_b200 as R  # noqa: E402
-from oracle import adam8 as OA  # noqa: E402
-from oracle import dbuffer as OD  # noqa: E402
-from oracle import fp8 as F  # noqa: E402
-from oracle import planner as OP  # noqa: E402
-from synth import workloads as W  # noqa: E402
-
-from gpu_helpers import bf16_bits, f32, logical_grads, logical_params, place_gpu  # noqa: E402
-
-
-def units_for(m):
-    q = 2048
-    lay = W.llama32_1b_layer(0)
-    yield "toy", [t.numel for t in W.toy().units[0].tensors], q, 4
-    yield "llama-attn", [t.numel for t in lay.tensors][:4] + [2048, 2048], q, 2
-    yield "ragged", [5000, 77, 4109, 2048 * 3, 1, 40000, 2048 * 11 + 3], q, 2
+from parity_cases import all_cases  # noqa: E402
+from rank_ctx import ProcCtx, drive_proc  # noqa: E402
 
 
 def main():
@@ -49,369 +29,23 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     comm = R.init_comm(rank, world, local)
-    ok = True
     msgs = []
-    for name, es, q, eb in units_for(world):
-        gs = [min(q, e) for e in es]
-        o = OP.plan(es, gs, world, OP.gcoll_elems(eb))
-        c = R.plan(es, gs, world, elem_bytes=eb)
-        S, E = c.S, sum(es)
-        dt = torch.bfloat16 if eb == 2 else torch.float32
-        p_log = logical_params(5, E)
-        # ---- AllGather: only my shard is valid before the collective
-        full_ref = place_gpu(c, p_log, dt)
-        param_full = torch.zeros_like(full_ref)
-        param_full[rank * S:(rank + 1) * S] = full_ref[rank * S:(rank + 1) * S]
-        grad_full = place_gpu(c, logical_grads(5, rank, E), dt, fill=float("nan"))
-        grad_f32 = grad_full if eb == 4 else torch.empty(world * S, dtype=torch.float32,
-                                                         device="cuda")
-        u = R.Unit(c, rank, param_full, grad_full, grad_f32, qblock=q, comm=comm)
-        R.all_gather(u)
-        torch.cuda.synchronize()
-        exp = OD.place_logical(o, p_log.numpy())
-        exp_bits = OD.to_bf16_rne(exp) if eb == 2 else exp.view(np.uint32)
-        got_bits = bf16_bits(param_full) if eb == 2 else f32(param_full).view(np.uint32)
-        if not np.array_equal(got_bits, exp_bits):
-            ok = False
-            msgs.append(f"{name}: AllGather mismatch")
-        # ---- ReduceScatter (fused cast/scale)
-        R.reduce_scatter(u)
-        torch.cuda.synchronize()
-        bufs = []
-        for r in range(world):
-            src = OD.place_logical(o, logical_grads(5, r, E).numpy(), fill=np.nan)
-            bufs.append(OD.grouped_cast_scale(o, OD.to_bf16_rne(src) if eb == 2 else src,
-                                              eb == 2))
-        y_all = OD.reduce_scatter(o, bufs)  # the oracle's reduced shard of every rank
-        y_ref = y_all[rank]
-        y = f32(grad_f32[rank * S:(rank + 1) * S])
-        if world & (world - 1) == 0:
-            # m a power of two: x * fl(1/m) is exact on the dyadic inputs, so
-            # every summation order gives the same bits -- NCCL's too
-            if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
-                ok = False
-                msgs.append(f"{name}: ReduceScatter not bit exact (max {np.abs(y - y_ref).max()})")
-        else:  # NCCL's order differs from rank order: the fp32 bound
-            y64 = OD.reduce_scatter_f64(o, bufs)[rank]
-            absum = sum(np.abs(x[rank * S:(rank + 1) * S].astype(np.float64)) for x in bufs)
-            if np.any(np.abs(y.astype(np.float64) - y64) > 1e-6 * absum + 1e-30):
-                ok = False
-                msgs.append(f"{name}: ReduceScatter outside 1e-6 * sum|x|")
-        # ---- N1: the same two collectives as single kernels over NVLink peer memory
-        p2p = R.P2P(comm, [param_full, grad_full] if eb == 2 else [param_full])
-        param_full.zero_()
-        param_full[rank * S:(rank + 1) * S] = full_ref[rank * S:(rank + 1) * S]
-        R.all_gather_p2p(u, p2p)
-        torch.cuda.synchronize()
-        got_bits = bf16_bits(param_full) if eb == 2 else f32(param_full).view(np.uint32)
-        if not np.array_equal(got_bits, exp_bits):
-            ok = False
-            msgs.append(f"{name}: p2p AllGather mismatch")
-        if eb == 2:
-            grad_f32.fill_(float("nan"))
-            R.reduce_scatter_p2p(u, p2p)
-            torch.cuda.synchronize()
-            y = f32(grad_f32[rank * S:(rank + 1) * S])
-            if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
-                ok = False
-                msgs.append(f"{name}: p2p ReduceScatter not bit exact")
-            # repeated calls (epochs advance, barriers re-arm)
-            for _ in range(3):
-                R.reduce_scatter_p2p(u, p2p)
-                R.all_gather_p2p(u, p2p)
-            torch.cuda.synchronize()
-            y = f32(grad_f32[rank * S:(rank + 1) * S])
-            if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
-                ok = False
-                msgs.append(f"{name}: repeated p2p ReduceScatter drifted")
-        p2p.close()
-        if eb == 4 and world & (world - 1):
-            # fp32 unit, m not a power of two: NCCL's fp32 summation order
-            # differs from rank order, so the reduced gradient at cancelling
-            # elements -- and the Adam result there -- is not unique (the RS
-            # is checked against its bound above).  The oracle takes no input
-            # from the device, so this unit's Adam is checked at m = 2 / 4 and
-            # at world 1 instead.
-            continue
-        # ---- 8-bit Adam on my shard
-        master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
-        nb = u.num_blocks
-        mq = torch.zeros(S, dtype=torch.int8, device="cuda")
-        vq = torch.zeros(S, dtype=torch.uint8, device="cuda")
-        ma = torch.zeros(nb, dtype=torch.float32, device="cuda")
-        va = torch.zeros(nb, dtype=torch.float32, device="cuda")
-        fused_in = [t.clone() for t in (master, mq, vq, ma, va)]
-        gather_in = [t.clone() for t in (master, mq, vq, ma, va)]
-        torch.cuda.synchronize()
-        R.step_8bit_adam(u, master, mq, vq, ma, va, R.AdamConfig(), 1)
-        if eb == 2:
-            # a6 + a7 + a8 in one kernel over NVLink: bit-identical to RS -> Adam
-            p2p = R.P2P(comm, [param_full, grad_full])
-            R.reduce_scatter_adam_p2p(u, p2p, R.AdamConfig(), 1, state=fused_in)
-            torch.cuda.synchronize()
-            for a, b in zip(fused_in, (master, mq, vq, ma, va)):
-                if not torch.equal(a.view(torch.uint8), b.view(torch.uint8)):
-                    ok = False
-                    msgs.append(f"{name}: fused RS+Adam differs from RS then Adam")
-                    break
-            p2p.close()
-        R.all_gather(u)
-        torch.cuda.synchronize()
-        # the oracle's Adam runs on the oracle's reduced gradients (no oracle
-        # input comes from the device); here they equal the GPU's bit for bit
-        # (p2p rank-order RS, or NCCL at m a power of two -- both checked above)
-        ref_full = []
-        for r in range(world):
-            blocks = OP.rank_blocks(o, r, q)
-            p0 = OD.shard(o, OD.place_logical(o, p_log.numpy()), r)
-            st = OA.step_8bit_adam(p0, y_all[r], np.zeros(S, np.int8),
-                                   np.zeros(S, np.uint8), np.zeros(len(blocks), np.float32),
-                                   np.zeros(len(blocks), np.float32), blocks, OA.AdamCfg(), 1,
-                                   out_bf16=(eb == 2))
-            ref_full.append(st)
-        mine = ref_full[rank]
-        blocks = OP.rank_blocks(o, rank, q)
-        mask = np.zeros(S, bool)
-        for off, n in blocks:
-            mask[off:off + n] = True
-        gm = f32(master)
-        err = (np.abs(gm - mine[0]) / (np.abs(mine[0]) + 1e-3))[mask]
-        dm = np.abs(mq.cpu().numpy().astype(int) - mine[1].astype(int))[mask]
-        dv = np.abs(vq.cpu().numpy().astype(int) - mine[2].astype(int))[mask]
-        if err.max(initial=0) > 1e-5 or dm.max(initial=0) > 1 or dv.max(initial=0) > 1:
-            ok = False
-            msgs.append(f"{name}: Adam mismatch err={err.max(initial=0)} dm={dm.max(initial=0)}")
-        # second AllGather: every rank's updated shard
-        if eb == 2:
-            got = OD.bf16_to_f32(bf16_bits(param_full)).astype(np.float64)
-            exp = OD.bf16_to_f32(np.concatenate([s[5] for s in ref_full])).astype(np.float64)
-        else:
-            got = f32(param_full).astype(np.float64)
-            exp = np.concatenate([s[5] for s in ref_full]).astype(np.float64)
-        p32 = np.abs(np.concatenate([s[0] for s in ref_full]).astype(np.float64))
-        full_mask = np.zeros(world * S, bool)
-        for l, e in zip(o.starts, o.numel):
-            full_mask[l:l + e] = True
-        tol = 1e-5 * (p32 + 1e-3) + (2.0 ** -7 * p32 if eb == 2 else 0)
-        if np.any((np.abs(got - exp) > tol)[full_mask]):
-            ok = False
-            msgs.append(f"{name}: post-Adam AllGather mismatch {np.abs(got - exp)[full_mask].max()}")
-        if eb == 2:
-            # a6 + a7 + a8 + a4 in one kernel: the pushed parameters equal the
-            # unfused RS -> Adam -> AllGather result bit for bit on every tensor
-            # element, and the optimizer state equals the unfused state
-            pf_ref = param_full.clone()
-            param_full.fill_(float("nan"))
-            dist.barrier()
-            p2p = R.P2P(comm, [param_full, grad_full])
-            R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 1, state=gather_in)
-            torch.cuda.synchronize()
-            fm = torch.from_numpy(full_mask).cuda()
-            if not torch.equal(param_full.view(torch.int16)[fm], pf_ref.view(torch.int16)[fm]):
-                ok = False
-                msgs.append(f"{name}: fused RS+Adam+AG parameters differ from RS -> Adam -> AG")
-            for a, b in zip(gather_in, (master, mq, vq, ma, va)):
-                if not torch.equal(a.view(torch.uint8), b.view(torch.uint8)):
-                    ok = False
-                    msgs.append(f"{name}: fused RS+Adam+AG state differs from RS then Adam")
-                    break
-            # repeated steps re-arm the barriers; peers' params keep agreeing
-            for t in range(2, 5):
-                R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), t, state=gather_in)
-            torch.cuda.synchronize()
-            h = torch.tensor([float(param_full.view(torch.int16)[fm].to(torch.int64).sum().item())],
-                             dtype=torch.float64)
-            hs = [torch.zeros_like(h) for _ in range(world)]
-            dist.all_gather(hs, h)
-            if len(set(x.item() for x in hs)) != 1:
-                ok = False
-                msgs.append(f"{name}: ranks disagree on the parameters after repeated fused steps")
-            p2p.close()
-        del u
-    # ---- random-normal bf16 grads: fp32 RS tolerance (non-exact sums)
-    es = [300001, 4097]
-    o = OP.plan(es, [1, 1], world, 8)
-    c = R.plan(es, [1, 1], world, elem_bytes=2)
-    S = c.S
-    rng = np.random.default_rng(100 + rank)
-    g_np = [OD.to_bf16_rne(np.random.default_rng(100 + r).normal(0, 1e-2, world * S).astype(np.float32))
-            for r in range(world)]
-    for a, b in o.padding_intervals():
-        for g in g_np:
-            g[a:b] = 0
-    grad_full = torch.from_numpy(g_np[rank].view(np.int16)).cuda().view(torch.bfloat16)
-    grad_f32 = torch.empty(world * S, dtype=torch.float32, device="cuda")
-    pf = torch.zeros(world * S, dtype=torch.bfloat16, device="cuda")
-    u = R.Unit(c, rank, pf, grad_full, grad_f32, qblock=1, comm=comm)
-    R.reduce_scatter(u)
+    keep = []
+    for name, fn, kw in all_cases():
+        ctx = ProcCtx(rank, world, comm)
+        drive_proc(fn(ctx, **kw))
+        msgs += [f"{name}: {m}" for m in ctx.msgs]
+        keep.append(ctx)
     torch.cuda.synchronize()
-    xs = [OD.grouped_cast_scale(o, g, True) for g in g_np]
-    yref = OD.reduce_scatter_f64(o, xs)[rank]
-    absum = sum(np.abs(x[rank * S:(rank + 1) * S].astype(np.float64)) for x in xs)
-    y = f32(grad_f32[rank * S:(rank + 1) * S]).astype(np.float64)
-    if np.any(np.abs(y - yref) > 1e-6 * absum + 1e-30):
-        ok = False
-        msgs.append("random-normal RS outside 1e-6 * sum|x|")
-    # fused p2p path: rank-order fp32 sum == the oracle's rank-order sum bit for bit
-    p2p = R.P2P(comm, [grad_full])
-    grad_f32.zero_()
-    R.reduce_scatter_p2p(u, p2p)
-    torch.cuda.synchronize()
-    y32 = f32(grad_f32[rank * S:(rank + 1) * S])
-    yord = OD.reduce_scatter(o, xs)[rank]
-    if not np.array_equal(y32.view(np.uint32), yord.view(np.uint32)):
-        ok = False
-        msgs.append("random-normal p2p RS differs from the rank-order oracle sum")
-    p2p.close()
-    del u
-    del rng
-    # ---- ranks owning no quantization block (one whole-tensor block on rank 0):
-    # the fused RS+Adam+AG kernel still launches on every rank (its barriers
-    # count every rank) and equals RS -> Adam -> AG
-    es = [4096 * 8]
-    c = R.plan(es, es, world, elem_bytes=2)
-    o = OP.plan(es, es, world, OP.gcoll_elems(2))
-    S = c.S
-    p_log = logical_params(9, es[0])
-    pf0 = place_gpu(c, p_log, torch.bfloat16)
-    param_full = pf0.clone()
-    grad_full = place_gpu(c, logical_grads(9, rank, es[0]), torch.bfloat16)
-    grad_f32 = torch.zeros(world * S, dtype=torch.float32, device="cuda")
-    u = R.Unit(c, rank, param_full, grad_full, grad_f32, qblock=2048, comm=comm)
-    nb = u.num_blocks
-    master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
-    st_a = [master, torch.zeros(S, dtype=torch.int8, device="cuda"),
-            torch.zeros(S, dtype=torch.uint8, device="cuda"),
-            torch.zeros(max(nb, 1), device="cuda"), torch.zeros(max(nb, 1), device="cuda")]
-    st_b = [t.clone() for t in st_a]
-    p2p = R.P2P(comm, [param_full, grad_full])
-    R.reduce_scatter_p2p(u, p2p)
-    R.step_8bit_adam(u, *st_a, R.AdamConfig(), 1)
-    R.all_gather_p2p(u, p2p)
-    torch.cuda.synchronize()
-    pf_ref = param_full.clone()
-    param_full.copy_(pf0)
     dist.barrier()
-    for _ in range(2):  # twice: the epochs of every rank stay in step
-        R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 1, state=[t.clone() for t in st_b])
-    st_c = [t.clone() for t in st_b]
-    param_full.copy_(pf0)
-    dist.barrier()
-    R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 1, state=st_c)
-    torch.cuda.synchronize()
-    if nb == 0 and rank == 0:
-        ok = False
-        msgs.append("owner-less case: rank 0 should own the block")
-    if not torch.equal(param_full.view(torch.int16)[:es[0]], pf_ref.view(torch.int16)[:es[0]]):
-        ok = False
-        msgs.append(f"owner-less ranks: fused RS+Adam+AG differs (rank {rank}, {nb} blocks)")
-    for a_, b_ in zip(st_c, st_a):
-        if not torch.equal(a_.view(torch.uint8), b_.view(torch.uint8)):
-            ok = False
-            msgs.append(f"owner-less ranks: fused state differs (rank {rank})")
-            break
-    p2p.close()
-    del u
-    # ---- N2 tiles through the fused kernel: 32x32 quantization tiles (the
-    # paper's 8-bit Adam setup) at 32-row granularity take the fused
-    # kernel's strided peer-load path; it must equal RS -> tiled Adam -> AG
-    shapes = [(96, 64), (64, 40), (130,), (256, 96)]
-    es = [int(np.prod(sh)) for sh in shapes]
-    gs = [32 * sh[1] if len(sh) == 2 else e for sh, e in zip(shapes, es)]
-    specs = [("tile", sh[1], 32, 32) if len(sh) == 2 else ("flat", e) for sh, e in zip(shapes, es)]
-    c = R.plan(es, gs, world, elem_bytes=2)
-    o = OP.plan(es, gs, world, OP.gcoll_elems(2))
-    S = c.S
-    p_log = logical_params(11, sum(es))
-    pf0 = place_gpu(c, p_log, torch.bfloat16)
-    param_full = pf0.clone()
-    grad_full = place_gpu(c, logical_grads(11, rank, sum(es)), torch.bfloat16)
-    grad_f32 = torch.zeros(world * S, dtype=torch.float32, device="cuda")
-    u = R.Unit(c, rank, param_full, grad_full, grad_f32, comm=comm, qspec=specs)
-    nb = u.num_blocks
-    master = torch.from_numpy(OD.shard(o, OD.place_logical(o, p_log.numpy()), rank).copy()).cuda()
-    st_a = [master, torch.zeros(S, dtype=torch.int8, device="cuda"),
-            torch.zeros(S, dtype=torch.uint8, device="cuda"),
-            torch.zeros(max(nb, 1), device="cuda"), torch.zeros(max(nb, 1), device="cuda")]
-    st_b = [t.clone() for t in st_a]
-    p2p = R.P2P(comm, [param_full, grad_full])
-    R.reduce_scatter_p2p(u, p2p)
-    R.step_8bit_adam(u, *st_a, R.AdamConfig(), 2)
-    R.all_gather_p2p(u, p2p)
-    torch.cuda.synchronize()
-    pf_ref = param_full.clone()
-    param_full.copy_(pf0)
-    dist.barrier()
-    R.reduce_scatter_adam_gather_p2p(u, p2p, R.AdamConfig(), 2, state=st_b)
-    torch.cuda.synchronize()
-    mask = torch.zeros(world * S, dtype=torch.bool, device="cuda")
-    for l, e in zip(c.starts, es):
-        mask[l:l + e] = True
-    if not torch.equal(param_full.view(torch.int16)[mask], pf_ref.view(torch.int16)[mask]):
-        ok = False
-        msgs.append("tiles: fused RS+Adam+AG parameters differ from RS -> Adam -> AG")
-    for a_, b_ in zip(st_b, st_a):
-        if not torch.equal(a_.view(torch.uint8), b_.view(torch.uint8)):
-            ok = False
-            msgs.append("tiles: fused state differs from RS then tiled Adam")
-            break
-    p2p.close()
-    del u
-    # ---- N2: FP8 block quantization fused with the AllGather over NVLink
-    shapes = [(256, 384), (512, 128), (128, 200), (130, 128), (384, 64), (1024, 256)]
-    es = [r * c for r, c in shapes]
-    gs = [min(128, r) * c for r, c in shapes]
-    c = R.plan(es, gs, world, elem_bytes=1)
-    o = OP.plan(es, gs, world, OP.gcoll_elems(1))
-    specs = F.tile_specs([cc for _, cc in shapes])
-    logical = np.random.default_rng(7).normal(0, 0.02, sum(es)).astype(np.float32)
-    full = np.zeros(world * c.S, np.float32)
-    off = 0
-    for l, e in zip(c.starts, es):
-        full[l:l + e] = logical[off:off + e]
-        off += e
-    exp_codes, exp_scales = F.quantize_all_gather(o, full, specs)
-    master = torch.from_numpy(full[rank * c.S:(rank + 1) * c.S].copy()).cuda()
-    codes = torch.full((world * c.S,), 0xAB, dtype=torch.uint8, device="cuda")
-    scales = torch.full((len(exp_scales),), float("nan"), device="cuda")
-    p2p = R.P2P(comm, [codes, scales])
-    fu = R.Fp8Unit(c, specs, rank, master, codes, scales, comm=comm)
-    mask = np.zeros(world * c.S, bool)
-    for l, e in zip(c.starts, es):
-        mask[l:l + e] = True
-    for it in range(3):  # repeated calls: epochs advance, barriers re-arm
-        fu.quantize_all_gather(p2p)
-        torch.cuda.synchronize()
-        got = codes.cpu().numpy()
-        if not (np.array_equal(got[mask], exp_codes[mask]) and np.all(got[~mask] == 0xAB)
-                and np.array_equal(scales.cpu().numpy().view(np.uint32), exp_scales.view(np.uint32))):
-            ok = False
-            msgs.append(f"FP8 quantize+AllGather mismatch (call {it})")
-            break
-    fu.close()
-    p2p.close()
-    # ---- K-slot unsharded ring: shards gathered into
-    # reused slots, fused RS+Adam writing the persistent shards
-    from test_gpu_ring import ring_case
-    good, why = ring_case(world, rank, comm=comm, p2p_factory=lambda bufs: R.P2P(comm, bufs))
-    if not good:
-        ok = False
-        msgs.append("ring: " + "; ".join(why[:4]))
-    # ---- N3: distributed Muon (Algorithm 2): gather to roots, NS, scatter + apply
-    from test_gpu_muon import SHAPES as MUON_SHAPES, muon_case
-    for prec in ("f32", "bf16"):
-        good, why = muon_case(world, rank, MUON_SHAPES, 5, 2, prec, comm=comm,
-                              p2p_factory=lambda uu, ww: R.P2P(comm, [uu, ww]))
-        if not good:
-            ok = False
-            msgs.append(f"Muon {prec}: " + "; ".join(why[:4]))
-    comm.close()
-    flag = torch.tensor([0 if ok else 1])
+    flag = torch.tensor([1 if msgs else 0])
     dist.all_reduce(flag)
     if msgs:
-        print(f"[rank {rank}] " + "; ".join(msgs), flush=True)
+        print(f"[rank {rank}] " + "; ".join(msgs[:20]), flush=True)
     if rank == 0:
         print(f"dist parity world={world}: {'PASS' if flag.item() == 0 else 'FAIL'}", flush=True)
+    del keep
+    comm.close()
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 0 else 1)
 

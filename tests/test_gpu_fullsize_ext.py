@@ -24,9 +24,7 @@ from oracle import planner as OP
 from synth import hashgen as H
 from synth import workloads as W
 
-pytestmark = [pytest.mark.gpu,
-              pytest.mark.xfail(strict=False, reason="full-size harness moved from scripts/; "
-                                "first B200 run pending")]
+pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module", autouse=True)
