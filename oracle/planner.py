@@ -236,9 +236,12 @@ ORDER_DEFAULT, ORDER_BLOCK, ORDER_SHAPE, ORDER_BEST = 0, 1, 2, 3
 
 def order_perm(es, gs, ordering: int, keys=None) -> List[int]:
     """Tensor orders of P:279: (i) default; (ii) sorted by sharding block
-    size; (iii) sorted by tensor shape.  Readings (R18): descending,
+    size; (iii) sorted by tensor shape.  Reading R29: descending,
     stable; the shape order sorts by a caller-supplied shape key (identical
-    shapes become adjacent)."""
+    shapes become adjacent).  Pinned (tests/test_oracle_planner.py): the
+    buffer order read off the layout's starts is descending and stable; with
+    whole-tensor blocks S is the textbook linear-partition optimum of the
+    sorted sequence."""
     idx = list(range(len(es)))
     if ordering == ORDER_DEFAULT:
         return idx

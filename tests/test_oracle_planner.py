@@ -130,6 +130,63 @@ def test_whole_tensor_blocks_is_linear_partition():
         assert lay.S == -(-opt // gc) * gc
 
 
+# ------------------------------------------------------------- tensor orders
+def test_block_order_puts_tensors_in_descending_block_size():
+    """P:279 (ii) "sorting by sharding block size" (reading: descending,
+    stable): in the planned buffer the tensors appear in non-increasing
+    g_t, ties in input order -- read off the layout's starts, not the
+    permutation code.  Ascending order would fail this."""
+    rng = random.Random(11)
+    for _ in range(300):
+        n = rng.randint(2, 8)
+        gs = [rng.choice([1, 2, 4, 8, 16]) for _ in range(n)]
+        es = [g * rng.randint(1, 6) for g in gs]
+        m = rng.randint(1, 4)
+        lay = P.plan_ordered(es, gs, m, 2, P.ORDER_BLOCK)
+        assert P.validate(lay) == []
+        in_buffer = sorted(range(n), key=lambda i: lay.starts[i])
+        keys = [(-gs[i], i) for i in in_buffer]
+        assert keys == sorted(keys)  # descending g, stable
+        # a permutation of the input layout problem: the same multiset
+        assert sorted(lay.numel) == sorted(es)
+
+
+def test_shape_order_groups_equal_keys_descending():
+    """P:279 (iii) "sorting by tensor shape": descending shape key, stable;
+    tensors of equal shape end up adjacent in the buffer."""
+    rng = random.Random(12)
+    for _ in range(200):
+        n = rng.randint(2, 8)
+        keys = [rng.choice([3, 5, 7]) for _ in range(n)]
+        es = [k * 32 for k in keys]
+        gs = [32] * n
+        lay = P.plan_ordered(es, gs, 2, 8, P.ORDER_SHAPE, keys=keys)
+        order = sorted(range(n), key=lambda i: lay.starts[i])
+        ks = [(-keys[i], i) for i in order]
+        assert ks == sorted(ks)
+
+
+def test_block_order_whole_tensor_blocks_is_linear_partition_of_sorted_sequence():
+    """With g_t = e_t the block order is the sizes sorted descending, and the
+    planner's S must be the textbook linear-partition optimum of THAT
+    sequence (rounded to g_coll) -- generally different from the optimum
+    of the input order, which is asserted to happen."""
+    rng = random.Random(13)
+    differs = 0
+    for _ in range(300):
+        n = rng.randint(2, 8)
+        es = [rng.randint(1, 200) for _ in range(n)]
+        m = rng.randint(2, 5)
+        gc = rng.choice([1, 2, 4])
+        lay = P.plan_ordered(es, es, m, gc, P.ORDER_BLOCK)
+        srt = sorted(es, reverse=True)
+        assert lay.S == -(-_painter(srt, m) // gc) * gc
+        differs += _painter(srt, m) != _painter(es, m)
+        best = P.plan_ordered(es, es, m, gc, P.ORDER_BEST)
+        assert best.S == min(lay.S, P.plan(es, es, m, gc).S)
+    assert differs > 0
+
+
 # ------------------------------------------------------------- brute force
 def _rand_instance(rng):
     n = rng.randint(1, 6)
