@@ -29,12 +29,15 @@ init, P:491, reported as plan_ms):
   --collectives nccl: ncclAllGather; cast kernel + ncclReduceScatter (fp32) per
       unit; one a8 launch over every shard.
 
-value = whole-job algorithmic GB/s of the step, with the workload's bytes fixed
-        by SURVEY §8(d) independent of the implementation = sum over ranks of
-        [AG (m-1) S 2 + RS (m-1) S 4 + cast m S 6 + Adam 18 per owned element
-        + 16 per block] (summed over units) / max-rank step time.  The fused
-        path moves fewer physical bytes for the same work; per_op and
-        roofline report physical rates.
+value = BJ's metric as named, from PHYSICAL bytes / max-rank step time:
+        N = 1: "8-bit Adam shard HBM GB/s" -- the HBM bytes the step moves
+               (fused kernel: 16 B per owned element + 16 B per block);
+        N > 1: "AG+RS bus GB/s" -- the NVLink bytes every rank receives for
+               the unit AllGathers and ReduceScatters, summed over ranks.
+        value_composite_gbs keeps SURVEY §8(d)'s unfused work-normalised
+        accounting (24 B per element at N = 1), which is not a physical rate.
+extras = scripts/bench_extras.py (configs 3-5, N2 rows, per-unit bus GB/s,
+        ZeRO-3 overlap); --no-extras skips them.
 """
 from __future__ import annotations
 
@@ -67,6 +70,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: max(3, steps // 10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the extra measurements (configs 3-5, tiles, dynamic codec, "
+                         "per-unit collectives, ZeRO-3 overlap; scripts/bench_extras.py)")
+    ap.add_argument("--extras", default="",
+                    help="comma-separated subset of the extras to run (default: all)")
     ap.add_argument("--no-fuse-adam", action="store_true",
                     help="p2p path: separate ReduceScatter kernel + one 8-bit Adam launch instead "
                          "of the fused ReduceScatter+Adam kernel")
@@ -100,6 +108,8 @@ def load_peaks():
 
 
 NVLINK_PEAK_GBS = 770.0  # measured per-direction peer bandwidth, B200_PROFILING.md
+NVLINK_SPEC_GBS = 900.0  # NVLink 5 per direction per GPU (nominal)
+HBM_SPEC_GBS = 8000.0    # B200 HBM3e (nominal)
 
 
 # ---------------------------------------------------------------- clocks
@@ -383,12 +393,13 @@ def profile_traffic(kernel):
 _ORACLE_INPUTS = {}
 
 
-def oracle_sample_step(world, n_blocks, seed=0):
+def oracle_sample_step(world, n_blocks, seed=0, phases=None):
     """The oracle (as it stands) on a bounded sample of the workload: a slice
     of n_blocks 2048-element blocks of the layer unit, planned for `world`
     simulated ranks; AG, cast/scale, RS and 8-bit Adam for EVERY rank.
     Inputs are generated once per (world, n_blocks) outside the timing.
-    Returns (seconds, whole-job algorithmic bytes, elements)."""
+    Returns (seconds, whole-job algorithmic bytes, elements); `phases`, if a
+    dict, receives the seconds of each op."""
     import numpy as np
 
     from oracle import adam8 as OA
@@ -410,28 +421,88 @@ def oracle_sample_step(world, n_blocks, seed=0):
     E, S = o.E, o.S
     t0 = time.perf_counter()
     OD.all_gather([OD.shard(o, params16, k) for k in range(world)])
+    t1 = time.perf_counter()
     xs = [OD.grouped_cast_scale(o, g, True) for g in grads]
+    t2 = time.perf_counter()
     ys = OD.reduce_scatter(o, xs)
+    t3 = time.perf_counter()
     for r in range(world):
         blocks = OP.rank_blocks(o, r, QBLOCK)
         nb = len(blocks)
         OA.step_8bit_adam(OD.shard(o, master, r), ys[r], np.zeros(S, np.int8),
                           np.zeros(S, np.uint8), np.zeros(nb, np.float32),
                           np.zeros(nb, np.float32), blocks, OA.AdamCfg(), 1)
-    dt = time.perf_counter() - t0
-    nbytes = world * ((world - 1) * S * 2 + (world - 1) * S * 4 + world * S * 6) + 18 * E + 16 * n_blocks
-    return dt, nbytes, E
+    t4 = time.perf_counter()
+    if phases is not None:
+        phases.update({"ag_s": t1 - t0, "cast_s": t2 - t1, "rs_s": t3 - t2, "adam_s": t4 - t3})
+    dt = t4 - t0
+    return dt, metric_bytes(world, S, E, n_blocks), E
 
 
-def cpu_baseline(world, target_s=10.0):
+def metric_bytes(world, S, E, n_blocks):
+    """Bytes the line's `value` counts for one step of work (run_ours's value
+    definition, so both arms report the same metric for the same work):
+    world 1 -- the fused step's HBM bytes, 16 B per element + 16 B per block;
+    world m > 1 -- every rank's AG + RS wire bytes, m * 2 (m-1) S 2."""
+    if world == 1:
+        return 16 * E + 16 * n_blocks
+    return world * 2 * (world - 1) * S * 2
+
+
+def _mp_worker(args):
+    world, n_blocks, seed = args
+    dt, nb, E = oracle_sample_step(world, n_blocks, seed)  # inputs (untimed), then warm
+    t0 = time.perf_counter()
+    dt, nb, E = oracle_sample_step(world, n_blocks, seed)
+    return t0, time.perf_counter(), nb, E
+
+
+def cpu_baseline(world, target_s=10.0, procs=8):
+    """The oracle on the host cores (SURVEY §8(d) 'oracle beside it'):
+    one process, numpy single thread, on a calibrated sample of the layer
+    unit; per-op seconds of that sample; the oracle planner's time per unit
+    (the two unit kinds of the workload); and a multi-process variant
+    (`procs` worker processes, one core each, every worker running the same
+    single-process oracle step on its own slice of the workload)."""
+    import multiprocessing as mp
+
+    from oracle import planner as OP
     dt, nb, E = oracle_sample_step(world, 256)
     blocks = max(256, int(256 * target_s / max(dt, 1e-3)))
     blocks = min(blocks, 1 << 16)
-    dt, nb, E = oracle_sample_step(world, blocks)
+    ph = {}
+    dt, nb, E = oracle_sample_step(world, blocks, phases=ph)
+    _ORACLE_INPUTS.clear()
+    # planner per unit (one-time, host): the oracle's Algorithm 1
+    plan_s = {}
+    for name, u in (("layer", build_units(1)[1]), ("root", build_units(1)[0])):
+        es = [t.numel for t in u.tensors]
+        gs = [min(QBLOCK, e) for e in es]
+        t0 = time.perf_counter()
+        OP.plan(es, gs, world, OP.gcoll_elems(2))
+        plan_s[name] = time.perf_counter() - t0
+    # multi-process: `procs` workers, each 1/procs of the sample
+    mp_res = None
+    try:
+        per = max(16, blocks // procs)
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            rs = pool.map(_mp_worker, [(world, per, 100 + i) for i in range(procs)])
+        t_beg, t_end = min(r[0] for r in rs), max(r[1] for r in rs)
+        mp_bytes = sum(r[2] for r in rs)
+        mp_res = {"value": mp_bytes / (t_end - t_beg) / 1e9, "unit": UNIT, "cores": procs,
+                  "sample": f"{procs} processes x {per} blocks (2048 elem) each, the same "
+                            f"single-process oracle step per worker, {t_end - t_beg:.1f} s wall"}
+    except Exception as e:  # recorded, not hidden
+        mp_res = {"error": f"{type(e).__name__}: {e}"}
     return {"value": nb / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{E} params ({blocks} x 2048-elem blocks of the layer unit), "
                       f"{world} simulated rank(s), AG+cast+RS+8-bit Adam, numpy single thread, "
-                      f"{dt:.1f} s", "host": host_info()}
+                      f"{dt:.1f} s", "host": host_info(),
+            "per_op_s": ph, "per_op_gbs": {
+                "adam": (18 * E + 16 * blocks) / ph["adam_s"] / 1e9,
+                "cast": world * world * (E // world) * 6 / ph["cast_s"] / 1e9},
+            "planner_s_per_unit": plan_s, "multiprocess": mp_res}
 
 
 def host_info():
@@ -620,12 +691,52 @@ def run_ours(args):
                 "bytes": "physical wire bytes into each rank per launch",
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
     roof["share_of_step"] = shares[dom] / max(1e-9, ms_local)
-    value = job_bytes / (ms / K * 1e-3) / 1e9
+    spec = HBM_SPEC_GBS if roof["bound"] == "hbm" else NVLINK_SPEC_GBS
+    roof["frac_vs_spec"] = roof["achieved"] / spec
+    roof["spec_peak"] = spec
+    # value = BJ's metric as named, physical bytes only (never above the peaks):
+    #   N = 1: 8-bit Adam shard HBM GB/s -- the HBM bytes the step's kernels
+    #          move (fused: 16 B per owned element + 16 B per block; unfused:
+    #          cast m S 6 + Adam 18 B per element + 16 B per block), summed
+    #          over ranks, / step time;
+    #   N > 1: AG+RS bus GB/s -- the bytes each rank receives over NVLink for
+    #          the unit collectives (AG (m-1) S 2; RS (m-1) S 2 on the fused
+    #          p2p path (bf16 wire), (m-1) S 4 for NCCL's fp32 RS), summed over
+    #          ranks, / step time.
+    if fuse:
+        hbm_rank = fused_hbm
+    else:
+        hbm_rank = ab["cast"] + ab["adam"]
+    wire_rank = wire_ag + wire_rs
+    if world == 1:
+        value_bytes = sum_over_ranks(hbm_rank, world)
+        value_def = ("8-bit Adam shard HBM GB/s (whole job): physical HBM bytes of the step "
+                     "(fused: 16 B/owned elem + 16 B/block) / step time")
+    else:
+        value_bytes = sum_over_ranks(wire_rank, world)
+        value_def = ("AG+RS bus GB/s (whole job, sum over ranks): NVLink bytes into each rank "
+                     "for the unit AllGathers and ReduceScatters / step time")
+    value = value_bytes / (ms / K * 1e-3) / 1e9
+    composite = job_bytes / (ms / K * 1e-3) / 1e9
+    hbm_job = sum_over_ranks(hbm_rank, world) / (ms / K * 1e-3) / 1e9
+    bus_job = sum_over_ranks(wire_rank, world) / (ms / K * 1e-3) / 1e9 if world > 1 else None
 
     # ---------------- e2e: host buffers through the C-ABI, copies inside
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p, fuse)
+        e2e = run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, value_bytes, p2p, fuse)
+    # ---------------- extras (scripts/bench_extras.py): configs 3-5, N2 rows, per-unit bus
+    extras = None
+    if not args.no_extras:
+        import importlib.util
+        spec_ = importlib.util.spec_from_file_location(
+            "bench_extras", os.path.join(ROOT, "scripts", "bench_extras.py"))
+        BX = importlib.util.module_from_spec(spec_)
+        spec_.loader.exec_module(BX)
+        ctx = {"rank": rank, "world": world, "comm": comm, "stream": stream, "db": db,
+               "lays": lays, "cfg": cfg, "t": t + 1000, "p2p": p2p, "reps": 10}
+        which = set(x for x in args.extras.split(",") if x) or None
+        extras = BX.run_all(R, ctx, which)
     # ---------------- CPU baseline (oracle) on rank 0
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -651,6 +762,13 @@ def run_ours(args):
                        "l2": f"no flush: per-step working set {sum(sizes) / 2 ** 30:.1f} GiB "
                              f"per rank >> L2 ({L2_BYTES >> 20} MiB)",
                        "plan_ms": plan_ms},
+            "value_definition": value_def,
+            "value_composite_gbs": composite,
+            "value_composite_definition": "SURVEY §8(d) unfused algorithmic bytes (AG (m-1)S2 + "
+                                          "RS (m-1)S4 + cast mS6 + Adam 18/elem + 16/block) / step "
+                                          "time: work-normalised, NOT a physical rate (the fused "
+                                          "kernel moves fewer bytes)",
+            "hbm_gbs_job": hbm_job, "ag_rs_bus_gbs_job": bus_job,
             "step_ms": step_dist,
             "per_op": {"adam_hbm_gbs": adam_gbs, "adam_ms_per_launch": adam_ms,
                        "cast_hbm_gbs": cast_gbs, "cast_ms_per_step": cast_ms,
@@ -668,6 +786,7 @@ def run_ours(args):
             "nccl_calls": 0 if p2p is not None else cnt["ag"] + cnt["rs"],
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "extras": extras,
         }
         print(json.dumps(line), flush=True)
     if p2p is not None:
@@ -680,10 +799,13 @@ def run_ours(args):
 
 
 def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2p=None, fuse=False):
-    """Same step, through the public C-ABI calls, with the step's inputs (this
-    rank's bf16 gradient buffers) copied host->device from pinned memory and
-    the step's result (the updated bf16 parameter shards) copied back, every
-    step, inside the timed region."""
+    """Same metric (job_bytes per step), end to end through the public C-ABI
+    with HOST buffers: every step copies this rank's bf16 gradient buffers in
+    from pinned host memory and the updated bf16 parameter shards back out,
+    inside the timed region.  Fused p2p paths: ONE library call per step,
+    rsdb_dbuffer_step_host, which pipelines per unit (H2D copy stream | fused
+    kernel | D2H copy stream) inside the library; other paths: the copies and
+    the step's calls serially on one stream."""
     import torch
     K = args.e2e_steps or max(3, args.steps // 10)
     host_g, host_p = [], []
@@ -721,47 +843,15 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2
         for v, h, lay in zip(views, host_p, lays):
             h.copy_(v["param_full"][rank * lay.S:(rank + 1) * lay.S], non_blocking=True)
 
-    # pipelined schedule (fused p2p paths): per unit, in backward order, the
-    # H2D copy of its gradients (copy stream), its fused kernel (compute
-    # stream) and the D2H copy of its updated shard (second copy stream), so
-    # the two PCIe directions and the kernels overlap.  Cross-step hazards are
-    # ordered with events: a unit's gradients are overwritten only after its
-    # previous kernel, its shard only after its previous D2H.
     pipelined = p2p is not None and fuse in (True, "unit+ag", "dbuffer", "dbuffer+ag")
-    n = len(db.units)
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(n)]
-    ev_k = [None] * n
-    ev_out = [None] * n
 
-    def e2e_step_pipelined(tt):
-        for i in reversed(range(n)):
-            u, v = db.units[i], views[i]
-            with torch.cuda.stream(s_in):
-                if ev_k[i] is not None:
-                    s_in.wait_event(ev_k[i])
-                v["grad_full"].copy_(host_g[i], non_blocking=True)
-                ev_in[i].record(s_in)
-            stream.wait_event(ev_in[i])
-            if ev_out[i] is not None:
-                stream.wait_event(ev_out[i])
-            if world > 1:
-                R.reduce_scatter_adam_gather_p2p(u, p2p, cfg, tt, stream=stream)
-            else:
-                R.reduce_scatter_adam_p2p(u, None, cfg, tt, stream=stream)
-            ev_k[i] = torch.cuda.Event()
-            ev_k[i].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_k[i])
-                lay = lays[i]
-                host_p[i].copy_(v["param_full"][rank * lay.S:(rank + 1) * lay.S], non_blocking=True)
-                ev_out[i] = torch.cuda.Event()
-                ev_out[i].record(s_out)
+    def e2e_step_host(tt):  # the library's host-buffer entry point
+        db.step_host(cfg, tt, host_g, host_p, p2p if world > 1 else None, stream)
 
     if pipelined:
         for u in db.units:  # the first step's AllGather (the kernels push the following ones)
             R.all_gather_p2p(u, p2p, stream)
-    run = e2e_step_pipelined if pipelined else e2e_step
+    run = e2e_step_host if pipelined else e2e_step
     with torch.cuda.stream(stream):
         run(t)
         t += 1
@@ -770,24 +860,19 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    s_in.wait_event(ev0)
-    s_out.wait_event(ev0)
     with torch.cuda.stream(stream):
         for _ in range(K):
             run(t)
             t += 1
-    end_in, end_out = torch.cuda.Event(), torch.cuda.Event()
-    end_in.record(s_in)
-    end_out.record(s_out)
-    stream.wait_event(end_in)
-    stream.wait_event(end_out)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     return {"value": job_bytes / (ms / K * 1e-3) / 1e9, "unit": UNIT, "steps": K,
             "ms_per_step": ms / K, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "schedule": ("per-unit pipeline: H2D copy stream | fused kernel | D2H copy stream"
-                         if pipelined else "serial on one stream")}
+            "api": "rsdb_dbuffer_step_host (host buffers through the C-ABI)" if pipelined
+                   else "rsdb_* device calls + torch pinned copies",
+            "schedule": ("per-unit pipeline inside the library: H2D copy stream | fused kernel | "
+                         "D2H copy stream" if pipelined else "serial on one stream")}
 
 
 def main():

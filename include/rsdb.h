@@ -209,7 +209,9 @@ typedef struct rsdb_unit rsdb_unit;
  * group op and optimizer still usable -- used by single-GPU tests), the rank
  * this process holds, buffers (16-byte aligned: EMISMATCH otherwise) and the
  * 8-bit Adam block size qblock (block table via rsdb_layout_rank_blocks;
- * EMISMATCH if a block would straddle).  The layout is copied. */
+ * EMISMATCH if a block would straddle; qblock = 0: a collectives-only unit
+ * with no optimizer block table -- the 8-bit Adam calls then have nothing to
+ * update).  EINVAL if qblock < 0.  The layout is copied. */
 rsdb_status rsdb_unit_create(const rsdb_layout*, rsdb_comm* comm_or_null, int32_t rank,
                              const rsdb_unit_bufs* bufs, int64_t qblock, rsdb_unit** out);
 /* The same with per-tensor quantization specs (2-D tiles, N2): specs[n]. */
@@ -310,6 +312,16 @@ rsdb_status rsdb_p2p_set_timeout(rsdb_p2p*, double seconds);
 /* Synchronises the device, reads and clears this rank's error flag into
  * *flags (0 = every barrier completed); ECUDA if a barrier timed out. */
 rsdb_status rsdb_p2p_check(rsdb_p2p*, int64_t* flags);
+/* An independent collective channel over p's mappings, for collectives that
+ * run concurrently on different streams (e.g. an AllGather prefetched on a
+ * copy stream while the compute stream runs a ReduceScatter, "optimized
+ * communication overlapping").  Same buffers and peers, its own epoch and its
+ * own signal words: channel c uses bytes [256c, 256c + 256) of every rank's
+ * signal buffer, so c in [1, RSDB_P2P_SIGNAL_BYTES / 256).  Within a channel
+ * the SPMD rule holds (same calls in the same order on every rank); two calls
+ * on different channels may overlap.  The channel borrows p's mappings: free
+ * it before p.  EINVAL (null, c out of range, p itself a channel). */
+rsdb_status rsdb_p2p_channel(const rsdb_p2p* p, int32_t channel, rsdb_p2p** out);
 void rsdb_p2p_free(rsdb_p2p*);
 /* The unit's grad_full (bf16 units) / param_full must lie inside one of the
  * registered buffers at the same offset on every rank (true for DBuffer
@@ -401,6 +413,31 @@ rsdb_status rsdb_dbuffer_reduce_scatter_adam_gather(rsdb_dbuffer*, rsdb_p2p* p2p
  * (fp32, ties to the lower code). */
 rsdb_status rsdb_dbuffer_step_8bit_adam_dynamic(rsdb_dbuffer*, const rsdb_adam_cfg*, int64_t step,
                                                 void* stream);
+/* End-to-end step from HOST memory (the path a user without device-resident
+ * gradients takes; P:93-94's Copy-In/RS/Adam/Copy-Out chain with the copies
+ * pipelined).  For every unit in FSDP backward order (last unit first, the
+ * same order on every rank):
+ *   1. H2D: host_grads[u] -> the unit's GRAD_FULL (bf16, m*S elements, in the
+ *      planned layout: padding included) on a library-owned copy stream;
+ *   2. the fused ReduceScatter + 8-bit Adam kernel of the unit on `stream`
+ *      (rsdb_reduce_scatter_adam_gather_p2p at world > 1, so every rank's
+ *      gathered buffer receives the update; rsdb_reduce_scatter_adam_p2p at
+ *      world 1), with the unit's DBuffer-bound optimizer state;
+ *   3. D2H: this rank's updated bf16 shard (S elements at param_full + rank*S)
+ *      -> host_shards[u] on a second library-owned copy stream.
+ * Unit u's copy-in overlaps unit u+1's kernel and copy-out.  Ordering across
+ * calls is kept with per-unit events (a unit's gradients are overwritten only
+ * after its previous kernel, its shard only after its previous copy-out).
+ * Stream-ordered: the copies start after the work already on `stream`, and
+ * `stream` reaches the end of the call only when every copy is done, so a
+ * cudaStreamSynchronize(stream) makes host_shards valid.
+ *   host_grads[n_units], host_shards[n_units]: host pointers, caller-owned;
+ *     pinned (cudaHostAlloc / torch pin_memory) for asynchronous copies.
+ *   p2p_or_null: required at world > 1 (maps GRAD_FULL and PARAM_FULL).
+ * Errors: EINVAL (null pointer, step < 1), EMISMATCH (f32 units), ECUDA. */
+rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer*, rsdb_p2p* p2p_or_null, const rsdb_adam_cfg*,
+                                   int64_t step, const void* const* host_grads, void* const* host_shards,
+                                   void* stream);
 /* Grouped zero of every unit's gradient buffer ("zero"). */
 rsdb_status rsdb_dbuffer_zero_grads(rsdb_dbuffer*, void* stream);
 void rsdb_dbuffer_free(rsdb_dbuffer*);
@@ -498,6 +535,20 @@ rsdb_status rsdb_muon_bind(rsdb_muon*, const rsdb_muon_bufs*);
  * must map every rank's `u` and `workspace`. */
 rsdb_status rsdb_muon_step(rsdb_muon*, rsdb_p2p* p2p_or_null, const rsdb_muon_cfg*, void* stream);
 void rsdb_muon_free(rsdb_muon*);
+/* The Newton-Schulz GEMM of the bf16 mode (Alg. 2 l.10, reading R22), a
+ * hand-written tcgen05 kernel (TMA 128-B swizzled tiles -> tcgen05.mma, fp32
+ * accumulators in TMEM, fused epilogue):
+ *   C = alpha * A . B^T + beta * D     (and, if CT != NULL, CT = C^T)
+ * A: M x K, B: N x K, D / C: M x N, CT: N x M -- all row-major bf16 device
+ * matrices with leading dimensions (elements) lda, ldb, ldd, ldc, ldct that
+ * are multiples of 8 and 16-B aligned base pointers (D unused when beta = 0).
+ * fp32 accumulation, one bf16 rounding of alpha*acc + beta*D.  C must not
+ * overlap A, B or D.  rsdb_muon_step's bf16 mode issues three per iteration
+ * (A = W W^T; B = cA A + bA; W' = B W + aW with W'^T).  EINVAL on bad
+ * dimensions / alignment, ECUDA on launch errors. */
+rsdb_status rsdb_ns_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, const void* B,
+                              int64_t ldb, float alpha, float beta, const void* D, int64_t ldd, void* C,
+                              int64_t ldc, void* CT, int64_t ldct, void* stream);
 
 /* ======================================================================== */
 /* K-slot unsharded ring: only K units' gathered         */

@@ -443,6 +443,20 @@ class P2P:
             out.append(self)
         return out
 
+    def channel(self, c: int) -> "P2P":
+        """rsdb_p2p_channel: an independent collective channel (own epoch and
+        signal words) over the same mappings, for collectives that overlap on
+        different streams.  Close it before this object."""
+        h = C.c_void_p()
+        check(lib.rsdb_p2p_channel(self._h, int(c), C.byref(h)))
+        ch = P2P.__new__(P2P)
+        ch._h = h
+        ch.comm = self.comm
+        ch.signal = self.signal
+        ch.bufs = self.bufs
+        ch.parent = self
+        return ch
+
     def set_timeout(self, seconds: float) -> None:
         check(lib.rsdb_p2p_set_timeout(self._h, float(seconds)))
 
@@ -584,6 +598,19 @@ class DBuffer:
     def step_8bit_adam_dynamic(self, cfg: AdamConfig, step: int, stream=None) -> None:
         """One launch of 8-bit Adam with the dynamic code map over every unit."""
         check(lib.rsdb_dbuffer_step_8bit_adam_dynamic(self._h, C.byref(cfg), step, _stream(stream)))
+
+    def step_host(self, cfg: AdamConfig, step: int, host_grads, host_shards,
+                  p2p: Optional["P2P"] = None, stream=None) -> None:
+        """rsdb_dbuffer_step_host: per unit (backward order) H2D of host_grads[u]
+        (pinned host tensor, m*S bf16), the fused RS + 8-bit Adam (+ AllGather
+        push) kernel, D2H of the rank's updated bf16 shard into host_shards[u]."""
+        n = len(self.units)
+        if len(host_grads) != n or len(host_shards) != n:
+            raise ValueError("one host gradient and one host shard buffer per unit")
+        g = (C.c_void_p * n)(*[_ptr(t) for t in host_grads])
+        s = (C.c_void_p * n)(*[_ptr(t) for t in host_shards])
+        check(lib.rsdb_dbuffer_step_host(self._h, p2p.handle if p2p is not None else None,
+                                         C.byref(cfg), step, g, s, _stream(stream)))
 
     def zero_grads(self, stream=None) -> None:
         check(lib.rsdb_dbuffer_zero_grads(self._h, _stream(stream)))
@@ -734,6 +761,18 @@ class Muon:
 
 
 # ---------------------------------------------------------------- K-slot unsharded ring
+def ns_gemm_bf16(A, B, C, alpha=1.0, beta=0.0, D=None, CT=None, stream=None) -> None:
+    """rsdb_ns_gemm_bf16: C = alpha A B^T + beta D (and CT = C^T), bf16 2-D
+    torch tensors, row-major with unit column stride (the tcgen05 Newton-Schulz
+    GEMM of Muon's bf16 mode)."""
+    M, K = A.shape
+    N = B.shape[0]
+    check(lib.rsdb_ns_gemm_bf16(M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), float(alpha),
+                                float(beta), _ptr(D), D.stride(0) if D is not None else 0, _ptr(C),
+                                C.stride(0), _ptr(CT), CT.stride(0) if CT is not None else 0,
+                                _stream(stream)))
+
+
 def all_gather_shards_p2p(unit: Unit, p2p: Optional["P2P"] = None, stream=None) -> None:
     """AllGather of every rank's persistent shard into the unit's param_full."""
     check(lib.rsdb_all_gather_shards_p2p(unit.handle, p2p.handle if p2p is not None else None,

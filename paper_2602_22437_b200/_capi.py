@@ -101,6 +101,7 @@ _SIGS = {
     "rsdb_ipc_handle": (i32, [vp, C.c_char_p]),
     "rsdb_p2p_create": (i32, [vp, i32, C.POINTER(vp), P_i64, C.c_char_p, C.POINTER(vp)]),
     "rsdb_p2p_free": (None, [vp]),
+    "rsdb_p2p_channel": (i32, [vp, i32, C.POINTER(vp)]),
     "rsdb_p2p_create_local": (i32, [vp, i32, C.POINTER(vp), P_i64, C.POINTER(vp)]),
     "rsdb_p2p_set_timeout": (i32, [vp, C.c_double]),
     "rsdb_p2p_check": (i32, [vp, P_i64]),
@@ -120,6 +121,7 @@ _SIGS = {
     "rsdb_step_8bit_adam_dynamic": (i32, [vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dynamic_code_maps": (i32, [C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "rsdb_dbuffer_zero_grads": (i32, [vp, vp]),
+    "rsdb_dbuffer_step_host": (i32, [vp, vp, C.POINTER(AdamCfg), i64, C.POINTER(vp), C.POINTER(vp), vp]),
     "rsdb_dbuffer_reduce_scatter_adam": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_reduce_scatter_adam_gather": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dbuffer_free": (None, [vp]),
@@ -139,6 +141,7 @@ _SIGS = {
     "rsdb_muon_bind": (i32, [vp, C.POINTER(MuonBufs)]),
     "rsdb_muon_step": (i32, [vp, vp, C.POINTER(MuonCfg), vp]),
     "rsdb_muon_free": (None, [vp]),
+    "rsdb_ns_gemm_bf16": (i32, [i32, i32, i32, vp, i64, vp, i64, C.c_float, C.c_float, vp, i64, vp, i64, vp, i64, vp]),
     "rsdb_unit_set_shard": (i32, [vp, vp]),
     "rsdb_unit_rebind": (i32, [vp, C.POINTER(UnitBufs)]),
     "rsdb_all_gather_shards_p2p": (i32, [vp, vp, vp]),

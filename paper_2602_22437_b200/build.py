@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "librsdb.so")
-SOURCES = ["planner.cc", "capi.cc", "capi_ext.cc", "kernels.cu", "p2p.cu", "fp8.cu", "muon.cu", "adam_dyn.cu"]
+SOURCES = ["planner.cc", "capi.cc", "capi_ext.cc", "kernels.cu", "p2p.cu", "fp8.cu", "muon.cu", "adam_dyn.cu", "ns_umma.cu"]
 HEADERS = ["planner.hpp", "capi_internal.hpp", "kernels.cuh", "adam_dev.cuh", "p2p_dev.cuh", "devmath.cuh"]
 
 

@@ -3,15 +3,20 @@
 //
 // The two 256-entry maps (signed for m, unsigned for v) are built on the host
 // in double exactly as R25 writes them, rounded once to float and kept in
-// __constant__ memory together with bucket tables; every CTA copies them to
-// shared memory.  Per block: dequantise (map[code] * A), the same fp32 AdamW
-// update as the linear kernels (adam_elem), block absmax, then requantise
-// each moment to the nearest map value of y = fl(m / A) -- the oracle's
-// decision in the oracle's precision: hi = first code with map[hi] >= y,
-// code = hi if fl(map[hi] - y) < fl(y - map[hi-1]) else hi - 1.  hi is found
-// without a binary search: a 1792-entry table indexed by the exponent and 6
-// mantissa bits of |y| (one bucket spans <= 1.6 % in value, <= 2 map values)
-// gives a lower bound, corrected by a short forward scan.  Full contiguous
+// __constant__ memory; every CTA copies them to shared memory REPLICATED PER
+// LANE (map[k] at word k * 32 + lane), so the data-dependent lookups of a warp
+// never conflict on a bank (the round-1 kernel, with one copy and a bucket
+// table, was bound by 3-4-way conflicted lookups at 0.39 of HBM).  Per block:
+// dequantise (map[code] * A), the same fp32 AdamW update as the linear
+// kernels (adam_elem), block absmax, then requantise each moment to the
+// nearest map value of y = fl(m / A) -- the oracle's decision in the oracle's
+// precision: hi = first code with map[hi] >= y (clamped to [1, 255]), code =
+// hi if fl(map[hi] - y) < fl(y - map[hi-1]) else hi - 1.  hi is found from
+// the map's closed form (R25: decade i holds 2^i (signed) / 2^(i+1)
+// (unsigned) equally spaced values of [0.1 D_i, D_i]): decade by six fp32
+// comparisons, index inside the decade by one multiply-add, then two
+// correcting scans on the exact fp32 map values (normally zero steps), so
+// the decision is the table's, not the approximation's.  Full contiguous
 // 2048-element blocks use 16-B vector loads (4 elements per thread per quad);
 // other blocks a masked element path; blocks > 2048 elements two passes.
 #include <cuda_bf16.h>
@@ -26,21 +31,11 @@
 namespace rsdb {
 
 constexpr int DYN_NT = 256;
-constexpr int DYN_E0 = 100;                        // |y| < 2^(100-127) share bucket 0
-constexpr int DYN_NB = (127 - DYN_E0 + 1) * 64;    // buckets: exponents E0..127 x 6 mantissa bits
 
 struct DynTables {
-  float map[2][256];              // [0] signed (first moment), [1] unsigned (second)
-  uint8_t lb[3][DYN_NB];          // lower bounds of hi: [0] signed y>0, [1] signed y<0, [2] unsigned
+  float map[2][256];  // [0] signed (first moment), [1] unsigned (second)
 };
 __constant__ DynTables c_dyn;
-
-__host__ __device__ inline int dyn_bucket(float a) {  // a = |y| >= 0
-  uint32_t bits;
-  memcpy(&bits, &a, 4);
-  const int k = int(bits >> 17) - (DYN_E0 << 6);
-  return k < 0 ? 0 : (k >= DYN_NB ? DYN_NB - 1 : k);
-}
 
 // R25: values +-D_i * (0.1 + (j + 0.5) * (0.9 / (n - 1))), D_i = 1e-6 .. 1e0,
 // n = 2^i + 1 (signed) or 2^(i+1) + 1 (unsigned); plus 0 and 1; ascending
@@ -68,64 +63,79 @@ void dyn_maps(float m_map[256], float v_map[256]) {
   build_dyn_map(false, v_map);
 }
 
-// lower bound of "first index with map >= y" over every y in bucket b of sign s
-static void build_lb(const float* map, bool negative, uint8_t* lb) {
-  for (int b = 0; b < DYN_NB; ++b) {
-    // bucket b holds |y| in [lo, hi): lo = float with bits (b + E0*64) << 17
-    uint32_t lo_bits = uint32_t(b + (DYN_E0 << 6)) << 17, hi_bits = lo_bits + (1u << 17);
-    float lo, hi;
-    memcpy(&lo, &lo_bits, 4);
-    memcpy(&hi, &hi_bits, 4);
-    if (b == 0) lo = 0.f;
-    const float ymin = negative ? -hi : lo;  // smallest y of the bucket
-    int k = 0;
-    while (k < 255 && map[k] < ymin) ++k;
-    lb[b] = uint8_t(k);
-  }
-}
-
 static cudaError_t ensure_dyn_tables() {
   static bool done = false;
   if (done) return cudaSuccess;
   static DynTables h;
   dyn_maps(h.map[0], h.map[1]);
-  build_lb(h.map[0], false, h.lb[0]);
-  build_lb(h.map[0], true, h.lb[1]);
-  build_lb(h.map[1], false, h.lb[2]);
   const cudaError_t e = cudaMemcpyToSymbol(c_dyn, &h, sizeof h);
   if (e == cudaSuccess) done = true;
   return e;
 }
 
-// nearest map value of y (R25): hi from the bucket bound + forward scan
-__device__ __forceinline__ uint32_t dyn_code(const float* map, const uint8_t* lb_pos, const uint8_t* lb_neg,
-                                             float y) {
-  int hi = (y < 0.f ? lb_neg : lb_pos)[dyn_bucket(fabsf(y))];
-  while (hi < 255 && map[hi] < y) ++hi;
-  hi = hi < 1 ? 1 : hi;
-  const float d_hi = __fsub_rn(map[hi], y);
-  const float d_lo = __fsub_rn(y, map[hi - 1]);
-  return uint32_t(d_hi < d_lo ? hi : hi - 1);
+// lane-replicated map: entry k of this lane's copy
+__device__ __forceinline__ float rmap(const float* rep, int k, int lane) { return rep[(k << 5) | lane]; }
+
+// candidate position of a = |y| <= 1 among the map's positive decade values
+// (R25 closed form): first index of decade i is base + 2^(i+w) - 1 with w = 0
+// (signed: the 127 positive values start at 128) or 1 (unsigned: start at 1)
+template <bool SIGNED>
+__device__ __forceinline__ int dyn_candidate(float a) {
+  constexpr int W = SIGNED ? 0 : 1;
+  const int i = int(a >= 1e-6f) + int(a >= 1e-5f) + int(a >= 1e-4f) + int(a >= 1e-3f) + int(a >= 1e-2f) +
+                int(a >= 1e-1f);
+  const float Dinv = i == 0 ? 1e6f : i == 1 ? 1e5f : i == 2 ? 1e4f : i == 3 ? 1e3f : i == 4 ? 1e2f
+                   : i == 5 ? 1e1f : 1.f;
+  const int cnt = 1 << (i + W);
+  const float t = fmaf(a, Dinv, -0.1f) * (float(cnt) * (1.f / 0.9f)) - 0.5f;
+  int j = __float2int_rn(t);
+  j = j < 0 ? 0 : (j >= cnt ? cnt - 1 : j);
+  return (SIGNED ? 127 : 0) + cnt + j;  // signed: 127 + 2^i + j ; unsigned: 2^(i+1) - 1 + j + 1
+}
+
+// nearest map value of y (R25, the oracle's fp32 rule; ties -> lower code)
+template <bool SIGNED>
+__device__ __forceinline__ uint32_t dyn_code(const float* rep, int lane, float y) {
+  int k;
+  if (SIGNED) {
+    const int p = dyn_candidate<true>(fabsf(y));
+    k = y < 0.f ? 254 - p + 1 : p;  // -map[p] sits at 254 - p; hi is the index after it
+  } else {
+    k = dyn_candidate<false>(y);
+  }
+  k = k < 1 ? 1 : (k > 255 ? 255 : k);
+  float hi = rmap(rep, k, lane), lo = rmap(rep, k - 1, lane);
+  while (hi < y && k < 255) {  // exact: hi = first index with map[hi] >= y, clamped
+    ++k;
+    lo = hi;
+    hi = rmap(rep, k, lane);
+  }
+  while (lo >= y && k > 1) {
+    --k;
+    hi = lo;
+    lo = rmap(rep, k - 1, lane);
+  }
+  return uint32_t(__fsub_rn(hi, y) < __fsub_rn(y, lo) ? k : k - 1);
 }
 
 struct DynSmem {
-  float map[2][256];
-  uint8_t lb[3][DYN_NB];
+  float rep[2][256 * 32];  // lane-replicated maps (64 KB)
 };
 
 template <bool PARAM_BF16>
 __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __restrict__ tbl, int64_t nblocks,
                                                           AdamPtrs P, AdamScalars s) {
-  __shared__ DynSmem T;
+  extern __shared__ __align__(16) float dyn_smem[];
+  DynSmem& T = *reinterpret_cast<DynSmem*>(dyn_smem);
   __shared__ float red_m[2][DYN_NT / 32], red_v[2][DYN_NT / 32];
-  {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&c_dyn);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(&T);
-    for (int i = threadIdx.x; i < int(sizeof(DynSmem) / 4); i += DYN_NT) dst[i] = src[i];
+  for (int i = threadIdx.x; i < 2 * 256 * 32; i += DYN_NT) {
+    const int w = i >> 13, k = (i >> 5) & 255;
+    T.rep[w][i & 8191] = c_dyn.map[w][k];
   }
   __syncthreads();
-  const float* mapm = T.map[0];
-  const float* mapv = T.map[1];
+  const int lane = int(threadIdx.x) & 31;
+  const float* mapm = T.rep[0];
+  const float* mapv = T.rep[1];
   constexpr uint32_t zero_m = 127, zero_v = 0;  // codes of 0.0 in the two maps
   uint8_t* mq = reinterpret_cast<uint8_t*>(P.mq);
   using G = AdamGeom<DYN_NT>;  // 2 quads per thread
@@ -137,10 +147,10 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
     float* rv = red_v[it & 1];
     // R27: A = 0, NaN or +inf -> the code of 0 everywhere
     auto qm = [&](float m, float am) {
-      return am > 0.f && am <= FLT_MAX_F ? dyn_code(mapm, T.lb[0], T.lb[1], __fdiv_rn(m, am)) : zero_m;
+      return am > 0.f && am <= FLT_MAX_F ? dyn_code<true>(mapm, lane, __fdiv_rn(m, am)) : zero_m;
     };
     auto qv = [&](float v, float av) {
-      return av > 0.f && av <= FLT_MAX_F ? dyn_code(mapv, T.lb[2], T.lb[2], __fdiv_rn(v, av)) : zero_v;
+      return av > 0.f && av <= FLT_MAX_F ? dyn_code<false>(mapv, lane, __fdiv_rn(v, av)) : zero_v;
     };
     float am = 0.f, av = 0.f;
     const bool fast = blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
@@ -160,8 +170,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
                              __int_as_float(gv.w)};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float mt = __fmul_rn(mapm[(cm >> (8 * j)) & 0xffu], Am);
-          const float vt = __fmul_rn(mapv[(cv >> (8 * j)) & 0xffu], Av);
+          const float mt = __fmul_rn(rmap(mapm, int((cm >> (8 * j)) & 0xffu), lane), Am);
+          const float vt = __fmul_rn(rmap(mapv, int((cv >> (8 * j)) & 0xffu), lane), Av);
           const ElemOut r = adam_elem(pp[j], gg[j], mt, vt, s);
           p[4 * k + j] = r.p;
           m[4 * k + j] = r.m;
@@ -189,8 +199,8 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
     } else {
       auto elem = [&](int i, float& m, float& v) -> float {  // update element i, returns new p
         const int64_t o = blk_off(blk, i);
-        const float mt = __fmul_rn(mapm[mq[blk.state_off + o]], Am);
-        const float vt = __fmul_rn(mapv[P.vq[blk.state_off + o]], Av);
+        const float mt = __fmul_rn(rmap(mapm, mq[blk.state_off + o], lane), Am);
+        const float vt = __fmul_rn(rmap(mapv, P.vq[blk.state_off + o], lane), Av);
         const ElemOut r = adam_elem(P.master[blk.state_off + o], P.grad[blk.grad_off + o], mt, vt, s);
         m = r.m;
         v = r.v;
@@ -250,17 +260,26 @@ cudaError_t launch_adam8_dyn(const AdamBlock* tbl, int64_t nblocks, const AdamPt
                              cudaStream_t st) {
   if (nblocks == 0) return cudaSuccess;
   if (cudaError_t e = ensure_dyn_tables()) return e;
+  constexpr int smem = int(sizeof(DynSmem));
+  static bool attr = false;
+  if (!attr) {
+    if (cudaError_t e = cudaFuncSetAttribute(adam8_dyn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+      return e;
+    if (cudaError_t e = cudaFuncSetAttribute(adam8_dyn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+      return e;
+    attr = true;
+  }
   int per = 0;
   if (p.param_bf16)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adam8_dyn_kernel<true>, DYN_NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adam8_dyn_kernel<true>, DYN_NT, smem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adam8_dyn_kernel<false>, DYN_NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adam8_dyn_kernel<false>, DYN_NT, smem);
   const int64_t cap = int64_t(num_sms()) * (per < 1 ? 1 : per);
   const int grid = int(nblocks < cap ? nblocks : cap);
   if (p.param_bf16)
-    adam8_dyn_kernel<true><<<grid, DYN_NT, 0, st>>>(tbl, nblocks, p, s);
+    adam8_dyn_kernel<true><<<grid, DYN_NT, smem, st>>>(tbl, nblocks, p, s);
   else
-    adam8_dyn_kernel<false><<<grid, DYN_NT, 0, st>>>(tbl, nblocks, p, s);
+    adam8_dyn_kernel<false><<<grid, DYN_NT, smem, st>>>(tbl, nblocks, p, s);
   return cudaGetLastError();
 }
 

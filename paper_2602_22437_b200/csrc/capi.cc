@@ -271,7 +271,11 @@ static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t ra
   if (L.elem_bytes == 2 && bufs.grad_full == bufs.grad_f32)
     return fail(RSDB_EMISMATCH, "bf16 unit: grad_full must not alias grad_f32");
   std::vector<rsdb::QTile> qb;
-  if (rsdb_status st = tiles_of(L, rank, specs, &qb)) return st;
+  const bool no_blocks = std::all_of(specs.begin(), specs.end(), [](const rsdb::QSpec& q) {
+    return q.row_len == 0 && q.tile_rows == 0 && q.tile_cols == 0;
+  });  // qblock = 0: collectives-only unit
+  if (!no_blocks)
+    if (rsdb_status st = tiles_of(L, rank, specs, &qb)) return st;
   u->L = L;
   u->comm = comm;
   u->rank = rank;
@@ -296,6 +300,7 @@ static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t ra
 rsdb_status rsdb_unit_create(const rsdb_layout* l, rsdb_comm* comm, int32_t rank,
                              const rsdb_unit_bufs* bufs, int64_t qblock, rsdb_unit** out) {
   if (!l || !bufs || !out) return fail(RSDB_EINVAL, "null argument");
+  if (qblock < 0) return fail(RSDB_EINVAL, "qblock must be >= 0 (0: no optimizer blocks)");
   auto u = std::make_unique<rsdb_unit>();
   if (rsdb_status st = build_unit(l->L, comm, rank, *bufs, make_specs(l->L, qblock, nullptr), u.get(),
                                   nullptr))
@@ -542,6 +547,24 @@ void rsdb_p2p_free(rsdb_p2p* p) {
   delete p;
 }
 
+rsdb_status rsdb_p2p_channel(const rsdb_p2p* p, int32_t channel, rsdb_p2p** out) {
+  if (!p || !out) return fail(RSDB_EINVAL, "null argument");
+  if (channel < 1 || channel >= RSDB_P2P_SIGNAL_BYTES / (P2P_CHANNEL_WORDS * 8))
+    return fail(RSDB_EINVAL, "channel must be in [1, %d)", RSDB_P2P_SIGNAL_BYTES / (P2P_CHANNEL_WORDS * 8));
+  if (p->channel != 0) return fail(RSDB_EINVAL, "create channels from the base p2p object");
+  auto c = std::make_unique<rsdb_p2p>();
+  c->comm = p->comm;
+  c->n = p->n;
+  c->local = p->local;
+  c->size = p->size;
+  c->peer = p->peer;  // borrowed mappings (c->opened stays empty: p owns them)
+  c->timeout_ns = p->timeout_ns;
+  c->grid_div = p->grid_div;
+  c->channel = channel;
+  *out = c.release();
+  return OK_CLEAR();
+}
+
 rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* all_bufs,
                                   const int64_t* sizes, rsdb_p2p** out) {
   if (!comm || n_bufs < 1 || !all_bufs || !sizes || !out)
@@ -575,7 +598,8 @@ rsdb_status rsdb_p2p_set_timeout(rsdb_p2p* p, double seconds) {
 
 rsdb_status rsdb_p2p_check(rsdb_p2p* p, int64_t* flags) {
   if (!p || !flags) return fail(RSDB_EINVAL, "null argument");
-  uint64_t* w = reinterpret_cast<uint64_t*>(p->local[0]) + rsdb::P2P_ERR_WORD;
+  uint64_t* w = reinterpret_cast<uint64_t*>(p->local[0]) + int64_t(p->channel) * P2P_CHANNEL_WORDS +
+                rsdb::P2P_ERR_WORD;
   uint64_t v = 0;
   CUDA_TRY(cudaMemcpy(&v, w, sizeof v, cudaMemcpyDeviceToHost));  // synchronises the device
   *flags = int64_t(v);
@@ -604,9 +628,10 @@ extern "C++" rsdb_status p2p_find(const rsdb_p2p* p, const void* ptr, int64_t by
 }
 
 extern "C++" void p2p_signals(const rsdb_p2p* p, int m, rsdb::P2PSignals* sg) {
-  sg->local = reinterpret_cast<uint64_t*>(p->local[0]);
+  const int64_t w = int64_t(p->channel) * P2P_CHANNEL_WORDS;
+  sg->local = reinterpret_cast<uint64_t*>(p->local[0]) + w;
   for (int r = 0; r < rsdb::P2P_MAX_RANKS; ++r)
-    sg->peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) : nullptr;
+    sg->peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) + w : nullptr;
   sg->timeout_ns = p->timeout_ns;
   sg->grid_div = p->grid_div;
 }
@@ -1030,6 +1055,61 @@ rsdb_status rsdb_dbuffer_step_8bit_adam_dynamic(rsdb_dbuffer* d, const rsdb_adam
                    d->param_bf16};
   CUDA_TRY(rsdb::launch_adam8_dyn(static_cast<const rsdb::AdamBlock*>(d->blocks.p), d->nblocks, p, s,
                                   S_(stream)));
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam_cfg* cfg, int64_t step,
+                                   const void* const* host_grads, void* const* host_shards, void* stream) {
+  if (!d || !host_grads || !host_shards) return fail(RSDB_EINVAL, "null argument");
+  if (!d->param_bf16) return fail(RSDB_EMISMATCH, "the host step needs bf16 units");
+  const size_t n = d->units.size();
+  for (size_t u = 0; u < n; ++u)
+    if (!host_grads[u] || !host_shards[u]) return fail(RSDB_EINVAL, "null host buffer for unit %zu", u);
+  if (!d->host) {
+    auto h = std::make_unique<HostPipe>();
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+    for (auto* v : {&h->ev_in, &h->ev_k, &h->ev_out}) {
+      v->assign(n, nullptr);
+      for (auto& e : *v) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    h->k_rec.assign(n, 0);
+    h->out_rec.assign(n, 0);
+    d->host = std::move(h);
+  }
+  HostPipe& h = *d->host;
+  cudaStream_t st = S_(stream);
+  // the copies start after everything already on the caller's stream
+  CUDA_TRY(cudaEventRecord(h.ev_start, st));
+  CUDA_TRY(cudaStreamWaitEvent(h.s_in, h.ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(h.s_out, h.ev_start, 0));
+  for (size_t i = n; i-- > 0;) {  // FSDP backward order, the same on every rank
+    rsdb_unit* u = d->units[i].get();
+    const size_t gbytes = size_t(int64_t(u->L.m) * u->L.S * 2);
+    const size_t sbytes = size_t(u->L.S * 2);
+    // gradients: overwrite only after this unit's previous kernel (whose done
+    // barrier also means no peer still reads them)
+    if (h.k_rec[i]) CUDA_TRY(cudaStreamWaitEvent(h.s_in, h.ev_k[i], 0));
+    if (gbytes) CUDA_TRY(cudaMemcpyAsync(u->bufs.grad_full, host_grads[i], gbytes, cudaMemcpyHostToDevice, h.s_in));
+    CUDA_TRY(cudaEventRecord(h.ev_in[i], h.s_in));
+    CUDA_TRY(cudaStreamWaitEvent(st, h.ev_in[i], 0));
+    // the shard: rewrite only after its previous copy-out
+    if (h.out_rec[i]) CUDA_TRY(cudaStreamWaitEvent(st, h.ev_out[i], 0));
+    if (rsdb_status e = rs_adam_unit(u, p, nullptr, cfg, step, stream, u->L.m > 1)) return e;
+    CUDA_TRY(cudaEventRecord(h.ev_k[i], st));
+    h.k_rec[i] = 1;
+    CUDA_TRY(cudaStreamWaitEvent(h.s_out, h.ev_k[i], 0));
+    const char* shard = static_cast<const char*>(u->bufs.param_full) + int64_t(u->rank) * u->L.S * 2;
+    if (sbytes) CUDA_TRY(cudaMemcpyAsync(host_shards[i], shard, sbytes, cudaMemcpyDeviceToHost, h.s_out));
+    CUDA_TRY(cudaEventRecord(h.ev_out[i], h.s_out));
+    h.out_rec[i] = 1;
+  }
+  // stream order: the call is complete when the caller's stream reaches here
+  if (n) {
+    CUDA_TRY(cudaStreamWaitEvent(st, h.ev_in[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(st, h.ev_out[0], 0));
+  }
   return OK_CLEAR();
 }
 

@@ -114,6 +114,9 @@ struct rsdb_muon {
   std::vector<int64_t> xoff;  // element offset of matrix t in its root's workspace
   std::vector<int32_t> mine;  // matrices this rank is the root of
   int64_t ws_bytes = 0, x2_off = 0, a_off = 0, b_off = 0, ss_off = 0;  // bytes, this rank
+  // bf16 (tensor-core) mode: W, W^T and their next-iteration copies, padded
+  // leading dimensions (multiples of 8 elements, ns_umma.cu)
+  int64_t w_off = 0, wt_off = 0, w2_off = 0, w2t_off = 0;
   DevTable mom, gat, app;
   DevTable cublas_ws;  // cuBLAS workspace (MUON_CUBLAS_WS bytes)
   int64_t n_mom = 0, max_mom = 0, n_gat = 0, c_gat = 0, n_app = 0, c_app = 0;
@@ -203,12 +206,30 @@ rsdb_status rsdb_muon_create(const rsdb_layout* l, const int64_t* rows, const in
     maxk = std::max(maxk, k * k);
   }
   int64_t off = used[size_t(rank)];
-  u->x2_off = off;
-  off += align_up(maxrc * u->esz, A);
-  u->a_off = off;
-  off += align_up(maxk * u->esz, A);
-  u->b_off = off;
-  off += align_up(maxk * u->esz, A);
+  if (u->bf16) {  // padded W / W^T pairs (2 iterations) + padded A, B
+    int64_t maxw = 0, maxkk = 0;
+    for (int32_t t : u->mine) {
+      const int64_t k = std::min(u->rows[size_t(t)], u->cols[size_t(t)]);
+      const int64_t L = std::max(u->rows[size_t(t)], u->cols[size_t(t)]);
+      maxw = std::max({maxw, k * align_up(L, 8), L * align_up(k, 8)});
+      maxkk = std::max(maxkk, k * align_up(k, 8));
+    }
+    for (int64_t* o : {&u->w_off, &u->wt_off, &u->w2_off, &u->w2t_off}) {
+      *o = off;
+      off += align_up(maxw * 2, A);
+    }
+    u->a_off = off;
+    off += align_up(maxkk * 2, A);
+    u->b_off = off;
+    off += align_up(maxkk * 2, A);
+  } else {
+    u->x2_off = off;
+    off += align_up(maxrc * u->esz, A);
+    u->a_off = off;
+    off += align_up(maxk * u->esz, A);
+    u->b_off = off;
+    off += align_up(maxk * u->esz, A);
+  }
   u->ss_off = off;
   off += align_up(int64_t(u->mine.size()) * 8, A);
   u->ws_bytes = std::max<int64_t>(off, A);
@@ -307,9 +328,57 @@ static cublasStatus_t muon_gemm(cublasHandle_t h, bool bf16, cublasOperation_t t
                      ldb, &beta, static_cast<float*>(C), ldc);
 }
 
-// R22 on the root's matrix t (row-major rows x cols at X), result left in X
+// R22 in bf16 on the tensor cores (ns_umma.cu): W = the matrix as k x L
+// (k = min(rows, cols)), kept in both layouts; per iteration three
+// tcgen05 GEMMs with the quintic's combinations in their epilogues
+static rsdb_status muon_newton_schulz_umma(rsdb_muon* u, int32_t t, int idx, const rsdb_muon_cfg* cfg,
+                                           cudaStream_t st) {
+  char* ws = static_cast<char*>(u->b.workspace);
+  char* X = ws + u->xoff[size_t(t)] * 2;
+  double* ss = reinterpret_cast<double*>(ws + u->ss_off) + idx;
+  const int64_t R = u->rows[size_t(t)], C = u->cols[size_t(t)];
+  if (cfg->ns_steps == 0) {  // normalisation only
+    CUDA_TRY(rsdb::launch_muon_normalize(X, R * C, 1, ss, cfg->eps, st));
+    return RSDB_OK;
+  }
+  const bool tall = R > C;
+  const int k = int(tall ? C : R), L = int(tall ? R : C);
+  const int64_t Lp = align_up(L, 8), kp = align_up(k, 8);
+  char* P = ws + u->w_off;    // W   (k x L, ld Lp)
+  char* PT = ws + u->wt_off;  // W^T (L x k, ld kp)
+  char* Q = ws + u->w2_off;
+  char* QT = ws + u->w2t_off;
+  char* Am = ws + u->a_off;   // k x k, ld kp
+  char* Bm = ws + u->b_off;
+  // X (R x C) -> s X, (s X)^T: wide: W = sX, W^T = (sX)^T; tall: W^T = sX, W = (sX)^T
+  if (!tall)
+    CUDA_TRY(rsdb::launch_muon_scale_transpose(X, int(R), int(C), ss, cfg->eps, P, Lp, PT, kp, st));
+  else
+    CUDA_TRY(rsdb::launch_muon_scale_transpose(X, int(R), int(C), ss, cfg->eps, PT, kp, P, Lp, st));
+  const float a = 3.4445f, b = -4.7750f, c = 2.0315f;
+  for (int it = 0; it < cfg->ns_steps; ++it) {
+    // A = W W^T
+    CUDA_TRY(rsdb::launch_umma_gemm(k, k, L, P, Lp, P, Lp, 1.f, 0.f, nullptr, 0, Am, kp, nullptr, 0, st));
+    // B = c A A + b A   (A symmetric: A A = A A^T)
+    CUDA_TRY(rsdb::launch_umma_gemm(k, k, k, Am, kp, Am, kp, c, b, Am, kp, Bm, kp, nullptr, 0, st));
+    // W' = B W + a W, and W'^T   (B-op rows of W^T)
+    CUDA_TRY(rsdb::launch_umma_gemm(k, L, k, Bm, kp, PT, kp, 1.f, a, P, Lp, Q, Lp, QT, kp, st));
+    std::swap(P, Q);
+    std::swap(PT, QT);
+  }
+  // the result back into the matrix slot (rows x cols, contiguous)
+  if (!tall)
+    CUDA_TRY(rsdb::launch_muon_copy2d(P, Lp, int(R), int(C), X, st));
+  else
+    CUDA_TRY(rsdb::launch_muon_copy2d(PT, kp, int(R), int(C), X, st));
+  return RSDB_OK;
+}
+
+// R22 on the root's matrix t (row-major rows x cols at X), result left in X;
+// fp32 parity mode on cuBLAS SGEMM, bf16 on the hand-written tcgen05 GEMM
 static rsdb_status muon_newton_schulz(rsdb_muon* u, int32_t t, int idx, const rsdb_muon_cfg* cfg, cudaStream_t st) {
   const bool bf = u->bf16 != 0;
+  if (bf) return muon_newton_schulz_umma(u, t, idx, cfg, st);
   char* ws = static_cast<char*>(u->b.workspace);
   char* X = ws + u->xoff[size_t(t)] * u->esz;
   char* X2 = ws + u->x2_off;
@@ -390,6 +459,21 @@ rsdb_status rsdb_muon_step(rsdb_muon* u, rsdb_p2p* p, const rsdb_muon_cfg* cfg, 
 }
 
 void rsdb_muon_free(rsdb_muon* u) { delete u; }
+
+rsdb_status rsdb_ns_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, const void* B,
+                              int64_t ldb, float alpha, float beta, const void* D, int64_t ldd, void* C,
+                              int64_t ldc, void* CT, int64_t ldct, void* stream) {
+  if (M < 0 || N < 0 || K < 1 || !A || !B || !C || (beta != 0.f && !D))
+    return fail(RSDB_EINVAL, "rsdb_ns_gemm_bf16: bad dimensions or null pointer");
+  if (lda < K || ldb < K || ldc < N || (beta != 0.f && ldd < N) || (CT && ldct < M) ||
+      ((lda | ldb | ldc | (beta != 0.f ? ldd : 0) | (CT ? ldct : 0)) & 7) ||
+      !aligned16(A) || !aligned16(B) || !aligned16(C) || (beta != 0.f && !aligned16(D)))
+    return fail(RSDB_EINVAL, "rsdb_ns_gemm_bf16: leading dimensions must be >= the row length and multiples "
+                             "of 8, pointers 16-B aligned");
+  if (rsdb_status st = require_device()) return st;
+  CUDA_TRY(rsdb::launch_umma_gemm(M, N, K, A, lda, B, ldb, alpha, beta, D, ldd, C, ldc, CT, ldct, S_(stream)));
+  return OK_CLEAR();
+}
 
 // ---------------------------------------------------------------------------
 // K-slot unsharded ring

@@ -98,7 +98,25 @@ inline void* param_target(const rsdb_unit* u) {
   return static_cast<char*>(u->shard) - int64_t(u->rank) * u->L.S * u->L.elem_bytes;
 }
 
+// rsdb_dbuffer_step_host: two library-owned copy streams (H2D, D2H) and, per
+// unit, the events ordering the pipeline across units and across steps
+struct HostPipe {
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k, ev_out;  // per unit
+  std::vector<char> k_rec, out_rec;              // recorded at least once
+  ~HostPipe() {
+    for (auto* v : {&ev_in, &ev_k, &ev_out})
+      for (cudaEvent_t e : *v)
+        if (e) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+  }
+};
+
 struct rsdb_dbuffer {
+  std::unique_ptr<HostPipe> host;  // created by the first rsdb_dbuffer_step_host
   std::vector<std::unique_ptr<rsdb_unit>> units;
   void* base[RSDB_NKINDS]{};
   int64_t nblocks = 0;
@@ -122,7 +140,9 @@ struct rsdb_p2p {
   uint64_t epoch = 0;
   uint64_t timeout_ns = 60ull * 1000000000ull;  // barrier spin limit (rsdb_p2p_set_timeout)
   int32_t grid_div = 1;  // logical ranks sharing the device (local mode: world)
+  int32_t channel = 0;   // signal words [32c, 32c+32) of every rank's signal buffer (rsdb_p2p_channel)
 };
+constexpr int P2P_CHANNEL_WORDS = 32;  // 256 B per channel, 16 channels in RSDB_P2P_SIGNAL_BYTES
 
 struct rsdb_copy_plan {
   DevTable segs;

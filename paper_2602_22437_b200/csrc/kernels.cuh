@@ -150,5 +150,15 @@ cudaError_t launch_muon_apply(const MuonSeg* segs, int64_t nseg, int64_t nchunks
                               int bf16, float* master, void* param_bf16, double lr, int m, int rank,
                               const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
 cudaError_t launch_muon_normalize(void* x, int64_t n, int bf16, double* ss, double eps, cudaStream_t st);
+// N3 tensor-core Newton-Schulz (ns_umma.cu, muon.cu)
+cudaError_t launch_muon_scale_transpose(const void* x, int rows, int cols, double* ss, double eps, void* same,
+                                        int64_t ld_same, void* trans, int64_t ld_trans, cudaStream_t st);
+cudaError_t launch_muon_copy2d(const void* src, int64_t ld, int rows, int cols, void* dst, cudaStream_t st);
+// C[M x N] = alpha * A[M x K] . B[N x K]^T (+ beta * D), bf16 in / out, fp32
+// accumulation in TMEM; CT (optional) receives C^T.  All K-major (row-major,
+// contraction dim contiguous); ld* in elements, multiples of 8; 16-B aligned.
+cudaError_t launch_umma_gemm(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                             float alpha, float beta, const void* D, int64_t ldd, void* C, int64_t ldc, void* CT,
+                             int64_t ldct, cudaStream_t st);
 
 }  // namespace rsdb

@@ -152,6 +152,70 @@ __global__ void __launch_bounds__(MUON_NT) muon_scale_kernel(void* __restrict__ 
   }
 }
 
+// Normalisation fused with the layout change of the tensor-core
+// Newton-Schulz (ns_umma.cu): X (rows x cols, contiguous bf16) -> s*X into
+// `same` (rows x cols, ld ld_same) and (s*X)^T into `trans` (cols x rows, ld
+// ld_trans), s = 1 / (||X||_F + eps) from muon_sumsq_kernel (the same fp32
+// product as muon_scale_kernel).  32 x 32 tiles through shared memory, so
+// both writes are coalesced.
+__global__ void __launch_bounds__(256) muon_scale_transpose_kernel(const __nv_bfloat16* __restrict__ x, int rows,
+                                                                   int cols, const double* ss, double eps,
+                                                                   __nv_bfloat16* same, int64_t ld_same,
+                                                                   __nv_bfloat16* trans, int64_t ld_trans) {
+  __shared__ __nv_bfloat16 tile[32][33];
+  const float f = float(1.0 / (sqrt(*ss) + eps));
+  const int tx = int(threadIdx.x) & 31, ty = int(threadIdx.x) >> 5;  // 32 x 8
+  const int64_t tiles_c = (cols + 31) / 32, tiles = tiles_c * ((rows + 31) / 32);
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int r0 = int(t / tiles_c) * 32, c0 = int(t % tiles_c) * 32;
+    for (int i = ty; i < 32; i += 8) {
+      const int r = r0 + i, c = c0 + tx;
+      if (r < rows && c < cols) {
+        const __nv_bfloat16 v = __float2bfloat16_rn(__bfloat162float(x[int64_t(r) * cols + c]) * f);
+        same[int64_t(r) * ld_same + c] = v;
+        tile[i][tx] = v;
+      }
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+      const int c = c0 + i, r = r0 + tx;
+      if (c < cols && r < rows) trans[int64_t(c) * ld_trans + r] = tile[tx][i];
+    }
+    __syncthreads();
+  }
+}
+
+// strided -> contiguous copy (the Newton-Schulz result back into the matrix slot)
+__global__ void __launch_bounds__(256) muon_copy2d_kernel(const __nv_bfloat16* __restrict__ src, int64_t ld,
+                                                          int rows, int cols, __nv_bfloat16* __restrict__ dst) {
+  const int64_t n = int64_t(rows) * cols;
+  for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < n; i += int64_t(gridDim.x) * 256)
+    dst[i] = src[(i / cols) * ld + i % cols];
+}
+
+static int grid_for(int64_t items);
+
+cudaError_t launch_muon_scale_transpose(const void* x, int rows, int cols, double* ss, double eps, void* same,
+                                        int64_t ld_same, void* trans, int64_t ld_trans, cudaStream_t st) {
+  const int64_t n = int64_t(rows) * cols;
+  if (n == 0) return cudaSuccess;
+  if (cudaError_t e = cudaMemsetAsync(ss, 0, sizeof(double), st)) return e;
+  muon_sumsq_kernel<true><<<grid_for((n + MUON_NT - 1) / MUON_NT), MUON_NT, 0, st>>>(x, n, ss);
+  const int64_t tiles = ((rows + 31) / 32) * int64_t((cols + 31) / 32);
+  muon_scale_transpose_kernel<<<grid_for(tiles), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(x), rows, cols, ss, eps, static_cast<__nv_bfloat16*>(same), ld_same,
+      static_cast<__nv_bfloat16*>(trans), ld_trans);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_muon_copy2d(const void* src, int64_t ld, int rows, int cols, void* dst, cudaStream_t st) {
+  const int64_t n = int64_t(rows) * cols;
+  if (n == 0) return cudaSuccess;
+  muon_copy2d_kernel<<<grid_for((n + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), ld, rows,
+                                                                cols, static_cast<__nv_bfloat16*>(dst));
+  return cudaGetLastError();
+}
+
 static int grid_for(int64_t items) {
   const int64_t cap = int64_t(num_sms()) * 8;
   return int(items < 1 ? 1 : (items < cap ? items : cap));

@@ -1,0 +1,504 @@
+"""Extra measurements of the default `bench.py` run (its `extras` key), so the
+round-end driver run carries every BASELINE config and every SURVEY §8(f) row
+that has a kernel, not only the headline step:
+
+  per_unit        (N>1) AllGather / ReduceScatter bus GB/s per FSDP unit of
+                  config 2 (layer unit, root unit): BJ's metric as named
+  kernels         the §8(a) kernels outside the fused step, on the bench's own
+                  DBuffer: a6 cast/scale per unit, a8 unfused 8-bit Adam (one
+                  launch), N2 dynamic-code-map Adam (one launch)
+  tiles_32x32     N2: the paper's own 8-bit Adam setup (32x32 blocks,
+                  32-row granularity) on the whole Llama-3.2-1B DBuffer
+  muon_8b_layer   config 3 / N3: one distributed-Muon step (Alg. 2) over the
+                  Llama-3-8B decoder layer, Newton-Schulz TFLOP/s
+  dsv3_ragged_vs_rowwise  config 4: zero-copy RaggedShard AG/RS against the
+                  FSDP2 row-wise layout's Copy-Out / Copy-In + collective
+  bucket_sweep    config 5: padding and rank-chunk alignment of aligned ragged
+                  vs even split (host), and (N>1) AllGather bus GB/s of both
+  zero3_overlap   (N>1) N4: FSDP's reshard schedule (K=2 gathered slots, AG
+                  before forward and before backward, prefetched on a copy
+                  stream) under a synthetic compute stream: exposed comm time
+
+Every timing is CUDA events on the launching stream, median of `reps`, max
+over ranks.  Measurement only: parity lives in tests/ (only tests/ run the
+oracle).  Each item is independent; an exception is recorded in the item
+(`{"error": ...}`) and the next item runs.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HBM_SPEC_GBS = 8000.0
+NVLINK_SPEC_GBS = 900.0
+
+
+def _max(x, world):
+    if world == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def _barrier(world):
+    if world > 1:
+        dist.barrier()
+
+
+def timed(fn, reps, stream, world, warm=2):
+    """Median ms per call of fn (launching on `stream`), max over ranks."""
+    with torch.cuda.stream(stream):
+        for _ in range(warm):
+            fn()
+    stream.synchronize()
+    _barrier(world)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    with torch.cuda.stream(stream):
+        for a, b in evs:
+            a.record(stream)
+            fn()
+            b.record(stream)
+    stream.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in evs)
+    return _max(ms[len(ms) // 2], world)
+
+
+def _peaks():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1590.0))
+    except Exception:
+        return 6650.0, 1590.0
+
+
+def _run(name, fn, out):
+    t0 = time.perf_counter()
+    try:
+        out[name] = fn()
+    except Exception as e:  # recorded, not hidden: the item shows the error
+        out[name] = {"error": f"{type(e).__name__}: {e}"}
+    if isinstance(out[name], dict):
+        out[name]["wall_s"] = round(time.perf_counter() - t0, 2)
+
+
+# ---------------------------------------------------------------- per-unit collectives
+def per_unit(R, ctx):
+    """BJ metric as named: AG and RS bus GB/s per FSDP unit (nccl-tests
+    convention, bus bytes = (m-1) S b per rank), p2p kernels over NVLink,
+    on the bench DBuffer's first layer unit and its root unit."""
+    db, p2p, st, world = ctx["db"], ctx["p2p"], ctx["stream"], ctx["world"]
+    res = {}
+    for name, idx in (("layer", 1), ("root", 0)):
+        u = db.units[idx]
+        lay = u.layout
+        S, m = lay.S, lay.m
+        t_ag = timed(lambda: R.all_gather_p2p(u, p2p, st), ctx["reps"], st, world)
+        t_rs = timed(lambda: R.reduce_scatter_p2p(u, p2p, st), ctx["reps"], st, world)
+        bus = (m - 1) * S * 2
+        res[name] = {"S": S, "params": lay.E, "ag_ms": t_ag, "rs_ms": t_rs,
+                     "ag_bus_gbs": bus / t_ag / 1e6, "rs_bus_gbs": bus / t_rs / 1e6,
+                     "ag_frac_of_900": bus / t_ag / 1e6 / NVLINK_SPEC_GBS,
+                     "rs_frac_of_900": bus / t_rs / 1e6 / NVLINK_SPEC_GBS,
+                     "rs_wire": "bf16 (cast + 1/m fused into the reduction)"}
+    return res
+
+
+# ---------------------------------------------------------------- standalone kernels on the bench DBuffer
+def kernels(R, ctx):
+    db, st, world, lays, cfg = ctx["db"], ctx["stream"], ctx["world"], ctx["lays"], ctx["cfg"]
+    hbm, _ = _peaks()
+    rank = ctx["rank"]
+    n_el = n_blk = 0
+    for lay in lays:
+        b = lay.rank_blocks(rank, 2048)
+        n_el += sum(n for _, n in b)
+        n_blk += len(b)
+    adam_bytes = 18 * n_el + 16 * n_blk
+    t = [ctx["t"]]
+
+    def adam():
+        db.step_8bit_adam(cfg, t[0], st)
+        t[0] += 1
+
+    def adam_dyn():
+        db.step_8bit_adam_dynamic(cfg, t[0], st)
+        t[0] += 1
+
+    out = {}
+    ms = timed(adam, ctx["reps"], st, world)
+    out["adam8_unfused"] = {"kernel": "adam8_tma_kernel", "ms": ms, "gbs": adam_bytes / ms / 1e6,
+                            "frac": adam_bytes / ms / 1e6 / hbm, "bytes": "18 B/elem + 16 B/block"}
+    ms = timed(adam_dyn, ctx["reps"], st, world)
+    out["adam8_dynamic"] = {"kernel": "adam8_dyn_kernel", "ms": ms, "gbs": adam_bytes / ms / 1e6,
+                            "frac": adam_bytes / ms / 1e6 / hbm, "bytes": "18 B/elem + 16 B/block"}
+    cast_bytes = sum(l.m * l.S * 6 for l in lays)
+    ms = timed(lambda: [R.unit_cast_scale(u, st) for u in db.units], ctx["reps"], st, world)
+    out["cast_scale"] = {"kernel": "cast_scale_kernel", "launches": len(db.units), "ms": ms,
+                         "gbs": cast_bytes / ms / 1e6, "frac": cast_bytes / ms / 1e6 / hbm,
+                         "bytes": "6 B per element of m*S (bf16 in, fp32 out)"}
+    return out
+
+
+# ---------------------------------------------------------------- N2: 32x32 tiles
+def tiles(R, ctx):
+    from synth import workloads as W
+    world, rank, comm, st, cfg = ctx["world"], ctx["rank"], ctx["comm"], ctx["stream"], ctx["cfg"]
+    hbm, _ = _peaks()
+    lays, qs = [], []
+    for u in W.llama32_1b().units:
+        es = [t.numel for t in u.tensors]
+        gs = [R.block_elems(t.shape, ("rows", 32)) if len(t.shape) == 2
+              else R.block_elems(t.shape, ("flat", 2048)) for t in u.tensors]
+        sp = [("tile", t.shape[-1], 32, 32) if len(t.shape) == 2 else ("flat", min(2048, g))
+              for t, g in zip(u.tensors, gs)]
+        lays.append(R.plan(es, gs, world, elem_bytes=2))
+        qs.append(sp)
+    sizes, _ = R.arena_sizes(lays, rank, qspec=qs)
+    arenas = [torch.zeros(max(1, n), dtype=torch.uint8, device="cuda") for n in sizes]
+    g = torch.Generator(device="cuda").manual_seed(rank)
+    arenas[R._c.RSDB_KIND_GRAD_F32].view(torch.float32).normal_(0.0, 1e-3, generator=g)
+    arenas[R._c.RSDB_KIND_MASTER].view(torch.float32).normal_(0.0, 2e-2, generator=g)
+    db = R.DBuffer(lays, rank, arenas, comm=comm, qspec=qs)
+    n_el = sum(l.S for l in lays)  # upper bound: the owned elements (zero padding here)
+    own = 0
+    for l, q in zip(lays, qs):
+        own += sum(r * c for _, r, c, _ in l.rank_tiles(rank, q))
+    t = [1]
+
+    def step():
+        db.step_8bit_adam(cfg, t[0], st)
+        t[0] += 1
+
+    ms = timed(step, ctx["reps"], st, world, warm=3)
+    nb = db.num_blocks
+    byts = 18 * own + 16 * nb
+    res = {"kernel": "adam8_tma_kernel (tile path)", "tiles": nb, "elems": own, "shard_elems": n_el,
+           "padding": sum(l.padding for l in lays), "ms": ms, "gbs": byts / ms / 1e6,
+           "frac": byts / ms / 1e6 / hbm, "bytes": "18 B/elem + 16 B/tile"}
+    db.close()
+    del arenas
+    torch.cuda.empty_cache()
+    return res
+
+
+# ---------------------------------------------------------------- config 3 / N3: distributed Muon
+def muon(R, ctx):
+    from synth import hashgen as H
+    from synth import workloads as W
+    world, rank, comm, st = ctx["world"], ctx["rank"], ctx["comm"], ctx["stream"]
+    _, tc_peak = _peaks()
+    unit = W.llama3_8b_layer(0)
+    shapes = [t.shape if len(t.shape) == 2 else None for t in unit.tensors]
+    es = [t.numel for t in unit.tensors]
+    lay = R.plan(es, [1] * len(es), world, elem_bytes=2)
+    S = lay.S
+    mk = lambda s: H.values_torch(7, s, rank * S, S, 14, device="cuda")  # noqa: E731
+    master, buf, grad = mk(1), mk(2), mk(3)
+    u = torch.zeros(S, device="cuda")
+    param = torch.zeros(S, dtype=torch.bfloat16, device="cuda")
+    mu = R.Muon(lay, shapes, rank, comm=comm, precision="bf16")
+    ws = torch.zeros(mu.workspace_bytes, dtype=torch.uint8, device="cuda")
+    mu.bind(master, buf, grad, u, ws, param_bf16=param)
+    p2p = R.P2P(comm, [u, ws]) if world > 1 else None
+    reps = max(3, ctx["reps"] // 2)
+    t_full = timed(lambda: mu.step(R.MuonConfig(), p2p, st), reps, st, world)
+    t_zero = timed(lambda: mu.step(R.MuonConfig(ns_steps=0), p2p, st), reps, st, world)
+    roots = [mu.root(i) for i in range(len(shapes))]
+    load = [0] * world
+    for i, s in enumerate(shapes):
+        if s is not None:
+            k, L = min(s), max(s)
+            load[roots[i]] += 5 * (4 * k * k * L + 2 * k ** 3)
+    t_ns = max(t_full - t_zero, 1e-6)
+    tf = max(load) / (t_ns * 1e-3) / 1e12
+    if p2p is not None:
+        torch.cuda.synchronize()
+        p2p.close()
+    mu.close()
+    # the tcgen05 GEMM alone on the layer's two big Newton-Schulz shapes
+    gemm = {}
+    for name, (M_, N_, K_) in (("W_Wt_4096x4096x14336", (4096, 4096, 14336)),
+                               ("B_W_4096x14336x4096", (4096, 14336, 4096))):
+        a_ = torch.randn(M_, K_, device="cuda").to(torch.bfloat16)
+        b_ = torch.randn(N_, K_, device="cuda").to(torch.bfloat16)
+        c_ = torch.empty(M_, N_, device="cuda", dtype=torch.bfloat16)
+        ms = timed(lambda: R.ns_gemm_bf16(a_, b_, c_, stream=st), reps, st, 1)
+        tf = 2 * M_ * N_ * K_ / (ms * 1e-3) / 1e12
+        gemm[name] = {"ms": ms, "tflops": tf, "frac_of_measured_bf16": tf / tc_peak}
+        del a_, b_, c_
+    return {"workload": "llama-3-8b decoder layer, element-granularity RaggedShard, bf16 NS",
+            "ns_gemm": gemm, "ns_kernel": "umma_gemm_kernel (tcgen05.mma + TMA + TMEM)",
+            "matrices": sum(s is not None for s in shapes), "roots": roots,
+            "step_ms": t_full, "step_without_ns_ms": t_zero, "ns_ms": t_ns,
+            "ns_tflops_busiest_root": tf, "ns_frac_of_measured_bf16": tf / tc_peak,
+            "peak_bf16_tflops": tc_peak}
+
+
+# ---------------------------------------------------------------- config 4: DSV3 ragged vs row-wise
+def dsv3(R, ctx):
+    from synth import workloads as W
+    world, rank, comm, st, p2p_main = ctx["world"], ctx["rank"], ctx["comm"], ctx["stream"], ctx["p2p"]
+    m = world
+    unit = W.dsv3_moe_unit()
+    es = [t.numel for t in unit.tensors]
+    E = sum(es)
+    reps = max(3, ctx["reps"] // 2)
+    out = {"params": E, "tensors": len(es)}
+    # ragged: planner layout, 128-row blocks, zero-copy views; AG in place, RS
+    # = the fused cast + scale + reduction (p2p kernels; at m = 1 the group op)
+    gs = [R.block_elems(t.shape, t.gran) for t in unit.tensors]
+    lay = R.plan(es, gs, m)
+    S = lay.S
+    pf = torch.zeros(m * S, dtype=torch.bfloat16, device="cuda")
+    gf = torch.randn(m * S, device="cuda").to(torch.bfloat16)
+    g32 = torch.zeros(m * S, dtype=torch.float32, device="cuda")
+    u = R.Unit(lay, rank, pf, gf, g32, qblock=0, comm=comm)
+    p2p = R.P2P(comm, [pf, gf]) if m > 1 else None
+    t_ag = timed(lambda: R.all_gather_p2p(u, p2p, st), reps, st, world)
+    t_rs = timed(lambda: R.reduce_scatter_p2p(u, p2p, st), reps, st, world)
+    out["ragged"] = {"S": S, "pad_ratio": lay.padding / E, "ag_ms": t_ag, "rs_ms": t_rs,
+                     "copy_ms": 0.0, "path": "p2p kernels, zero-copy views"}
+    if p2p is not None:
+        torch.cuda.synchronize()
+        p2p.close()
+    del u, pf, gf, g32
+    # row-wise (FSDP2 Shard(0)): NCCL AllGather + Copy-Out; Copy-In (cast, 1/m) + NCCL RS
+    shard_rows, cols, off = [], [], []
+    P = 0
+    for t in unit.tensors:
+        rows = t.shape[0]
+        c = t.numel // rows
+        sr = -(-rows // m)
+        shard_rows.append(sr)
+        cols.append(c)
+        off.append(P)
+        P += sr * c
+    P = -(-P // 8) * 8
+    flat = torch.zeros(m * P, dtype=torch.bfloat16, device="cuda")
+    params = [torch.zeros(t.numel, dtype=torch.bfloat16, device="cuda") for t in unit.tensors]
+    grads = [torch.randn(t.numel, device="cuda").to(torch.bfloat16) for t in unit.tensors]
+    rsbuf = torch.zeros(m * P, dtype=torch.float32, device="cuda")
+    seg_out, seg_in = [], []
+    for ti, t in enumerate(unit.tensors):
+        rows = t.shape[0]
+        for r in range(m):
+            r0 = r * shard_rows[ti]
+            n_rows = max(0, min(shard_rows[ti], rows - r0))
+            if n_rows == 0:
+                continue
+            n = n_rows * cols[ti]
+            seg_out.append((flat.data_ptr() + 2 * (r * P + off[ti]),
+                            params[ti].data_ptr() + 2 * r0 * cols[ti], n))
+            seg_in.append((grads[ti].data_ptr() + 2 * r0 * cols[ti],
+                           rsbuf.data_ptr() + 4 * (r * P + off[ti]), n))
+    copy_out = R.CopyPlan(seg_out, R.RSDB_BF16, R.RSDB_BF16, 1.0)
+    copy_in = R.CopyPlan(seg_in, R.RSDB_BF16, R.RSDB_F32, 1.0 / m)
+    lay_rw = R.layout_from_starts([m * P], [1], m, P, [0])
+    u_rw = R.Unit(lay_rw, rank, flat, torch.zeros(m * P, dtype=torch.bfloat16, device="cuda"),
+                  rsbuf, qblock=0, comm=comm)
+    t_co = timed(lambda: copy_out.run(st), reps, st, world)
+    t_ci = timed(lambda: copy_in.run(st), reps, st, world)
+    row = {"S": P, "pad_ratio": (m * P - E) / E, "copy_out_ms": t_co, "copy_in_ms": t_ci,
+           "copy_segments": len(seg_out), "copy_kernel": "copy_seg_kernel",
+           "copy_gbs": (2 + 2) * E / t_co / 1e6}
+    if m > 1:
+        t_agn = timed(lambda: R.all_gather(u_rw, st), reps, st, world)
+        t_rsn = timed(lambda: R.unit_reduce_scatter_f32(u_rw, st), reps, st, world)
+        row.update({"nccl_ag_ms": t_agn, "nccl_rs_ms": t_rsn, "ag_ms": t_agn + t_co,
+                    "rs_ms": t_ci + t_rsn,
+                    "copy_share_ag": t_co / (t_agn + t_co), "copy_share_rs": t_ci / (t_ci + t_rsn)})
+    else:
+        row.update({"ag_ms": t_co, "rs_ms": t_ci,
+                    "note": "m = 1: the collectives are the identity; what remains is the "
+                            "interleaved Copy-Out / Copy-In the row-wise layout needs"})
+    out["rowwise"] = row
+    out["ragged_over_rowwise_ag+rs"] = ((out["ragged"]["ag_ms"] + out["ragged"]["rs_ms"]) /
+                                         (row["ag_ms"] + row["rs_ms"]))
+    del u_rw, copy_in, copy_out
+    return out
+
+
+# ---------------------------------------------------------------- config 5: bucket sweep
+def bucket_sweep(R, ctx):
+    from synth import workloads as W
+    world, rank, comm, st = ctx["world"], ctx["rank"], ctx["comm"], ctx["stream"]
+    rows = []
+    for mb in (1, 4, 16, 64, 256, 1024):
+        u = W.bucket(mb)
+        es = [t.numel for t in u.tensors]
+        E = sum(es)
+        for m in (2, 4, 8):
+            lay = R.plan(es, [1] * len(es), m, elem_bytes=2)
+            s_even = -(-E // m)
+            rows.append({"mb": mb, "m": m, "E": E, "S_ragged": lay.S, "S_even": s_even,
+                         "pad_ragged": lay.padding / E, "pad_even": (m * s_even - E) / E,
+                         "ragged_chunk_align_bytes": 16 if (lay.S * 2) % 16 == 0 else 2,
+                         "even_chunk_align_bytes": 2 if s_even % 2 else (4 if s_even % 4 else 8)})
+    res = {"host": rows}
+    if world > 1:
+        timed_rows = []
+        for mb in (16, 256, 1024):
+            u = W.bucket(mb)
+            es = [t.numel for t in u.tensors]
+            E = sum(es)
+            for name in ("ragged", "even"):
+                if name == "ragged":
+                    lay = R.plan(es, [1] * len(es), world, elem_bytes=2)
+                else:
+                    S = -(-E // world)
+                    lay = R.layout_from_starts([world * S], [1], world, S, [0])
+                S = lay.S
+                pf = torch.zeros(world * S + 64, dtype=torch.bfloat16, device="cuda")
+                gf = torch.zeros(world * S + 64, dtype=torch.bfloat16, device="cuda")
+                g32 = torch.zeros(world * S + 64, dtype=torch.float32, device="cuda")
+                un = R.Unit(lay, rank, pf, gf, g32, qblock=0, comm=comm)
+                t = timed(lambda: R.all_gather(un, st), 5, st, world)
+                timed_rows.append({"mb": mb, "layout": name, "S": S, "nccl_ag_ms": t,
+                                   "ag_bus_gbs": (world - 1) * S * 2 / t / 1e6})
+                del un, pf, gf, g32
+        res["nccl_allgather"] = timed_rows
+    return res
+
+
+# ---------------------------------------------------------------- N4: ZeRO-3 reshard schedule + overlap
+def zero3(R, ctx, tokens=4096):
+    """FSDP's reshard schedule on the bench workload with K = 2 gathered slots:
+    forward: AG(u+1) on a copy-engine stream while a synthetic forward GEMM of
+    unit u runs on the compute stream; backward (reverse): AG(u-1) prefetched
+    the same way, the synthetic backward GEMMs (2x forward) of unit u, then
+    the fused RS + 8-bit Adam of unit u.  The synthetic compute is a bf16
+    GEMM of tokens x 2048 x (params/2048) per unit (2 * params * tokens flop
+    forward) -- plumbing standing in for the model (out of scope).  Reports
+    the step time with and without the collectives and the exposed fraction."""
+    from synth import hashgen as H
+    import bench
+    world, rank, comm = ctx["world"], ctx["rank"], ctx["comm"]
+    units = bench.build_units(16)
+    lays = []
+    for u in units:
+        es = [t.numel for t in u.tensors]
+        gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+        lays.append(R.plan(es, gs, world, elem_bytes=2))
+    K = 2
+    max_full = max(l.m * l.S for l in lays)
+    slots = [(torch.zeros(max_full, dtype=torch.bfloat16, device="cuda"),
+              torch.zeros(max_full, dtype=torch.bfloat16, device="cuda"),
+              torch.zeros(8, dtype=torch.float32, device="cuda")) for _ in range(K)]
+    offs, acc = [], 0
+    for l in lays:
+        offs.append(acc)
+        acc += (l.S + 7) // 8 * 8
+    shards = torch.zeros(acc, dtype=torch.bfloat16, device="cuda")
+    rus, states = [], []
+    for ui, l in enumerate(lays):
+        S = l.S
+        shard = shards[offs[ui]:offs[ui] + S]
+        shard.copy_(H.values_torch(ui, H.STREAM_PARAM, rank * S, S, 12, device="cuda").to(torch.bfloat16))
+        ru = R.Unit(l, rank, slots[0][0], slots[0][1], slots[0][2].repeat(1), qblock=2048, comm=comm)
+        ru.set_shard(shard)
+        nb = ru.num_blocks
+        states.append([H.values_torch(ui, H.STREAM_PARAM, rank * S, S, 12, device="cuda"),
+                       H.codes_torch(ui, H.STREAM_MCODE, rank * S, S, True, device="cuda"),
+                       H.codes_torch(ui, H.STREAM_VCODE, rank * S, S, False, device="cuda"),
+                       H.absmax_torch(ui, H.STREAM_ABSM, rank * 10 ** 7, max(nb, 1), 14, device="cuda"),
+                       H.absmax_torch(ui, H.STREAM_ABSV, rank * 10 ** 7, max(nb, 1), 22, device="cuda")])
+        rus.append(ru)
+    for sl in slots:
+        sl[1].copy_(H.values_torch(0, H.STREAM_GRAD0 + rank, 0, max_full, 14, device="cuda").to(torch.bfloat16))
+    p2p = R.P2P(comm, [t for sl in slots for t in sl[:2]] + [shards])
+    p_ag = p2p.channel(1)  # the prefetched AllGathers overlap the RS+Adam kernels: own channel
+    cfg = R.AdamConfig()
+    comp, cstream = torch.cuda.Stream(), torch.cuda.Stream()
+    x = torch.randn(tokens, 2048, device="cuda", dtype=torch.bfloat16)
+    wts = [torch.randn(2048, max(1, l.E // 2048), device="cuda", dtype=torch.bfloat16) * 0.01
+           for l in lays]
+    n = len(rus)
+    ev_g = [torch.cuda.Event() for _ in range(n)]    # unit gathered (forward / backward)
+    ev_free = [torch.cuda.Event() for _ in range(K)]  # slot no longer read by compute
+    used = [False] * K
+    t = [1]
+
+    def gather(i, s, with_comm):
+        cstream.wait_event(ev_free[s]) if used[s] else None
+        with torch.cuda.stream(cstream):
+            if with_comm:
+                rus[i].rebind(*slots[s])
+                R.all_gather_shards_p2p(rus[i], p_ag, cstream)
+            ev_g[i].record(cstream)
+
+    def step(with_comm=True, with_compute=True):
+        seq = list(range(n)) + list(reversed(range(n)))
+        slot = {}
+        # prefetch the first unit
+        slot[(0, 0)] = 0
+        gather(seq[0], 0, with_comm)
+        for j, i in enumerate(seq):
+            s = j % K
+            if j + 1 < len(seq):  # prefetch the next unit's gather into the other slot
+                gather(seq[j + 1], (j + 1) % K, with_comm)
+            comp.wait_event(ev_g[i])
+            with torch.cuda.stream(comp):
+                if with_compute:
+                    y = x @ wts[i]
+                    if j >= n:  # backward: 2x the forward flop
+                        y = x @ wts[i]
+                        y = x @ wts[i]
+                if j >= n and with_comm:
+                    rus[i].rebind(*slots[s])
+                    R.reduce_scatter_adam_p2p(rus[i], p2p, cfg, t[0], state=states[i], stream=comp)
+                ev_free[s].record(comp)
+                used[s] = True
+        t[0] += 1
+
+    def run(reps, **kw):
+        for _ in range(2):
+            step(**kw)
+        torch.cuda.synchronize()
+        _barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        for _ in range(reps):
+            step(**kw)
+        comp.wait_stream(cstream)
+        e1.record(comp)
+        torch.cuda.synchronize()
+        return _max(e0.elapsed_time(e1) / reps, world)
+
+    reps = 5
+    t_full = run(reps)
+    t_comp = run(reps, with_comm=False)
+    t_comm = run(reps, with_compute=False)
+    torch.cuda.synchronize()
+    p_ag.close()
+    p2p.close()
+    exposed = max(0.0, t_full - t_comp)
+    flop = sum(2 * tokens * 2048 * max(1, l.E // 2048) for l in lays) * 4  # fwd 1x + bwd 3x GEMMs
+    return {"schedule": "reshard (ZeRO-3): K=2 slots, AG before forward and before backward, "
+                        "prefetched on a copy-engine stream; fused RS+Adam per unit after its backward",
+            "tokens_per_rank": tokens, "synthetic_gemm_tflop": flop / 1e12,
+            "step_ms": t_full, "compute_only_ms": t_comp, "comm_only_ms": t_comm,
+            "exposed_comm_ms": exposed, "exposed_frac_of_comm": exposed / max(t_comm, 1e-9),
+            "gathered_bytes_per_rank": K * max_full * 2 * 2,
+            "resident_gathered_bytes_per_rank": sum(l.m * l.S for l in lays) * 2 * 2}
+
+
+def run_all(R, ctx, which=None):
+    """ctx: rank, world, comm, stream, db, lays, cfg, t, p2p, reps."""
+    out = {}
+    items = [("kernels", kernels), ("tiles_32x32", tiles), ("muon_8b_layer", muon),
+             ("dsv3_ragged_vs_rowwise", dsv3), ("bucket_sweep", bucket_sweep)]
+    if ctx["world"] > 1:
+        items = [("per_unit", per_unit)] + items + [("zero3_overlap", zero3)]
+    for name, fn in items:
+        if which is None or name in which:
+            _run(name, lambda fn=fn: fn(R, ctx), out)
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    return out

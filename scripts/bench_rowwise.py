@@ -83,7 +83,7 @@ def main():
     pf = torch.zeros(m * S, dtype=torch.bfloat16, device="cuda")
     gf = torch.randn(m * S, device="cuda").to(torch.bfloat16)
     g32 = torch.zeros(m * S, dtype=torch.float32, device="cuda")
-    u = R.Unit(lay, rank, pf, gf, g32, qblock=1, comm=comm)
+    u = R.Unit(lay, rank, pf, gf, g32, qblock=0, comm=comm)
     p2p = R.P2P(comm, [pf, gf]) if args.path == "p2p" else None
     if p2p is None:
         ag = [lambda: R.all_gather(u, st)]
@@ -138,7 +138,7 @@ def main():
     lay_rw = R.layout_from_starts([m * P], [1], m, P, [0])
     grad_dummy = torch.zeros(1, dtype=torch.bfloat16, device="cuda")
     u_rw = R.Unit(lay_rw, rank, flat, torch.zeros(m * P, dtype=torch.bfloat16, device="cuda"),
-                  rsbuf, qblock=1, comm=comm)
+                  rsbuf, qblock=0, comm=comm)
     ag = [lambda: R.all_gather(u_rw, st), lambda: copy_out.run(st)]
     rs = [lambda: copy_in.run(st), lambda: R.unit_reduce_scatter_f32(u_rw, st)]
     t_ag, pa = timed(ag, args.iters, st)

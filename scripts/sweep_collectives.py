@@ -87,7 +87,7 @@ def main():
             pf = torch.zeros(world * S, dtype=torch.bfloat16, device="cuda")
             gf = torch.zeros(world * S, dtype=torch.bfloat16, device="cuda")
             g32 = torch.zeros(world * S, dtype=torch.float32, device="cuda")
-            unit = R.Unit(lay, rank, pf, gf, g32, qblock=1, comm=comm)
+            unit = R.Unit(lay, rank, pf, gf, g32, qblock=0, comm=comm)
             p2p = None
             if args.path == "p2p":
                 if (S * 2) % 16:

@@ -26,6 +26,7 @@ from oracle import dbuffer as OD
 from oracle import fp8 as F
 from oracle import muon as MU
 from oracle import planner as OP
+from synth import hashgen as H
 from synth import workloads as W
 
 from gpu_helpers import bf16_bits, f32, logical_grads, logical_params, place_gpu
@@ -256,6 +257,40 @@ def rs_random_case(ctx):
     y32 = f32(grad_f32[rank * S:(rank + 1) * S])
     if not np.array_equal(y32.view(np.uint32), OD.reduce_scatter(o, xs)[rank].view(np.uint32)):
         ctx.fail("random-normal p2p RS differs from the rank-order oracle sum")
+
+
+def channels_case(ctx):
+    """rsdb_p2p_channel: AllGathers and ReduceScatters alternating over
+    channels 0, 1 and 2 of one mapping (independent epochs and signal words)
+    give the oracle's results: AG bit exact, RS = the rank-order sum bit for
+    bit."""
+    rank, world = ctx.rank, ctx.world
+    es = [100003, 517, 2048 * 9]
+    o, c = _plans(es, [1, 1, 1], world, 2)
+    S = c.S
+    pf = torch.zeros(world * S, dtype=torch.bfloat16, device="cuda")
+    gf = torch.zeros(world * S, dtype=torch.bfloat16, device="cuda")
+    g32 = torch.zeros(world * S, dtype=torch.float32, device="cuda")
+    u = R.Unit(c, rank, pf, gf, g32, qblock=0, comm=ctx.comm)
+    p2p = yield from ctx.p2p([pf, gf])
+    chans = [p2p] * 3 if p2p is None else [p2p, p2p.channel(1), p2p.channel(2)]
+    ctx.keep = getattr(ctx, "keep", []) + chans
+    for it in range(4):
+        shards = [OD.to_bf16_rne(H.values_np(30 + it, 1 + r, 0, S, 12)) for r in range(world)]
+        pf[rank * S:(rank + 1) * S].copy_(torch.from_numpy(shards[rank].view(np.int16)).view(torch.bfloat16))
+        R.all_gather_p2p(u, chans[it % 3])
+        yield
+        if not np.array_equal(bf16_bits(pf), OD.all_gather(shards)):
+            ctx.fail(f"AllGather on channel {it % 3} (iteration {it}) is not the concatenation")
+        g_np = [OD.to_bf16_rne(OD.place_logical(o, H.values_np(40 + it, 16 + r, 0, o.E, 14)))
+                for r in range(world)]
+        gf.copy_(torch.from_numpy(g_np[rank].view(np.int16)).view(torch.bfloat16))
+        R.reduce_scatter_p2p(u, chans[(it + 1) % 3])
+        yield
+        ref = OD.reduce_scatter(o, [OD.grouped_cast_scale(o, g, True) for g in g_np])[rank]
+        y = f32(g32[rank * S:(rank + 1) * S])
+        if not np.array_equal(y.view(np.uint32), ref.view(np.uint32)):
+            ctx.fail(f"ReduceScatter on channel {(it + 1) % 3} (iteration {it}) != oracle")
 
 
 def _fused_vs_unfused(ctx, tag, es, gs, seed, step, qblock=2048, qspec=None, oracle_check=True):
@@ -553,6 +588,7 @@ def all_cases():
     return [
         ("units", units_case, {}),
         ("rs_random", rs_random_case, {}),
+        ("channels", channels_case, {}),
         ("ownerless", ownerless_case, {}),
         ("tiles", tiles_case, {}),
         ("long_blocks", long_blocks_case, {}),

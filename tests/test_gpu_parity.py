@@ -504,6 +504,68 @@ def test_dbuffer_one_launch_equals_per_unit_oracle():
     db.close()
 
 
+def test_dbuffer_step_host_world1():
+    """rsdb_dbuffer_step_host (the e2e entry point): host bf16 gradients in,
+    per-unit fused RS + 8-bit Adam, host bf16 shards out -- two steps, each
+    against the oracle's step on the same state (state resynced to the
+    oracle's after step 1, as in _adam_case), host shards = RNE(GPU master)."""
+    decl = [[2048 * 3 + 5, 77, 4096], [256 * 128, 256], [2048 * 7]]
+    q, m, rank = 2048, 1, 0
+    lays_o, lays_c = [], []
+    for es in decl:
+        o, c = _plans(es, [min(q, e) for e in es], m, 2)
+        lays_o.append(o)
+        lays_c.append(c)
+    sizes, offs = R.arena_sizes(lays_c, rank, q, 256)
+    ar = [torch.zeros(max(1, s), dtype=torch.uint8, device="cuda") for s in sizes]
+    db = R.DBuffer(lays_c, rank, ar, qblock=q, align=256)
+    views, host_g, host_p, g_logs = [], [], [], []
+    for ui, (es, c) in enumerate(zip(decl, lays_c)):
+        E, S, off = sum(es), c.S, offs[ui]
+        nb = len(c.rank_blocks(rank, q))
+        v = {"param_full": ar[0][off[0]:off[0] + S * 2].view(torch.bfloat16),
+             "master": ar[3][off[3]:off[3] + S * 4].view(torch.float32),
+             "mq": ar[4][off[4]:off[4] + S].view(torch.int8), "vq": ar[5][off[5]:off[5] + S],
+             "ma": ar[6][off[6]:off[6] + nb * 4].view(torch.float32),
+             "va": ar[7][off[7]:off[7] + nb * 4].view(torch.float32)}
+        v["master"].copy_(place_gpu(c, logical_params(ui, E), torch.float32))
+        views.append(v)
+        g = logical_grads(ui, rank, E)
+        g_logs.append(g)
+        host_g.append(place_gpu(c, g, torch.bfloat16).cpu().pin_memory())
+        host_p.append(torch.zeros(S, dtype=torch.bfloat16).pin_memory())
+    cfg = R.AdamConfig()
+    st = torch.cuda.Stream()
+    for step in (1, 2):
+        ins_all = [[v[k].cpu().numpy().copy() for k in ("master", "mq", "vq", "ma", "va")]
+                   for v in views]
+        db.step_host(cfg, step, host_g, host_p, None, st)
+        st.synchronize()
+        for ui, (o, v, ins) in enumerate(zip(lays_o, views, ins_all)):
+            blocks = OP.rank_blocks(o, rank, q)
+            g_or = OD.bf16_to_f32(OD.to_bf16_rne(OD.place_logical(o, g_logs[ui].numpy())))
+            ref = OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], blocks,
+                                    OA.AdamCfg(), step)
+            _check_adam(o, rank, blocks, (v["master"], v["mq"], v["vq"], v["ma"], v["va"],
+                                          v["param_full"]), ref, ins, 2, cfg.lr)
+            assert np.array_equal(bf16_bits(host_p[ui]), bf16_bits(v["param_full"].cpu()))
+            assert np.array_equal(bf16_bits(host_p[ui]),
+                                  bf16_bits(v["master"].cpu().to(torch.bfloat16)))
+    db.close()
+
+
+def test_dbuffer_step_host_rejects_null():
+    c = R.plan([4096], [2048], 1, elem_bytes=2)
+    sizes, _ = R.arena_sizes([c], 0, 2048, 256)
+    ar = [torch.zeros(max(1, s), dtype=torch.uint8, device="cuda") for s in sizes]
+    db = R.DBuffer([c], 0, ar, qblock=2048, align=256)
+    with pytest.raises(R.RsdbError):
+        db.step_host(R.AdamConfig(), 1, [None], [None])
+    with pytest.raises(ValueError):
+        db.step_host(R.AdamConfig(), 1, [], [])
+    db.close()
+
+
 # ------------------------------------------------------------------ copies
 def test_copy_plan_parity():
     rng = np.random.default_rng(0)
