@@ -549,6 +549,15 @@ void rsdb_muon_free(rsdb_muon*);
 rsdb_status rsdb_ns_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, const void* B,
                               int64_t ldb, float alpha, float beta, const void* D, int64_t ldd, void* C,
                               int64_t ldc, void* CT, int64_t ldct, void* stream);
+/* The same for a product the caller knows is SYMMETRIC (M = N, e.g. W W^T,
+ * or c A A + b A with A symmetric -- the first two GEMMs of every
+ * Newton-Schulz iteration): only the output tiles reaching the upper triangle
+ * are computed (~half the flops); the upper triangle (diagonal included) is
+ * stored directly and the lower triangle as its mirror image, so C is exactly
+ * symmetric.  Same arguments and errors as rsdb_ns_gemm_bf16 (C is M x M). */
+rsdb_status rsdb_ns_gemm_bf16_sym(int32_t M, int32_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                                  float alpha, float beta, const void* D, int64_t ldd, void* C, int64_t ldc,
+                                  void* stream);
 
 /* ======================================================================== */
 /* K-slot unsharded ring: only K units' gathered         */

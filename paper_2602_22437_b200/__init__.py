@@ -773,6 +773,15 @@ def ns_gemm_bf16(A, B, C, alpha=1.0, beta=0.0, D=None, CT=None, stream=None) -> 
                                 _stream(stream)))
 
 
+def ns_gemm_bf16_sym(A, B, C, alpha=1.0, beta=0.0, D=None, stream=None) -> None:
+    """rsdb_ns_gemm_bf16_sym: C = alpha A B^T + beta D for a product known to
+    be symmetric (M x M): upper-triangle tiles computed, lower mirrored."""
+    M, K = A.shape
+    check(lib.rsdb_ns_gemm_bf16_sym(M, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), float(alpha), float(beta),
+                                    _ptr(D), D.stride(0) if D is not None else 0, _ptr(C), C.stride(0),
+                                    _stream(stream)))
+
+
 def all_gather_shards_p2p(unit: Unit, p2p: Optional["P2P"] = None, stream=None) -> None:
     """AllGather of every rank's persistent shard into the unit's param_full."""
     check(lib.rsdb_all_gather_shards_p2p(unit.handle, p2p.handle if p2p is not None else None,

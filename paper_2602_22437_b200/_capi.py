@@ -142,6 +142,7 @@ _SIGS = {
     "rsdb_muon_step": (i32, [vp, vp, C.POINTER(MuonCfg), vp]),
     "rsdb_muon_free": (None, [vp]),
     "rsdb_ns_gemm_bf16": (i32, [i32, i32, i32, vp, i64, vp, i64, C.c_float, C.c_float, vp, i64, vp, i64, vp, i64, vp]),
+    "rsdb_ns_gemm_bf16_sym": (i32, [i32, i32, vp, i64, vp, i64, C.c_float, C.c_float, vp, i64, vp, i64, vp]),
     "rsdb_unit_set_shard": (i32, [vp, vp]),
     "rsdb_unit_rebind": (i32, [vp, C.POINTER(UnitBufs)]),
     "rsdb_all_gather_shards_p2p": (i32, [vp, vp, vp]),

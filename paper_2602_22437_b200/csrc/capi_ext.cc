@@ -357,10 +357,10 @@ static rsdb_status muon_newton_schulz_umma(rsdb_muon* u, int32_t t, int idx, con
     CUDA_TRY(rsdb::launch_muon_scale_transpose(X, int(R), int(C), ss, cfg->eps, PT, kp, P, Lp, st));
   const float a = 3.4445f, b = -4.7750f, c = 2.0315f;
   for (int it = 0; it < cfg->ns_steps; ++it) {
-    // A = W W^T
-    CUDA_TRY(rsdb::launch_umma_gemm(k, k, L, P, Lp, P, Lp, 1.f, 0.f, nullptr, 0, Am, kp, nullptr, 0, st));
-    // B = c A A + b A   (A symmetric: A A = A A^T)
-    CUDA_TRY(rsdb::launch_umma_gemm(k, k, k, Am, kp, Am, kp, c, b, Am, kp, Bm, kp, nullptr, 0, st));
+    // A = W W^T (symmetric: the upper-triangle tiles + their mirror)
+    CUDA_TRY(rsdb::launch_umma_gemm(k, k, L, P, Lp, P, Lp, 1.f, 0.f, nullptr, 0, Am, kp, nullptr, 0, st, true));
+    // B = c A A + b A   (A symmetric: A A = A A^T; B symmetric too)
+    CUDA_TRY(rsdb::launch_umma_gemm(k, k, k, Am, kp, Am, kp, c, b, Am, kp, Bm, kp, nullptr, 0, st, true));
     // W' = B W + a W, and W'^T   (B-op rows of W^T)
     CUDA_TRY(rsdb::launch_umma_gemm(k, L, k, Bm, kp, PT, kp, 1.f, a, P, Lp, Q, Lp, QT, kp, st));
     std::swap(P, Q);
@@ -472,6 +472,22 @@ rsdb_status rsdb_ns_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, in
                              "of 8, pointers 16-B aligned");
   if (rsdb_status st = require_device()) return st;
   CUDA_TRY(rsdb::launch_umma_gemm(M, N, K, A, lda, B, ldb, alpha, beta, D, ldd, C, ldc, CT, ldct, S_(stream)));
+  return OK_CLEAR();
+}
+
+rsdb_status rsdb_ns_gemm_bf16_sym(int32_t M, int32_t K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                                  float alpha, float beta, const void* D, int64_t ldd, void* C, int64_t ldc,
+                                  void* stream) {
+  if (M < 0 || K < 1 || !A || !B || !C || (beta != 0.f && !D))
+    return fail(RSDB_EINVAL, "rsdb_ns_gemm_bf16_sym: bad dimensions or null pointer");
+  if (lda < K || ldb < K || ldc < M || (beta != 0.f && ldd < M) ||
+      ((lda | ldb | ldc | (beta != 0.f ? ldd : 0)) & 7) || !aligned16(A) || !aligned16(B) || !aligned16(C) ||
+      (beta != 0.f && !aligned16(D)))
+    return fail(RSDB_EINVAL, "rsdb_ns_gemm_bf16_sym: leading dimensions must be >= the row length and "
+                             "multiples of 8, pointers 16-B aligned");
+  if (rsdb_status st = require_device()) return st;
+  CUDA_TRY(rsdb::launch_umma_gemm(M, M, K, A, lda, B, ldb, alpha, beta, D, ldd, C, ldc, nullptr, 0, S_(stream),
+                                  true));
   return OK_CLEAR();
 }
 

@@ -184,6 +184,25 @@ __device__ __forceinline__ bool adam_tma_ok(const AdamBlock& b) {
          ((b.grad_off | b.param_off) & 3) == 0;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+// the mbarrier receives one arrival when this thread's prior cp.asyncs land
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent, STAGES-deep prefetch ring in shared memory, one 2048-element
+// stage per block.  Every stage's mbarrier expects NT arrivals: a full
+// contiguous block is fetched by thread 0 with four 1-D bulk copies (TMA,
+// complete_tx) while the other threads just arrive; a 2-D tile (N2, the
+// paper's 32 x 32 blocks) is fetched by every thread with cp.async --
+// each 4-element quad from its own row address into the stage's flat
+// element order -- and cp.async.mbarrier.arrive; other blocks (tails,
+// misaligned, > 2048) are loaded directly by the consumer.
 template <int NT, bool PARAM_BF16, int STAGES>
 __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restrict__ tbl,
                                                        int64_t nblocks, AdamPtrs P, AdamScalars s) {
@@ -191,29 +210,47 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
   AdamStage* stage = reinterpret_cast<AdamStage*>(adam_smem);
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ float red_m[2][AdamGeom<NT>::WARPS], red_v[2][AdamGeom<NT>::WARPS];
+  using G = AdamGeom<NT>;
 
-  // thread 0 fills stage `st` with block b (or just arrives if b is not TMA-able)
+  // every thread: its part of filling stage `st` with block b
   auto issue = [&](int64_t b, int st) {
     const AdamBlock nb = tbl[b];
     if (adam_tma_ok(nb)) {
-      mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
-      bulk_g2s(stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
-      bulk_g2s(stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
-      bulk_g2s(stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
-      bulk_g2s(stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
+        bulk_g2s(stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
+        bulk_g2s(stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
+        bulk_g2s(stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
+        bulk_g2s(stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
+      } else {
+        mbar_arrive(&full[st]);
+      }
+    } else if (nb.len <= ADAM_TILE && adam_tile_fast(nb)) {
+#pragma unroll
+      for (int k = 0; k < G::Q; ++k) {
+        const int e0 = G::quad(k);
+        if (e0 < nb.len) {
+          const int64_t a = blk_off(nb, e0);
+          cp_async16(stage[st].p + e0, P.master + nb.state_off + a);
+          cp_async16(stage[st].g + e0, P.grad + nb.grad_off + a);
+          cp_async4(stage[st].mq + e0, P.mq + nb.state_off + a);
+          cp_async4(stage[st].vq + e0, P.vq + nb.state_off + a);
+        }
+      }
+      cp_async_arrive(&full[st]);
     } else {
       mbar_arrive(&full[st]);
     }
   };
   if (threadIdx.x == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], NT);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int st = 0; st < STAGES; ++st) {
-      const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
-      if (b < nblocks) issue(b, st);
-    }
   }
   __syncthreads();
+  for (int st = 0; st < STAGES; ++st) {
+    const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
+    if (b < nblocks) issue(b, st);
+  }
   int it = 0;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
     const int st = it % STAGES;
@@ -226,12 +263,10 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
     // refill this stage with block b + STAGES*grid once every thread has
     // consumed it (called right after the absmax barrier)
     auto refill = [&]() {
-      if (threadIdx.x == 0) {
-        const int64_t nb = b + int64_t(STAGES) * gridDim.x;
-        if (nb < nblocks) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async writes
-          issue(nb, st);
-        }
+      const int64_t nb = b + int64_t(STAGES) * gridDim.x;
+      if (nb < nblocks) {
+        if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads -> async writes
+        issue(nb, st);
       }
     };
     mbar_wait(&full[st], ph);
@@ -246,8 +281,9 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
         load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off,
                             P.mq + blk.state_off, P.vq + blk.state_off, sm, sv);
         adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
-      } else if (adam_tile_fast(blk)) {
-        load_tile<NT>(r, blk, P, sm, sv);
+      } else if (adam_tile_fast(blk)) {  // staged by cp.async (quads past len: garbage, masked)
+        const AdamStage& S = stage[st];
+        load_fast<NT, false>(r, S.p, S.g, S.mq, S.vq, sm, sv);
         adam_block_tail<NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill);
       } else {
         load_generic<NT>(r, blk, P, sm, sv);

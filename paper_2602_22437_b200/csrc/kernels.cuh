@@ -155,10 +155,12 @@ cudaError_t launch_muon_scale_transpose(const void* x, int rows, int cols, doubl
                                         int64_t ld_same, void* trans, int64_t ld_trans, cudaStream_t st);
 cudaError_t launch_muon_copy2d(const void* src, int64_t ld, int rows, int cols, void* dst, cudaStream_t st);
 // C[M x N] = alpha * A[M x K] . B[N x K]^T (+ beta * D), bf16 in / out, fp32
-// accumulation in TMEM; CT (optional) receives C^T.  All K-major (row-major,
+// accumulation in TMEM; CT (optional) receives C^T.  sym: the caller
+// guarantees C is symmetric (M == N, e.g. W W^T): only the tiles reaching the
+// upper triangle are computed and the rest of C is their mirror image.  All K-major (row-major,
 // contraction dim contiguous); ld* in elements, multiples of 8; 16-B aligned.
 cudaError_t launch_umma_gemm(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
                              float alpha, float beta, const void* D, int64_t ldd, void* C, int64_t ldc, void* CT,
-                             int64_t ldct, cudaStream_t st);
+                             int64_t ldct, cudaStream_t st, bool sym = false);
 
 }  // namespace rsdb

@@ -101,7 +101,32 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-template <bool HAS_D, bool HAS_T>
+// tile t -> (m0, n0).  Full: m-tiles fastest.  SYM (C symmetric, M == N):
+// only tiles that reach the upper triangle (n0 + BN - 1 >= m0), column by
+// column -- the rest of C is written by mirroring (epilogue)
+template <bool SYM>
+__device__ __forceinline__ void tile_coords(int t, int mt, int& m0, int& n0) {
+  if constexpr (!SYM) {
+    m0 = (t % mt) * UG_BM;
+    n0 = (t / mt) * UG_BN;
+  } else {
+    int j = 0;
+    for (;; ++j) {
+      const int rows = min(mt, (j + 1) * (UG_BN / UG_BM));  // m-tiles of column j touching col >= row
+      if (t < rows) break;
+      t -= rows;
+    }
+    m0 = t * UG_BM;
+    n0 = j * UG_BN;
+  }
+}
+__host__ __device__ inline int sym_tiles(int mt, int nt) {
+  int n = 0;
+  for (int j = 0; j < nt; ++j) n += (mt < (j + 1) * (UG_BN / UG_BM)) ? mt : (j + 1) * (UG_BN / UG_BM);
+  return n;
+}
+
+template <bool HAS_D, bool HAS_T, bool SYM>
 __global__ void __launch_bounds__(UG_THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M,
                      int N, int K, UmmaEpi ep) {
@@ -114,7 +139,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
   const int mt = (M + UG_BM - 1) / UG_BM, nt = (N + UG_BN - 1) / UG_BN;
-  const int tiles = mt * nt, kblocks = (K + UG_BK - 1) / UG_BK;
+  const int tiles = SYM ? sym_tiles(mt, nt) : mt * nt, kblocks = (K + UG_BK - 1) / UG_BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < UG_STAGES; ++s) {
@@ -144,7 +169,8 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % mt) * UG_BM, n0 = (t / mt) * UG_BN;
+        int m0, n0;
+        tile_coords<SYM>(t, mt, m0, n0);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + s, ph ^ 1);
           uint8_t* sa = smem + s * UG_STAGE_BYTES;
@@ -192,7 +218,8 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     int as = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t % mt) * UG_BM, n0 = (t / mt) * UG_BN;
+      int m0, n0;
+      tile_coords<SYM>(t, mt, m0, n0);
       mbar_wait(tfull + as, aph);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
@@ -228,7 +255,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
             }
           }
           __nv_bfloat16* cp = ep.C + int64_t(row) * ep.ldc + col0;
-          if (full_cols) {
+          if (SYM && col0 < row + 1) {  // the part left of the diagonal comes from the mirror writes
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j >= row && col0 + j < N) cp[j] = __float2bfloat16_rn(v[j]);
+          } else if (full_cols) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8)
               *reinterpret_cast<uint4*>(cp + j) = make_uint4(pack2(v[j], v[j + 1]), pack2(v[j + 2], v[j + 3]),
@@ -239,11 +270,12 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
               if (col0 + j < N) cp[j] = __float2bfloat16_rn(v[j]);
           }
         }
-        if constexpr (HAS_T) {  // C^T[col][row]: the 32 lanes write 32 consecutive rows (64 B)
+        if constexpr (HAS_T || SYM) {  // C^T[col][row]: the 32 lanes write 32 consecutive rows (64 B)
           if (row < M) {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) ep.CT[int64_t(col0 + j) * ep.ldct + row] = __float2bfloat16_rn(v[j]);
+              if (col0 + j < N && (!SYM || col0 + j > row))
+                ep.CT[int64_t(col0 + j) * ep.ldct + row] = __float2bfloat16_rn(v[j]);
           }
         }
       }
@@ -291,8 +323,9 @@ static cudaError_t encode_kmajor(CUtensorMap* map, const void* base, int64_t row
 
 cudaError_t launch_umma_gemm(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
                              float alpha, float beta, const void* D, int64_t ldd, void* C, int64_t ldc, void* CT,
-                             int64_t ldct, cudaStream_t st) {
+                             int64_t ldct, cudaStream_t st, bool sym) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if (sym && (M != N || CT)) return cudaErrorInvalidValue;
   if (K <= 0 || (lda * 2) % 16 || (ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(A) % 16) ||
       (reinterpret_cast<uintptr_t>(B) % 16))
     return cudaErrorInvalidValue;
@@ -305,23 +338,32 @@ cudaError_t launch_umma_gemm(int M, int N, int K, const void* A, int64_t lda, co
              static_cast<__nv_bfloat16*>(CT), ldd, ldc, ldct};
   static bool attr = false;
   if (!attr) {
-    for (auto k : {umma_gemm_kernel<false, false>, umma_gemm_kernel<true, false>, umma_gemm_kernel<false, true>,
-                   umma_gemm_kernel<true, true>})
+    for (auto k : {umma_gemm_kernel<false, false, false>, umma_gemm_kernel<true, false, false>,
+                   umma_gemm_kernel<false, true, false>, umma_gemm_kernel<true, true, false>,
+                   umma_gemm_kernel<false, false, true>, umma_gemm_kernel<true, false, true>})
       if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(UG_SMEM)))
         return e;
     attr = true;
   }
-  const int tiles = ((M + UG_BM - 1) / UG_BM) * ((N + UG_BN - 1) / UG_BN);
+  const int mt = (M + UG_BM - 1) / UG_BM, nt = (N + UG_BN - 1) / UG_BN;
+  const int tiles = sym ? sym_tiles(mt, nt) : mt * nt;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   const bool hd = beta != 0.f, ht = CT != nullptr;
-  if (hd && ht)
-    umma_gemm_kernel<true, true><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
+  if (sym) {
+    ep.CT = ep.C;
+    ep.ldct = ep.ldc;
+    if (hd)
+      umma_gemm_kernel<true, false, true><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
+    else
+      umma_gemm_kernel<false, false, true><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
+  } else if (hd && ht)
+    umma_gemm_kernel<true, true, false><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
   else if (hd)
-    umma_gemm_kernel<true, false><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
+    umma_gemm_kernel<true, false, false><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
   else if (ht)
-    umma_gemm_kernel<false, true><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
+    umma_gemm_kernel<false, true, false><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
   else
-    umma_gemm_kernel<false, false><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
+    umma_gemm_kernel<false, false, false><<<grid, UG_THREADS, UG_SMEM, st>>>(ma, mb, M, N, K, ep);
   return cudaGetLastError();
 }
 

@@ -230,9 +230,16 @@ def muon(R, ctx):
         b_ = torch.randn(N_, K_, device="cuda").to(torch.bfloat16)
         c_ = torch.empty(M_, N_, device="cuda", dtype=torch.bfloat16)
         ms = timed(lambda: R.ns_gemm_bf16(a_, b_, c_, stream=st), reps, st, 1)
-        tf = 2 * M_ * N_ * K_ / (ms * 1e-3) / 1e12
-        gemm[name] = {"ms": ms, "tflops": tf, "frac_of_measured_bf16": tf / tc_peak}
+        tg = 2 * M_ * N_ * K_ / (ms * 1e-3) / 1e12
+        gemm[name] = {"ms": ms, "tflops": tg, "frac_of_measured_bf16": tg / tc_peak}
         del a_, b_, c_
+    a_ = torch.randn(4096, 14336, device="cuda").to(torch.bfloat16)
+    c_ = torch.empty(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    ms = timed(lambda: R.ns_gemm_bf16_sym(a_, a_, c_, stream=st), reps, st, 1)
+    gemm["W_Wt_sym_4096x4096x14336"] = {
+        "ms": ms, "effective_tflops": 2 * 4096 * 4096 * 14336 / (ms * 1e-3) / 1e12,
+        "note": "symmetric product: upper-triangle tiles only (272 of 512), effective = full-product flop / time"}
+    del a_, c_
     return {"workload": "llama-3-8b decoder layer, element-granularity RaggedShard, bf16 NS",
             "ns_gemm": gemm, "ns_kernel": "umma_gemm_kernel (tcgen05.mma + TMA + TMEM)",
             "matrices": sum(s is not None for s in shapes), "roots": roots,

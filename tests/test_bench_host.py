@@ -66,3 +66,17 @@ def test_peaks_from_measured_file():
         assert src.startswith("measured") and 4000 < peak < 9000
     else:
         assert src.startswith("fallback")
+
+
+def test_bench_scripts_compile():
+    """bench.py loads scripts/bench_extras.py at run time: keep it importable."""
+    import py_compile
+    for f in ("bench.py", os.path.join("scripts", "bench_extras.py")):
+        py_compile.compile(os.path.join(ROOT, f), doraise=True)
+
+
+def test_metric_bytes_definition():
+    """value's bytes: world 1 = the fused step's HBM bytes (16 B/elem + 16 B/block);
+    world m = every rank's AG + RS wire bytes, m * 2 (m-1) S 2."""
+    assert bench.metric_bytes(1, 4096, 4096, 2) == 16 * 4096 + 32
+    assert bench.metric_bytes(4, 1000, 3990, 2) == 4 * 2 * 3 * 1000 * 2

@@ -25,6 +25,10 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
+def _ld(cols, pad):
+    return (cols + 7) // 8 * 8 + pad
+
+
 def _mat(rows, cols, ld, seed, scale=1.0):
     g = torch.Generator(device="cuda").manual_seed(seed)
     buf = torch.randn(rows, ld, device="cuda", generator=g) * scale
@@ -32,11 +36,11 @@ def _mat(rows, cols, ld, seed, scale=1.0):
 
 
 def _check(M, N, K, alpha=1.0, beta=0.0, with_t=False, pad=0, seed=0):
-    A = _mat(M, K, K + pad, seed)
-    B = _mat(N, K, K + pad, seed + 1)
-    D = _mat(M, N, N + pad, seed + 2) if beta != 0.0 else None
-    C = torch.full((M, N + pad), float("nan"), device="cuda", dtype=torch.bfloat16)[:, :N]
-    CT = torch.zeros(N, M + pad, device="cuda", dtype=torch.bfloat16)[:, :M] if with_t else None
+    A = _mat(M, K, _ld(K, pad), seed)
+    B = _mat(N, K, _ld(K, pad), seed + 1)
+    D = _mat(M, N, _ld(N, pad), seed + 2) if beta != 0.0 else None
+    C = torch.full((M, _ld(N, pad)), float("nan"), device="cuda", dtype=torch.bfloat16)[:, :N]
+    CT = torch.zeros(N, _ld(M, pad), device="cuda", dtype=torch.bfloat16)[:, :M] if with_t else None
     R.ns_gemm_bf16(A, B, C, alpha, beta, D, CT)
     torch.cuda.synchronize()
     ref = alpha * (A.float() @ B.float().T)
@@ -59,7 +63,7 @@ def test_ns_gemm_full_tiles(M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K,pad", [(24, 40, 24, 0), (200, 300, 136, 8), (1, 64, 8, 0), (130, 260, 72, 16),
-                                       (1000, 1000, 1000, 0)])
+                                       (1000, 1000, 1000, 0), (37, 11, 5, 0)])
 def test_ns_gemm_ragged(M, N, K, pad):
     _check(M, N, K, pad=pad)
 
@@ -97,6 +101,32 @@ def test_ns_gemm_quintic_iteration_8b_shape():
     mag = Bm.float().abs() @ W.float().abs() + abs(a) * W.float().abs()
     assert ((W2.float() - ref).abs() <= 2 ** -8 * ref.abs() + 2 * k * 2 ** -24 * mag).all()
     assert torch.equal(W2t.view(torch.int16), W2.T.contiguous().view(torch.int16))
+
+
+@pytest.mark.parametrize("M,K,beta", [(128, 64, 0.0), (1024, 4096, 0.0), (1000, 136, 0.0), (24, 40, 0.0),
+                                      (1024, 1024, -4.775), (640, 72, 3.0)])
+def test_ns_gemm_symmetric(M, K, beta):
+    """rsdb_ns_gemm_bf16_sym: W W^T (and c A A + b A with A symmetric):
+    upper-triangle tiles + mirror; C exactly symmetric, every element within
+    the bound, including the mirrored ones."""
+    W = _mat(M, K, _ld(K, 0), 7)
+    if beta != 0.0:  # A symmetric operand, D = A
+        A0 = (W.float() @ W.float().T / K).to(torch.bfloat16)
+        W = A0
+        K = M
+    C = torch.full((M, _ld(M, 0)), float("nan"), device="cuda", dtype=torch.bfloat16)[:, :M]
+    alpha = 2.0315 if beta != 0.0 else 1.0
+    R.ns_gemm_bf16_sym(W, W, C, alpha, beta, W if beta != 0.0 else None)
+    torch.cuda.synchronize()
+    ref = alpha * (W.float() @ W.float().T)
+    mag = abs(alpha) * (W.float().abs() @ W.float().abs().T)
+    if beta != 0.0:
+        ref = ref + beta * W.float()
+        mag = mag + abs(beta) * W.float().abs()
+    assert torch.isfinite(C.float()).all()
+    assert torch.equal(C.view(torch.int16), C.T.contiguous().view(torch.int16))
+    err = (C.float() - ref).abs()
+    assert (err <= 2.0 ** -8 * ref.abs() + 2 * K * 2.0 ** -24 * mag + 1e-30).all()
 
 
 def test_ns_gemm_rejects_bad_arguments():
