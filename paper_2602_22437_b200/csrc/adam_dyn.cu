@@ -76,9 +76,13 @@ static cudaError_t ensure_dyn_tables() {
 // lane-replicated map: entry k of this lane's copy
 __device__ __forceinline__ float rmap(const float* rep, int k, int lane) { return rep[(k << 5) | lane]; }
 
-// candidate position of a = |y| <= 1 among the map's positive decade values
-// (R25 closed form): first index of decade i is base + 2^(i+w) - 1 with w = 0
-// (signed: the 127 positive values start at 128) or 1 (unsigned: start at 1)
+// Candidate position of a = |y| <= 1 among the map's positive decade values
+// (R25 closed form; decade i holds 2^(i+w) equally spaced values of
+// [0.1 D_i, D_i], w = 0 signed / 1 unsigned, whose first index is 128 + 2^i - 1
+// (signed) or 2^(i+1) - 1 (unsigned)).  Plain fp32 operations (_rn: no FMA
+// contraction) so tests/test_oracle_codemap.py can replay it bit for bit:
+// for EVERY fp32 y in [-1, 1] the true hi (first index with map >= y,
+// clamped to [1, 255]) lies within one of the clamped candidate.
 template <bool SIGNED>
 __device__ __forceinline__ int dyn_candidate(float a) {
   constexpr int W = SIGNED ? 0 : 1;
@@ -87,35 +91,43 @@ __device__ __forceinline__ int dyn_candidate(float a) {
   const float Dinv = i == 0 ? 1e6f : i == 1 ? 1e5f : i == 2 ? 1e4f : i == 3 ? 1e3f : i == 4 ? 1e2f
                    : i == 5 ? 1e1f : 1.f;
   const int cnt = 1 << (i + W);
-  const float t = fmaf(a, Dinv, -0.1f) * (float(cnt) * (1.f / 0.9f)) - 0.5f;
-  int j = __float2int_rn(t);
+  float u = __fsub_rn(__fmul_rn(a, Dinv), 0.1f);
+  u = __fmul_rn(__fmul_rn(u, __int2float_rn(cnt)), 1.0f / 0.9f);
+  int j = __float2int_rn(__fsub_rn(u, 0.5f));
   j = j < 0 ? 0 : (j >= cnt ? cnt - 1 : j);
-  return (SIGNED ? 127 : 0) + cnt + j;  // signed: 127 + 2^i + j ; unsigned: 2^(i+1) - 1 + j + 1
+  return (SIGNED ? 127 : 0) + cnt + j;
 }
 
-// nearest map value of y (R25, the oracle's fp32 rule; ties -> lower code)
+// nearest map value of y (R25, the oracle's fp32 rule; ties -> lower code),
+// branch free: hi is one of c-1, c, c+1 (c the clamped candidate), decided by
+// two comparisons on the exact map values map[c-2 .. c+1] (4 conflict-free
+// lookups in this lane's copy)
 template <bool SIGNED>
 __device__ __forceinline__ uint32_t dyn_code(const float* rep, int lane, float y) {
-  int k;
+  int c;
   if (SIGNED) {
     const int p = dyn_candidate<true>(fabsf(y));
-    k = y < 0.f ? 254 - p + 1 : p;  // -map[p] sits at 254 - p; hi is the index after it
+    c = y < 0.f ? 255 - p : p;  // -map[p] sits at 254 - p; hi is the index after it
   } else {
-    k = dyn_candidate<false>(y);
+    c = dyn_candidate<false>(y);
   }
-  k = k < 1 ? 1 : (k > 255 ? 255 : k);
-  float hi = rmap(rep, k, lane), lo = rmap(rep, k - 1, lane);
-  while (hi < y && k < 255) {  // exact: hi = first index with map[hi] >= y, clamped
-    ++k;
-    lo = hi;
-    hi = rmap(rep, k, lane);
-  }
-  while (lo >= y && k > 1) {
-    --k;
-    hi = lo;
-    lo = rmap(rep, k - 1, lane);
-  }
-  return uint32_t(__fsub_rn(hi, y) < __fsub_rn(y, lo) ? k : k - 1);
+  c = c < 2 ? 2 : (c > 254 ? 254 : c);
+  const float* q = rep + ((c - 2) << 5) + lane;
+  const float v0 = q[0], v1 = q[32], v2 = q[64], v3 = q[96];
+  const bool a1 = v1 >= y, a2 = v2 >= y;
+  const int hi = a1 ? c - 1 : (a2 ? c : c + 1);
+  const float hv = a1 ? v1 : (a2 ? v2 : v3);
+  const float lv = a1 ? v0 : (a2 ? v1 : v2);
+  return uint32_t(__fsub_rn(hv, y) < __fsub_rn(y, lv) ? hi : hi - 1);
+}
+
+// y = fl32(x / A) through fp64: float(double(x) * RN64(1/A)) -- the relative
+// error of the double product (< 2^-51.9) is below the distance of any
+// quotient of two floats to a float rounding boundary (>= 2^-49 relative),
+// so this is exactly the IEEE fp32 quotient the oracle takes (no slow path,
+// no branch); rA = 1.0 / double(A) once per block
+__device__ __forceinline__ float div_exact(float x, double rA) {
+  return __double2float_rn(__dmul_rn(double(x), rA));
 }
 
 struct DynSmem {
@@ -123,7 +135,7 @@ struct DynSmem {
 };
 
 template <bool PARAM_BF16>
-__global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __restrict__ tbl, int64_t nblocks,
+__global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* __restrict__ tbl, int64_t nblocks,
                                                           AdamPtrs P, AdamScalars s) {
   extern __shared__ __align__(16) float dyn_smem[];
   DynSmem& T = *reinterpret_cast<DynSmem*>(dyn_smem);
@@ -146,11 +158,16 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
     float* rm = red_m[it & 1];
     float* rv = red_v[it & 1];
     // R27: A = 0, NaN or +inf -> the code of 0 everywhere
-    auto qm = [&](float m, float am) {
-      return am > 0.f && am <= FLT_MAX_F ? dyn_code<true>(mapm, lane, __fdiv_rn(m, am)) : zero_m;
-    };
-    auto qv = [&](float v, float av) {
-      return av > 0.f && av <= FLT_MAX_F ? dyn_code<false>(mapv, lane, __fdiv_rn(v, av)) : zero_v;
+    // block-uniform: A finite and > 0 (else the code of 0), 1/A in fp64
+    double rAm = 0.0, rAv = 0.0;
+    bool okm = false, okv = false;
+    auto qm = [&](float m, float) { return okm ? dyn_code<true>(mapm, lane, div_exact(m, rAm)) : zero_m; };
+    auto qv = [&](float v, float) { return okv ? dyn_code<false>(mapv, lane, div_exact(v, rAv)) : zero_v; };
+    auto set_div = [&](float am_, float av_) {
+      okm = am_ > 0.f && am_ <= FLT_MAX_F;
+      okv = av_ > 0.f && av_ <= FLT_MAX_F;
+      rAm = okm ? 1.0 / double(am_) : 0.0;
+      rAv = okv ? 1.0 / double(av_) : 0.0;
     };
     float am = 0.f, av = 0.f;
     const bool fast = blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
@@ -181,6 +198,7 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
         }
       }
       block_max2<G::WARPS>(am, av, rm, rv);
+      set_div(am, av);
 #pragma unroll
       for (int k = 0; k < G::Q; ++k) {
         const int a = G::quad(k);
@@ -229,6 +247,7 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
           }
         }
         block_max2<G::WARPS>(am, av, rm, rv);
+        set_div(am, av);
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
           const int i = int(threadIdx.x) + e * DYN_NT;
@@ -242,6 +261,7 @@ __global__ void __launch_bounds__(DYN_NT) adam8_dyn_kernel(const AdamBlock* __re
           av = fmax_nan(av, v);
         }
         block_max2<G::WARPS>(am, av, rm, rv);
+        set_div(am, av);
         for (int i = threadIdx.x; i < blk.len; i += DYN_NT) {
           float m, v;
           const float p = elem(i, m, v);

@@ -281,6 +281,7 @@ static rsdb_status build_unit(const rsdb::Layout& L, rsdb_comm* comm, int32_t ra
   u->rank = rank;
   u->bufs = bufs;
   u->nblocks = int64_t(qb.size());
+  u->has_tiles = std::any_of(qb.begin(), qb.end(), [](const rsdb::QTile& t) { return t.rows > 1; });
   auto iv = rsdb::padding_intervals(L);
   std::vector<int64_t> pad;
   for (auto& [a, b] : iv) pad.push_back(a), pad.push_back(b);
@@ -421,7 +422,7 @@ rsdb_status rsdb_step_8bit_adam(rsdb_unit* u, const rsdb_adam_state* st, const r
                    static_cast<float*>(st->v_absmax),    static_cast<const float*>(u->bufs.grad_f32),
                    param_target(u),                      u->L.elem_bytes == 2};
   CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, p, s,
-                              0, S_(stream)));
+                              u->has_tiles, S_(stream)));
   return OK_CLEAR();
 }
 
@@ -919,6 +920,7 @@ static rsdb_status dbuffer_create_impl(const rsdb_layout* const* units, int32_t 
     }
     db->m = L.m;
     db->rank = rank;
+    db->has_tiles |= unit->has_tiles;
     db->grad_bytes.push_back(int64_t(L.m) * L.S * L.elem_bytes);
     db->units.push_back(std::move(unit));
   }
@@ -1034,7 +1036,7 @@ rsdb_status rsdb_dbuffer_step_8bit_adam(rsdb_dbuffer* d, const rsdb_adam_cfg* cf
                    static_cast<const float*>(d->base[RSDB_KIND_GRAD_F32]),
                    d->base[RSDB_KIND_PARAM_FULL],
                    d->param_bf16};
-  CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(d->blocks.p), d->nblocks, p, s, 0,
+  CUDA_TRY(rsdb::launch_adam8(static_cast<const rsdb::AdamBlock*>(d->blocks.p), d->nblocks, p, s, d->has_tiles,
                               S_(stream)));
   return OK_CLEAR();
 }

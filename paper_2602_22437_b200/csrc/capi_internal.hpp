@@ -83,6 +83,7 @@ struct rsdb_unit {
   rsdb_unit_bufs bufs{};
   int64_t qblock = 0;
   int64_t nblocks = 0;
+  int32_t has_tiles = 0;  // 2-D quantization tiles in the block table (N2)
   int64_t npad = 0;
   DevTable pad;     // int64 lo, hi pairs
   DevTable blocks;  // rsdb::AdamBlock, unit-relative (state = shard, grad/param = +rank*S)
@@ -125,6 +126,7 @@ struct rsdb_dbuffer {
   DevTable blocks_compact;  // rsdb::AdamBlockC over the fused table (flat blocks only), or empty
   DevTable unit_bases;      // rsdb::UnitBase per unit for the compact table
   int32_t n_units = 0;
+  int32_t has_tiles = 0;    // 2-D quantization tiles in the table (N2)
   int32_t m = 1, rank = 0;
   int32_t param_bf16 = 1;
   std::vector<int64_t> grad_bytes;  // per unit, for grouped zero

@@ -295,6 +295,158 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
   }
 }
 
+__device__ __forceinline__ bool pairable(const AdamBlock& b) {
+  return b.len <= ADAM_TILE / 2 && adam_tile_fast(b);
+}
+
+// Tile tables (N2, 32 x 32 quantization blocks): item w = table
+// entries 2w and 2w+1.  Two tiles of <= 1024 elements share one stage (tile A
+// in elements [0, 1024), tile B in [1024, 2048)), staged by every thread with
+// cp.async and updated together (adam_pair_tail).  An item that cannot pair
+// (a 1-D tensor's flat block, an odd tile) stages its first entry like
+// adam8_tma_kernel and updates its second with direct loads.
+template <int NT, bool PARAM_BF16, int STAGES>
+__global__ void __launch_bounds__(NT) adam8_pair_kernel(const AdamBlock* __restrict__ tbl,
+                                                        int64_t nblocks, AdamPtrs P, AdamScalars s) {
+  extern __shared__ __align__(128) uint8_t adam_smem[];
+  AdamStage* stage = reinterpret_cast<AdamStage*>(adam_smem);
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ float red[2][4 * AdamGeom<NT>::WARPS];
+  using G = AdamGeom<NT>;
+  const int64_t nitems = (nblocks + 1) / 2;
+  auto stage_tile = [&](const AdamBlock& nb, int st, int base) {  // this thread's quads of one tile
+#pragma unroll
+    for (int k = 0; k < G::Q; ++k) {
+      const int e0 = G::quad(k) - base;  // element of the tile held by this quad
+      if (e0 >= 0 && e0 < nb.len) {
+        const int64_t a = blk_off(nb, e0);
+        cp_async16(stage[st].p + base + e0, P.master + nb.state_off + a);
+        cp_async16(stage[st].g + base + e0, P.grad + nb.grad_off + a);
+        cp_async4(stage[st].mq + base + e0, P.mq + nb.state_off + a);
+        cp_async4(stage[st].vq + base + e0, P.vq + nb.state_off + a);
+      }
+    }
+  };
+  auto issue = [&](int64_t w, int st) {
+    const AdamBlock a = tbl[2 * w];
+    const bool has_b = 2 * w + 1 < nblocks;
+    if (has_b && pairable(a)) {
+      const AdamBlock b = tbl[2 * w + 1];
+      if (pairable(b)) {
+        stage_tile(a, st, 0);
+        stage_tile(b, st, ADAM_TILE / 2);
+        cp_async_arrive(&full[st]);
+        return;
+      }
+    }
+    if (adam_tma_ok(a)) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
+        bulk_g2s(stage[st].p, P.master + a.state_off, sizeof(float) * ADAM_TILE, &full[st]);
+        bulk_g2s(stage[st].g, P.grad + a.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
+        bulk_g2s(stage[st].mq, P.mq + a.state_off, ADAM_TILE, &full[st]);
+        bulk_g2s(stage[st].vq, P.vq + a.state_off, ADAM_TILE, &full[st]);
+      } else {
+        mbar_arrive(&full[st]);
+      }
+    } else if (a.len <= ADAM_TILE && adam_tile_fast(a)) {
+      stage_tile(a, st, 0);
+      cp_async_arrive(&full[st]);
+    } else {
+      mbar_arrive(&full[st]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], NT);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  for (int st = 0; st < STAGES; ++st) {
+    const int64_t w = blockIdx.x + int64_t(st) * gridDim.x;
+    if (w < nitems) issue(w, st);
+  }
+  int it = 0;
+  for (int64_t w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+    const int st = it % STAGES;
+    const uint32_t ph = uint32_t(it / STAGES) & 1u;
+    float* rd = red[it & 1];
+    auto refill = [&]() {
+      const int64_t nw = w + int64_t(STAGES) * gridDim.x;
+      if (nw < nitems) {
+        if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nw, st);
+      }
+    };
+    mbar_wait(&full[st], ph);
+    const AdamBlock a = tbl[2 * w];
+    const bool has_b = 2 * w + 1 < nblocks;
+    const AdamBlock b = has_b ? tbl[2 * w + 1] : a;
+    if (has_b && pairable(a) && pairable(b)) {
+      adam_pair_tail<NT, PARAM_BF16>(stage[st], a, b, P, s, rd, refill);
+      continue;
+    }
+    // unpaired item: the first entry from the stage (or direct), the second direct
+    float* rm = rd;
+    float* rv = rd + G::WARPS;
+    {
+      const float sm = P.mabs[a.slot] / 127.0f, sv = P.vabs[a.slot] / 255.0f;
+      BlockRegs<NT> r;
+      if (adam_tma_ok(a)) {
+        load_fast<NT, false>(r, stage[st].p, stage[st].g, stage[st].mq, stage[st].vq, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 1>(r, a, P, s, rm, rv, refill);
+      } else if (a.len <= ADAM_TILE && adam_tile_fast(a)) {
+        load_fast<NT, false>(r, stage[st].p, stage[st].g, stage[st].mq, stage[st].vq, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 2>(r, a, P, s, rm, rv, refill);
+      } else if (a.len <= ADAM_TILE && adam_fast(a)) {
+        load_fast<NT, true>(r, P.master + a.state_off, P.grad + a.grad_off, P.mq + a.state_off,
+                            P.vq + a.state_off, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 1>(r, a, P, s, rm, rv, refill);
+      } else if (a.len <= ADAM_TILE) {
+        load_generic<NT>(r, a, P, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 0>(r, a, P, s, rm, rv, refill);
+      } else {
+        adam_block_two_pass<NT, PARAM_BF16>(a, sm, sv, P, s, rm, rv, refill, GradF32{P.grad + a.grad_off});
+      }
+    }
+    if (has_b) {
+      // the reduction slots of the first entry may still be read: use the other pair
+      float* rm2 = red[(it + 1) & 1];
+      float* rv2 = rm2 + G::WARPS;
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+      const float sm = P.mabs[b.slot] / 127.0f, sv = P.vabs[b.slot] / 255.0f;
+      BlockRegs<NT> r;
+      if (b.len <= ADAM_TILE && adam_fast(b)) {
+        load_fast<NT, true>(r, P.master + b.state_off, P.grad + b.grad_off, P.mq + b.state_off,
+                            P.vq + b.state_off, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 1>(r, b, P, s, rm2, rv2, NoHook{});
+      } else if (b.len <= ADAM_TILE && adam_tile_fast(b)) {
+        load_tile<NT>(r, b, P, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 2>(r, b, P, s, rm2, rv2, NoHook{});
+      } else if (b.len <= ADAM_TILE) {
+        load_generic<NT>(r, b, P, sm, sv);
+        adam_block_tail<NT, PARAM_BF16, 0>(r, b, P, s, rm2, rv2, NoHook{});
+      } else {
+        adam_block_two_pass<NT, PARAM_BF16>(b, sm, sv, P, s, rm2, rv2, NoHook{}, GradF32{P.grad + b.grad_off});
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    }
+  }
+}
+
+template <int NT, bool BF, int ST>
+static cudaError_t launch_adam8_pair(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
+                                     const AdamScalars& s, cudaStream_t st) {
+  const size_t smem = sizeof(AdamStage) * ST;
+  static int occ = [&] {
+    cudaFuncSetAttribute(adam8_pair_kernel<NT, BF, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    return resident_blocks(adam8_pair_kernel<NT, BF, ST>, NT, smem);
+  }();
+  const int64_t items = (nblocks + 1) / 2;
+  const int64_t blocks = std::min<int64_t>(items, int64_t(num_sms()) * occ);
+  adam8_pair_kernel<NT, BF, ST><<<blocks, NT, smem, st>>>(tbl, nblocks, p, s);
+  return cudaGetLastError();
+}
+
 template <int NT, bool BF, int ST>
 static cudaError_t launch_adam8_tma(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
                                     const AdamScalars& s, cudaStream_t st) {
@@ -314,8 +466,11 @@ static cudaError_t launch_adam8_tma(const AdamBlock* tbl, int64_t nblocks, const
 // stages, profiles/r1/).  Blocks it cannot bulk-load (tails,
 // misaligned, 2-D tiles, longer than 2048) take its direct-load paths.
 cudaError_t launch_adam8(const AdamBlock* table_dev, int64_t nblocks, const AdamPtrs& p,
-                         const AdamScalars& s, int32_t /*max_len*/, cudaStream_t st) {
+                         const AdamScalars& s, int32_t tiles, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
+  if (tiles)  // 2-D quantization tiles (N2): two tiles per stage
+    return p.param_bf16 ? launch_adam8_pair<128, true, 3>(table_dev, nblocks, p, s, st)
+                        : launch_adam8_pair<128, false, 3>(table_dev, nblocks, p, s, st);
   return p.param_bf16 ? launch_adam8_tma<128, true, 3>(table_dev, nblocks, p, s, st)
                       : launch_adam8_tma<128, false, 3>(table_dev, nblocks, p, s, st);
 }

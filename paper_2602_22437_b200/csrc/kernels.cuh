@@ -46,9 +46,10 @@ struct AdamPtrs {
 cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t n, float scale,
                               const int64_t* pad_dev, int32_t npad, cudaStream_t st);
 
-// a8 over `nblocks` table entries.
+// a8 over `nblocks` table entries; tiles != 0: the table holds 2-D tiles
+// (N2), updated two per stage (adam8_pair_kernel).
 cudaError_t launch_adam8(const AdamBlock* table_dev, int64_t nblocks, const AdamPtrs& p,
-                         const AdamScalars& s, int32_t max_len, cudaStream_t st);
+                         const AdamScalars& s, int32_t tiles, cudaStream_t st);
 
 struct CopySeg {
   const void* src;

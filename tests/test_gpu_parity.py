@@ -353,6 +353,10 @@ TILE_CASES = [
     ([(2048, 512), (512,), (100, 96)], [("tile", 512, 32, 32), ("flat", 512), ("tile", 96, 32, 32)], 32, 3, 2),
     ([(256, 128)], [("tile", 128, 128, 128)], 128, 2, 0),          # 128x128 tiles: two-pass path
     ([(64, 30), (40, 66)], [("tile", 30, 8, 5), ("tile", 66, 8, 6)], 8, 2, 1),  # masked strided path
+    # Llama-like mix at world 1: many tile pairs, a flat block between tensors
+    # (unpaired items), a 1-row tail tile
+    ([(128, 2048), (2048,), (64, 512), (33, 64)],
+     [("tile", 2048, 32, 32), ("flat", 2048), ("tile", 512, 32, 32), ("tile", 64, 32, 32)], 32, 1, 0),
 ]
 
 
