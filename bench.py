@@ -228,11 +228,15 @@ class NvlinkCounters:
                     fid = getattr(N, f)
                     vals = N.nvmlDeviceGetFieldValues(self.h, [(fid, link) for link in range(18)])
                     tot, n = 0, 0
+                    codes = set()
                     for v in vals:
+                        codes.add(int(v.nvmlReturn))
                         if v.nvmlReturn == 0:
                             tot += int(v.value.ullVal)
                             n += 1
                     out[f"{name}_{d}"] = tot * unit if n else None
+                    if not n:
+                        out[f"{name}_{d}_nvml_return"] = sorted(codes)  # 3 = NOT_SUPPORTED
             except Exception as e:
                 out[f"{name}_error"] = f"{type(e).__name__}: {e}"
         return out
@@ -777,7 +781,9 @@ def run_ours(args):
     nvlink = None
     if nvl is not None:
         nvlink = {"rank": rank, "counters": NvlinkCounters.delta(nvl0, nvl1, K),
-                  "error": nvl.err, "algorithmic_wire_in_bytes_per_step": wire_rank,
+                  "error": nvl.err, "nvml_raw": nvl1, "algorithmic_wire_in_bytes_per_step": wire_rank,
+                  "ncu": "profiles/r2/ (nvlrx__bytes / nvltx__bytes of the fused kernel, rank 0 "
+                         "under ncu: scripts/ncu_nvlink_rank0.sh)",
                   "note": "NVML NVLink counters of this rank's GPU around the timed region "
                           "(all links; data = payload KiB counters, bytes = raw link bytes)"}
         if nvlink["counters"]:

@@ -86,15 +86,20 @@ __device__ __forceinline__ float rmap(const float* rep, int k, int lane) { retur
 template <bool SIGNED>
 __device__ __forceinline__ int dyn_candidate(float a) {
   constexpr int W = SIGNED ? 0 : 1;
-  const int i = int(a >= 1e-6f) + int(a >= 1e-5f) + int(a >= 1e-4f) + int(a >= 1e-3f) + int(a >= 1e-2f) +
-                int(a >= 1e-1f);
-  const float Dinv = i == 0 ? 1e6f : i == 1 ? 1e5f : i == 2 ? 1e4f : i == 3 ? 1e3f : i == 4 ? 1e2f
-                   : i == 5 ? 1e1f : 1.f;
-  const int cnt = 1 << (i + W);
+  // decade i = #{thresholds 1e-6 .. 1e-1 <= a}: a select cascade (no jump
+  // table), Dinv = 10^(6-i) and cnt = 2^(i+W) carried along exactly
+  float Dinv = 1.f;
+  int cnt = 1 << (6 + W);
+  if (a < 1e-1f) Dinv = 1e1f, cnt = 1 << (5 + W);
+  if (a < 1e-2f) Dinv = 1e2f, cnt = 1 << (4 + W);
+  if (a < 1e-3f) Dinv = 1e3f, cnt = 1 << (3 + W);
+  if (a < 1e-4f) Dinv = 1e4f, cnt = 1 << (2 + W);
+  if (a < 1e-5f) Dinv = 1e5f, cnt = 1 << (1 + W);
+  if (a < 1e-6f) Dinv = 1e6f, cnt = 1 << W;
   float u = __fsub_rn(__fmul_rn(a, Dinv), 0.1f);
   u = __fmul_rn(__fmul_rn(u, __int2float_rn(cnt)), 1.0f / 0.9f);
   int j = __float2int_rn(__fsub_rn(u, 0.5f));
-  j = j < 0 ? 0 : (j >= cnt ? cnt - 1 : j);
+  j = min(max(j, 0), cnt - 1);
   return (SIGNED ? 127 : 0) + cnt + j;
 }
 

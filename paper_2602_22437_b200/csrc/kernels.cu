@@ -195,14 +195,6 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Persistent, STAGES-deep prefetch ring in shared memory, one 2048-element
-// stage per block.  Every stage's mbarrier expects NT arrivals: a full
-// contiguous block is fetched by thread 0 with four 1-D bulk copies (TMA,
-// complete_tx) while the other threads just arrive; a 2-D tile (N2, the
-// paper's 32 x 32 blocks) is fetched by every thread with cp.async --
-// each 4-element quad from its own row address into the stage's flat
-// element order -- and cp.async.mbarrier.arrive; other blocks (tails,
-// misaligned, > 2048) are loaded directly by the consumer.
 template <int NT, bool PARAM_BF16, int STAGES>
 __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restrict__ tbl,
                                                        int64_t nblocks, AdamPtrs P, AdamScalars s) {
@@ -210,47 +202,29 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
   AdamStage* stage = reinterpret_cast<AdamStage*>(adam_smem);
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ float red_m[2][AdamGeom<NT>::WARPS], red_v[2][AdamGeom<NT>::WARPS];
-  using G = AdamGeom<NT>;
 
-  // every thread: its part of filling stage `st` with block b
+  // thread 0 fills stage `st` with block b (or just arrives if b is not TMA-able)
   auto issue = [&](int64_t b, int st) {
     const AdamBlock nb = tbl[b];
     if (adam_tma_ok(nb)) {
-      if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
-        bulk_g2s(stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
-        bulk_g2s(stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
-        bulk_g2s(stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
-        bulk_g2s(stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
-      } else {
-        mbar_arrive(&full[st]);
-      }
-    } else if (nb.len <= ADAM_TILE && adam_tile_fast(nb)) {
-#pragma unroll
-      for (int k = 0; k < G::Q; ++k) {
-        const int e0 = G::quad(k);
-        if (e0 < nb.len) {
-          const int64_t a = blk_off(nb, e0);
-          cp_async16(stage[st].p + e0, P.master + nb.state_off + a);
-          cp_async16(stage[st].g + e0, P.grad + nb.grad_off + a);
-          cp_async4(stage[st].mq + e0, P.mq + nb.state_off + a);
-          cp_async4(stage[st].vq + e0, P.vq + nb.state_off + a);
-        }
-      }
-      cp_async_arrive(&full[st]);
+      mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
+      bulk_g2s(stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
+      bulk_g2s(stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
     } else {
       mbar_arrive(&full[st]);
     }
   };
   if (threadIdx.x == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], NT);
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < STAGES; ++st) {
+      const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
+      if (b < nblocks) issue(b, st);
+    }
   }
   __syncthreads();
-  for (int st = 0; st < STAGES; ++st) {
-    const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
-    if (b < nblocks) issue(b, st);
-  }
   int it = 0;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
     const int st = it % STAGES;
@@ -263,10 +237,12 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
     // refill this stage with block b + STAGES*grid once every thread has
     // consumed it (called right after the absmax barrier)
     auto refill = [&]() {
-      const int64_t nb = b + int64_t(STAGES) * gridDim.x;
-      if (nb < nblocks) {
-        if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads -> async writes
-        issue(nb, st);
+      if (threadIdx.x == 0) {
+        const int64_t nb = b + int64_t(STAGES) * gridDim.x;
+        if (nb < nblocks) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async writes
+          issue(nb, st);
+        }
       }
     };
     mbar_wait(&full[st], ph);
@@ -281,9 +257,8 @@ __global__ void __launch_bounds__(NT) adam8_tma_kernel(const AdamBlock* __restri
         load_fast<NT, true>(r, P.master + blk.state_off, P.grad + blk.grad_off,
                             P.mq + blk.state_off, P.vq + blk.state_off, sm, sv);
         adam_block_tail<NT, PARAM_BF16, 1>(r, blk, P, s, rm, rv, refill);
-      } else if (adam_tile_fast(blk)) {  // staged by cp.async (quads past len: garbage, masked)
-        const AdamStage& S = stage[st];
-        load_fast<NT, false>(r, S.p, S.g, S.mq, S.vq, sm, sv);
+      } else if (adam_tile_fast(blk)) {
+        load_tile<NT>(r, blk, P, sm, sv);
         adam_block_tail<NT, PARAM_BF16, 2>(r, blk, P, s, rm, rv, refill);
       } else {
         load_generic<NT>(r, blk, P, sm, sv);
@@ -299,18 +274,29 @@ __device__ __forceinline__ bool pairable(const AdamBlock& b) {
   return b.len <= ADAM_TILE / 2 && adam_tile_fast(b);
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
 // Tile tables (N2, 32 x 32 quantization blocks): item w = table
 // entries 2w and 2w+1.  Two tiles of <= 1024 elements share one stage (tile A
 // in elements [0, 1024), tile B in [1024, 2048)), staged by every thread with
 // cp.async and updated together (adam_pair_tail).  An item that cannot pair
 // (a 1-D tensor's flat block, an odd tile) stages its first entry like
 // adam8_tma_kernel and updates its second with direct loads.
+// Latency: the table entries of the item a stage will hold next are loaded
+// into registers at the START of the current item (their latency hides under
+// its update), and the item's four absmax values travel with the stage
+// (cp.async into ent_abs, completing on the stage's mbarrier), so the update
+// of an item never waits on a dependent global load.
 template <int NT, bool PARAM_BF16, int STAGES>
-__global__ void __launch_bounds__(NT) adam8_pair_kernel(const AdamBlock* __restrict__ tbl,
+__global__ void __launch_bounds__(NT, 4) adam8_pair_kernel(const AdamBlock* __restrict__ tbl,
                                                         int64_t nblocks, AdamPtrs P, AdamScalars s) {
   extern __shared__ __align__(128) uint8_t adam_smem[];
   AdamStage* stage = reinterpret_cast<AdamStage*>(adam_smem);
   __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ AdamBlock ent[STAGES][2];
+  __shared__ __align__(16) float ent_abs[STAGES][4];  // m_A, v_A, m_B, v_B
   __shared__ float red[2][4 * AdamGeom<NT>::WARPS];
   using G = AdamGeom<NT>;
   const int64_t nitems = (nblocks + 1) / 2;
@@ -327,34 +313,33 @@ __global__ void __launch_bounds__(NT) adam8_pair_kernel(const AdamBlock* __restr
       }
     }
   };
-  auto issue = [&](int64_t w, int st) {
-    const AdamBlock a = tbl[2 * w];
-    const bool has_b = 2 * w + 1 < nblocks;
-    if (has_b && pairable(a)) {
-      const AdamBlock b = tbl[2 * w + 1];
-      if (pairable(b)) {
-        stage_tile(a, st, 0);
-        stage_tile(b, st, ADAM_TILE / 2);
-        cp_async_arrive(&full[st]);
-        return;
+  // every thread, entries a (and b if has_b) of the item going into stage st
+  auto issue = [&](const AdamBlock a, const AdamBlock b, bool has_b, int st) {
+    if (threadIdx.x == 0) {
+      ent[st][0] = a;
+      ent[st][1] = b;
+      cp_async4(&ent_abs[st][0], P.mabs + a.slot);
+      cp_async4(&ent_abs[st][1], P.vabs + a.slot);
+      if (has_b) {
+        cp_async4(&ent_abs[st][2], P.mabs + b.slot);
+        cp_async4(&ent_abs[st][3], P.vabs + b.slot);
       }
     }
-    if (adam_tma_ok(a)) {
+    if (has_b && pairable(a) && pairable(b)) {
+      stage_tile(a, st, 0);
+      stage_tile(b, st, ADAM_TILE / 2);
+    } else if (adam_tma_ok(a)) {
       if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
+        mbar_expect_tx(&full[st], ADAM_STAGE_TX);
         bulk_g2s(stage[st].p, P.master + a.state_off, sizeof(float) * ADAM_TILE, &full[st]);
         bulk_g2s(stage[st].g, P.grad + a.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
         bulk_g2s(stage[st].mq, P.mq + a.state_off, ADAM_TILE, &full[st]);
         bulk_g2s(stage[st].vq, P.vq + a.state_off, ADAM_TILE, &full[st]);
-      } else {
-        mbar_arrive(&full[st]);
       }
     } else if (a.len <= ADAM_TILE && adam_tile_fast(a)) {
       stage_tile(a, st, 0);
-      cp_async_arrive(&full[st]);
-    } else {
-      mbar_arrive(&full[st]);
     }
+    cp_async_arrive(&full[st]);  // NT arrivals per phase, each when its thread's copies land
   };
   if (threadIdx.x == 0) {
     for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], NT);
@@ -363,33 +348,46 @@ __global__ void __launch_bounds__(NT) adam8_pair_kernel(const AdamBlock* __restr
   __syncthreads();
   for (int st = 0; st < STAGES; ++st) {
     const int64_t w = blockIdx.x + int64_t(st) * gridDim.x;
-    if (w < nitems) issue(w, st);
+    if (w < nitems) {
+      const bool hb = 2 * w + 1 < nblocks;
+      const AdamBlock a = tbl[2 * w];
+      issue(a, hb ? tbl[2 * w + 1] : a, hb, st);
+    }
   }
   int it = 0;
   for (int64_t w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
     const int st = it % STAGES;
     const uint32_t ph = uint32_t(it / STAGES) & 1u;
     float* rd = red[it & 1];
+    // the entries of the item this stage holds next: loads issued now, used in refill
+    const int64_t nw = w + int64_t(STAGES) * gridDim.x;
+    const bool has_next = nw < nitems;
+    const bool nhb = 2 * nw + 1 < nblocks;
+    AdamBlock na{}, nbb{};
+    if (has_next) {
+      na = tbl[2 * nw];
+      nbb = nhb ? tbl[2 * nw + 1] : na;
+    }
     auto refill = [&]() {
-      const int64_t nw = w + int64_t(STAGES) * gridDim.x;
-      if (nw < nitems) {
+      if (has_next) {
         if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(nw, st);
+        issue(na, nbb, nhb, st);
       }
     };
     mbar_wait(&full[st], ph);
-    const AdamBlock a = tbl[2 * w];
+    const AdamBlock a = ent[st][0];
     const bool has_b = 2 * w + 1 < nblocks;
-    const AdamBlock b = has_b ? tbl[2 * w + 1] : a;
+    const AdamBlock b = ent[st][1];
+    const float4 ab = *reinterpret_cast<const float4*>(ent_abs[st]);
     if (has_b && pairable(a) && pairable(b)) {
-      adam_pair_tail<NT, PARAM_BF16>(stage[st], a, b, P, s, rd, refill);
+      adam_pair_tail<NT, PARAM_BF16>(stage[st], a, b, ab.x, ab.y, ab.z, ab.w, P, s, rd, refill);
       continue;
     }
     // unpaired item: the first entry from the stage (or direct), the second direct
     float* rm = rd;
     float* rv = rd + G::WARPS;
     {
-      const float sm = P.mabs[a.slot] / 127.0f, sv = P.vabs[a.slot] / 255.0f;
+      const float sm = ab.x / 127.0f, sv = ab.y / 255.0f;
       BlockRegs<NT> r;
       if (adam_tma_ok(a)) {
         load_fast<NT, false>(r, stage[st].p, stage[st].g, stage[st].mq, stage[st].vq, sm, sv);
@@ -409,11 +407,11 @@ __global__ void __launch_bounds__(NT) adam8_pair_kernel(const AdamBlock* __restr
       }
     }
     if (has_b) {
-      // the reduction slots of the first entry may still be read: use the other pair
+      // the first entry's reduction slots may still be read: the other pair, fenced by barriers
       float* rm2 = red[(it + 1) & 1];
       float* rv2 = rm2 + G::WARPS;
       asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-      const float sm = P.mabs[b.slot] / 127.0f, sv = P.vabs[b.slot] / 255.0f;
+      const float sm = ab.z / 127.0f, sv = ab.w / 255.0f;
       BlockRegs<NT> r;
       if (b.len <= ADAM_TILE && adam_fast(b)) {
         load_fast<NT, true>(r, P.master + b.state_off, P.grad + b.grad_off, P.mq + b.state_off,
@@ -468,9 +466,9 @@ static cudaError_t launch_adam8_tma(const AdamBlock* tbl, int64_t nblocks, const
 cudaError_t launch_adam8(const AdamBlock* table_dev, int64_t nblocks, const AdamPtrs& p,
                          const AdamScalars& s, int32_t tiles, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
-  if (tiles)  // 2-D quantization tiles (N2): two tiles per stage
-    return p.param_bf16 ? launch_adam8_pair<128, true, 3>(table_dev, nblocks, p, s, st)
-                        : launch_adam8_pair<128, false, 3>(table_dev, nblocks, p, s, st);
+  if (tiles)  // 2-D quantization tiles (N2): two tiles per stage, 2 stages (occupancy: 4 CTAs/SM)
+    return p.param_bf16 ? launch_adam8_pair<128, true, 2>(table_dev, nblocks, p, s, st)
+                        : launch_adam8_pair<128, false, 2>(table_dev, nblocks, p, s, st);
   return p.param_bf16 ? launch_adam8_tma<128, true, 3>(table_dev, nblocks, p, s, st)
                       : launch_adam8_tma<128, false, 3>(table_dev, nblocks, p, s, st);
 }

@@ -11,6 +11,8 @@ that has a kernel, not only the headline step:
                   32-row granularity) on the whole Llama-3.2-1B DBuffer
   muon_8b_layer   config 3 / N3: one distributed-Muon step (Alg. 2) over the
                   Llama-3-8B decoder layer, Newton-Schulz TFLOP/s
+  fp8_allgather   N2 / config 4: the fused FP8 128x128 quantize + AllGather of
+                  the DSV3 FFN unit (and the bf16 AllGather it replaces, N>1)
   dsv3_ragged_vs_rowwise  config 4: zero-copy RaggedShard AG/RS against the
                   FSDP2 row-wise layout's Copy-Out / Copy-In + collective
   bucket_sweep    config 5: padding and rank-chunk alignment of aligned ragged
@@ -246,6 +248,54 @@ def muon(R, ctx):
             "step_ms": t_full, "step_without_ns_ms": t_zero, "ns_ms": t_ns,
             "ns_tflops_busiest_root": tf, "ns_frac_of_measured_bf16": tf / tc_peak,
             "peak_bf16_tflops": tc_peak}
+
+
+# ---------------------------------------------------------------- N2: FP8 128x128 quantize + AllGather
+def fp8(R, ctx):
+    """DeepSeek-V3 FFN unit (27 matrices, 128-row granularity, 1-byte
+    elements): the fused FP8 quantize + AllGather kernel against
+    the bf16 AllGather of the same weights."""
+    from synth import hashgen as H
+    from synth import workloads as W
+    world, rank, comm, st = ctx["world"], ctx["rank"], ctx["comm"], ctx["stream"]
+    hbm, _ = _peaks()
+    unit = W.dsv3_ffn_fp8_unit()
+    shapes = [t.shape for t in unit.tensors]
+    es = [t.numel for t in unit.tensors]
+    gs = [128 * c for _, c in shapes]
+    specs = [("tile", c, 128, 128) for _, c in shapes]
+    lay = R.plan(es, gs, world, elem_bytes=1)
+    S = lay.S
+    master = H.values_torch(3, H.STREAM_PARAM, rank * S, S, 12, device="cuda")
+    codes = torch.zeros(world * S, dtype=torch.uint8, device="cuda")
+    u0 = R.Fp8Unit(lay, specs, rank, master, codes, torch.empty(1, device="cuda"), comm=comm)
+    ntiles = u0.num_tiles
+    u0.close()
+    scales = torch.zeros(max(1, ntiles), dtype=torch.float32, device="cuda")
+    p2p = R.P2P(comm, [codes, scales]) if world > 1 else None
+    fu = R.Fp8Unit(lay, specs, rank, master, codes, scales, comm=comm)
+    t_fp8 = timed(lambda: fu.quantize_all_gather(p2p, st), ctx["reps"], st, world)
+    out = {"params": sum(es), "tiles": ntiles, "S": S, "fp8_quant_ag_ms": t_fp8,
+           "kernel": "fp8_quant_ag_kernel", "hbm_gbs": 5 * S / t_fp8 / 1e6,
+           "hbm_frac": 5 * S / t_fp8 / 1e6 / hbm, "hbm_bytes": "4 B read + 1 B written per owned element"}
+    fu.close()
+    if p2p is not None:
+        torch.cuda.synchronize()
+        p2p.close()
+        wire = (world - 1) * S
+        out["fp8_wire_gbs"] = wire / t_fp8 / 1e6
+        lay16 = R.plan(es, gs, world, elem_bytes=2)
+        pf = torch.zeros(world * lay16.S, dtype=torch.bfloat16, device="cuda")
+        gf = torch.zeros(world * lay16.S, dtype=torch.bfloat16, device="cuda")
+        g32 = torch.zeros(8, dtype=torch.float32, device="cuda")
+        u16 = R.Unit(lay16, rank, pf, gf, g32.repeat(1), qblock=0, comm=comm)
+        p16 = R.P2P(comm, [pf])
+        t16 = timed(lambda: R.all_gather_p2p(u16, p16, st), ctx["reps"], st, world)
+        torch.cuda.synchronize()
+        p16.close()
+        out.update({"bf16_ag_ms": t16, "speedup_vs_bf16_ag": t16 / t_fp8,
+                    "bf16_ag_wire_gbs": (world - 1) * lay16.S * 2 / t16 / 1e6})
+    return out
 
 
 # ---------------------------------------------------------------- config 4: DSV3 ragged vs row-wise
@@ -500,7 +550,7 @@ def run_all(R, ctx, which=None):
     """ctx: rank, world, comm, stream, db, lays, cfg, t, p2p, reps."""
     out = {}
     items = [("kernels", kernels), ("tiles_32x32", tiles), ("muon_8b_layer", muon),
-             ("dsv3_ragged_vs_rowwise", dsv3), ("bucket_sweep", bucket_sweep)]
+             ("fp8_allgather", fp8), ("dsv3_ragged_vs_rowwise", dsv3), ("bucket_sweep", bucket_sweep)]
     if ctx["world"] > 1:
         items = [("per_unit", per_unit)] + items + [("zero3_overlap", zero3)]
     for name, fn in items:
