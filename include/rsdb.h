@@ -179,7 +179,8 @@ int32_t rsdb_comm_world(const rsdb_comm*);
 void rsdb_comm_free(rsdb_comm*);
 /* Single-device multi-rank mode (testing / debugging the p2p path on one
  * GPU): a communicator for logical rank `rank` of `world` <= 8 ranks that all
- * live in THIS process on the CURRENT device -- one comm per logical rank.
+ * live in THIS process, rank `rank` on the CURRENT device (the ranks may
+ * share one device or be spread over several) -- one comm per logical rank.
  * It has no NCCL communicator: the NCCL entry points (rsdb_all_gather,
  * rsdb_reduce_scatter, rsdb_unit_reduce_scatter_f32) return EINVAL on its
  * units; every p2p / fused / FP8 / Muon / ring call works, through a p2p
@@ -297,11 +298,13 @@ rsdb_status rsdb_ipc_handle(const void* dev_ptr, uint8_t out[RSDB_IPC_BYTES]);
 rsdb_status rsdb_p2p_create(rsdb_comm* comm, int32_t n_bufs, void* const* local_bufs,
                             const int64_t* sizes, const uint8_t* all_handles, rsdb_p2p** out);
 /* Local mode (comm from rsdb_comm_create_local): all_bufs holds world *
- * n_bufs device pointers on the current device, rank-major (all_bufs[r *
- * n_bufs + i] = logical rank r's buffer i; i = 0 the zero-filled signal
+ * n_bufs device pointers, rank-major (all_bufs[r * n_bufs + i] = logical
+ * rank r's buffer i, on rank r's device; i = 0 the zero-filled signal
  * buffers, one per rank); sizes[i] as above, equal for every rank.  Each
- * logical rank creates its own p2p object over the same table.  EMISMATCH if
- * comm is not local. */
+ * logical rank creates its own p2p object over the same table.  Ranks on the
+ * same device share its SMs (grids divided by their number); peer access to
+ * the other devices is enabled (ECUDA if there is no P2P path).  EMISMATCH
+ * if comm is not local. */
 rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* all_bufs,
                                   const int64_t* sizes, rsdb_p2p** out);
 /* Barrier spin limit of the p2p kernels (default 60 s): a kernel whose peer

@@ -575,7 +575,6 @@ rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* 
   auto p = std::make_unique<rsdb_p2p>();
   p->comm = comm;
   p->n = n_bufs;
-  p->grid_div = comm->world;  // every logical rank's kernel must fit on the device at once
   p->peer.assign(size_t(n_bufs), std::vector<char*>(size_t(comm->world), nullptr));
   for (int32_t i = 0; i < n_bufs; ++i) {
     if (sizes[i] < 0) return fail(RSDB_EINVAL, "buffer %d size invalid", i);
@@ -587,6 +586,32 @@ rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* 
     p->local.push_back(p->peer[size_t(i)][size_t(comm->rank)]);
     p->size.push_back(sizes[i]);
   }
+  // logical ranks may live on several devices of this process (one process
+  // driving N GPUs, e.g. to profile one rank's kernel while its peers run):
+  // the grid is shared only among the ranks on this rank's device, and the
+  // other devices' memory is made accessible (peer access over NVLink)
+  int32_t same = 0;
+  for (int32_t r = 0; r < comm->world; ++r) {
+    cudaPointerAttributes at{};
+    CUDA_TRY(cudaPointerGetAttributes(&at, all_bufs[int64_t(r) * n_bufs]));
+    if (at.device == comm->device) {
+      ++same;
+    } else {
+      int ok = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&ok, comm->device, at.device));
+      if (!ok) return fail(RSDB_ECUDA, "device %d cannot access device %d (no P2P path)", comm->device, at.device);
+      int cur = 0;
+      CUDA_TRY(cudaGetDevice(&cur));
+      CUDA_TRY(cudaSetDevice(comm->device));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();  // clear
+      cudaSetDevice(cur);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(RSDB_ECUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", comm->device, at.device,
+                    cudaGetErrorString(e));
+    }
+  }
+  p->grid_div = same < 1 ? 1 : same;
   *out = p.release();
   return OK_CLEAR();
 }
