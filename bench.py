@@ -602,8 +602,8 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{WORKLOAD} per-layer FSDP units (bounded oracle sample)",
-                       "qblock": QBLOCK, "parallelism": f"fsdp{world} (simulated ranks)"},
+            "config": dict(workload_config(args, world),
+                           sample="bounded oracle sample of the layer unit, every simulated rank"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{E} params per step ({blocks} blocks), {world} "
                                        "simulated rank(s), numpy single thread",
@@ -611,6 +611,16 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    """config keys shared by both arms (the reference arm runs the oracle on a
+    bounded sample of THIS workload; its `cpu_baseline.sample` says which)."""
+    units = build_units(args.layers)
+    E = sum(t.numel for u in units for t in u.tensors)
+    return {"workload": f"{WORKLOAD}: {len(units)} FSDP units (root + {args.layers} layers), {E} params, "
+                        "bf16 params/grads, 2048-elem 8-bit Adam blocks, warm synthetic states",
+            "units": len(units), "params": E, "qblock": QBLOCK, "parallelism": f"fsdp{world}"}
 
 
 # ---------------------------------------------------------------- main arm
@@ -820,11 +830,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{WORKLOAD}: {len(lays)} FSDP units (root + {args.layers} "
-                                   f"layers), {E} params, bf16 params/grads, 2048-elem 8-bit "
-                                   "Adam blocks, warm synthetic states",
-                       "units": len(lays), "params": E, "qblock": QBLOCK,
-                       "parallelism": f"fsdp{world}",
+            "config": {**workload_config(args, world),
                        "collectives": args.collectives,
                        "fused": {"dbuffer": "rs+adam, one launch per step",
                                  True: "rs+adam, one launch per unit",

@@ -472,7 +472,7 @@ def zero3(R, ctx, tokens=4096):
     p2p = R.P2P(comm, [t for sl in slots for t in sl[:2]] + [shards])
     p_ag = p2p.channel(1)  # the prefetched AllGathers overlap the RS+Adam kernels: own channel
     cfg = R.AdamConfig()
-    comp, cstream = torch.cuda.Stream(), torch.cuda.Stream()
+    comp, cstream, rstream = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     x = torch.randn(tokens, 2048, device="cuda", dtype=torch.bfloat16)
     wts = [torch.randn(2048, max(1, l.E // 2048), device="cuda", dtype=torch.bfloat16) * 0.01
            for l in lays]
@@ -507,11 +507,15 @@ def zero3(R, ctx, tokens=4096):
                     if j >= n:  # backward: 2x the forward flop
                         y = x @ wts[i]
                         y = x @ wts[i]
-                if j >= n and with_comm:
+                if not (j >= n and with_comm):
+                    ev_free[s].record(comp)
+            if j >= n and with_comm:  # the unit's RS + Adam overlaps the next unit's backward
+                rstream.wait_stream(comp)
+                with torch.cuda.stream(rstream):
                     rus[i].rebind(*slots[s])
-                    R.reduce_scatter_adam_p2p(rus[i], p2p, cfg, t[0], state=states[i], stream=comp)
-                ev_free[s].record(comp)
-                used[s] = True
+                    R.reduce_scatter_adam_p2p(rus[i], p2p, cfg, t[0], state=states[i], stream=rstream)
+                    ev_free[s].record(rstream)
+            used[s] = True
         t[0] += 1
 
     def run(reps, **kw):
@@ -524,6 +528,7 @@ def zero3(R, ctx, tokens=4096):
         for _ in range(reps):
             step(**kw)
         comp.wait_stream(cstream)
+        comp.wait_stream(rstream)
         e1.record(comp)
         torch.cuda.synchronize()
         return _max(e0.elapsed_time(e1) / reps, world)
@@ -538,19 +543,142 @@ def zero3(R, ctx, tokens=4096):
     exposed = max(0.0, t_full - t_comp)
     flop = sum(2 * tokens * 2048 * max(1, l.E // 2048) for l in lays) * 4  # fwd 1x + bwd 3x GEMMs
     return {"schedule": "reshard (ZeRO-3): K=2 slots, AG before forward and before backward, "
-                        "prefetched on a copy-engine stream; fused RS+Adam per unit after its backward",
+                        "prefetched on a copy-engine stream (p2p channel 1); fused RS+Adam per unit on its own stream "
+                        "after the unit's backward, overlapping the next unit's backward",
             "tokens_per_rank": tokens, "synthetic_gemm_tflop": flop / 1e12,
+            "synthetic_gemm_tflops": flop / (t_comp * 1e-3) / 1e12,
             "step_ms": t_full, "compute_only_ms": t_comp, "comm_only_ms": t_comm,
             "exposed_comm_ms": exposed, "exposed_frac_of_comm": exposed / max(t_comm, 1e-9),
             "gathered_bytes_per_rank": K * max_full * 2 * 2,
             "resident_gathered_bytes_per_rank": sum(l.m * l.S for l in lays) * 2 * 2}
 
 
+# ---------------------------------------------------------------- N4: allocation dynamics
+def memory_replay(R, ctx, m=8, steps=3, lag_us=200):
+    """Replays the buffer allocations of one training step of the bench
+    workload (Llama-3.2-1B, 17 units, planned for an FSDP group of m = 8;
+    one GPU holds one rank's buffers) through PyTorch's caching allocator,
+    under three allocation policies, and reports peak RESERVED memory:
+
+      dbuffer       this library's reshard schedule (K-slot ring): K = 2 slots
+                    of gathered parameters / gradients / fp32 reduce buffer
+                    sized for the largest unit, allocated once, reused in
+                    event order -- nothing allocated per step;
+      per_param     FSDP2-style eager per-parameter allocation: per unit and
+                    pass, the AllGather output (m S bf16) on the comm stream,
+                    the unsharded parameters one tensor each (Copy-Out), in
+                    backward one gradient tensor each, the fp32 ReduceScatter
+                    input (m S, Copy-In) and output (S); stream order kept
+                    with events, tensors freed after their last use;
+      record_stream FSDP1 / DeepSpeed-style: the same flat buffers allocated
+                    on the comm stream, consumed on the compute stream and
+                    released through Tensor.record_stream, so a block returns
+                    to the pool only when the allocator sees the compute
+                    stream pass it.
+
+    Compute is a `lag_us` sleep kernel per unit and pass, so the CPU runs
+    ahead of the GPU as in training.  Only the FSDP buffers are replayed (no
+    activations): the paper's 16-30 % is on whole training steps."""
+    import gc
+    world = ctx["world"]
+    if world > 1:
+        return {"skipped": "single-GPU replay (run at N = 1)"}
+    units = __import__("bench").build_units(16)
+    sizes = []
+    for u in units:
+        es = [t.numel for t in u.tensors]
+        gs = [R.block_elems(t.shape, t.gran) for t in u.tensors]
+        lay = R.plan(es, gs, m, elem_bytes=2)
+        sizes.append((lay.S, es))
+    dev = torch.device("cuda")
+    comp, comm_st = torch.cuda.Stream(), torch.cuda.Stream()
+    cycles = int(lag_us * 1.9e3)
+
+    def run(policy):
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_reserved()
+        keep = []
+        if policy == "dbuffer":  # K = 2 reshard slots (the ring schedule), batched, allocated once
+            mx = max(m * S for S, _ in sizes)
+            keep = [torch.empty(mx, dtype=dt, device=dev) for _ in range(2)
+                    for dt in (torch.bfloat16, torch.bfloat16, torch.float32)]
+        for _ in range(steps):
+            for phase in ("fwd", "bwd"):
+                order = range(len(sizes)) if phase == "fwd" else reversed(range(len(sizes)))
+                for ui in order:
+                    S, es = sizes[ui]
+                    if policy == "dbuffer":
+                        with torch.cuda.stream(comp):
+                            torch.cuda._sleep(cycles)
+                        continue
+                    with torch.cuda.stream(comm_st):
+                        comm_st.wait_stream(comp)
+                        ag = torch.empty(m * S, dtype=torch.bfloat16, device=dev)
+                        ag.zero_()
+                    ev = torch.cuda.Event()
+                    ev.record(comm_st)
+                    comp.wait_event(ev)
+                    with torch.cuda.stream(comp):
+                        if policy == "per_param":
+                            params = [torch.empty(e, dtype=torch.bfloat16, device=dev) for e in es]
+                            for p_ in params[:1]:
+                                p_.zero_()
+                        else:
+                            ag.record_stream(comp)
+                        torch.cuda._sleep(cycles)
+                        if phase == "bwd":
+                            if policy == "per_param":
+                                grads = [torch.empty(e, dtype=torch.bfloat16, device=dev) for e in es]
+                                rs_in = torch.empty(m * S, dtype=torch.float32, device=dev)
+                                rs_in.zero_()
+                            else:
+                                grads = [torch.empty(m * S, dtype=torch.bfloat16, device=dev)]
+                                rs_in = None
+                            ev2 = torch.cuda.Event()
+                            ev2.record(comp)
+                    if phase == "bwd":
+                        with torch.cuda.stream(comm_st):
+                            comm_st.wait_event(ev2)
+                            if policy == "per_param":
+                                rs_out = torch.empty(S, dtype=torch.float32, device=dev)
+                                rs_out.zero_()
+                                ev3 = torch.cuda.Event()
+                                ev3.record(comm_st)
+                                comp.wait_event(ev3)  # explicit stream order, no record_stream
+                                del rs_out, rs_in
+                            else:
+                                rs = torch.empty(m * S, dtype=torch.float32, device=dev)
+                                rs.zero_()
+                                grads[0].record_stream(comm_st)
+                                del rs
+                        del grads
+                    if policy == "per_param":
+                        del params
+                    del ag
+        torch.cuda.synchronize()
+        out = {"peak_reserved_bytes": torch.cuda.max_memory_reserved() - base,
+               "peak_allocated_bytes": torch.cuda.max_memory_allocated()}
+        del keep
+        return out
+
+    res = {p: run(p) for p in ("dbuffer", "per_param", "record_stream")}
+    d = res["dbuffer"]["peak_reserved_bytes"]
+    for p in ("per_param", "record_stream"):
+        res[p]["reserved_vs_dbuffer"] = res[p]["peak_reserved_bytes"] / max(1, d)
+    res["workload"] = f"llama-3.2-1b FSDP buffers, m = {m} (one rank), {steps} steps, {lag_us} us compute per unit-pass"
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_all(R, ctx, which=None):
     """ctx: rank, world, comm, stream, db, lays, cfg, t, p2p, reps."""
     out = {}
     items = [("kernels", kernels), ("tiles_32x32", tiles), ("muon_8b_layer", muon),
-             ("fp8_allgather", fp8), ("dsv3_ragged_vs_rowwise", dsv3), ("bucket_sweep", bucket_sweep)]
+             ("fp8_allgather", fp8), ("dsv3_ragged_vs_rowwise", dsv3), ("bucket_sweep", bucket_sweep),
+             ("memory_replay", memory_replay)]
     if ctx["world"] > 1:
         items = [("per_unit", per_unit)] + items + [("zero3_overlap", zero3)]
     for name, fn in items:

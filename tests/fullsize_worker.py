@@ -11,8 +11,10 @@ every unit are checked against the oracle, block by block:
   check         = codes +-1, params 1e-5 (|p|+lr), absmax 1e-6, bf16 shard
 
 Plus, after a second AllGather (or the one fused into the step for the "+ag"
-scopes), every rank holds the identical full parameter buffers (checksum
-all-gather).  FULLSIZE_SCOPE = unit | dbuffer | unit+ag | dbuffer+ag.  Runs standalone (world 1) or under
+scopes): every rank's gathered buffer holds, at every other rank's checked
+blocks, the oracle's updated bf16 parameters (element-wise, same tolerance),
+and the whole gathered arena is byte-identical on every rank (rank 0's
+broadcast over gloo, compared element by element).  FULLSIZE_SCOPE = unit | dbuffer | unit+ag | dbuffer+ag.  Runs standalone (world 1) or under
 torchrun.  Exit 0 iff all checks pass on every rank.
 """
 import os
@@ -78,6 +80,7 @@ def main():
         bench.step(R, db, cfg, 1, st, p2p=p2p, fuse={"unit": True}.get(scope, scope))
     st.synchronize()
     ok, msgs = True, []
+    checked = []  # (unit, global position, len, oracle bf16 bits, oracle master) of every checked block
     ocfg = OA.AdamCfg()
     for ui, b, off, n, logical, pre in picks:
         v = views[ui]
@@ -108,6 +111,7 @@ def main():
         if not good:
             ok = False
             msgs.append(f"unit {ui} block {b}: err {err.max():.2e} dm {dm.max()} dv {dv.max()}")
+        checked.append((ui, rank * lay.S + off, n, ref[5], ref[0]))
     # AllGather: every rank ends with the same full parameter buffers (the
     # "+ag" scopes already did it inside the fused kernel)
     if not scope.endswith("+ag"):
@@ -115,12 +119,27 @@ def main():
             for u in db.units:
                 R.all_gather_p2p(u, p2p, st)
     st.synchronize()
-    h = torch.tensor([float(arenas[0].view(torch.int32).to(torch.int64).sum().item() % (1 << 40))],
-                     dtype=torch.float64)
+    # (1) element-wise against the oracle: every rank's checked blocks, read
+    # from THIS rank's gathered buffer at the owner's shard position
+    allc = [checked]
     if world > 1:
-        hs = [torch.zeros_like(h) for _ in range(world)]
-        dist.all_gather(hs, h)
-        if len(set(x.item() for x in hs)) != 1:
+        allc = [None] * world
+        dist.all_gather_object(allc, checked)
+    for owner, lst in enumerate(allc):
+        for ui, pos, n, ref16, ref32 in lst:
+            got = views[ui]["param_full"][pos:pos + n].view(torch.int16).cpu().numpy().view(np.uint16)
+            gv = OD.bf16_to_f32(got).astype(np.float64)
+            rv = OD.bf16_to_f32(ref16).astype(np.float64)
+            r0 = np.abs(ref32).astype(np.float64)
+            if not np.all(np.abs(gv - rv) <= 1e-5 * (r0 + cfg.lr) + 2.0 ** -7 * r0):
+                ok = False
+                msgs.append(f"gathered block of rank {owner} (unit {ui}, pos {pos}) differs from the oracle")
+    # (2) the whole gathered parameter arena identical on every rank, byte for byte
+    if world > 1:
+        mine = arenas[0].cpu()
+        ref_arena = mine.clone() if rank == 0 else torch.empty_like(mine)
+        dist.broadcast(ref_arena, src=0)
+        if not torch.equal(mine, ref_arena):
             ok = False
             msgs.append("full parameter buffers differ across ranks after AllGather")
     p2p.close()

@@ -352,6 +352,32 @@ def test_extension_entry_points_error_behaviour():
     assert e.value.status == _capi.RSDB_ECUDA
 
 
+def test_round2_entry_points_error_behaviour():
+    """Round-2 entry points check their arguments before any device work:
+    rsdb_ns_gemm_bf16(_sym) (N3), rsdb_dbuffer_step_host, rsdb_p2p_channel,
+    rsdb_unit_create with qblock < 0; valid GEMM arguments without a GPU give
+    ECUDA (no CPU fallback)."""
+    lib = _capi.lib
+    C = __import__("ctypes")
+    f = C.c_float
+    # dimensions / leading dimensions: K < 1, ld not a multiple of 8, ld < row length
+    for args in ((16, 16, 0, 16, 16, 16), (16, 16, 16, 20, 16, 16), (16, 16, 16, 8, 16, 16)):
+        M, N, K, lda, ldb, ldc = args
+        st = lib.rsdb_ns_gemm_bf16(M, N, K, 4096, lda, 4096, ldb, f(1.0), f(0.0), None, 0, 4096, ldc,
+                                   None, 0, None)
+        assert st == _capi.RSDB_EINVAL, args
+    st = lib.rsdb_ns_gemm_bf16(16, 16, 16, 4096, 16, 4096, 16, f(1.0), f(0.0), None, 0, 4096, 16, None, 0, None)
+    assert st == _capi.RSDB_ECUDA
+    assert lib.rsdb_ns_gemm_bf16_sym(16, 16, 4096, 16, 4096, 16, f(1.0), f(2.0), None, 0, 4096, 16,
+                                     None) == _capi.RSDB_EINVAL  # beta != 0 needs D
+    assert lib.rsdb_dbuffer_step_host(None, None, None, 1, None, None, None) == _capi.RSDB_EINVAL
+    out = C.c_void_p()
+    assert lib.rsdb_p2p_channel(None, 1, C.byref(out)) == _capi.RSDB_EINVAL
+    lay = R.plan([4096], [2048], 1)
+    bufs = _capi.UnitBufs(4096, 8192, 16384)
+    assert lib.rsdb_unit_create(lay.handle, None, 0, C.byref(bufs), -1, C.byref(out)) == _capi.RSDB_EINVAL
+
+
 # ------------------------------------------------ header <-> binding agreement
 _STRUCTS = {  # C typedef -> ctypes class in the binding
     "rsdb_qspec": "QSpec", "rsdb_unit_bufs": "UnitBufs", "rsdb_adam_cfg": "AdamCfg",
