@@ -447,6 +447,20 @@ def profile_traffic(kernel):
     return None
 
 
+def profile_nvlink(kernel, world):
+    """NVLink bytes per launch of `kernel` at this world size from the
+    committed ncu capture (profiles/ncu_nvlink.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_nvlink.json")
+    try:
+        with open(p) as f:
+            e = json.load(f).get(kernel)
+        if e and e.get("workload") == WORKLOAD and e.get("n_gpus") == world:
+            return e
+    except Exception:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------- CPU baseline (oracle)
 _ORACLE_INPUTS = {}
 
@@ -742,8 +756,13 @@ def run_ours(args):
             # the peers + its own pushes), so this is the per-direction load.
             wire_in = wire_rs + (wire_ag if fuse_ag else 0)
             ach = wire_in / (rs_ms * 1e-3) / 1e9
+            nv = profile_nvlink(dom, world)
             roof = {"kernel": dom, "bound": "nvlink", "achieved": ach, "peak": NVLINK_PEAK_GBS,
-                    "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "traffic": None,
+                    "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS,
+                    "traffic": nv["nvlrx_bytes_per_launch"] if nv else None,
+                    "traffic_user": nv["nvlrx_user_bytes_per_launch"] if nv else None,
+                    "traffic_source": (nv["source"] + ": ncu nvlrx__bytes (all NVLink bytes in, protocol "
+                                       "included) / nvlrx__bytes_data_user (payload)") if nv else None,
                     "bytes": "physical wire bytes into each rank per launch: (m-1) S 2 gradient "
                              "reads" + (" + (m-1) S 2 parameter pushes from the peers (the fused "
                                         "AllGather)" if fuse_ag else ""),

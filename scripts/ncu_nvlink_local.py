@@ -13,7 +13,10 @@ kernels are already running and its barriers complete.  Without ncu it
 prints per-step CUDA-event times of rank 0's stream and the algorithmic wire
 bytes per rank, so the counters can be compared with them.
 
-  python scripts/ncu_nvlink_local.py [--gpus 2] [--steps 5]
+  CUDA_MODULE_LOADING=EAGER python scripts/ncu_nvlink_local.py [--gpus 2] [--steps 5]
+
+(EAGER: a lazily loaded kernel's module load can wait for a context that a
+peer's barrier kernel keeps busy.)
 """
 import argparse
 import json
@@ -27,6 +30,10 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2602_22437_b200 as R  # noqa: E402
+
+
+def log(msg):
+    print(f"[ncu_nvlink_local] {msg}", file=sys.stderr, flush=True)
 
 
 def main():
@@ -43,9 +50,11 @@ def main():
             comms.append(c)
             lays, db, arenas, views, _, _ = bench.setup(r, n, r, units, c)
             ctx.append((lays, db, arenas, torch.cuda.Stream(device=r)))
+        log(f"rank {r} set up on cuda:{r}")
     p2ps = R.P2P.local_group(comms, [[a[0], a[1]] for _, _, a, _ in ctx])
     for p in p2ps:
-        p.set_timeout(60.0)
+        p.set_timeout(20.0)
+    log("p2p mapped")
     cfg = R.AdamConfig()
     order = list(reversed(range(n)))  # rank 0 last: its (profiled) launch finds the peers running
     for r in order:
@@ -55,6 +64,9 @@ def main():
                 R.all_gather_p2p(u, p2ps[r], st)
     for r in range(n):
         torch.cuda.synchronize(r)
+    for p in p2ps:
+        p.check()
+    log("first AllGather done")
     ev = []
     for t in range(1, args.steps + 1):
         for r in order:
