@@ -690,6 +690,11 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if p2p is not None and world > 1:
+        # align the ranks' streams ON THE DEVICE before the first event: the
+        # host barrier + synchronize leave the ranks' launch times skewed by
+        # milliseconds, which would otherwise be charged to the first step
+        p2p.barrier(stream)
     ev0.record(stream)
     with torch.cuda.stream(stream):
         for i in range(args.steps):

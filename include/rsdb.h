@@ -315,6 +315,11 @@ rsdb_status rsdb_p2p_set_timeout(rsdb_p2p*, double seconds);
 /* Synchronises the device, reads and clears this rank's error flag into
  * *flags (0 = every barrier completed); ECUDA if a barrier timed out. */
 rsdb_status rsdb_p2p_check(rsdb_p2p*, int64_t* flags);
+/* A device-side barrier of every rank on `stream`: when the stream passes
+ * it, every rank's stream has reached its own call (the start / done
+ * barriers of the p2p kernels, with no data).  Same SPMD rule as the
+ * collectives.  EINVAL on a null p2p; world 1: no-op. */
+rsdb_status rsdb_p2p_barrier(rsdb_p2p*, void* stream);
 /* An independent collective channel over p's mappings, for collectives that
  * run concurrently on different streams (e.g. an AllGather prefetched on a
  * copy stream while the compute stream runs a ReduceScatter, "optimized

@@ -457,6 +457,10 @@ class P2P:
         ch.parent = self
         return ch
 
+    def barrier(self, stream=None) -> None:
+        """rsdb_p2p_barrier: device-side barrier of every rank on `stream`."""
+        check(lib.rsdb_p2p_barrier(self._h, _stream(stream)))
+
     def set_timeout(self, seconds: float) -> None:
         check(lib.rsdb_p2p_set_timeout(self._h, float(seconds)))
 

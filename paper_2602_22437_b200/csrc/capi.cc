@@ -698,6 +698,17 @@ rsdb_status rsdb_reduce_scatter_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   return OK_CLEAR();
 }
 
+rsdb_status rsdb_p2p_barrier(rsdb_p2p* p, void* stream) {
+  if (!p) return fail(RSDB_EINVAL, "null p2p");
+  const int m = p->comm->world;
+  if (m == 1) return OK_CLEAR();
+  rsdb::P2PSignals sg;
+  p2p_signals(p, m, &sg);
+  ++p->epoch;
+  CUDA_TRY(rsdb::launch_p2p_barrier(sg, p->comm->rank, m, p->epoch, S_(stream)));
+  return OK_CLEAR();
+}
+
 rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
   rsdb::P2PSignals sg;
   if (!u) return fail(RSDB_EINVAL, "null unit");

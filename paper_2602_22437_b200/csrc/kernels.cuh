@@ -83,6 +83,8 @@ constexpr int P2P_ERR_WORD = 17;  // signal-buffer word: barrier timeout flag
 cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,
                           const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
                           cudaStream_t st);
+// device-side barrier of all ranks on `st` (start + done phases)
+cudaError_t launch_p2p_barrier(const P2PSignals& sg, int rank, int m, uint64_t epoch, cudaStream_t st);
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
 // K-slot ring: gather every rank's persistent shard (shards.p[r], bytes_S) into dst

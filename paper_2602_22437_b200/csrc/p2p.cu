@@ -276,6 +276,20 @@ cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank,
   }
 }
 
+cudaError_t launch_p2p_barrier(const P2PSignals& sg, int rank, int m, uint64_t epoch, cudaStream_t st) {
+  switch (m) {
+#define BAR_CASE(M)                                                 \
+  case M:                                                           \
+    p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);    \
+    p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);    \
+    return cudaGetLastError();
+    BAR_CASE(2) BAR_CASE(3) BAR_CASE(4) BAR_CASE(5) BAR_CASE(6) BAR_CASE(7) BAR_CASE(8)
+#undef BAR_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st) {
   switch (m) {

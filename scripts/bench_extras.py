@@ -555,26 +555,25 @@ def zero3(R, ctx, tokens=4096):
 
 # ---------------------------------------------------------------- N4: allocation dynamics
 def memory_replay(R, ctx, m=8, steps=3, lag_us=200):
-    """Replays the buffer allocations of one training step of the bench
-    workload (Llama-3.2-1B, 17 units, planned for an FSDP group of m = 8;
-    one GPU holds one rank's buffers) through PyTorch's caching allocator,
-    under three allocation policies, and reports peak RESERVED memory:
+    """Replays the buffer allocations of training steps of the bench workload
+    (Llama-3.2-1B, 17 units, planned for an FSDP group of m = 8; one GPU holds
+    one rank's buffers) through PyTorch's caching allocator under four
+    policies and reports peak RESERVED memory:
 
-      dbuffer       this library's reshard schedule (K-slot ring): K = 2 slots
-                    of gathered parameters / gradients / fp32 reduce buffer
-                    sized for the largest unit, allocated once, reused in
-                    event order -- nothing allocated per step;
-      per_param     FSDP2-style eager per-parameter allocation: per unit and
-                    pass, the AllGather output (m S bf16) on the comm stream,
-                    the unsharded parameters one tensor each (Copy-Out), in
-                    backward one gradient tensor each, the fp32 ReduceScatter
-                    input (m S, Copy-In) and output (S); stream order kept
-                    with events, tensors freed after their last use;
-      record_stream FSDP1 / DeepSpeed-style: the same flat buffers allocated
-                    on the comm stream, consumed on the compute stream and
-                    released through Tensor.record_stream, so a block returns
-                    to the pool only when the allocator sees the compute
-                    stream pass it.
+      dbuffer       DBuffer batched allocation: per unit and pass ONE
+                    allocation holding the unit's gathered parameters (m S
+                    bf16), gradients (m S bf16) and fp32 reduce buffer (m S),
+                    freed deterministically -- the comm stream waits for the
+                    compute stream before its next allocation (no record_stream);
+      ring_k2       this library's K-slot ring: K = 2 such batched slots sized
+                    for the largest unit, allocated once;
+      per_param     FSDP2-style eager per-parameter allocation: the AllGather
+                    output (m S bf16) on the comm stream, the unsharded
+                    parameters one tensor each (Copy-Out), in backward one
+                    gradient tensor each, the fp32 ReduceScatter input (m S,
+                    Copy-In) and output (S); stream order kept with events;
+      record_stream FSDP1 / DeepSpeed-style flat buffers allocated on the
+                    comm stream and released through Tensor.record_stream.
 
     Compute is a `lag_us` sleep kernel per unit and pass, so the CPU runs
     ahead of the GPU as in training.  Only the FSDP buffers are replayed (no
@@ -600,33 +599,36 @@ def memory_replay(R, ctx, m=8, steps=3, lag_us=200):
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
         base = torch.cuda.memory_reserved()
+        base_alloc = torch.cuda.memory_allocated()
         keep = []
-        if policy == "dbuffer":  # K = 2 reshard slots (the ring schedule), batched, allocated once
+        if policy == "ring_k2":
             mx = max(m * S for S, _ in sizes)
-            keep = [torch.empty(mx, dtype=dt, device=dev) for _ in range(2)
-                    for dt in (torch.bfloat16, torch.bfloat16, torch.float32)]
+            keep = [torch.empty(8 * mx, dtype=torch.uint8, device=dev) for _ in range(2)]
         for _ in range(steps):
             for phase in ("fwd", "bwd"):
                 order = range(len(sizes)) if phase == "fwd" else reversed(range(len(sizes)))
                 for ui in order:
                     S, es = sizes[ui]
-                    if policy == "dbuffer":
+                    if policy == "ring_k2":
                         with torch.cuda.stream(comp):
                             torch.cuda._sleep(cycles)
                         continue
                     with torch.cuda.stream(comm_st):
-                        comm_st.wait_stream(comp)
-                        ag = torch.empty(m * S, dtype=torch.bfloat16, device=dev)
-                        ag.zero_()
+                        comm_st.wait_stream(comp)  # explicit order: reuse only after compute is done
+                        if policy == "dbuffer":
+                            buf = torch.empty(8 * m * S, dtype=torch.uint8, device=dev)  # one batched block
+                            buf[:2 * m * S].zero_()
+                        else:
+                            ag = torch.empty(m * S, dtype=torch.bfloat16, device=dev)
+                            ag.zero_()
                     ev = torch.cuda.Event()
                     ev.record(comm_st)
                     comp.wait_event(ev)
                     with torch.cuda.stream(comp):
                         if policy == "per_param":
                             params = [torch.empty(e, dtype=torch.bfloat16, device=dev) for e in es]
-                            for p_ in params[:1]:
-                                p_.zero_()
-                        else:
+                            params[0].zero_()
+                        elif policy == "record_stream":
                             ag.record_stream(comp)
                         torch.cuda._sleep(cycles)
                         if phase == "bwd":
@@ -634,9 +636,8 @@ def memory_replay(R, ctx, m=8, steps=3, lag_us=200):
                                 grads = [torch.empty(e, dtype=torch.bfloat16, device=dev) for e in es]
                                 rs_in = torch.empty(m * S, dtype=torch.float32, device=dev)
                                 rs_in.zero_()
-                            else:
+                            elif policy == "record_stream":
                                 grads = [torch.empty(m * S, dtype=torch.bfloat16, device=dev)]
-                                rs_in = None
                             ev2 = torch.cuda.Event()
                             ev2.record(comp)
                     if phase == "bwd":
@@ -647,26 +648,30 @@ def memory_replay(R, ctx, m=8, steps=3, lag_us=200):
                                 rs_out.zero_()
                                 ev3 = torch.cuda.Event()
                                 ev3.record(comm_st)
-                                comp.wait_event(ev3)  # explicit stream order, no record_stream
-                                del rs_out, rs_in
-                            else:
+                                comp.wait_event(ev3)
+                                del rs_out, rs_in, grads
+                            elif policy == "record_stream":
                                 rs = torch.empty(m * S, dtype=torch.float32, device=dev)
                                 rs.zero_()
                                 grads[0].record_stream(comm_st)
-                                del rs
-                        del grads
+                                del rs, grads
+                            else:
+                                buf[2 * m * S:].zero_()  # the gradient + fp32 reduce parts
                     if policy == "per_param":
                         del params
-                    del ag
+                    if policy == "dbuffer":
+                        del buf
+                    else:
+                        del ag
         torch.cuda.synchronize()
         out = {"peak_reserved_bytes": torch.cuda.max_memory_reserved() - base,
-               "peak_allocated_bytes": torch.cuda.max_memory_allocated()}
+               "peak_allocated_bytes": torch.cuda.max_memory_allocated() - base_alloc}
         del keep
         return out
 
-    res = {p: run(p) for p in ("dbuffer", "per_param", "record_stream")}
+    res = {p: run(p) for p in ("dbuffer", "ring_k2", "per_param", "record_stream")}
     d = res["dbuffer"]["peak_reserved_bytes"]
-    for p in ("per_param", "record_stream"):
+    for p in ("ring_k2", "per_param", "record_stream"):
         res[p]["reserved_vs_dbuffer"] = res[p]["peak_reserved_bytes"] / max(1, d)
     res["workload"] = f"llama-3.2-1b FSDP buffers, m = {m} (one rank), {steps} steps, {lag_us} us compute per unit-pass"
     torch.cuda.empty_cache()

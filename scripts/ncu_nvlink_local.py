@@ -40,6 +40,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=2)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--mode", choices=["fused", "noag", "rs"], default="fused",
+                    help="fused: RS + Adam + AG pushes (the bench step); noag: RS + Adam (peer "
+                         "loads only); rs: the standalone p2p ReduceScatter kernel per unit")
     args = ap.parse_args()
     n = args.gpus
     units = bench.build_units(16)
@@ -75,7 +78,13 @@ def main():
                 if r == 0:
                     a = torch.cuda.Event(enable_timing=True)
                     a.record(st)
-                db.reduce_scatter_adam_gather(cfg, t, p2ps[r], st)
+                if args.mode == "fused":
+                    db.reduce_scatter_adam_gather(cfg, t, p2ps[r], st)
+                elif args.mode == "noag":
+                    db.reduce_scatter_adam(cfg, t, p2ps[r], st)
+                else:
+                    for u in reversed(db.units):
+                        R.reduce_scatter_p2p(u, p2ps[r], st)
                 if r == 0:
                     b = torch.cuda.Event(enable_timing=True)
                     b.record(st)
@@ -85,9 +94,10 @@ def main():
     for p in p2ps:
         p.check()
     lays = ctx[0][0]
-    wire = sum(2 * (l.m - 1) * l.S * 2 for l in lays)  # RS reads + AG pushes into each rank
+    per = 2 if args.mode == "fused" else 1  # RS reads (+ AG pushes) into each rank
+    wire = sum(per * (l.m - 1) * l.S * 2 for l in lays)
     ms = [a.elapsed_time(b) for a, b in ev]
-    print(json.dumps({"n_gpus": n, "mode": "one process, one logical rank per GPU",
+    print(json.dumps({"n_gpus": n, "mode": args.mode, "setup": "one process, one logical rank per GPU",
                       "ms_per_step_rank0": ms, "wire_in_bytes_per_rank_per_step": wire,
                       "wire_out_bytes_per_rank_per_step": wire,
                       "wire_in_gbs_best": wire / min(ms) / 1e6}), flush=True)

@@ -570,6 +570,58 @@ def test_dbuffer_step_host_rejects_null():
     db.close()
 
 
+def test_dbuffer_tiles_one_launch_equals_oracle():
+    """The DBuffer step over units planned with 32-row granularity and 32x32
+    tiles (the paper's 8-bit Adam setup; dispatched to the paired-tile
+    kernel) against the oracle's tiled step, unit by unit, at world 2."""
+    decl = [[(256, 512), (512,), (96, 64)], [(64, 2048), (2048,)], [(40, 128), (33, 32)]]
+    m, rank = 2, 1
+    units = []
+    for shapes in decl:
+        es = [int(np.prod(s)) for s in shapes]
+        gs = [32 * s[-1] if len(s) == 2 else min(2048, e) for s, e in zip(shapes, es)]
+        specs = [("tile", s[-1], 32, 32) if len(s) == 2 else ("flat", min(2048, e)) for s, e in zip(shapes, es)]
+        o, c = _plans(es, gs, m, 2)
+        units.append((es, specs, o, c))
+    lays_c = [u[3] for u in units]
+    qs = [u[1] for u in units]
+    sizes, offs = R.arena_sizes(lays_c, rank, qspec=qs)
+    ar = [torch.zeros(max(1, sz), dtype=torch.uint8, device="cuda") for sz in sizes]
+    db = R.DBuffer(lays_c, rank, ar, qspec=qs)
+    refs, ins_all, views, tiles_all = [], [], [], []
+    for ui, (es, specs, o, c) in enumerate(units):
+        E, S, off = sum(es), c.S, offs[ui]
+        tiles = OP.rank_tiles(o, rank, specs)
+        nb = len(tiles)
+        v = {"param_full": ar[0][off[0]:off[0] + m * S * 2].view(torch.bfloat16),
+             "grad_f32": ar[2][off[2]:off[2] + m * S * 4].view(torch.float32),
+             "master": ar[3][off[3]:off[3] + S * 4].view(torch.float32),
+             "mq": ar[4][off[4]:off[4] + S].view(torch.int8), "vq": ar[5][off[5]:off[5] + S],
+             "ma": ar[6][off[6]:off[6] + nb * 4].view(torch.float32),
+             "va": ar[7][off[7]:off[7] + nb * 4].view(torch.float32)}
+        p_log, g_log = logical_params(20 + ui, E), logical_grads(20 + ui, rank, E)
+        v["master"].copy_(place_gpu(c, p_log, torch.float32)[rank * S:(rank + 1) * S])
+        v["grad_f32"].copy_(place_gpu(c, g_log, torch.float32))
+        v["mq"].copy_(H.codes_torch(ui, H.STREAM_MCODE, 0, S, True, device="cuda"))
+        v["vq"].copy_(H.codes_torch(ui, H.STREAM_VCODE, 0, S, False, device="cuda"))
+        v["ma"].copy_(H.absmax_torch(ui, H.STREAM_ABSM, 0, nb, 14, device="cuda"))
+        v["va"].copy_(H.absmax_torch(ui, H.STREAM_ABSV, 0, nb, 22, device="cuda"))
+        ins = [v[k].cpu().numpy().copy() for k in ("master", "mq", "vq", "ma", "va")]
+        g_or = OD.shard(o, OD.place_logical(o, g_log.numpy()), rank)
+        refs.append(OA.step_8bit_adam(ins[0], g_or, ins[1], ins[2], ins[3], ins[4], tiles, OA.AdamCfg(), 3))
+        ins_all.append(ins)
+        views.append(v)
+        tiles_all.append(tiles)
+    assert db.num_blocks == sum(len(t) for t in tiles_all)
+    cfg = R.AdamConfig()
+    db.step_8bit_adam(cfg, 3)
+    torch.cuda.synchronize()
+    for (es, specs, o, c), v, ref, ins, tiles in zip(units, views, refs, ins_all, tiles_all):
+        _check_adam(o, rank, tiles, (v["master"], v["mq"], v["vq"], v["ma"], v["va"], v["param_full"]),
+                    ref, ins, 2, cfg.lr)
+    db.close()
+
+
 # ------------------------------------------------------------------ copies
 def test_copy_plan_parity():
     rng = np.random.default_rng(0)
