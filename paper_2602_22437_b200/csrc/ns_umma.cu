@@ -126,6 +126,31 @@ __host__ __device__ inline int sym_tiles(int mt, int nt) {
   return n;
 }
 
+// mbarrier wait that traps after ~4 s instead of hanging the device if a
+// phase never completes (a protocol bug surfaces as a launch error)
+__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) return;
+    if ((it & 1023) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (it == 0)
+        t0 = t;
+      else if (t - t0 > 4000000000ull)
+        __trap();
+    }
+  }
+}
+
 template <bool HAS_D, bool HAS_T, bool SYM>
 __global__ void __launch_bounds__(UG_THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M,
@@ -148,7 +173,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull + s, 1);
-      mbar_init(tempty + s, 128);
+      mbar_init(tempty + s, 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -172,7 +197,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         int m0, n0;
         tile_coords<SYM>(t, mt, m0, n0);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(empty + s, ph ^ 1);
+          mbar_wait_guard(empty + s, ph ^ 1);
           uint8_t* sa = smem + s * UG_STAGE_BYTES;
           mbar_arrive_expect_tx(full + s, UG_STAGE_BYTES);
           tma_load_2d(sa, &tma_a, full + s, kb * UG_BK, m0);
@@ -189,11 +214,11 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
       int s = 0, as = 0;
       uint32_t ph = 0, aph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        mbar_wait(tempty + as, aph ^ 1);  // the epilogue drained this accumulator
+        mbar_wait_guard(tempty + as, aph ^ 1);  // the epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(as * UG_BN);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(full + s, ph);
+          mbar_wait_guard(full + s, ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * UG_STAGE_BYTES);
           const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + UG_A_BYTES);
@@ -220,7 +245,7 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int m0, n0;
       tile_coords<SYM>(t, mt, m0, n0);
-      mbar_wait(tfull + as, aph);
+      mbar_wait_guard(tfull + as, aph);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(as * UG_BN);
@@ -280,7 +305,8 @@ __global__ void __launch_bounds__(UG_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty + as);  // 128 arrivals: accumulator free
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + as);  // one arrival per epilogue warp
       if (++as == 2) {
         as = 0;
         aph ^= 1;

@@ -678,12 +678,63 @@ def memory_replay(R, ctx, m=8, steps=3, lag_us=200):
     return res
 
 
+# ---------------------------------------------------------------- the e2e path's roofline: PCIe
+def pcie(R, ctx, mb=512, reps=5):
+    """Host <-> device copy rates from pinned memory (the bound of `e2e`,
+    which moves every rank's bf16 gradients in and its shard out per step):
+    H2D alone, D2H alone, both at once on two streams, and with the copies
+    split over two streams per direction."""
+    st = ctx["stream"]
+    n = mb << 20
+    h_in = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s2 = torch.cuda.Stream()
+
+    def rate(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        st.wait_event(t0)
+        for _ in range(reps):
+            fn()
+        s2.wait_stream(st)
+        st.wait_stream(s2)
+        t1.record(st)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / reps
+
+    def h2d():
+        with torch.cuda.stream(st):
+            d_in.copy_(h_in, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(st):
+            h_out.copy_(d_out, non_blocking=True)
+
+    def both():
+        s2.wait_stream(st)
+        with torch.cuda.stream(st):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+        st.wait_stream(s2)
+
+    t_in, t_out, t_both = rate(h2d), rate(d2h), rate(both)
+    return {"bytes_each_way": n, "h2d_gbs": n / t_in / 1e6, "d2h_gbs": n / t_out / 1e6,
+            "bidirectional_gbs_each_way": n / t_both / 1e6,
+            "note": "pinned host memory, cudaMemcpyAsync; the e2e step is bound by the bidirectional rate"}
+
+
 def run_all(R, ctx, which=None):
     """ctx: rank, world, comm, stream, db, lays, cfg, t, p2p, reps."""
     out = {}
     items = [("kernels", kernels), ("tiles_32x32", tiles), ("muon_8b_layer", muon),
              ("fp8_allgather", fp8), ("dsv3_ragged_vs_rowwise", dsv3), ("bucket_sweep", bucket_sweep),
-             ("memory_replay", memory_replay)]
+             ("memory_replay", memory_replay), ("pcie", pcie)]
     if ctx["world"] > 1:
         items = [("per_unit", per_unit)] + items + [("zero3_overlap", zero3)]
     for name, fn in items:
