@@ -433,7 +433,10 @@ rsdb_status rsdb_dbuffer_step_8bit_adam_dynamic(rsdb_dbuffer*, const rsdb_adam_c
  *      world 1), with the unit's DBuffer-bound optimizer state;
  *   3. D2H: this rank's updated bf16 shard (S elements at param_full + rank*S)
  *      -> host_shards[u] on a second library-owned copy stream.
- * Unit u's copy-in overlaps unit u+1's kernel and copy-out.  Ordering across
+ * Unit u's copy-in overlaps unit u+1's kernel and copy-out; a unit whose
+ * shard exceeds 16 M elements runs as ceil(S / 16 M) block-range launches
+ * (a count that depends only on S, so it is the same on every rank) whose
+ * copy-outs overlap the next launch.  Ordering across
  * calls is kept with per-unit events (a unit's gradients are overwritten only
  * after its previous kernel, its shard only after its previous copy-out).
  * Stream-ordered: the copies start after the work already on `stream`, and

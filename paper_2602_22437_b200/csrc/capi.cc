@@ -728,7 +728,8 @@ rsdb_status rsdb_all_gather_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) {
 }
 
 static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state* st,
-                                const rsdb_adam_cfg* cfg, int64_t step, void* stream, bool gather) {
+                                const rsdb_adam_cfg* cfg, int64_t step, void* stream, bool gather,
+                                int64_t first_block = 0, int64_t block_count = -1) {
   if (!u) return fail(RSDB_EINVAL, "null unit");
   if (u->L.elem_bytes != 2) return fail(RSDB_EMISMATCH, "fused ReduceScatter + Adam needs a bf16 unit");
   rsdb::AdamScalars s;
@@ -766,7 +767,9 @@ static rsdb_status rs_adam_unit(rsdb_unit* u, rsdb_p2p* p, const rsdb_adam_state
                     static_cast<float*>(st->v_absmax),    nullptr,
                     param_target(u),                      1};
   const float scale = float(1.0 / double(m));
-  CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(u->blocks.p), u->nblocks, g, m,
+  const int64_t nb = block_count < 0 ? u->nblocks : block_count;  // a block range (rsdb_dbuffer_step_host)
+  if (nb == 0 && m == 1) return OK_CLEAR();
+  CUDA_TRY(rsdb::launch_rs_adam_p2p(static_cast<const rsdb::AdamBlock*>(u->blocks.p) + first_block, nb, g, m,
                                     scale, ap, s, m > 1 ? &sg : nullptr, u->rank,
                                     m > 1 ? p->epoch : 0, S_(stream), push ? &q : nullptr));
   return OK_CLEAR();
@@ -1114,6 +1117,43 @@ rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
     }
     h->k_rec.assign(n, 0);
     h->out_rec.assign(n, 0);
+    // chunks of <= 16 M shard elements (32 MB of bf16 copy-out) at block
+    // boundaries, from the unit's block table (read back once).  The chunk
+    // COUNT comes from S, the same on every rank, because at world > 1 every
+    // chunk launch is a collective (its barriers count all ranks).  A unit
+    // with 2-D tiles (whose rows interleave across neighbouring tiles) is
+    // updated by its first launch; its other launches are empty (barriers only)
+    constexpr int64_t CHUNK = int64_t(16) << 20;
+    h->chunks.resize(n);
+    h->ev_chunk.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+      rsdb_unit* u = d->units[i].get();
+      const int64_t S = u->L.S;
+      const int64_t nc = std::max<int64_t>(1, (S + CHUNK - 1) / CHUNK);
+      std::vector<rsdb::AdamBlock> tb(size_t(u->nblocks));
+      if (u->nblocks)
+        CUDA_TRY(cudaMemcpy(tb.data(), u->blocks.p, tb.size() * sizeof(rsdb::AdamBlock), cudaMemcpyDeviceToHost));
+      const bool flat = std::all_of(tb.begin(), tb.end(), [](const rsdb::AdamBlock& x) { return x.cols == x.len; });
+      // chunk c takes the blocks starting in [c S / nc, (c+1) S / nc)
+      int64_t b = 0;
+      for (int64_t c = 0; c < nc; ++c) {
+        const int64_t lim = (c + 1) * S / nc;
+        const int64_t first = b;
+        while (b < u->nblocks && (c == nc - 1 || !flat || tb[size_t(b)].state_off < lim)) ++b;
+        h->chunks[i].push_back({first, b - first, 0, 0});
+      }
+      auto& ch = h->chunks[i];
+      for (size_t c = 0; c < ch.size(); ++c) {  // shard cover: [start of this chunk's first block, next's)
+        ch[c].lo = c == 0 ? 0 : (ch[c].count ? tb[size_t(ch[c].first)].state_off : ch[c - 1].hi);
+        ch[c].hi = S;
+        if (c) ch[c - 1].hi = ch[c].lo;
+      }
+      if (!flat)  // one copy-out of the whole shard, after the (single) real launch
+        for (size_t c = 0; c < ch.size(); ++c) ch[c].lo = ch[c].hi = c == 0 ? 0 : S;
+      if (!flat) ch[0].hi = S;
+      h->ev_chunk[i].assign(ch.size(), nullptr);
+      for (auto& e : h->ev_chunk[i]) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     d->host = std::move(h);
   }
   HostPipe& h = *d->host;
@@ -1134,12 +1174,21 @@ rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
     CUDA_TRY(cudaStreamWaitEvent(st, h.ev_in[i], 0));
     // the shard: rewrite only after its previous copy-out
     if (h.out_rec[i]) CUDA_TRY(cudaStreamWaitEvent(st, h.ev_out[i], 0));
-    if (rsdb_status e = rs_adam_unit(u, p, nullptr, cfg, step, stream, u->L.m > 1)) return e;
+    // the unit in block-range chunks: chunk c's copy-out overlaps chunk c+1's kernel
+    const char* shard = static_cast<const char*>(u->bufs.param_full) + int64_t(u->rank) * u->L.S * 2;
+    for (size_t c = 0; c < h.chunks[i].size(); ++c) {
+      const HostPipe::Chunk& ck = h.chunks[i][c];
+      if (rsdb_status e = rs_adam_unit(u, p, nullptr, cfg, step, stream, u->L.m > 1, ck.first, ck.count))
+        return e;
+      CUDA_TRY(cudaEventRecord(h.ev_chunk[i][c], st));
+      CUDA_TRY(cudaStreamWaitEvent(h.s_out, h.ev_chunk[i][c], 0));
+      if (ck.hi > ck.lo)
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(host_shards[i]) + ck.lo * 2, shard + ck.lo * 2,
+                                 size_t(ck.hi - ck.lo) * 2, cudaMemcpyDeviceToHost, h.s_out));
+    }
+    (void)sbytes;
     CUDA_TRY(cudaEventRecord(h.ev_k[i], st));
     h.k_rec[i] = 1;
-    CUDA_TRY(cudaStreamWaitEvent(h.s_out, h.ev_k[i], 0));
-    const char* shard = static_cast<const char*>(u->bufs.param_full) + int64_t(u->rank) * u->L.S * 2;
-    if (sbytes) CUDA_TRY(cudaMemcpyAsync(host_shards[i], shard, sbytes, cudaMemcpyDeviceToHost, h.s_out));
     CUDA_TRY(cudaEventRecord(h.ev_out[i], h.s_out));
     h.out_rec[i] = 1;
   }

@@ -106,7 +106,17 @@ struct HostPipe {
   cudaEvent_t ev_start = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_k, ev_out;  // per unit
   std::vector<char> k_rec, out_rec;              // recorded at least once
+  // per unit: block-range chunks [first block, count, shard lo, shard hi) so
+  // a chunk's copy-out overlaps the next chunk's kernel, and one event each
+  struct Chunk {
+    int64_t first, count, lo, hi;
+  };
+  std::vector<std::vector<Chunk>> chunks;
+  std::vector<std::vector<cudaEvent_t>> ev_chunk;
   ~HostPipe() {
+    for (auto& v : ev_chunk)
+      for (cudaEvent_t e : v)
+        if (e) cudaEventDestroy(e);
     for (auto* v : {&ev_in, &ev_k, &ev_out})
       for (cudaEvent_t e : *v)
         if (e) cudaEventDestroy(e);

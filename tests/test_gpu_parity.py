@@ -558,6 +558,47 @@ def test_dbuffer_step_host_world1():
     db.close()
 
 
+def test_dbuffer_step_host_chunked_equals_device_step():
+    """A unit larger than step_host's 16 M-element copy-out chunk (3 chunks)
+    next to small ones: the chunked host-buffer step is bit-identical to the
+    device-resident fused step on the same inputs (states, shard, host copy)."""
+    decl = [[20_000_000, 17_000_000 + 5], [2048 * 3 + 7, 77], [4096]]
+    q = 2048
+    res = []
+    for mode in ("host", "device"):
+        lays = [R.plan(es, [min(q, e) for e in es], 1, elem_bytes=2) for es in decl]
+        sizes, offs = R.arena_sizes(lays, 0, q, 256)
+        ar = [torch.zeros(max(1, sz), dtype=torch.uint8, device="cuda") for sz in sizes]
+        db = R.DBuffer(lays, 0, ar, qblock=q, align=256)
+        host_g, host_p = [], []
+        for ui, (es, c) in enumerate(zip(decl, lays)):
+            E, S, off = sum(es), c.S, offs[ui]
+            ar[3][off[3]:off[3] + S * 4].view(torch.float32).copy_(place_gpu(c, logical_params(ui, E), torch.float32))
+            g = place_gpu(c, logical_grads(ui, 0, E), torch.bfloat16)
+            if mode == "device":
+                ar[1][off[1]:off[1] + S * 2].view(torch.bfloat16).copy_(g)
+            host_g.append(g.cpu().pin_memory())
+            host_p.append(torch.zeros(S, dtype=torch.bfloat16).pin_memory())
+        cfg = R.AdamConfig()
+        for t in (1, 2):
+            if mode == "host":
+                db.step_host(cfg, t, host_g, host_p)
+            else:
+                db.reduce_scatter_adam_gather(cfg, t)
+        torch.cuda.synchronize()
+        res.append(([a.cpu() for a in ar[3:]], ar[0].cpu(), host_p))
+        db.close()
+    (st_h, pf_h, hp), (st_d, pf_d, _) = res
+    for a, b in zip(st_h, st_d):
+        assert torch.equal(a, b)
+    assert torch.equal(pf_h, pf_d)
+    lays = [R.plan(es, [min(q, e) for e in es], 1, elem_bytes=2) for es in decl]
+    _, offs = R.arena_sizes(lays, 0, q, 256)
+    for ui, c in enumerate(lays):
+        shard = pf_h[offs[ui][0]:offs[ui][0] + c.S * 2].view(torch.int16)
+        assert torch.equal(hp[ui].view(torch.int16), shard), ui
+
+
 def test_dbuffer_step_host_rejects_null():
     c = R.plan([4096], [2048], 1, elem_bytes=2)
     sizes, _ = R.arena_sizes([c], 0, 2048, 256)
