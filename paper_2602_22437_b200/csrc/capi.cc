@@ -1126,6 +1126,7 @@ rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
     constexpr int64_t CHUNK = int64_t(16) << 20;
     h->chunks.resize(n);
     h->ev_chunk.resize(n);
+    h->ev_chunk_in.resize(n);
     for (size_t i = 0; i < n; ++i) {
       rsdb_unit* u = d->units[i].get();
       const int64_t S = u->L.S;
@@ -1153,6 +1154,8 @@ rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
       if (!flat) ch[0].hi = S;
       h->ev_chunk[i].assign(ch.size(), nullptr);
       for (auto& e : h->ev_chunk[i]) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->ev_chunk_in[i].assign(ch.size(), nullptr);
+      for (auto& e : h->ev_chunk_in[i]) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     d->host = std::move(h);
   }
@@ -1169,15 +1172,32 @@ rsdb_status rsdb_dbuffer_step_host(rsdb_dbuffer* d, rsdb_p2p* p, const rsdb_adam
     // gradients: overwrite only after this unit's previous kernel (whose done
     // barrier also means no peer still reads them)
     if (h.k_rec[i]) CUDA_TRY(cudaStreamWaitEvent(h.s_in, h.ev_k[i], 0));
-    if (gbytes) CUDA_TRY(cudaMemcpyAsync(u->bufs.grad_full, host_grads[i], gbytes, cudaMemcpyHostToDevice, h.s_in));
-    CUDA_TRY(cudaEventRecord(h.ev_in[i], h.s_in));
-    CUDA_TRY(cudaStreamWaitEvent(st, h.ev_in[i], 0));
+    // world 1: the gradients chunk by chunk too (chunk c's kernel needs exactly
+    // its shard range); world > 1: the whole buffer (every owner's ranges)
+    const bool chunk_in = u->L.m == 1 && h.chunks[i].size() > 1;
+    if (!chunk_in) {
+      if (gbytes)
+        CUDA_TRY(cudaMemcpyAsync(u->bufs.grad_full, host_grads[i], gbytes, cudaMemcpyHostToDevice, h.s_in));
+      CUDA_TRY(cudaEventRecord(h.ev_in[i], h.s_in));
+      CUDA_TRY(cudaStreamWaitEvent(st, h.ev_in[i], 0));
+    } else {
+      for (size_t c = 0; c < h.chunks[i].size(); ++c) {
+        const HostPipe::Chunk& ck = h.chunks[i][c];
+        if (ck.hi > ck.lo)
+          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(u->bufs.grad_full) + ck.lo * 2,
+                                   static_cast<const char*>(host_grads[i]) + ck.lo * 2, size_t(ck.hi - ck.lo) * 2,
+                                   cudaMemcpyHostToDevice, h.s_in));
+        CUDA_TRY(cudaEventRecord(h.ev_chunk_in[i][c], h.s_in));
+      }
+      CUDA_TRY(cudaEventRecord(h.ev_in[i], h.s_in));
+    }
     // the shard: rewrite only after its previous copy-out
     if (h.out_rec[i]) CUDA_TRY(cudaStreamWaitEvent(st, h.ev_out[i], 0));
     // the unit in block-range chunks: chunk c's copy-out overlaps chunk c+1's kernel
     const char* shard = static_cast<const char*>(u->bufs.param_full) + int64_t(u->rank) * u->L.S * 2;
     for (size_t c = 0; c < h.chunks[i].size(); ++c) {
       const HostPipe::Chunk& ck = h.chunks[i][c];
+      if (chunk_in) CUDA_TRY(cudaStreamWaitEvent(st, h.ev_chunk_in[i][c], 0));
       if (rsdb_status e = rs_adam_unit(u, p, nullptr, cfg, step, stream, u->L.m > 1, ck.first, ck.count))
         return e;
       CUDA_TRY(cudaEventRecord(h.ev_chunk[i][c], st));

@@ -112,8 +112,11 @@ struct HostPipe {
     int64_t first, count, lo, hi;
   };
   std::vector<std::vector<Chunk>> chunks;
-  std::vector<std::vector<cudaEvent_t>> ev_chunk;
+  std::vector<std::vector<cudaEvent_t>> ev_chunk, ev_chunk_in;
   ~HostPipe() {
+    for (auto& v : ev_chunk_in)
+      for (cudaEvent_t e : v)
+        if (e) cudaEventDestroy(e);
     for (auto& v : ev_chunk)
       for (cudaEvent_t e : v)
         if (e) cudaEventDestroy(e);
