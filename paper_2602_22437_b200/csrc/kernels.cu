@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(NT, 4) adam8_pair_kernel(const AdamBlock* __re
     for (int k = 0; k < G::Q; ++k) {
       const int e0 = G::quad(k) - base;  // element of the tile held by this quad
       if (e0 >= 0 && e0 < nb.len) {
-        const int64_t a = blk_off(nb, e0);
+        const int64_t a = blk_off_p2(nb, e0);
         cp_async16(stage[st].p + base + e0, P.master + nb.state_off + a);
         cp_async16(stage[st].g + base + e0, P.grad + nb.grad_off + a);
         cp_async4(stage[st].mq + base + e0, P.mq + nb.state_off + a);

@@ -408,9 +408,13 @@ def bucket_sweep(R, ctx):
             for name in ("ragged", "even"):
                 if name == "ragged":
                     lay = R.plan(es, [1] * len(es), world, elem_bytes=2)
-                else:
+                else:  # FSDP1 flat even split: tensors back to back, S = ceil(E/m) (2-B aligned chunks)
                     S = -(-E // world)
-                    lay = R.layout_from_starts([world * S], [1], world, S, [0])
+                    starts, acc = [], 0
+                    for e in es:
+                        starts.append(acc)
+                        acc += e
+                    lay = R.layout_from_starts(es, [1] * len(es), world, S, starts, require_gcoll=False)
                 S = lay.S
                 pf = torch.zeros(world * S + 64, dtype=torch.bfloat16, device="cuda")
                 gf = torch.zeros(world * S + 64, dtype=torch.bfloat16, device="cuda")
@@ -490,6 +494,8 @@ def zero3(R, ctx, tokens=4096):
                 R.all_gather_shards_p2p(rus[i], p_ag, cstream)
             ev_g[i].record(cstream)
 
+    overlap_rs = [False]
+
     def step(with_comm=True, with_compute=True):
         seq = list(range(n)) + list(reversed(range(n)))
         slot = {}
@@ -507,9 +513,12 @@ def zero3(R, ctx, tokens=4096):
                     if j >= n:  # backward: 2x the forward flop
                         y = x @ wts[i]
                         y = x @ wts[i]
-                if not (j >= n and with_comm):
+                if j >= n and with_comm and not overlap_rs[0]:  # serial: RS + Adam on the compute stream
+                    rus[i].rebind(*slots[s])
+                    R.reduce_scatter_adam_p2p(rus[i], p2p, cfg, t[0], state=states[i], stream=comp)
+                if not (j >= n and with_comm and overlap_rs[0]):
                     ev_free[s].record(comp)
-            if j >= n and with_comm:  # the unit's RS + Adam overlaps the next unit's backward
+            if j >= n and with_comm and overlap_rs[0]:  # RS + Adam overlapping the next unit's backward
                 rstream.wait_stream(comp)
                 with torch.cuda.stream(rstream):
                     rus[i].rebind(*slots[s])
@@ -535,6 +544,9 @@ def zero3(R, ctx, tokens=4096):
 
     reps = 5
     t_full = run(reps)
+    overlap_rs[0] = True
+    t_full_ov = run(reps)
+    overlap_rs[0] = False
     t_comp = run(reps, with_comm=False)
     t_comm = run(reps, with_compute=False)
     torch.cuda.synchronize()
@@ -543,8 +555,11 @@ def zero3(R, ctx, tokens=4096):
     exposed = max(0.0, t_full - t_comp)
     flop = sum(2 * tokens * 2048 * max(1, l.E // 2048) for l in lays) * 4  # fwd 1x + bwd 3x GEMMs
     return {"schedule": "reshard (ZeRO-3): K=2 slots, AG before forward and before backward, "
-                        "prefetched on a copy-engine stream (p2p channel 1); fused RS+Adam per unit on its own stream "
-                        "after the unit's backward, overlapping the next unit's backward",
+                        "prefetched on a copy-engine stream (p2p channel 1); fused RS+Adam per unit after the "
+                        "unit's backward on the compute stream (step_ms) or on its own stream overlapping the "
+                        "next unit's backward (step_ms_rs_overlapped)",
+            "step_ms_rs_overlapped": t_full_ov,
+            "exposed_frac_rs_overlapped": max(0.0, t_full_ov - t_comp) / max(t_comm, 1e-9),
             "tokens_per_rank": tokens, "synthetic_gemm_tflop": flop / 1e12,
             "synthetic_gemm_tflops": flop / (t_comp * 1e-3) / 1e12,
             "step_ms": t_full, "compute_only_ms": t_comp, "comm_only_ms": t_comm,
