@@ -301,11 +301,12 @@ __global__ void __launch_bounds__(NT, 4) adam8_pair_kernel(const AdamBlock* __re
   using G = AdamGeom<NT>;
   const int64_t nitems = (nblocks + 1) / 2;
   auto stage_tile = [&](const AdamBlock& nb, int st, int base) {  // this thread's quads of one tile
+    const bool full32 = nb.len == 1024 && nb.cols == 32;
 #pragma unroll
     for (int k = 0; k < G::Q; ++k) {
       const int e0 = G::quad(k) - base;  // element of the tile held by this quad
       if (e0 >= 0 && e0 < nb.len) {
-        const int64_t a = blk_off_p2(nb, e0);
+        const int64_t a = full32 ? int64_t(e0 >> 5) * nb.pitch + (e0 & 31) : blk_off_p2(nb, e0);
         cp_async16(stage[st].p + base + e0, P.master + nb.state_off + a);
         cp_async16(stage[st].g + base + e0, P.grad + nb.grad_off + a);
         cp_async4(stage[st].mq + base + e0, P.mq + nb.state_off + a);
@@ -380,7 +381,10 @@ __global__ void __launch_bounds__(NT, 4) adam8_pair_kernel(const AdamBlock* __re
     const AdamBlock b = ent[st][1];
     const float4 ab = *reinterpret_cast<const float4*>(ent_abs[st]);
     if (has_b && pairable(a) && pairable(b)) {
-      adam_pair_tail<NT, PARAM_BF16>(stage[st], a, b, ab.x, ab.y, ab.z, ab.w, P, s, rd, refill);
+      if (a.len == 1024 && b.len == 1024 && a.cols == 32 && b.cols == 32)  // full 32 x 32 tiles
+        adam_pair_tail<NT, PARAM_BF16, true>(stage[st], a, b, ab.x, ab.y, ab.z, ab.w, P, s, rd, refill);
+      else
+        adam_pair_tail<NT, PARAM_BF16, false>(stage[st], a, b, ab.x, ab.y, ab.z, ab.w, P, s, rd, refill);
       continue;
     }
     // unpaired item: the first entry from the stage (or direct), the second direct

@@ -181,7 +181,7 @@ def tiles(R, ctx):
     ms = timed(step, ctx["reps"], st, world, warm=3)
     nb = db.num_blocks
     byts = 18 * own + 16 * nb
-    res = {"kernel": "adam8_tma_kernel (tile path)", "tiles": nb, "elems": own, "shard_elems": n_el,
+    res = {"kernel": "adam8_pair_kernel (two 32x32 tiles per stage)", "tiles": nb, "elems": own, "shard_elems": n_el,
            "padding": sum(l.padding for l in lays), "ms": ms, "gbs": byts / ms / 1e6,
            "frac": byts / ms / 1e6 / hbm, "bytes": "18 B/elem + 16 B/tile"}
     db.close()
