@@ -80,22 +80,51 @@ __device__ __forceinline__ float rmap(const float* rep, int k, int lane) { retur
 // (R25 closed form; decade i holds 2^(i+w) equally spaced values of
 // [0.1 D_i, D_i], w = 0 signed / 1 unsigned, whose first index is 128 + 2^i - 1
 // (signed) or 2^(i+1) - 1 (unsigned)).  Plain fp32 operations (_rn: no FMA
-// contraction) so tests/test_oracle_codemap.py can replay it bit for bit:
+// contraction) so tests/test_dyn_candidate.py can replay it bit for bit:
 // for EVERY fp32 y in [-1, 1] the true hi (first index with map >= y,
 // clamped to [1, 255]) lies within one of the clamped candidate.
+// per-binade decade table (shared memory, 32 entries -- any lane pattern of
+// <= 32 distinct words is bank-conflict free up to the 8-B entry pairing):
+// for the binade [2^(E-127), 2^(E-126)) of biased exponent E = DYN_E0 + e,
+// x = the decade count of its lower end (#{thresholds 1e-6 .. 1e-1 <= 2^(E-127)})
+// and y = the one threshold inside the binade (bits; +inf if none).  Then
+// #{thresholds <= a} = x + (a >= y) for every a in the binade -- the same
+// comparisons as a six-step cascade on the same float thresholds.
+constexpr int DYN_E0 = 100;  // 2^-27 < 1e-6 / 10: everything below is decade 0
+struct DynDecade {
+  int2 bin[32];     // {decade count at the binade's start, threshold bits}
+  float dinv[8];    // 10^(6 - i), i = 0..6
+};
+__device__ __forceinline__ float dyn_th(int k) {  // thresholds 1e-6 .. 1e-1 (float32)
+  return k == 0 ? 1e-6f : k == 1 ? 1e-5f : k == 2 ? 1e-4f : k == 3 ? 1e-3f : k == 4 ? 1e-2f : 1e-1f;
+}
+__device__ __forceinline__ void dyn_decade_init(DynDecade& D) {
+  const int e = int(threadIdx.x);
+  if (e < 32) {
+    const float lo = __uint_as_float(uint32_t(DYN_E0 + e) << 23), hi = 2.f * lo;
+    int cnt = 0;
+    float t = __uint_as_float(0x7f800000u);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      if (dyn_th(k) <= lo) ++cnt;
+      else if (dyn_th(k) < hi) t = dyn_th(k);
+    }
+    D.bin[e] = make_int2(cnt, int(__float_as_uint(t)));
+  } else if (e < 32 + 7) {
+    const int i = e - 32;  // 10^(6 - i)
+    D.dinv[i] = i == 0 ? 1e6f : i == 1 ? 1e5f : i == 2 ? 1e4f : i == 3 ? 1e3f : i == 4 ? 1e2f : i == 5 ? 1e1f : 1.f;
+  }
+}
+
 template <bool SIGNED>
-__device__ __forceinline__ int dyn_candidate(float a) {
+__device__ __forceinline__ int dyn_candidate(const DynDecade& D, float a) {
   constexpr int W = SIGNED ? 0 : 1;
-  // decade i = #{thresholds 1e-6 .. 1e-1 <= a}: a select cascade (no jump
-  // table), Dinv = 10^(6-i) and cnt = 2^(i+W) carried along exactly
-  float Dinv = 1.f;
-  int cnt = 1 << (6 + W);
-  if (a < 1e-1f) Dinv = 1e1f, cnt = 1 << (5 + W);
-  if (a < 1e-2f) Dinv = 1e2f, cnt = 1 << (4 + W);
-  if (a < 1e-3f) Dinv = 1e3f, cnt = 1 << (3 + W);
-  if (a < 1e-4f) Dinv = 1e4f, cnt = 1 << (2 + W);
-  if (a < 1e-5f) Dinv = 1e5f, cnt = 1 << (1 + W);
-  if (a < 1e-6f) Dinv = 1e6f, cnt = 1 << W;
+  int e = int(__float_as_uint(a) >> 23) - DYN_E0;  // a >= 0, <= 1: e <= 27
+  e = e < 0 ? 0 : e;
+  const int2 bt = D.bin[e];
+  const int i = bt.x + int(a >= __int_as_float(bt.y));
+  const float Dinv = D.dinv[i];
+  const int cnt = 1 << (i + W);
   float u = __fsub_rn(__fmul_rn(a, Dinv), 0.1f);
   u = __fmul_rn(__fmul_rn(u, __int2float_rn(cnt)), 1.0f / 0.9f);
   int j = __float2int_rn(__fsub_rn(u, 0.5f));
@@ -108,13 +137,13 @@ __device__ __forceinline__ int dyn_candidate(float a) {
 // two comparisons on the exact map values map[c-2 .. c+1] (4 conflict-free
 // lookups in this lane's copy)
 template <bool SIGNED>
-__device__ __forceinline__ uint32_t dyn_code(const float* rep, int lane, float y) {
+__device__ __forceinline__ uint32_t dyn_code(const float* rep, const DynDecade& D, int lane, float y) {
   int c;
   if (SIGNED) {
-    const int p = dyn_candidate<true>(fabsf(y));
+    const int p = dyn_candidate<true>(D, fabsf(y));
     c = y < 0.f ? 255 - p : p;  // -map[p] sits at 254 - p; hi is the index after it
   } else {
-    c = dyn_candidate<false>(y);
+    c = dyn_candidate<false>(D, y);
   }
   c = c < 2 ? 2 : (c > 254 ? 254 : c);
   const float* q = rep + ((c - 2) << 5) + lane;
@@ -145,6 +174,8 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
   extern __shared__ __align__(16) float dyn_smem[];
   DynSmem& T = *reinterpret_cast<DynSmem*>(dyn_smem);
   __shared__ float red_m[2][DYN_NT / 32], red_v[2][DYN_NT / 32];
+  __shared__ DynDecade dec;
+  dyn_decade_init(dec);
   for (int i = threadIdx.x; i < 2 * 256 * 32; i += DYN_NT) {
     const int w = i >> 13, k = (i >> 5) & 255;
     T.rep[w][i & 8191] = c_dyn.map[w][k];
@@ -166,8 +197,8 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
     // block-uniform: A finite and > 0 (else the code of 0), 1/A in fp64
     double rAm = 0.0, rAv = 0.0;
     bool okm = false, okv = false;
-    auto qm = [&](float m, float) { return okm ? dyn_code<true>(mapm, lane, div_exact(m, rAm)) : zero_m; };
-    auto qv = [&](float v, float) { return okv ? dyn_code<false>(mapv, lane, div_exact(v, rAv)) : zero_v; };
+    auto qm = [&](float m, float) { return okm ? dyn_code<true>(mapm, dec, lane, div_exact(m, rAm)) : zero_m; };
+    auto qv = [&](float v, float) { return okv ? dyn_code<false>(mapv, dec, lane, div_exact(v, rAv)) : zero_v; };
     auto set_div = [&](float am_, float av_) {
       okm = am_ > 0.f && am_ <= FLT_MAX_F;
       okv = av_ > 0.f && av_ <= FLT_MAX_F;

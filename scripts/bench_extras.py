@@ -96,7 +96,8 @@ def per_unit(R, ctx):
     convention, bus bytes = (m-1) S b per rank), p2p kernels over NVLink,
     on the bench DBuffer's first layer unit and its root unit."""
     db, p2p, st, world = ctx["db"], ctx["p2p"], ctx["stream"], ctx["world"]
-    res = {}
+    # the fixed cost inside every p2p collective: its start + done barriers
+    res = {"barrier_pair_us": 1e3 * timed(lambda: p2p.barrier(st), ctx["reps"], st, world)}
     for name, idx in (("layer", 1), ("root", 0)):
         u = db.units[idx]
         lay = u.layout
