@@ -105,7 +105,9 @@ def per_unit(R, ctx):
         t_ag = timed(lambda: R.all_gather_p2p(u, p2p, st), ctx["reps"], st, world)
         t_rs = timed(lambda: R.reduce_scatter_p2p(u, p2p, st), ctx["reps"], st, world)
         bus = (m - 1) * S * 2
-        res[name] = {"S": S, "params": lay.E, "ag_ms": t_ag, "rs_ms": t_rs,
+        res[name] = {"S": S, "params": lay.E, "pad_ratio": lay.padding / max(1, lay.E),
+                     "ag_goodput_gbs": lay.E * 2 / t_ag / 1e6, "rs_goodput_gbs": lay.E * 2 / t_rs / 1e6,
+                     "ag_ms": t_ag, "rs_ms": t_rs,
                      "ag_bus_gbs": bus / t_ag / 1e6, "rs_bus_gbs": bus / t_rs / 1e6,
                      "ag_frac_of_900": bus / t_ag / 1e6 / NVLINK_SPEC_GBS,
                      "rs_frac_of_900": bus / t_rs / 1e6 / NVLINK_SPEC_GBS,
