@@ -871,6 +871,11 @@ def run_ours(args):
                                           "time: work-normalised, NOT a physical rate (the fused "
                                           "kernel moves fewer bytes)",
             "hbm_gbs_job": hbm_job, "ag_rs_bus_gbs_job": bus_job,
+            "params_updated_per_s": sum(l.E for l in lays) / (ms / K * 1e-3),
+            "scaling_note": ("value is BJ's metric as named: HBM GB/s at N = 1, AG+RS bus GB/s at N > 1 "
+                             "(no collective bytes exist at N = 1), so value_N / value_1 is not a scaling "
+                             "ratio; compare ag_rs_bus_gbs_job across N > 1 and params_updated_per_s "
+                             "(the same 1.24 B-parameter step at every N) across all N"),
             "step_ms": step_dist,
             "per_op": {"adam_hbm_gbs": adam_gbs, "adam_ms_per_launch": adam_ms,
                        "cast_hbm_gbs": cast_gbs, "cast_ms_per_step": cast_ms,
