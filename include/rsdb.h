@@ -312,6 +312,13 @@ rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* 
  * rank's signal buffer and returns (its results are then invalid) instead of
  * hanging the device.  EINVAL if seconds <= 0. */
 rsdb_status rsdb_p2p_set_timeout(rsdb_p2p*, double seconds);
+/* CTA budget of the SM-driven p2p kernels issued through this object
+ * (collectives, fused RS + Adam (+ AG), FP8 AllGather, Muon redistribution):
+ * at most max_ctas CTAs, so a collective overlapping compute on another
+ * stream leaves the rest of the SMs to it (overlapping; cf. NCCL's CTA
+ * budget).  0 (default) = the whole device.  Applies to the object it is set
+ * on (a channel from rsdb_p2p_channel has its own).  EINVAL if < 0. */
+rsdb_status rsdb_p2p_set_max_ctas(rsdb_p2p*, int32_t max_ctas);
 /* Synchronises the device, reads and clears this rank's error flag into
  * *flags (0 = every barrier completed); ECUDA if a barrier timed out. */
 rsdb_status rsdb_p2p_check(rsdb_p2p*, int64_t* flags);

@@ -461,6 +461,10 @@ class P2P:
         """rsdb_p2p_barrier: device-side barrier of every rank on `stream`."""
         check(lib.rsdb_p2p_barrier(self._h, _stream(stream)))
 
+    def set_max_ctas(self, n: int) -> None:
+        """rsdb_p2p_set_max_ctas: CTA budget of this object's kernels (0 = all SMs)."""
+        check(lib.rsdb_p2p_set_max_ctas(self._h, int(n)))
+
     def set_timeout(self, seconds: float) -> None:
         check(lib.rsdb_p2p_set_timeout(self._h, float(seconds)))
 

@@ -102,6 +102,7 @@ _SIGS = {
     "rsdb_p2p_create": (i32, [vp, i32, C.POINTER(vp), P_i64, C.c_char_p, C.POINTER(vp)]),
     "rsdb_p2p_free": (None, [vp]),
     "rsdb_p2p_channel": (i32, [vp, i32, C.POINTER(vp)]),
+    "rsdb_p2p_set_max_ctas": (i32, [vp, i32]),
     "rsdb_p2p_barrier": (i32, [vp, vp]),
     "rsdb_p2p_create_local": (i32, [vp, i32, C.POINTER(vp), P_i64, C.POINTER(vp)]),
     "rsdb_p2p_set_timeout": (i32, [vp, C.c_double]),

@@ -616,6 +616,12 @@ rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* 
   return OK_CLEAR();
 }
 
+rsdb_status rsdb_p2p_set_max_ctas(rsdb_p2p* p, int32_t max_ctas) {
+  if (!p || max_ctas < 0) return fail(RSDB_EINVAL, "null p2p or max_ctas < 0");
+  p->max_ctas = max_ctas;
+  return OK_CLEAR();
+}
+
 rsdb_status rsdb_p2p_set_timeout(rsdb_p2p* p, double seconds) {
   if (!p || !(seconds > 0)) return fail(RSDB_EINVAL, "rsdb_p2p_set_timeout: null p2p or seconds <= 0");
   p->timeout_ns = seconds >= 1.8e10 ? UINT64_MAX : uint64_t(seconds * 1e9);
@@ -660,6 +666,7 @@ extern "C++" void p2p_signals(const rsdb_p2p* p, int m, rsdb::P2PSignals* sg) {
     sg->peer[r] = r < m ? reinterpret_cast<uint64_t*>(p->peer[0][size_t(r)]) + w : nullptr;
   sg->timeout_ns = p->timeout_ns;
   sg->grid_div = p->grid_div;
+  sg->max_ctas = p->max_ctas;
 }
 
 extern "C++" rsdb_status p2p_common(rsdb_unit* u, rsdb_p2p* p, rsdb::P2PSignals* sg) {

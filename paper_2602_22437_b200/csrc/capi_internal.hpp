@@ -156,6 +156,7 @@ struct rsdb_p2p {
   uint64_t timeout_ns = 60ull * 1000000000ull;  // barrier spin limit (rsdb_p2p_set_timeout)
   int32_t grid_div = 1;  // logical ranks sharing the device (local mode: world)
   int32_t channel = 0;   // signal words [32c, 32c+32) of every rank's signal buffer (rsdb_p2p_channel)
+  int32_t max_ctas = 0;  // CTA budget of the kernels issued through this object (rsdb_p2p_set_max_ctas)
 };
 constexpr int P2P_CHANNEL_WORDS = 32;  // 256 B per channel, 16 channels in RSDB_P2P_SIGNAL_BYTES
 

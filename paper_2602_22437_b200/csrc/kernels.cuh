@@ -72,12 +72,15 @@ struct P2PSignals {
   uint64_t* peer[P2P_MAX_RANKS];    // every rank's signal buffer, mapped here
   uint64_t timeout_ns;              // barrier spin limit (then the error flag, no hang)
   int32_t grid_div;                 // host: ranks sharing this device (local mode), >= 1
+  int32_t max_ctas;                 // host: CTA budget of this channel's kernels (0 = the whole device)
 };
 // persistent grid of a barrier kernel: every rank's kernel must be resident at
 // once, so ranks sharing one device (rsdb_p2p_create_local) split its SMs
 inline int64_t grid_share(int64_t grid, const P2PSignals& sg) {
   const int64_t d = sg.grid_div > 1 ? sg.grid_div : 1;
-  return grid / d > 0 ? grid / d : 1;
+  int64_t g = grid / d > 0 ? grid / d : 1;
+  if (sg.max_ctas > 0 && g > sg.max_ctas) g = sg.max_ctas;  // leave SMs to overlapping compute
+  return g;
 }
 constexpr int P2P_ERR_WORD = 17;  // signal-buffer word: barrier timeout flag
 cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank, int m, float scale,

@@ -549,6 +549,9 @@ def zero3(R, ctx, tokens=4096):
     t_full = run(reps)
     overlap_rs[0] = True
     t_full_ov = run(reps)
+    p2p.set_max_ctas(32)  # the overlapped RS + Adam on a 32-CTA budget, the rest of the SMs to compute
+    t_full_cap = run(reps)
+    p2p.set_max_ctas(0)
     overlap_rs[0] = False
     t_comp = run(reps, with_comm=False)
     t_comm = run(reps, with_compute=False)
@@ -562,6 +565,8 @@ def zero3(R, ctx, tokens=4096):
                         "unit's backward on the compute stream (step_ms) or on its own stream overlapping the "
                         "next unit's backward (step_ms_rs_overlapped)",
             "step_ms_rs_overlapped": t_full_ov,
+            "step_ms_rs_overlapped_32cta": t_full_cap,
+            "exposed_frac_rs_overlapped_32cta": max(0.0, t_full_cap - t_comp) / max(t_comm, 1e-9),
             "exposed_frac_rs_overlapped": max(0.0, t_full_ov - t_comp) / max(t_comm, 1e-9),
             "tokens_per_rank": tokens, "synthetic_gemm_tflop": flop / 1e12,
             "synthetic_gemm_tflops": flop / (t_comp * 1e-3) / 1e12,

@@ -261,9 +261,9 @@ def rs_random_case(ctx):
 
 def channels_case(ctx):
     """rsdb_p2p_channel: AllGathers and ReduceScatters alternating over
-    channels 0, 1 and 2 of one mapping (independent epochs and signal words)
-    give the oracle's results: AG bit exact, RS = the rank-order sum bit for
-    bit."""
+    channels 0, 1 and 2 of one mapping (independent epochs and signal words;
+    channel 2 with a 3-CTA budget) give the oracle's results: AG bit exact,
+    RS = the rank-order sum bit for bit."""
     rank, world = ctx.rank, ctx.world
     es = [100003, 517, 2048 * 9]
     o, c = _plans(es, [1, 1, 1], world, 2)
@@ -274,6 +274,8 @@ def channels_case(ctx):
     u = R.Unit(c, rank, pf, gf, g32, qblock=0, comm=ctx.comm)
     p2p = yield from ctx.p2p([pf, gf])
     chans = [p2p] * 3 if p2p is None else [p2p, p2p.channel(1), p2p.channel(2)]
+    if p2p is not None:
+        chans[2].set_max_ctas(3)  # a capped CTA budget (rsdb_p2p_set_max_ctas): same results
     ctx.keep = getattr(ctx, "keep", []) + chans
     for it in range(4):
         shards = [OD.to_bf16_rne(H.values_np(30 + it, 1 + r, 0, S, 12)) for r in range(world)]
