@@ -373,6 +373,8 @@ def test_round2_entry_points_error_behaviour():
     assert lib.rsdb_dbuffer_step_host(None, None, None, 1, None, None, None) == _capi.RSDB_EINVAL
     out = C.c_void_p()
     assert lib.rsdb_p2p_channel(None, 1, C.byref(out)) == _capi.RSDB_EINVAL
+    assert lib.rsdb_p2p_set_max_ctas(None, 4) == _capi.RSDB_EINVAL
+    assert lib.rsdb_p2p_barrier(None, None) == _capi.RSDB_EINVAL
     lay = R.plan([4096], [2048], 1)
     bufs = _capi.UnitBufs(4096, 8192, 16384)
     assert lib.rsdb_unit_create(lay.handle, None, 0, C.byref(bufs), -1, C.byref(out)) == _capi.RSDB_EINVAL
