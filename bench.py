@@ -816,8 +816,8 @@ def run_ours(args):
     if nvl is not None:
         nvlink = {"rank": rank, "counters": NvlinkCounters.delta(nvl0, nvl1, K),
                   "error": nvl.err, "nvml_raw": nvl1, "algorithmic_wire_in_bytes_per_step": wire_rank,
-                  "ncu": "profiles/r2/ (nvlrx__bytes / nvltx__bytes of the fused kernel, rank 0 "
-                         "under ncu: scripts/ncu_nvlink_rank0.sh)",
+                  "ncu": "profiles/ncu_nvlink.json (nvlrx__bytes / nvltx__bytes of the fused kernel at "
+                         "N = 2, one process driving both GPUs: scripts/ncu_nvlink_local.py)",
                   "note": "NVML NVLink counters of this rank's GPU around the timed region "
                           "(all links; data = payload KiB counters, bytes = raw link bytes)"}
         if nvlink["counters"]:
