@@ -274,8 +274,8 @@ rsdb_status rsdb_dynamic_code_maps(float* m_map, float* v_map);
 /*    (bf16) from every rank r, sums fp32(G_r)*fl(1/m) in rank order 0..m-1  */
 /*    in fp32 (bit-identical to the oracle), zeroes padding, writes          */
 /*    grad_f32 + k*S.  Wire bytes (m-1)*S*2 per rank (half of fp32 RS).      */
-/*  - rsdb_all_gather_p2p: a4 -- rank k copies every peer's shard into its   */
-/*    own param_full (same offsets).                                         */
+/*  - rsdb_all_gather_p2p: a4 -- rank k's copy engine writes its own shard  */
+/*    into every peer's param_full (same offsets; pushes over NVLink).       */
 /* Ordering: a start barrier (every rank has issued the call, so all prior  */
 /* stream work -- grads / optimizer writes -- is complete) and a done        */
 /* barrier (every rank finished reading its peers) through a signal buffer;  */
@@ -310,7 +310,10 @@ rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* 
 /* Barrier spin limit of the p2p kernels (default 60 s): a kernel whose peer
  * never arrives stops waiting after `seconds`, sets an error flag in its
  * rank's signal buffer and returns (its results are then invalid) instead of
- * hanging the device.  EINVAL if seconds <= 0. */
+ * hanging the device.  The copy-engine AllGathers (rsdb_all_gather_p2p,
+ * rsdb_all_gather_shards_p2p) synchronise with stream memory operations
+ * instead of kernels and have no timeout: a missing peer stalls the stream.
+ * EINVAL if seconds <= 0. */
 rsdb_status rsdb_p2p_set_timeout(rsdb_p2p*, double seconds);
 /* CTA budget of the SM-driven p2p kernels issued through this object
  * (collectives, fused RS + Adam (+ AG), FP8 AllGather, Muon redistribution):
@@ -591,9 +594,11 @@ rsdb_status rsdb_unit_set_shard(rsdb_unit*, void* param_shard);
  * rsdb_unit_create (non-null, 16-B aligned, grad_full != grad_f32 for bf16). */
 rsdb_status rsdb_unit_rebind(rsdb_unit*, const rsdb_unit_bufs*);
 /* AllGather from the persistent shards: param_full[r*S ...] = shard of rank r
- * for every r (the local one by a local copy, the peers' over NVLink by the
- * copy engines, between the p2p start/done barriers).  p2p (NULL iff world
- * 1) must map every rank's shard buffer at the same offset. */
+ * for every r.  Each rank's copy engine pushes its own shard into region
+ * `rank` of every rank's param_full (its own by a local copy, the peers' over
+ * NVLink), between the p2p start/done barriers.  p2p (NULL iff world 1) must
+ * map every rank's param_full (the ring slot) at the same offset (EINVAL
+ * otherwise); the shard itself need not be mapped. */
 rsdb_status rsdb_all_gather_shards_p2p(rsdb_unit*, rsdb_p2p* p2p_or_null, void* stream);
 typedef struct rsdb_ring rsdb_ring;
 /* A ring of k slots handed out round robin: acquisition i gets slot i mod k

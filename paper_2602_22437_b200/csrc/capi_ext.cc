@@ -520,19 +520,19 @@ rsdb_status rsdb_all_gather_shards_p2p(rsdb_unit* u, rsdb_p2p* p, void* stream) 
   const int m = u->L.m;
   const int64_t bytes_S = u->L.S * u->L.elem_bytes;
   if (u->L.S == 0) return OK_CLEAR();
-  rsdb::P2PPtrs sh{};
+  rsdb::P2PPtrs dst{};
   rsdb::P2PSignals sg{};
   if (m > 1) {
     if (rsdb_status e = p2p_common(u, p, &sg)) return e;
     int32_t bi = 0;
     int64_t off = 0;
-    if (rsdb_status e = p2p_find(p, u->shard, bytes_S, &bi, &off)) return e;
-    for (int r = 0; r < m; ++r) sh.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
+    if (rsdb_status e = p2p_find(p, u->bufs.param_full, int64_t(m) * bytes_S, &bi, &off)) return e;
+    for (int r = 0; r < m; ++r) dst.p[r] = p->peer[size_t(bi)][size_t(r)] + off;
     ++p->epoch;
   } else {
-    sh.p[0] = u->shard;
+    dst.p[0] = u->bufs.param_full;
   }
-  CUDA_TRY(rsdb::launch_ag_shards(sh, u->bufs.param_full, bytes_S, u->rank, m, m > 1 ? &sg : nullptr,
+  CUDA_TRY(rsdb::launch_ag_shards(dst, u->shard, bytes_S, u->rank, m, m > 1 ? &sg : nullptr,
                                   m > 1 ? p->epoch : 0, S_(stream)));
   return OK_CLEAR();
 }

@@ -90,8 +90,9 @@ cudaError_t launch_rs_p2p(const P2PPtrs& grads, float* out, int64_t S, int rank,
 cudaError_t launch_p2p_barrier(const P2PSignals& sg, int rank, int m, uint64_t epoch, cudaStream_t st);
 cudaError_t launch_ag_p2p(const P2PPtrs& params, int64_t bytes_S, int rank, int m,
                           const P2PSignals& sg, uint64_t epoch, cudaStream_t st);
-// K-slot ring: gather every rank's persistent shard (shards.p[r], bytes_S) into dst
-cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, int rank, int m,
+// K-slot ring: push this rank's persistent shard (bytes_S) into region `rank`
+// of every rank's slot dsts.p[r] (mapped; dsts.p[rank] local)
+cudaError_t launch_ag_shards(const P2PPtrs& dsts, const void* shard, int64_t bytes_S, int rank, int m,
                              const P2PSignals* sg, uint64_t epoch, cudaStream_t st);
 // a6 + a7 + a8 fused: ReduceScatter of the bf16 gradients over NVLink and the
 // 8-bit Adam update of the local shard in one kernel (sg may be null iff m == 1);

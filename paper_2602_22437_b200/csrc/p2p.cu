@@ -8,9 +8,10 @@
 //        in rank order (fp32), padding -> 0, writes its fp32 shard.  Wire
 //        bytes per rank (m-1) S 2, vs (m-1) S 4 for the fp32 NCCL
 //        ReduceScatter, and no separate m*S cast pass.
-//  copy-engine AG       a4: rank k copies every peer's shard into its own
-//        buffer with cudaMemcpyAsync over the mappings (rotated peer order)
-//        between a start and a done barrier kernel.
+//  copy-engine AG       a4: rank k's copy engine pushes its shard into every
+//        peer's buffer with cudaMemcpyAsync over the mappings (rotated peer
+//        order) between a start and a done barrier made of stream memory
+//        operations (no kernel, no compute <-> copy engine hand-off).
 //  rs_adam_tma_kernel   a6+a7+a8 (+ a4 with PUSH): the ReduceScatter feeds
 //        the 8-bit Adam update of the shard; with PUSH every updated bf16
 //        parameter is also stored into every peer's gathered buffer -- the
@@ -20,6 +21,7 @@
 // DESIGN.md §7b, profiles/r1/); only the measured best of each is built.
 //
 // Start/done barriers between the ranks: p2p_dev.cuh.
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <type_traits>
@@ -202,8 +204,7 @@ static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int ran
   return cudaGetLastError();
 }
 
-// Start (phase 0) or done (phase 1) barrier alone, one CTA: brackets the
-// copy-engine AllGather variant (cudaMemcpyAsync over the IPC mappings).
+// Start (phase 0) or done (phase 1) barrier alone, one CTA (rsdb_p2p_barrier).
 template <int M>
 __global__ void __launch_bounds__(32) p2p_barrier_kernel(P2PSignals sg, int rank, uint64_t epoch, int phase) {
   if (phase == 0)
@@ -212,49 +213,104 @@ __global__ void __launch_bounds__(32) p2p_barrier_kernel(P2PSignals sg, int rank
     p2p_done(sg, rank, M, epoch);
 }
 
+// The same barrier phase as stream memory operations, for the copy-engine
+// AllGathers: write `epoch` into every peer's word (the write is preceded by
+// a stream-scoped system memory barrier, so this stream's earlier copies are
+// visible first), then wait until every peer's word in the local buffer
+// reaches it.  Executed by the stream front end: no kernel launch and no hand
+// off between the compute and copy engines around the copies, which cost ~9 us
+// per AllGather with barrier kernels (1 MB push: 23.3 vs 16.5 us; 64 MB:
+// 115.9 vs 106.1 us, profiles/r2/latency/probe_barrier.txt).  The wait has
+// no timeout: a rank that never arrives stalls the stream (as a collective
+// library would); the kernel barriers keep the rsdb_p2p_set_timeout guard.
+using WriteValue64_t = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using WaitValue64_t = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+static cudaError_t memop_fns(WriteValue64_t* w, WaitValue64_t* a) {
+  static WriteValue64_t fw = nullptr;
+  static WaitValue64_t fa = nullptr;
+  if (!fw || !fa) {
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaError_t e = cudaGetDriverEntryPoint("cuStreamWriteValue64", &f1, cudaEnableDefault, &q1)) return e;
+    if (cudaError_t e = cudaGetDriverEntryPoint("cuStreamWaitValue64", &f2, cudaEnableDefault, &q2)) return e;
+    if (!f1 || !f2 || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
+      return cudaErrorNotSupported;
+    fw = reinterpret_cast<WriteValue64_t>(f1);
+    fa = reinterpret_cast<WaitValue64_t>(f2);
+  }
+  *w = fw;
+  *a = fa;
+  return cudaSuccess;
+}
+static cudaError_t memop_barrier(const P2PSignals& sg, int rank, int m, uint64_t epoch, int phase,
+                                 cudaStream_t st) {
+  WriteValue64_t wr;
+  WaitValue64_t wt;
+  if (cudaError_t e = memop_fns(&wr, &wt)) return e;
+  for (int p = 1; p < m; ++p) {
+    const int r = (rank + p) % m;
+    if (wr(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(sg.peer[r] + 8 * phase + rank), epoch,
+           CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return cudaErrorLaunchFailure;
+  }
+  for (int p = 1; p < m; ++p) {
+    const int r = (rank + p) % m;
+    if (wt(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(sg.local + 8 * phase + r), epoch,
+           CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return cudaErrorLaunchFailure;
+  }
+  return cudaSuccess;
+}
+
 template <int M>
 static cudaError_t ag_ce_m(const P2PPtrs& params, int64_t bytes_S, int rank, const P2PSignals& sg,
                            uint64_t epoch, cudaStream_t st) {
-  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
-  char* mine = static_cast<char*>(const_cast<void*>(params.p[rank]));
-  for (int p = 1; p < M; ++p) {  // rotated peer order: a permutation per step (see ag_tma_kernel)
+  // PUSH: this rank's copy engine writes its own shard into every peer's
+  // buffer (same offsets).  A copy-engine pull from a peer costs ~10 us more
+  // to start and streams slower (1 MB: 14.7 vs 5.1 us; 64 MB: 100 vs 94 us,
+  // profiles/r2/latency/probe_barrier.txt).  The start barrier orders the
+  // writes after every peer's prior work on its buffer; the done barrier
+  // (signalled after this stream's copies complete) after every peer's
+  // pushes into this rank.
+  if (cudaError_t e = memop_barrier(sg, rank, M, epoch, 0, st)) return e;
+  const char* mine = static_cast<const char*>(params.p[rank]) + int64_t(rank) * bytes_S;
+  for (int p = 1; p < M; ++p) {  // rotated peer order: ranks do not all write one GPU at once
     const int r = (rank + p) % M;
-    const char* src = static_cast<const char*>(params.p[r]) + int64_t(r) * bytes_S;
-    cudaError_t e = cudaMemcpyAsync(mine + int64_t(r) * bytes_S, src, size_t(bytes_S),
-                                    cudaMemcpyDeviceToDevice, st);
+    char* dst = static_cast<char*>(const_cast<void*>(params.p[r])) + int64_t(rank) * bytes_S;
+    cudaError_t e = cudaMemcpyAsync(dst, mine, size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
   }
-  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
-  return cudaGetLastError();
+  return memop_barrier(sg, rank, M, epoch, 1, st);
 }
 
 // AllGather from persistent shards (K-slot ring mode):
-// dst[r*bytes_S ...] = shard_r for every rank r, the local shard by a local
-// copy and the peers' over NVLink by the copy engines (rotated peer order),
-// between the start/done barriers.
+// every rank's copy engine pushes its persistent shard into region `rank` of
+// every rank's slot (dsts.p[r]: rank r's slot, mapped; the own one by a local
+// copy), rotated peer order, between the start/done barriers (push and
+// stream-memory-operation barriers: see ag_ce_m).
 template <int M>
-static cudaError_t ag_shards_ce_m(const P2PPtrs& shards, char* dst, int64_t bytes_S, int rank,
+static cudaError_t ag_shards_ce_m(const P2PPtrs& dsts, const void* shard, int64_t bytes_S, int rank,
                                   const P2PSignals& sg, uint64_t epoch, cudaStream_t st) {
-  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
+  if (cudaError_t e = memop_barrier(sg, rank, M, epoch, 0, st)) return e;
   for (int p = 0; p < M; ++p) {
     const int r = (rank + p) % M;
-    cudaError_t e = cudaMemcpyAsync(dst + int64_t(r) * bytes_S, shards.p[r], size_t(bytes_S),
-                                    cudaMemcpyDeviceToDevice, st);
+    char* dst = static_cast<char*>(const_cast<void*>(dsts.p[r])) + int64_t(rank) * bytes_S;
+    cudaError_t e = cudaMemcpyAsync(dst, shard, size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
   }
-  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
-  return cudaGetLastError();
+  return memop_barrier(sg, rank, M, epoch, 1, st);
 }
 
-cudaError_t launch_ag_shards(const P2PPtrs& shards, void* dst, int64_t bytes_S, int rank, int m,
+cudaError_t launch_ag_shards(const P2PPtrs& dsts, const void* shard, int64_t bytes_S, int rank, int m,
                              const P2PSignals* sg, uint64_t epoch, cudaStream_t st) {
-  char* d = static_cast<char*>(dst);
-  if (m == 1) return cudaMemcpyAsync(d, shards.p[0], size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
+  if (m == 1)
+    return cudaMemcpyAsync(const_cast<void*>(dsts.p[0]), shard, size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
   if (!sg) return cudaErrorInvalidValue;
   switch (m) {
 #define AGS_CASE(MM) \
   case MM:           \
-    return ag_shards_ce_m<MM>(shards, d, bytes_S, rank, *sg, epoch, st);
+    return ag_shards_ce_m<MM>(dsts, shard, bytes_S, rank, *sg, epoch, st);
     AGS_CASE(2) AGS_CASE(3) AGS_CASE(4) AGS_CASE(5) AGS_CASE(6) AGS_CASE(7) AGS_CASE(8)
 #undef AGS_CASE
     default:

@@ -8,7 +8,7 @@
 //   [17]     error flag: bit 0 = a barrier wait exceeded sg.timeout_ns (the
 //            kernel then gives up waiting instead of hanging the device;
 //            rsdb_p2p_check reports and clears it)
-// p2p_start: block 0 publishes `epoch` to every peer (after a system fence),
+// p2p_start: block 0 publishes `epoch` to every peer (release store),
 // every CTA waits until all peers have published -- every rank's prior stream
 // work is then complete.  p2p_done: the last CTA (atomic counter) fences,
 // publishes to every peer and waits for all peers, so the kernel -- and the
@@ -57,10 +57,11 @@ __device__ __forceinline__ void wait_epoch(const P2PSignals& sg, const uint64_t*
 }
 
 __device__ __forceinline__ void p2p_start(const P2PSignals& sg, int rank, int m, uint64_t epoch) {
-  if (blockIdx.x == 0 && threadIdx.x < m && int(threadIdx.x) != rank) {
-    __threadfence_system();
+  // st.release.sys alone publishes everything before it (cumulative); a
+  // separate fence.sc.sys in front of it cost ~1 us per barrier
+  // (profiles/r2/latency/probe_barrier.txt)
+  if (blockIdx.x == 0 && threadIdx.x < m && int(threadIdx.x) != rank)
     st_release_sys(sg_peer(sg, int(threadIdx.x)) + rank, epoch);
-  }
   if (threadIdx.x == 0) {
     for (int r = 0; r < m; ++r) {
       if (r == rank) continue;
@@ -77,8 +78,9 @@ __device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, 
     unsigned int* ctr = reinterpret_cast<unsigned int*>(sg.local + 16);
     const unsigned int old = atomicAdd(ctr, 1u);
     if (old == gridDim.x - 1) {
+      // every CTA's fence + counter increment precede this one's (release
+      // pattern); the release stores below carry them to the peers
       atomicExch(ctr, 0u);
-      __threadfence_system();
 #pragma unroll
       for (int r = 0; r < P2P_MAX_RANKS; ++r)
         if (r < m && r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);

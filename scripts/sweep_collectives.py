@@ -28,12 +28,17 @@ import paper_2602_22437_b200 as R  # noqa: E402
 from synth import workloads as W  # noqa: E402
 
 
-def timeit(fn, iters, stream, world):
+def timeit(fn, iters, stream, world, gate=False):
     for _ in range(3):
         fn()
     stream.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if gate:  # hold the stream so the host enqueues every call before the first runs:
+        # the events then time the device alone, not the launch rate (small sizes)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(20_000_000)
+        fn()  # absorbs the ranks' skew at the end of the sleep
     e0.record(stream)
     for _ in range(iters):
         fn()
@@ -50,6 +55,8 @@ def main():
     ap.add_argument("--layouts", default="ragged,even,ideal")
     ap.add_argument("--ops", default="ag,rs")
     ap.add_argument("--path", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--gate", action="store_true",
+                    help="device-only timing: a sleep kernel holds the stream while the host enqueues")
     ap.add_argument("--workload", default="bucket",
                     help="bucket (config 5) | llama8b-layer | llama8b-root (config 3) | "
                          "dsv3 (config 4) | llama1b-layer | llama1b-root (config 2): whole units "
@@ -96,7 +103,12 @@ def main():
                 p2p = R.P2P(comm, [pf, gf])
             iters = max(5, min(50, int(4e9 / (world * S * 4))))
             for op in args.ops.split(","):
-                if op == "ag":
+                if op == "barrier":  # the start + done barrier pair alone (p2p path)
+                    if p2p is None:
+                        continue
+                    fn = lambda: p2p.barrier(st)  # noqa: E731
+                    nbytes = 0
+                elif op == "ag":
                     fn = ((lambda: R.all_gather(unit, st)) if p2p is None
                           else (lambda: R.all_gather_p2p(unit, p2p, st)))  # noqa: E731
                     nbytes = world * S * 2
@@ -109,12 +121,12 @@ def main():
                 else:
                     fn = lambda: R.reduce_scatter(unit, st)  # noqa: E731
                     nbytes = world * S * 4
-                ms = timeit(fn, iters, st, world)
+                ms = timeit(fn, iters, st, world, args.gate)
                 bus = nbytes / (ms * 1e-3) * (world - 1) / world / 1e9
                 good = E * (2 if op == "ag" else 4) / (ms * 1e-3) * (world - 1) / world / 1e9
                 if rank == 0:
                     print(json.dumps({"workload": args.workload,
-                                      "mb": mb, "layout": kind, "op": op, "path": args.path,
+                                      "mb": mb, "layout": kind, "op": op, "path": args.path, "gated": args.gate,
                                       "m": world, "S": S,
                                       "E": E, "ms": ms, "busbw_gbs": bus, "goodput_gbs": good,
                                       "pad": lay.padding, "nccl_env": {k: v for k, v in os.environ.items()
