@@ -265,6 +265,20 @@ rsdb_status rsdb_step_8bit_adam_dynamic(rsdb_unit*, const rsdb_adam_state*, cons
                                         int64_t step, void* stream);
 /* Host only: the two 256-value maps (ascending fp32) the dynamic codec uses. */
 rsdb_status rsdb_dynamic_code_maps(float* m_map, float* v_map);
+/* Host only: the lookup tables the dynamic codec's kernels decide codes with
+ * (the nearest-map-value rule above, tabulated; exported so tests can replay
+ * the kernels' decision).  For y = fl(x / A) in [-1, 1], with bits b of y,
+ * mag = b & 0x7fffffff, MB = 6 (m, signed map) or 7 (v, unsigned map),
+ * SH = 23 - MB, LOW = 2^SH - 1:
+ *   idx = max((mag >> SH) - (100 << MB), 0)   (+ (28 << MB) if y's sign bit is set, m only)
+ *   e   = table[idx]
+ *   yl  = mag & LOW, or LOW - (mag & LOW) if the sign bit is set (m only)
+ *   code = (e >> 24) + (yl >= (e & 0xffffff))
+ * m_table holds RSDB_DYN_TABLE_M_LEN entries, v_table RSDB_DYN_TABLE_V_LEN
+ * (caller-owned).  EINVAL on NULL. */
+#define RSDB_DYN_TABLE_M_LEN 3584
+#define RSDB_DYN_TABLE_V_LEN 3584
+rsdb_status rsdb_dynamic_code_tables(uint32_t* m_table, uint32_t* v_table);
 
 /* ======================================================================== */
 /* Fused collectives over NVLink peer memory.              */

@@ -384,6 +384,15 @@ def dynamic_code_maps():
     return list(m), list(v)
 
 
+def dynamic_code_tables():
+    """The code tables the dynamic codec's kernels decide with
+    (rsdb_dynamic_code_tables: layout in include/rsdb.h), as two lists of uint32."""
+    m = (C.c_uint32 * _c.RSDB_DYN_TABLE_M_LEN)()
+    v = (C.c_uint32 * _c.RSDB_DYN_TABLE_V_LEN)()
+    check(lib.rsdb_dynamic_code_tables(m, v))
+    return list(m), list(v)
+
+
 # ---------------------------------------------------------------- N1: NVLink peer memory
 def ipc_handle(t) -> bytes:
     buf = C.create_string_buffer(_c.RSDB_IPC_BYTES)

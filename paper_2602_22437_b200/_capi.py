@@ -20,6 +20,7 @@ RSDB_GRAN_FLAT, RSDB_GRAN_ROWS, RSDB_GRAN_WHOLE, RSDB_GRAN_ELEM = range(4)
 RSDB_NKINDS = 8
 RSDB_IPC_BYTES = 72
 RSDB_P2P_SIGNAL_BYTES = 4096
+RSDB_DYN_TABLE_M_LEN = RSDB_DYN_TABLE_V_LEN = 3584
 
 i32, i64, vp = C.c_int32, C.c_int64, C.c_void_p
 P_i64, P_i32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
@@ -122,6 +123,7 @@ _SIGS = {
     "rsdb_dbuffer_step_8bit_adam_dynamic": (i32, [vp, C.POINTER(AdamCfg), i64, vp]),
     "rsdb_step_8bit_adam_dynamic": (i32, [vp, C.POINTER(AdamState), C.POINTER(AdamCfg), i64, vp]),
     "rsdb_dynamic_code_maps": (i32, [C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "rsdb_dynamic_code_tables": (i32, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "rsdb_dbuffer_zero_grads": (i32, [vp, vp]),
     "rsdb_dbuffer_step_host": (i32, [vp, vp, C.POINTER(AdamCfg), i64, C.POINTER(vp), C.POINTER(vp), vp]),
     "rsdb_dbuffer_reduce_scatter_adam": (i32, [vp, vp, C.POINTER(AdamCfg), i64, vp]),

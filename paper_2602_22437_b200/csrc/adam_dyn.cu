@@ -2,25 +2,35 @@
 // of Dettmers et al. (reading R25) instead of the linear absmax code.
 //
 // The two 256-entry maps (signed for m, unsigned for v) are built on the host
-// in double exactly as R25 writes them, rounded once to float and kept in
-// __constant__ memory; every CTA copies them to shared memory REPLICATED PER
-// LANE (map[k] at word k * 32 + lane), so the data-dependent lookups of a warp
-// never conflict on a bank (the round-1 kernel, with one copy and a bucket
-// table, was bound by 3-4-way conflicted lookups at 0.39 of HBM).  Per block:
+// in double exactly as R25 writes them and rounded once to float.  Per block:
 // dequantise (map[code] * A), the same fp32 AdamW update as the linear
 // kernels (adam_elem), block absmax, then requantise each moment to the
 // nearest map value of y = fl(m / A) -- the oracle's decision in the oracle's
 // precision: hi = first code with map[hi] >= y (clamped to [1, 255]), code =
-// hi if fl(map[hi] - y) < fl(y - map[hi-1]) else hi - 1.  hi is found from
-// the map's closed form (R25: decade i holds 2^i (signed) / 2^(i+1)
-// (unsigned) equally spaced values of [0.1 D_i, D_i]): decade by six fp32
-// comparisons, index inside the decade by one multiply-add, then two
-// correcting scans on the exact fp32 map values (normally zero steps), so
-// the decision is the table's, not the approximation's.  Full contiguous
-// 2048-element blocks use 16-B vector loads (4 elements per thread per quad);
-// other blocks a masked element path; blocks > 2048 elements two passes.
+// hi if fl(map[hi] - y) < fl(y - map[hi-1]) else hi - 1.
+//
+// That decision is a non-decreasing step function of y with 255 steps, so
+// the kernel does not search the map: it looks it up.  The host cuts the
+// fp32 values of [-1, 1] into bins by their sign, exponent and top MB
+// mantissa bits (MB = 6 signed / 7 unsigned; magnitudes below 2^-27 share the
+// first bin) and evaluates the decision rule itself at the bin ends.  Every
+// bin holds at most one step: neighbouring map values of decade i lie
+// 0.9 D_i / 2^i (signed) or / 2^(i+1) (unsigned) apart, wider than any bin
+// (2^e / 2^MB for the binade [2^e, 2^(e+1)) below D_i) -- and
+// build_dyn_table checks it, the launch fails otherwise.  So one 32-bit
+// entry per bin -- the code at the bin's low end and the low mantissa bits
+// where the step sits -- gives the code with one lookup and one integer
+// comparison: ~10 instructions per moment instead of the ~40 of the
+// closed-form search it replaces (profiles/r2/dyn/).  The
+// tables are exported by rsdb_dynamic_code_tables; tests/test_dyn_table.py
+// replays the lookup against the oracle's rule, and
+// tests/dyn_table_exhaustive.py over every fp32 y in [-1, 1].
+// Full contiguous 2048-element blocks use 16-B vector loads (4 elements per
+// thread per quad); other blocks a masked element path; blocks > 2048
+// elements two passes.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -31,9 +41,16 @@
 namespace rsdb {
 
 constexpr int DYN_NT = 256;
+constexpr int DYN_E0 = 100;  // first binade with its own bins: [2^-27, 2^-26)
+constexpr int DYN_MB_M = 6, DYN_MB_V = 7;  // mantissa bits of the bin index
+constexpr int DYN_NB_M = 28 << DYN_MB_M;   // bins per sign, binades 2^-27 .. 2^0
+constexpr int DYN_NB_V = 28 << DYN_MB_V;
+static_assert(DYN_TABLE_M_LEN == 2 * DYN_NB_M && DYN_TABLE_V_LEN == DYN_NB_V, "table sizes");
 
 struct DynTables {
-  float map[2][256];  // [0] signed (first moment), [1] unsigned (second)
+  float map[2][256];              // [0] signed (first moment), [1] unsigned (second)
+  uint32_t tm[2 * DYN_NB_M];      // signed: [sign][bin]
+  uint32_t tv[DYN_NB_V];          // unsigned
 };
 __constant__ DynTables c_dyn;
 
@@ -63,96 +80,110 @@ void dyn_maps(float m_map[256], float v_map[256]) {
   build_dyn_map(false, v_map);
 }
 
+// the decision rule (host, fp32 arithmetic)
+static int dyn_rule(const float map[256], float y) {
+  int hi = int(std::lower_bound(map, map + 256, y) - map);  // first map[hi] >= y
+  hi = hi < 1 ? 1 : (hi > 255 ? 255 : hi);
+  const float d_hi = map[hi] - y, d_lo = y - map[hi - 1];
+  return d_hi < d_lo ? hi : hi - 1;
+}
+static float fbits(uint32_t b) {
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+
+// Entry of bin `idx` (magnitude bits [L, L + 2^SH), SH = 23 - MB; bin 0 also
+// takes every magnitude below) on side `neg`: bits 31..24 the code at the
+// bin's low end in y (the largest magnitude when negative), bits 23..0 the
+// comparison value: with yl = mag & LOW (positive) or LOW - (mag & LOW)
+// (negative), code = c0 + (yl >= thr); thr = LOW + 1 when the bin holds no
+// step.  Returns false if a bin holds more than one step (or bin 0 one).
+static bool build_dyn_table(const float map[256], int MB, bool neg, uint32_t* out, int nb) {
+  const int SH = 23 - MB;
+  const uint32_t LOW = (1u << SH) - 1, ONE = 0x3F800000u;
+  for (int idx = 0; idx < nb; ++idx) {
+    const uint32_t L = (uint32_t(DYN_E0 << MB) + uint32_t(idx)) << SH;
+    uint32_t lo = idx == 0 ? 0u : L, hi = L + LOW;
+    if (lo > ONE) lo = ONE;  // bins above 1.0 are never used: same entry as 1.0
+    if (hi > ONE) hi = ONE;
+    auto code = [&](uint32_t mag) { return dyn_rule(map, neg ? -fbits(mag) : fbits(mag)); };
+    const int c_small = code(lo), c_big = code(hi);  // at the smallest / largest magnitude
+    const int c0 = neg ? c_big : c_small, c1 = neg ? c_small : c_big;
+    uint32_t thr = LOW + 1;
+    if (c1 != c0) {
+      if (c1 != c0 + 1 || idx == 0) return false;
+      // transition magnitude: positive, the smallest with code c1; negative,
+      // the largest with code c1 (code(-mag) falls as mag grows)
+      uint32_t a = lo, b = hi;
+      if (!neg) {  // code(a) = c0, code(b) = c1: find the first b
+        while (b - a > 1) {
+          const uint32_t m = a + (b - a) / 2;
+          (code(m) == c1 ? b : a) = m;
+        }
+        thr = b & LOW;
+      } else {  // code(a) = c1, code(b) = c0: find the last a
+        while (b - a > 1) {
+          const uint32_t m = a + (b - a) / 2;
+          (code(m) == c1 ? a : b) = m;
+        }
+        thr = LOW - (a & LOW);
+      }
+    }
+    out[idx] = (uint32_t(c0) << 24) | thr;
+  }
+  return true;
+}
+
+static bool dyn_tables(DynTables& h) {
+  dyn_maps(h.map[0], h.map[1]);
+  return build_dyn_table(h.map[0], DYN_MB_M, false, h.tm, DYN_NB_M) &&
+         build_dyn_table(h.map[0], DYN_MB_M, true, h.tm + DYN_NB_M, DYN_NB_M) &&
+         build_dyn_table(h.map[1], DYN_MB_V, false, h.tv, DYN_NB_V);
+}
+
+bool dyn_code_tables(uint32_t* m_tab, uint32_t* v_tab) {
+  static DynTables h;
+  if (!dyn_tables(h)) return false;
+  std::memcpy(m_tab, h.tm, sizeof h.tm);
+  std::memcpy(v_tab, h.tv, sizeof h.tv);
+  return true;
+}
+
 static cudaError_t ensure_dyn_tables() {
   static bool done = false;
   if (done) return cudaSuccess;
   static DynTables h;
-  dyn_maps(h.map[0], h.map[1]);
+  if (!dyn_tables(h)) return cudaErrorInvalidValue;  // a bin with two steps: cannot happen for R25's maps
   const cudaError_t e = cudaMemcpyToSymbol(c_dyn, &h, sizeof h);
   if (e == cudaSuccess) done = true;
   return e;
 }
 
-// lane-replicated map: entry k of this lane's copy
-__device__ __forceinline__ float rmap(const float* rep, int k, int lane) { return rep[(k << 5) | lane]; }
+// dequantisation map replicated 8 times in shared memory (entry k of copy c
+// at word k * 8 + c, lane uses copy lane & 7): a warp's 32 lookups fall into
+// at most 4 words per bank
+__device__ __forceinline__ float rmap(const float* rep, int k, int lane) { return rep[(k << 3) | (lane & 7)]; }
 
-// Candidate position of a = |y| <= 1 among the map's positive decade values
-// (R25 closed form; decade i holds 2^(i+w) equally spaced values of
-// [0.1 D_i, D_i], w = 0 signed / 1 unsigned, whose first index is 128 + 2^i - 1
-// (signed) or 2^(i+1) - 1 (unsigned)).  Plain fp32 operations (_rn: no FMA
-// contraction) so tests/test_dyn_candidate.py can replay it bit for bit:
-// for EVERY fp32 y in [-1, 1] the true hi (first index with map >= y,
-// clamped to [1, 255]) lies within one of the clamped candidate.
-// per-binade decade table (shared memory, 32 entries -- any lane pattern of
-// <= 32 distinct words is bank-conflict free up to the 8-B entry pairing):
-// for the binade [2^(E-127), 2^(E-126)) of biased exponent E = DYN_E0 + e,
-// x = the decade count of its lower end (#{thresholds 1e-6 .. 1e-1 <= 2^(E-127)})
-// and y = the one threshold inside the binade (bits; +inf if none).  Then
-// #{thresholds <= a} = x + (a >= y) for every a in the binade -- the same
-// comparisons as a six-step cascade on the same float thresholds.
-constexpr int DYN_E0 = 100;  // 2^-27 < 1e-6 / 10: everything below is decade 0
-struct DynDecade {
-  int2 bin[32];     // {decade count at the binade's start, threshold bits}
-  float dinv[8];    // 10^(6 - i), i = 0..6
-};
-__device__ __forceinline__ float dyn_th(int k) {  // thresholds 1e-6 .. 1e-1 (float32)
-  return k == 0 ? 1e-6f : k == 1 ? 1e-5f : k == 2 ? 1e-4f : k == 3 ? 1e-3f : k == 4 ? 1e-2f : 1e-1f;
-}
-__device__ __forceinline__ void dyn_decade_init(DynDecade& D) {
-  const int e = int(threadIdx.x);
-  if (e < 32) {
-    const float lo = __uint_as_float(uint32_t(DYN_E0 + e) << 23), hi = 2.f * lo;
-    int cnt = 0;
-    float t = __uint_as_float(0x7f800000u);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      if (dyn_th(k) <= lo) ++cnt;
-      else if (dyn_th(k) < hi) t = dyn_th(k);
-    }
-    D.bin[e] = make_int2(cnt, int(__float_as_uint(t)));
-  } else if (e < 32 + 7) {
-    const int i = e - 32;  // 10^(6 - i)
-    D.dinv[i] = i == 0 ? 1e6f : i == 1 ? 1e5f : i == 2 ? 1e4f : i == 3 ? 1e3f : i == 4 ? 1e2f : i == 5 ? 1e1f : 1.f;
-  }
-}
-
+// the code of y = fl(m / A) in [-1, 1] (signed) / [0, 1] (unsigned): one
+// table lookup and one comparison (see the file comment)
 template <bool SIGNED>
-__device__ __forceinline__ int dyn_candidate(const DynDecade& D, float a) {
-  constexpr int W = SIGNED ? 0 : 1;
-  int e = int(__float_as_uint(a) >> 23) - DYN_E0;  // a >= 0, <= 1: e <= 27
-  e = e < 0 ? 0 : e;
-  const int2 bt = D.bin[e];
-  const int i = bt.x + int(a >= __int_as_float(bt.y));
-  const float Dinv = D.dinv[i];
-  const int cnt = 1 << (i + W);
-  float u = __fsub_rn(__fmul_rn(a, Dinv), 0.1f);
-  u = __fmul_rn(__fmul_rn(u, __int2float_rn(cnt)), 1.0f / 0.9f);
-  int j = __float2int_rn(__fsub_rn(u, 0.5f));
-  j = min(max(j, 0), cnt - 1);
-  return (SIGNED ? 127 : 0) + cnt + j;
-}
-
-// nearest map value of y (R25, the oracle's fp32 rule; ties -> lower code),
-// branch free: hi is one of c-1, c, c+1 (c the clamped candidate), decided by
-// two comparisons on the exact map values map[c-2 .. c+1] (4 conflict-free
-// lookups in this lane's copy)
-template <bool SIGNED>
-__device__ __forceinline__ uint32_t dyn_code(const float* rep, const DynDecade& D, int lane, float y) {
-  int c;
+__device__ __forceinline__ uint32_t dyn_code(const uint32_t* tab, float y) {
+  constexpr int MB = SIGNED ? DYN_MB_M : DYN_MB_V;
+  constexpr int SH = 23 - MB;
+  constexpr uint32_t LOW = (1u << SH) - 1;
+  const uint32_t b = __float_as_uint(y);
+  const uint32_t mag = b & 0x7fffffffu;
+  int idx = int(mag >> SH) - (DYN_E0 << MB);
+  idx = idx < 0 ? 0 : idx;
+  uint32_t yl = mag & LOW;
   if (SIGNED) {
-    const int p = dyn_candidate<true>(D, fabsf(y));
-    c = y < 0.f ? 255 - p : p;  // -map[p] sits at 254 - p; hi is the index after it
-  } else {
-    c = dyn_candidate<false>(D, y);
+    const uint32_t sgn = b >> 31;
+    idx += int(sgn) * DYN_NB_M;
+    yl ^= (0u - sgn) & LOW;
   }
-  c = c < 2 ? 2 : (c > 254 ? 254 : c);
-  const float* q = rep + ((c - 2) << 5) + lane;
-  const float v0 = q[0], v1 = q[32], v2 = q[64], v3 = q[96];
-  const bool a1 = v1 >= y, a2 = v2 >= y;
-  const int hi = a1 ? c - 1 : (a2 ? c : c + 1);
-  const float hv = a1 ? v1 : (a2 ? v2 : v3);
-  const float lv = a1 ? v0 : (a2 ? v1 : v2);
-  return uint32_t(__fsub_rn(hv, y) < __fsub_rn(y, lv) ? hi : hi - 1);
+  const uint32_t e = tab[idx];
+  return (e >> 24) + (yl >= (e & 0xffffffu) ? 1u : 0u);
 }
 
 // y = fl32(x / A) through fp64: float(double(x) * RN64(1/A)) -- the relative
@@ -164,22 +195,55 @@ __device__ __forceinline__ float div_exact(float x, double rA) {
   return __double2float_rn(__dmul_rn(double(x), rA));
 }
 
+constexpr int DYN_STAGES = 1;
 struct DynSmem {
-  float rep[2][256 * 32];  // lane-replicated maps (64 KB)
+  AdamStage stage[DYN_STAGES];  // TMA ring: the next block's inputs (20 KB)
+  float rep[2][256 * 8];        // dequantisation maps, 8 copies (16 KB)
+  uint32_t tm[2 * DYN_NB_M];    // code tables (28 KB)
+  uint32_t tv[DYN_NB_V];
 };
 
+// Persistent CTAs walk the block table; as soon as a block's inputs are in
+// registers, thread 0 bulk-copies the CTA's next block (fp32 master + grad,
+// both code arrays: 20 KB) into the one stage (as adam8_tma_kernel), so the
+// code decision of one block overlaps the loads of the next (without the
+// stage: long-scoreboard stalls 3.7 per issued instruction; with two stages
+// the 100 KB of shared memory leave 2 CTAs per SM and it is slower:
+// profiles/r2/dyn/).  Blocks a bulk copy cannot take (misaligned, partial,
+// 2-D, long) load directly.
 template <bool PARAM_BF16>
 __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* __restrict__ tbl, int64_t nblocks,
                                                           AdamPtrs P, AdamScalars s) {
-  extern __shared__ __align__(16) float dyn_smem[];
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
   DynSmem& T = *reinterpret_cast<DynSmem*>(dyn_smem);
+  __shared__ __align__(8) uint64_t full[DYN_STAGES];
   __shared__ float red_m[2][DYN_NT / 32], red_v[2][DYN_NT / 32];
-  __shared__ DynDecade dec;
-  dyn_decade_init(dec);
-  for (int i = threadIdx.x; i < 2 * 256 * 32; i += DYN_NT) {
-    const int w = i >> 13, k = (i >> 5) & 255;
-    T.rep[w][i & 8191] = c_dyn.map[w][k];
+  auto issue = [&](int64_t b, int st) {  // thread 0: stage st <- block b
+    const AdamBlock nb = tbl[b];
+    if (adam_tma_ok(nb)) {
+      mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
+      bulk_g2s(T.stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
+      bulk_g2s(T.stage[st].g, P.grad + nb.grad_off, sizeof(float) * ADAM_TILE, &full[st]);
+      bulk_g2s(T.stage[st].mq, P.mq + nb.state_off, ADAM_TILE, &full[st]);
+      bulk_g2s(T.stage[st].vq, P.vq + nb.state_off, ADAM_TILE, &full[st]);
+    } else {
+      mbar_arrive(&full[st]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < DYN_STAGES; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < DYN_STAGES; ++st) {
+      const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
+      if (b < nblocks) issue(b, st);
+    }
   }
+  for (int i = threadIdx.x; i < 2 * 256 * 8; i += DYN_NT) {
+    const int w = i >> 11, k = (i >> 3) & 255;
+    T.rep[w][i & 2047] = c_dyn.map[w][k];
+  }
+  for (int i = threadIdx.x; i < 2 * DYN_NB_M; i += DYN_NT) T.tm[i] = c_dyn.tm[i];
+  for (int i = threadIdx.x; i < DYN_NB_V; i += DYN_NT) T.tv[i] = c_dyn.tv[i];
   __syncthreads();
   const int lane = int(threadIdx.x) & 31;
   const float* mapm = T.rep[0];
@@ -189,16 +253,27 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
   using G = AdamGeom<DYN_NT>;  // 2 quads per thread
   int it = 0;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
+    const int st = it % DYN_STAGES;
+    const uint32_t ph = uint32_t(it / DYN_STAGES) & 1u;
     const AdamBlock blk = tbl[b];
     const float Am = P.mabs[blk.slot], Av = P.vabs[blk.slot];
     float* rm = red_m[it & 1];
     float* rv = red_v[it & 1];
+    auto refill = [&]() {  // after the absmax barrier: every thread has read stage st
+      if (threadIdx.x == 0) {
+        const int64_t nb = b + int64_t(DYN_STAGES) * gridDim.x;
+        if (nb < nblocks) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(nb, st);
+        }
+      }
+    };
     // R27: A = 0, NaN or +inf -> the code of 0 everywhere
     // block-uniform: A finite and > 0 (else the code of 0), 1/A in fp64
     double rAm = 0.0, rAv = 0.0;
     bool okm = false, okv = false;
-    auto qm = [&](float m, float) { return okm ? dyn_code<true>(mapm, dec, lane, div_exact(m, rAm)) : zero_m; };
-    auto qv = [&](float v, float) { return okv ? dyn_code<false>(mapv, dec, lane, div_exact(v, rAv)) : zero_v; };
+    auto qm = [&](float m) { return okm ? dyn_code<true>(T.tm, div_exact(m, rAm)) : zero_m; };
+    auto qv = [&](float v) { return okv ? dyn_code<false>(T.tv, div_exact(v, rAv)) : zero_v; };
     auto set_div = [&](float am_, float av_) {
       okm = am_ > 0.f && am_ <= FLT_MAX_F;
       okv = av_ > 0.f && av_ <= FLT_MAX_F;
@@ -206,17 +281,29 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
       rAv = okv ? 1.0 / double(av_) : 0.0;
     };
     float am = 0.f, av = 0.f;
-    const bool fast = blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
-                      (blk.grad_off & 3) == 0 && (blk.param_off & 3) == 0;
+    mbar_wait(&full[st], ph);
+    const bool staged = adam_tma_ok(blk);
+    const bool fast = staged || (blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
+                                 (blk.grad_off & 3) == 0 && (blk.param_off & 3) == 0);
     if (fast) {
+      const AdamStage& S = T.stage[st];
       float p[G::EPT], m[G::EPT], v[G::EPT];
 #pragma unroll
       for (int k = 0; k < G::Q; ++k) {
         const int a = G::quad(k);
-        const int4 pv = ld_na_v4(P.master + blk.state_off + a);
-        const int4 gv = ld_nc_v4(P.grad + blk.grad_off + a);
-        const uint32_t cm = ld_na_u32(mq + blk.state_off + a);
-        const uint32_t cv = ld_na_u32(P.vq + blk.state_off + a);
+        int4 pv, gv;
+        uint32_t cm, cv;
+        if (staged) {
+          pv = *reinterpret_cast<const int4*>(S.p + a);
+          gv = *reinterpret_cast<const int4*>(S.g + a);
+          cm = *reinterpret_cast<const uint32_t*>(S.mq + a);
+          cv = *reinterpret_cast<const uint32_t*>(S.vq + a);
+        } else {
+          pv = ld_na_v4(P.master + blk.state_off + a);
+          gv = ld_nc_v4(P.grad + blk.grad_off + a);
+          cm = ld_na_u32(mq + blk.state_off + a);
+          cv = ld_na_u32(P.vq + blk.state_off + a);
+        }
         const float pp[4] = {__int_as_float(pv.x), __int_as_float(pv.y), __int_as_float(pv.z),
                              __int_as_float(pv.w)};
         const float gg[4] = {__int_as_float(gv.x), __int_as_float(gv.y), __int_as_float(gv.z),
@@ -234,16 +321,17 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
         }
       }
       block_max2<G::WARPS>(am, av, rm, rv);
+      refill();
       set_div(am, av);
 #pragma unroll
       for (int k = 0; k < G::Q; ++k) {
         const int a = G::quad(k);
         const float* pk = &p[4 * k];
         st_f4(P.master + blk.state_off + a, make_float4(pk[0], pk[1], pk[2], pk[3]));
-        st_u32(mq + blk.state_off + a, qm(m[4 * k], am) | (qm(m[4 * k + 1], am) << 8) |
-                                           (qm(m[4 * k + 2], am) << 16) | (qm(m[4 * k + 3], am) << 24));
-        st_u32(P.vq + blk.state_off + a, qv(v[4 * k], av) | (qv(v[4 * k + 1], av) << 8) |
-                                             (qv(v[4 * k + 2], av) << 16) | (qv(v[4 * k + 3], av) << 24));
+        st_u32(mq + blk.state_off + a, qm(m[4 * k]) | (qm(m[4 * k + 1]) << 8) | (qm(m[4 * k + 2]) << 16) |
+                                           (qm(m[4 * k + 3]) << 24));
+        st_u32(P.vq + blk.state_off + a, qv(v[4 * k]) | (qv(v[4 * k + 1]) << 8) | (qv(v[4 * k + 2]) << 16) |
+                                             (qv(v[4 * k + 3]) << 24));
         if constexpr (PARAM_BF16)
           st_u2(static_cast<uint16_t*>(P.param) + blk.param_off + a,
                 make_uint2(pack_bf16x2(pk[0], pk[1]), pack_bf16x2(pk[2], pk[3])));
@@ -263,8 +351,8 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
       auto store = [&](int i, float p, float m, float v) {
         const int64_t o = blk_off(blk, i);
         P.master[blk.state_off + o] = p;
-        mq[blk.state_off + o] = uint8_t(qm(m, am));
-        P.vq[blk.state_off + o] = uint8_t(qv(v, av));
+        mq[blk.state_off + o] = uint8_t(qm(m));
+        P.vq[blk.state_off + o] = uint8_t(qv(v));
         if constexpr (PARAM_BF16)
           static_cast<__nv_bfloat16*>(P.param)[blk.param_off + o] = __float2bfloat16_rn(p);
         else
@@ -283,6 +371,7 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
           }
         }
         block_max2<G::WARPS>(am, av, rm, rv);
+        refill();
         set_div(am, av);
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
@@ -297,6 +386,7 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
           av = fmax_nan(av, v);
         }
         block_max2<G::WARPS>(am, av, rm, rv);
+        refill();
         set_div(am, av);
         for (int i = threadIdx.x; i < blk.len; i += DYN_NT) {
           float m, v;

@@ -449,6 +449,14 @@ rsdb_status rsdb_dynamic_code_maps(float* m_map, float* v_map) {
   return OK_CLEAR();
 }
 
+rsdb_status rsdb_dynamic_code_tables(uint32_t* m_table, uint32_t* v_table) {
+  static_assert(rsdb::DYN_TABLE_M_LEN == RSDB_DYN_TABLE_M_LEN && rsdb::DYN_TABLE_V_LEN == RSDB_DYN_TABLE_V_LEN,
+                "table lengths");
+  if (!m_table || !v_table) return fail(RSDB_EINVAL, "null argument");
+  if (!rsdb::dyn_code_tables(m_table, v_table)) return fail(RSDB_EINVAL, "a table bin holds two steps");
+  return OK_CLEAR();
+}
+
 // ---------------------------------------------------------------------------
 // fused collectives over NVLink peer memory (N1)
 // ---------------------------------------------------------------------------

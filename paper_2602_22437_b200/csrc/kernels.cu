@@ -178,11 +178,6 @@ cudaError_t launch_cast_scale(const void* src, int src_bf16, float* dst, int64_t
   return cudaGetLastError();
 }
 
-// bulk copies need 16-B aligned global addresses: codes at state_off % 16
-__device__ __forceinline__ bool adam_tma_ok(const AdamBlock& b) {
-  return b.len == ADAM_TILE && b.cols == b.len && (b.state_off & 15) == 0 &&
-         ((b.grad_off | b.param_off) & 3) == 0;
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");

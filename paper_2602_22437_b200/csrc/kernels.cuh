@@ -137,6 +137,10 @@ cudaError_t launch_fp8_quant_ag(const Fp8Tile* tiles, int64_t ntiles, const floa
 cudaError_t launch_adam8_dyn(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p, const AdamScalars& s,
                              cudaStream_t st);
 void dyn_maps(float m_map[256], float v_map[256]);  // host: the two maps (R25)
+// host: the kernel's code tables (layout: rsdb_dynamic_code_tables); false if
+// a bin would hold two steps of the decision rule
+constexpr int DYN_TABLE_M_LEN = 2 * (28 << 6), DYN_TABLE_V_LEN = 28 << 7;
+bool dyn_code_tables(uint32_t* m_tab, uint32_t* v_tab);
 
 // ---- N3: distributed Muon (muon.cu) ----
 struct MuonSeg {

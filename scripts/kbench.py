@@ -1,8 +1,7 @@
 #!/usr/bin/env python
 """Kernel micro-benchmark (1 GPU): the Adam and cast kernels on the
-Llama-3.2-1B DBuffer of bench.py, timed with CUDA events over R repetitions.
-Variant selection for the Adam kernel is the RSDB_ADAM_KERNEL environment
-variable (read once per process).  Prints one JSON line."""
+Llama-3.2-1B DBuffer of bench.py, timed with CUDA events over KB_REPS
+repetitions (default 20).  Prints one JSON line."""
 import json
 import os
 import sys
@@ -57,8 +56,7 @@ def main():
     st.synchronize()
     dyn_ms = e0.elapsed_time(e1) / reps
     peak, _ = bench.load_peaks()
-    out = {"variant": os.environ.get("RSDB_ADAM_KERNEL", "default"),
-           "adam_ms": adam_ms, "adam_gbs": ab["adam"] / adam_ms / 1e6,
+    out = {"adam_ms": adam_ms, "adam_gbs": ab["adam"] / adam_ms / 1e6,
            "adam_frac": ab["adam"] / adam_ms / 1e6 / peak,
            "cast_ms": cast_ms, "cast_gbs": ab["cast"] / cast_ms / 1e6,
            "cast_frac": ab["cast"] / cast_ms / 1e6 / peak,
