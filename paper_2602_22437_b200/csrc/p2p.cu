@@ -196,7 +196,11 @@ static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int ran
     cudaFuncSetAttribute(rs_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_tma_kernel<M>, RS_TMA_THREADS, smem);
-    return num_sms() * (b < 1 ? 1 : b);
+    // 2 CTAs per SM (6 tiles of every rank in flight per SM) already saturate
+    // the peer reads; the full occupancy (8) only adds contention: 128 MB unit
+    // at N = 2, 120 vs 130 us (profiles/r2/latency/rs_grid.txt)
+    b = b < 1 ? 1 : (b > 2 ? 2 : b);
+    return num_sms() * b;
   }();
   const int64_t tiles = (S + RS_TMA_TILE - 1) / RS_TMA_TILE;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, grid_share(grid, sg)));
