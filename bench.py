@@ -89,6 +89,9 @@ def parse():
     ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
                     help="p2p: fused single-kernel collectives over NVLink peer memory "
                          "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
+    ap.add_argument("--watchdog", type=float, default=0.0,
+                    help="debugging: after this many seconds every rank prints all its Python "
+                         "stacks and exits (faulthandler), instead of hanging until killed")
     return ap.parse_args()
 
 
@@ -997,6 +1000,9 @@ def run_e2e(R, db, lays, views, cfg, t, stream, world, rank, args, job_bytes, p2
 
 def main():
     args = parse()
+    if args.watchdog > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.watchdog, exit=True)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -324,10 +324,7 @@ rsdb_status rsdb_p2p_create_local(rsdb_comm* comm, int32_t n_bufs, void* const* 
 /* Barrier spin limit of the p2p kernels (default 60 s): a kernel whose peer
  * never arrives stops waiting after `seconds`, sets an error flag in its
  * rank's signal buffer and returns (its results are then invalid) instead of
- * hanging the device.  The copy-engine AllGathers (rsdb_all_gather_p2p,
- * rsdb_all_gather_shards_p2p) synchronise with stream memory operations
- * instead of kernels and have no timeout: a missing peer stalls the stream.
- * EINVAL if seconds <= 0. */
+ * hanging the device.  EINVAL if seconds <= 0. */
 rsdb_status rsdb_p2p_set_timeout(rsdb_p2p*, double seconds);
 /* CTA budget of the SM-driven p2p kernels issued through this object
  * (collectives, fused RS + Adam (+ AG), FP8 AllGather, Muon redistribution):

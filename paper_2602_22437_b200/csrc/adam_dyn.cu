@@ -150,14 +150,12 @@ bool dyn_code_tables(uint32_t* m_tab, uint32_t* v_tab) {
   return true;
 }
 
-static cudaError_t ensure_dyn_tables() {
-  static bool done = false;
-  if (done) return cudaSuccess;
+static cudaError_t ensure_dyn_tables() {  // once per device: __constant__ lives in each device's module
   static DynTables h;
-  if (!dyn_tables(h)) return cudaErrorInvalidValue;  // a bin with two steps: cannot happen for R25's maps
-  const cudaError_t e = cudaMemcpyToSymbol(c_dyn, &h, sizeof h);
-  if (e == cudaSuccess) done = true;
-  return e;
+  static const bool built = dyn_tables(h);
+  if (!built) return cudaErrorInvalidValue;  // a bin with two steps: cannot happen for R25's maps
+  if (!once_per_device(&c_dyn)) return cudaSuccess;
+  return cudaMemcpyToSymbol(c_dyn, &h, sizeof h);
 }
 
 // dequantisation map replicated 8 times in shared memory (entry k of copy c
@@ -407,13 +405,11 @@ cudaError_t launch_adam8_dyn(const AdamBlock* tbl, int64_t nblocks, const AdamPt
   if (nblocks == 0) return cudaSuccess;
   if (cudaError_t e = ensure_dyn_tables()) return e;
   constexpr int smem = int(sizeof(DynSmem));
-  static bool attr = false;
-  if (!attr) {
+  if (once_per_device(reinterpret_cast<const void*>(adam8_dyn_kernel<true>))) {
     if (cudaError_t e = cudaFuncSetAttribute(adam8_dyn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
       return e;
     if (cudaError_t e = cudaFuncSetAttribute(adam8_dyn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
       return e;
-    attr = true;
   }
   int per = 0;
   if (p.param_bf16)

@@ -11,11 +11,27 @@
 // on a persistent grid of (resident CTAs per SM) x (148 SMs).
 #include <cuda_bf16.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 
 #include "adam_dev.cuh"
 #include "kernels.cuh"
 
 namespace rsdb {
+
+// per-device state (function attributes, __constant__ tables) must be set
+// once on EVERY device a launcher runs on: one process may drive several
+// devices (rsdb_p2p_create_local across GPUs)
+bool once_per_device(const void* key) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  return seen.insert({key, dev}).second;
+}
 
 int num_sms() {
   static int n = 0;
@@ -434,10 +450,9 @@ template <int NT, bool BF, int ST>
 static cudaError_t launch_adam8_pair(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
                                      const AdamScalars& s, cudaStream_t st) {
   const size_t smem = sizeof(AdamStage) * ST;
-  static int occ = [&] {
+  if (once_per_device(reinterpret_cast<const void*>(adam8_pair_kernel<NT, BF, ST>)))
     cudaFuncSetAttribute(adam8_pair_kernel<NT, BF, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    return resident_blocks(adam8_pair_kernel<NT, BF, ST>, NT, smem);
-  }();
+  static int occ = resident_blocks(adam8_pair_kernel<NT, BF, ST>, NT, smem);
   const int64_t items = (nblocks + 1) / 2;
   const int64_t blocks = std::min<int64_t>(items, int64_t(num_sms()) * occ);
   adam8_pair_kernel<NT, BF, ST><<<blocks, NT, smem, st>>>(tbl, nblocks, p, s);
@@ -448,11 +463,9 @@ template <int NT, bool BF, int ST>
 static cudaError_t launch_adam8_tma(const AdamBlock* tbl, int64_t nblocks, const AdamPtrs& p,
                                     const AdamScalars& s, cudaStream_t st) {
   const size_t smem = sizeof(AdamStage) * ST;
-  static int occ = [&] {
-    cudaFuncSetAttribute(adam8_tma_kernel<NT, BF, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    return resident_blocks(adam8_tma_kernel<NT, BF, ST>, NT, smem);
-  }();
+  if (once_per_device(reinterpret_cast<const void*>(adam8_tma_kernel<NT, BF, ST>)))
+    cudaFuncSetAttribute(adam8_tma_kernel<NT, BF, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  static int occ = resident_blocks(adam8_tma_kernel<NT, BF, ST>, NT, smem);
   const int64_t blocks = std::min<int64_t>(nblocks, int64_t(num_sms()) * occ);
   adam8_tma_kernel<NT, BF, ST><<<blocks, NT, smem, st>>>(tbl, nblocks, p, s);
   return cudaGetLastError();

@@ -61,6 +61,8 @@ cudaError_t launch_copy_segments(const CopySeg* segs_dev, int64_t nseg, int64_t 
                                  int src_bf16, int dst_bf16, float scale, cudaStream_t st);
 
 int num_sms();
+// true the first time `key` is seen on the current device (per-device setup)
+bool once_per_device(const void* key);
 
 // ---- fused collectives over NVLink peer memory (p2p.cu) ----
 constexpr int P2P_MAX_RANKS = 8;

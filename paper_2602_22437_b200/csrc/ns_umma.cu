@@ -362,14 +362,13 @@ cudaError_t launch_umma_gemm(int M, int N, int K, const void* A, int64_t lda, co
   if (cudaError_t e = encode_kmajor(&mb, B, N, K, ldb, UG_BN)) return e;
   UmmaEpi ep{alpha, beta, static_cast<const __nv_bfloat16*>(D), static_cast<__nv_bfloat16*>(C),
              static_cast<__nv_bfloat16*>(CT), ldd, ldc, ldct};
-  static bool attr = false;
-  if (!attr) {
+  static const char attr_key = 0;
+  if (once_per_device(&attr_key)) {
     for (auto k : {umma_gemm_kernel<false, false, false>, umma_gemm_kernel<true, false, false>,
                    umma_gemm_kernel<false, true, false>, umma_gemm_kernel<true, true, false>,
                    umma_gemm_kernel<false, false, true>, umma_gemm_kernel<true, false, true>})
       if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(UG_SMEM)))
         return e;
-    attr = true;
   }
   const int mt = (M + UG_BM - 1) / UG_BM, nt = (N + UG_BN - 1) / UG_BN;
   const int tiles = sym ? sym_tiles(mt, nt) : mt * nt;

@@ -10,8 +10,7 @@
 //        ReduceScatter, and no separate m*S cast pass.
 //  copy-engine AG       a4: rank k's copy engine pushes its shard into every
 //        peer's buffer with cudaMemcpyAsync over the mappings (rotated peer
-//        order) between a start and a done barrier made of stream memory
-//        operations (no kernel, no compute <-> copy engine hand-off).
+//        order) between a start and a done barrier kernel.
 //  rs_adam_tma_kernel   a6+a7+a8 (+ a4 with PUSH): the ReduceScatter feeds
 //        the 8-bit Adam update of the shard; with PUSH every updated bf16
 //        parameter is also stored into every peer's gathered buffer -- the
@@ -21,7 +20,6 @@
 // DESIGN.md §7b, profiles/r1/); only the measured best of each is built.
 //
 // Start/done barriers between the ranks: p2p_dev.cuh.
-#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <type_traits>
@@ -192,8 +190,9 @@ static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int ran
                             const int64_t* pad, int npad, const P2PSignals& sg, uint64_t epoch,
                             cudaStream_t st) {
   const size_t smem = size_t(RS_TMA_TILE) * 2 * M * RS_TMA_STAGES;
-  static const int grid = [&] {
+  if (once_per_device(reinterpret_cast<const void*>(rs_tma_kernel<M>)))
     cudaFuncSetAttribute(rs_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  static const int grid = [&] {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_tma_kernel<M>, RS_TMA_THREADS, smem);
     // 2 CTAs per SM (6 tiles of every rank in flight per SM) already saturate
@@ -208,63 +207,14 @@ static cudaError_t rs_tma_m(const P2PPtrs& grads, float* out, int64_t S, int ran
   return cudaGetLastError();
 }
 
-// Start (phase 0) or done (phase 1) barrier alone, one CTA (rsdb_p2p_barrier).
+// Start (phase 0) or done (phase 1) barrier alone, one CTA: brackets the
+// copy-engine AllGathers; rsdb_p2p_barrier.
 template <int M>
 __global__ void __launch_bounds__(32) p2p_barrier_kernel(P2PSignals sg, int rank, uint64_t epoch, int phase) {
   if (phase == 0)
     p2p_start(sg, rank, M, epoch);
   else
     p2p_done(sg, rank, M, epoch);
-}
-
-// The same barrier phase as stream memory operations, for the copy-engine
-// AllGathers: write `epoch` into every peer's word (the write is preceded by
-// a stream-scoped system memory barrier, so this stream's earlier copies are
-// visible first), then wait until every peer's word in the local buffer
-// reaches it.  Executed by the stream front end: no kernel launch and no hand
-// off between the compute and copy engines around the copies, which cost ~9 us
-// per AllGather with barrier kernels (1 MB push: 23.3 vs 16.5 us; 64 MB:
-// 115.9 vs 106.1 us, profiles/r2/latency/probe_barrier.txt).  The wait has
-// no timeout: a rank that never arrives stalls the stream (as a collective
-// library would); the kernel barriers keep the rsdb_p2p_set_timeout guard.
-using WriteValue64_t = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-using WaitValue64_t = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-static cudaError_t memop_fns(WriteValue64_t* w, WaitValue64_t* a) {
-  static WriteValue64_t fw = nullptr;
-  static WaitValue64_t fa = nullptr;
-  if (!fw || !fa) {
-    void* f1 = nullptr;
-    void* f2 = nullptr;
-    cudaDriverEntryPointQueryResult q1, q2;
-    if (cudaError_t e = cudaGetDriverEntryPoint("cuStreamWriteValue64", &f1, cudaEnableDefault, &q1)) return e;
-    if (cudaError_t e = cudaGetDriverEntryPoint("cuStreamWaitValue64", &f2, cudaEnableDefault, &q2)) return e;
-    if (!f1 || !f2 || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
-      return cudaErrorNotSupported;
-    fw = reinterpret_cast<WriteValue64_t>(f1);
-    fa = reinterpret_cast<WaitValue64_t>(f2);
-  }
-  *w = fw;
-  *a = fa;
-  return cudaSuccess;
-}
-static cudaError_t memop_barrier(const P2PSignals& sg, int rank, int m, uint64_t epoch, int phase,
-                                 cudaStream_t st) {
-  WriteValue64_t wr;
-  WaitValue64_t wt;
-  if (cudaError_t e = memop_fns(&wr, &wt)) return e;
-  for (int p = 1; p < m; ++p) {
-    const int r = (rank + p) % m;
-    if (wr(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(sg.peer[r] + 8 * phase + rank), epoch,
-           CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-      return cudaErrorLaunchFailure;
-  }
-  for (int p = 1; p < m; ++p) {
-    const int r = (rank + p) % m;
-    if (wt(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(sg.local + 8 * phase + r), epoch,
-           CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-      return cudaErrorLaunchFailure;
-  }
-  return cudaSuccess;
 }
 
 template <int M>
@@ -276,8 +226,12 @@ static cudaError_t ag_ce_m(const P2PPtrs& params, int64_t bytes_S, int rank, con
   // profiles/r2/latency/probe_barrier.txt).  The start barrier orders the
   // writes after every peer's prior work on its buffer; the done barrier
   // (signalled after this stream's copies complete) after every peer's
-  // pushes into this rank.
-  if (cudaError_t e = memop_barrier(sg, rank, M, epoch, 0, st)) return e;
+  // pushes into this rank.  The barriers are kernels: stream memory
+  // operations (cuStreamWaitValue64) would save ~9 us of engine hand-offs
+  // but block the whole hardware queue while they wait, and streams share
+  // hardware queues -- in the ZeRO-3 schedule (AllGather stream + compute
+  // stream) that deadlocked two ranks (profiles/r2/latency/README.md).
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
   const char* mine = static_cast<const char*>(params.p[rank]) + int64_t(rank) * bytes_S;
   for (int p = 1; p < M; ++p) {  // rotated peer order: ranks do not all write one GPU at once
     const int r = (rank + p) % M;
@@ -285,25 +239,27 @@ static cudaError_t ag_ce_m(const P2PPtrs& params, int64_t bytes_S, int rank, con
     cudaError_t e = cudaMemcpyAsync(dst, mine, size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
   }
-  return memop_barrier(sg, rank, M, epoch, 1, st);
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
+  return cudaGetLastError();
 }
 
 // AllGather from persistent shards (K-slot ring mode):
 // every rank's copy engine pushes its persistent shard into region `rank` of
 // every rank's slot (dsts.p[r]: rank r's slot, mapped; the own one by a local
-// copy), rotated peer order, between the start/done barriers (push and
-// stream-memory-operation barriers: see ag_ce_m).
+// copy), rotated peer order, between the start/done barrier kernels (push:
+// see ag_ce_m).
 template <int M>
 static cudaError_t ag_shards_ce_m(const P2PPtrs& dsts, const void* shard, int64_t bytes_S, int rank,
                                   const P2PSignals& sg, uint64_t epoch, cudaStream_t st) {
-  if (cudaError_t e = memop_barrier(sg, rank, M, epoch, 0, st)) return e;
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 0);
   for (int p = 0; p < M; ++p) {
     const int r = (rank + p) % M;
     char* dst = static_cast<char*>(const_cast<void*>(dsts.p[r])) + int64_t(rank) * bytes_S;
     cudaError_t e = cudaMemcpyAsync(dst, shard, size_t(bytes_S), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
   }
-  return memop_barrier(sg, rank, M, epoch, 1, st);
+  p2p_barrier_kernel<M><<<1, 32, 0, st>>>(sg, rank, epoch, 1);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ag_shards(const P2PPtrs& dsts, const void* shard, int64_t bytes_S, int rank, int m,
@@ -588,10 +544,11 @@ static cudaError_t rs_adam_mbs(const AdamBlock* tbl, int64_t nblocks, const P2PP
                                cudaStream_t st, const AdamBlockC* ctbl, const UnitBase* ubase, int n_units) {
   constexpr int nst = RsaGeom<M>::STAGES;
   const size_t smem = size_t(RsaGeom<M>::STAGE_BYTES) * nst;
-  static const int grid = [&] {
-    int b = 0;
+  if (once_per_device(reinterpret_cast<const void*>(rs_adam_tma_kernel<M, true, SYNC, PUSH>)))
     cudaFuncSetAttribute(rs_adam_tma_kernel<M, true, SYNC, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
+  static const int grid = [&] {
+    int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_adam_tma_kernel<M, true, SYNC, PUSH>, RSA_NT, smem);
     return num_sms() * (b < 1 ? 1 : b);
   }();

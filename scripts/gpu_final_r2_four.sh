@@ -1,5 +1,5 @@
 # round 2 final check on 4 GPUs: multi-GPU parity, bench N=2/4 (p2p default + NCCL baseline), NVLink counters at N=4
-O=gpurun_out/final2m; mkdir -p $O
+O=gpurun_out/final3m; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 1500 python -m pytest tests/test_gpu_multi.py tests/test_gpu_fullsize.py -q -m gpu > $O/pytest_multi.log 2>&1; echo multi_rc=$?; tail -2 $O/pytest_multi.log
 for n in 2 4; do
