@@ -456,9 +456,10 @@ def profile_nvlink(kernel, world):
     p = os.path.join(ROOT, "profiles", "ncu_nvlink.json")
     try:
         with open(p) as f:
-            e = json.load(f).get(kernel)
-        if e and e.get("workload") == WORKLOAD and e.get("n_gpus") == world:
-            return e
+            es = json.load(f).get(kernel)
+        for e in (es if isinstance(es, list) else [es]):  # one capture per world size
+            if e and e.get("workload") == WORKLOAD and e.get("n_gpus") == world:
+                return e
     except Exception:
         pass
     return None
@@ -831,7 +832,7 @@ def run_ours(args):
         nvlink = {"rank": rank, "counters": NvlinkCounters.delta(nvl0, nvl1, K),
                   "error": nvl.err, "nvml_raw": nvl1, "algorithmic_wire_in_bytes_per_step": wire_rank,
                   "ncu": "profiles/ncu_nvlink.json (nvlrx__bytes / nvltx__bytes of the fused kernel at "
-                         "N = 2, one process driving both GPUs: scripts/ncu_nvlink_local.py)",
+                         "N = 2 and 4, one process driving the GPUs: scripts/ncu_nvlink_local.py)",
                   "note": "NVML NVLink counters of this rank's GPU around the timed region "
                           "(all links; data = payload KiB counters, bytes = raw link bytes)"}
         if nvlink["counters"]:
