@@ -89,9 +89,10 @@ def parse():
     ap.add_argument("--collectives", choices=["p2p", "nccl"], default="p2p",
                     help="p2p: fused single-kernel collectives over NVLink peer memory "
                          "(SURVEY N1); nccl: ncclAllGather / cast kernel + ncclReduceScatter")
-    ap.add_argument("--watchdog", type=float, default=0.0,
-                    help="debugging: after this many seconds every rank prints all its Python "
-                         "stacks and exits (faulthandler), instead of hanging until killed")
+    ap.add_argument("--watchdog", type=float, default=1800.0,
+                    help="after this many seconds every rank prints all its Python stacks and "
+                         "exits (faulthandler) instead of hanging until killed; 0 = off (the "
+                         "default run takes a few minutes)")
     return ap.parse_args()
 
 
