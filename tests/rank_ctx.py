@@ -112,33 +112,47 @@ def drive_proc(gen):
     torch.cuda.synchronize()
 
 
-def drive_local(world, case, *args, **kw):
-    """Run `case` for `world` logical ranks on the current device; returns the
-    contexts (their .msgs hold the failures).  Raises if the ranks' yield
-    counts differ (an SPMD bug) or a p2p barrier timed out."""
-    comms = [R.Comm.local(world, r) for r in range(world)]
-    streams = [torch.cuda.Stream() for _ in range(world)]
+def _sync_all(devs):
+    for d in sorted(set(devs)):
+        torch.cuda.synchronize(d)
+
+
+def drive_local(world, case, *args, devices=None, **kw):
+    """Run `case` for `world` logical ranks on the current device -- or rank r
+    on devices[r] (one process driving several GPUs, peer access over
+    NVLink); returns the contexts (their .msgs hold the failures).  Raises if
+    the ranks' yield counts differ (an SPMD bug) or a p2p barrier timed out."""
+    devs = list(devices) if devices else [torch.cuda.current_device()] * world
+    comms, streams = [], []
+    for r in range(world):
+        with torch.cuda.device(devs[r]):
+            comms.append(R.Comm.local(world, r))
+            streams.append(torch.cuda.Stream())
     shared = {}
     ctxs = [LocalCtx(r, world, comms[r], comms, shared, streams[r]) for r in range(world)]
-    torch.cuda.synchronize()
-    gens = [case(c, *args, **kw) for c in ctxs]
+    _sync_all(devs)
+    gens = []
+    for r, c in enumerate(ctxs):
+        with torch.cuda.device(devs[r]):
+            gens.append(case(c, *args, **kw))
     alive = [True] * world
     steps = [0] * world
     while any(alive):
         for r in range(world):
             if not alive[r]:
                 continue
-            with torch.cuda.stream(streams[r]):
+            with torch.cuda.device(devs[r]), torch.cuda.stream(streams[r]):
                 try:
                     next(gens[r])
                     steps[r] += 1
                 except StopIteration:
                     alive[r] = False
-        torch.cuda.synchronize()
+        _sync_all(devs)
         if any(alive) and not all(alive):
             raise RuntimeError(f"ranks left the case at different yields: {steps}")
-    for c in ctxs:
-        for p in c.p2ps:
-            p.check()  # raises if one of its barriers timed out
-    torch.cuda.synchronize()
+    for r, c in enumerate(ctxs):
+        with torch.cuda.device(devs[r]):
+            for p in c.p2ps:
+                p.check()  # raises if one of its barriers timed out
+    _sync_all(devs)
     return ctxs

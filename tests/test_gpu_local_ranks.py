@@ -29,3 +29,20 @@ def test_local_ranks(world):
                        capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-6000:], r.stderr[-3000:])
     assert r.returncode == 0 and f"world={world}: PASS" in r.stdout
+
+
+@pytest.mark.parametrize("devices", [[0, 1], [0, 1, 0, 1]])
+def test_local_ranks_across_devices(devices):
+    """The same cases with ONE process driving two GPUs (logical rank r on
+    devices[r]; two ranks per device in the second case): per-device kernel
+    setup (shared-memory attributes, constant tables) and peer mappings
+    across devices -- the single-process multi-GPU mode the NVLink counter
+    captures use (scripts/ncu_nvlink_local.py)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = len(devices)
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    r = subprocess.run([sys.executable, os.path.join(HERE, "local_ranks_worker.py"), str(world), "--devices",
+                        ",".join(map(str, devices))], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-6000:], r.stderr[-3000:])
+    assert r.returncode == 0 and "PASS" in r.stdout.splitlines()[-1]
