@@ -78,9 +78,12 @@ __device__ __forceinline__ void p2p_done(const P2PSignals& sg, int rank, int m, 
     unsigned int* ctr = reinterpret_cast<unsigned int*>(sg.local + 16);
     const unsigned int old = atomicAdd(ctr, 1u);
     if (old == gridDim.x - 1) {
-      // every CTA's fence + counter increment precede this one's (release
-      // pattern); the release stores below carry them to the peers
+      // every CTA's fence + counter increment precede this one's (their
+      // release patterns); this read of the counter + the fence below is the
+      // matching acquire pattern, so the release stores below carry every
+      // CTA's (remote) stores to the peers
       atomicExch(ctr, 0u);
+      __threadfence_system();
 #pragma unroll
       for (int r = 0; r < P2P_MAX_RANKS; ++r)
         if (r < m && r != rank) st_release_sys(sg.peer[r] + 8 + rank, epoch);
