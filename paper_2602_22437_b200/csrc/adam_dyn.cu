@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "adam_dev.cuh"
 #include "kernels.cuh"
@@ -286,56 +287,78 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
     if (fast) {
       const AdamStage& S = T.stage[st];
       float p[G::EPT], m[G::EPT], v[G::EPT];
+      // the source (stage / global) and the codec's "both absmax usable" test
+      // are block-uniform: compile each case as its own straight-line code
+      auto update = [&](auto staged_t) {
 #pragma unroll
-      for (int k = 0; k < G::Q; ++k) {
-        const int a = G::quad(k);
-        int4 pv, gv;
-        uint32_t cm, cv;
-        if (staged) {
-          pv = *reinterpret_cast<const int4*>(S.p + a);
-          gv = *reinterpret_cast<const int4*>(S.g + a);
-          cm = *reinterpret_cast<const uint32_t*>(S.mq + a);
-          cv = *reinterpret_cast<const uint32_t*>(S.vq + a);
-        } else {
-          pv = ld_na_v4(P.master + blk.state_off + a);
-          gv = ld_nc_v4(P.grad + blk.grad_off + a);
-          cm = ld_na_u32(mq + blk.state_off + a);
-          cv = ld_na_u32(P.vq + blk.state_off + a);
-        }
-        const float pp[4] = {__int_as_float(pv.x), __int_as_float(pv.y), __int_as_float(pv.z),
-                             __int_as_float(pv.w)};
-        const float gg[4] = {__int_as_float(gv.x), __int_as_float(gv.y), __int_as_float(gv.z),
-                             __int_as_float(gv.w)};
+        for (int k = 0; k < G::Q; ++k) {
+          const int a = G::quad(k);
+          int4 pv, gv;
+          uint32_t cm, cv;
+          if constexpr (decltype(staged_t)::value) {
+            pv = *reinterpret_cast<const int4*>(S.p + a);
+            gv = *reinterpret_cast<const int4*>(S.g + a);
+            cm = *reinterpret_cast<const uint32_t*>(S.mq + a);
+            cv = *reinterpret_cast<const uint32_t*>(S.vq + a);
+          } else {
+            pv = ld_na_v4(P.master + blk.state_off + a);
+            gv = ld_nc_v4(P.grad + blk.grad_off + a);
+            cm = ld_na_u32(mq + blk.state_off + a);
+            cv = ld_na_u32(P.vq + blk.state_off + a);
+          }
+          const float pp[4] = {__int_as_float(pv.x), __int_as_float(pv.y), __int_as_float(pv.z),
+                               __int_as_float(pv.w)};
+          const float gg[4] = {__int_as_float(gv.x), __int_as_float(gv.y), __int_as_float(gv.z),
+                               __int_as_float(gv.w)};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float mt = __fmul_rn(rmap(mapm, int((cm >> (8 * j)) & 0xffu), lane), Am);
-          const float vt = __fmul_rn(rmap(mapv, int((cv >> (8 * j)) & 0xffu), lane), Av);
-          const ElemOut r = adam_elem(pp[j], gg[j], mt, vt, s);
-          p[4 * k + j] = r.p;
-          m[4 * k + j] = r.m;
-          v[4 * k + j] = r.v;
-          am = fmax_nan(am, fabsf(r.m));
-          av = fmax_nan(av, r.v);
+          for (int j = 0; j < 4; ++j) {
+            const float mt = __fmul_rn(rmap(mapm, int((cm >> (8 * j)) & 0xffu), lane), Am);
+            const float vt = __fmul_rn(rmap(mapv, int((cv >> (8 * j)) & 0xffu), lane), Av);
+            const ElemOut r = adam_elem(pp[j], gg[j], mt, vt, s);
+            p[4 * k + j] = r.p;
+            m[4 * k + j] = r.m;
+            v[4 * k + j] = r.v;
+            am = fmax_nan(am, fabsf(r.m));
+            av = fmax_nan(av, r.v);
+          }
         }
-      }
+      };
+      if (staged)
+        update(std::true_type{});
+      else
+        update(std::false_type{});
       block_max2<G::WARPS>(am, av, rm, rv);
       refill();
       set_div(am, av);
+      auto store_all = [&](auto ok_t) {
+        auto QM = [&](float x) {
+          if constexpr (decltype(ok_t)::value) return dyn_code<true>(T.tm, div_exact(x, rAm));
+          else return qm(x);
+        };
+        auto QV = [&](float x) {
+          if constexpr (decltype(ok_t)::value) return dyn_code<false>(T.tv, div_exact(x, rAv));
+          else return qv(x);
+        };
 #pragma unroll
-      for (int k = 0; k < G::Q; ++k) {
-        const int a = G::quad(k);
-        const float* pk = &p[4 * k];
-        st_f4(P.master + blk.state_off + a, make_float4(pk[0], pk[1], pk[2], pk[3]));
-        st_u32(mq + blk.state_off + a, qm(m[4 * k]) | (qm(m[4 * k + 1]) << 8) | (qm(m[4 * k + 2]) << 16) |
-                                           (qm(m[4 * k + 3]) << 24));
-        st_u32(P.vq + blk.state_off + a, qv(v[4 * k]) | (qv(v[4 * k + 1]) << 8) | (qv(v[4 * k + 2]) << 16) |
-                                             (qv(v[4 * k + 3]) << 24));
-        if constexpr (PARAM_BF16)
-          st_u2(static_cast<uint16_t*>(P.param) + blk.param_off + a,
-                make_uint2(pack_bf16x2(pk[0], pk[1]), pack_bf16x2(pk[2], pk[3])));
-        else
-          st_f4(static_cast<float*>(P.param) + blk.param_off + a, make_float4(pk[0], pk[1], pk[2], pk[3]));
-      }
+        for (int k = 0; k < G::Q; ++k) {
+          const int a = G::quad(k);
+          const float* pk = &p[4 * k];
+          st_f4(P.master + blk.state_off + a, make_float4(pk[0], pk[1], pk[2], pk[3]));
+          st_u32(mq + blk.state_off + a, QM(m[4 * k]) | (QM(m[4 * k + 1]) << 8) | (QM(m[4 * k + 2]) << 16) |
+                                             (QM(m[4 * k + 3]) << 24));
+          st_u32(P.vq + blk.state_off + a, QV(v[4 * k]) | (QV(v[4 * k + 1]) << 8) | (QV(v[4 * k + 2]) << 16) |
+                                               (QV(v[4 * k + 3]) << 24));
+          if constexpr (PARAM_BF16)
+            st_u2(static_cast<uint16_t*>(P.param) + blk.param_off + a,
+                  make_uint2(pack_bf16x2(pk[0], pk[1]), pack_bf16x2(pk[2], pk[3])));
+          else
+            st_f4(static_cast<float*>(P.param) + blk.param_off + a, make_float4(pk[0], pk[1], pk[2], pk[3]));
+        }
+      };
+      if (okm && okv)
+        store_all(std::true_type{});
+      else
+        store_all(std::false_type{});
     } else {
       auto elem = [&](int i, float& m, float& v) -> float {  // update element i, returns new p
         const int64_t o = blk_off(blk, i);
