@@ -217,8 +217,20 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
   DynSmem& T = *reinterpret_cast<DynSmem*>(dyn_smem);
   __shared__ __align__(8) uint64_t full[DYN_STAGES];
   __shared__ float red_m[2][DYN_NT / 32], red_v[2][DYN_NT / 32];
+  // the block's table entry and its two stored absmax travel with the stage
+  // (entry stored by thread 0, absmax by cp.async completing on the stage's
+  // barrier), so no thread starts a block with the dependent global loads
+  // tbl[b] -> absmax[slot] (with them: long-scoreboard 2.9 per issue)
+  __shared__ AdamBlock ent[DYN_STAGES];
+  __shared__ __align__(8) float ent_abs[DYN_STAGES][2];
   auto issue = [&](int64_t b, int st) {  // thread 0: stage st <- block b
     const AdamBlock nb = tbl[b];
+    ent[st] = nb;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&ent_abs[st][0])), "l"(P.mabs + nb.slot)
+                 : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&ent_abs[st][1])), "l"(P.vabs + nb.slot)
+                 : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[st])) : "memory");
     if (adam_tma_ok(nb)) {
       mbar_arrive_expect_tx(&full[st], ADAM_STAGE_TX);
       bulk_g2s(T.stage[st].p, P.master + nb.state_off, sizeof(float) * ADAM_TILE, &full[st]);
@@ -230,7 +242,7 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
     }
   };
   if (threadIdx.x == 0) {
-    for (int st = 0; st < DYN_STAGES; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < DYN_STAGES; ++st) mbar_init(&full[st], 2);  // the copies' arrival + thread 0's
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int st = 0; st < DYN_STAGES; ++st) {
       const int64_t b = blockIdx.x + int64_t(st) * gridDim.x;
@@ -254,8 +266,9 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++it) {
     const int st = it % DYN_STAGES;
     const uint32_t ph = uint32_t(it / DYN_STAGES) & 1u;
-    const AdamBlock blk = tbl[b];
-    const float Am = P.mabs[blk.slot], Av = P.vabs[blk.slot];
+    mbar_wait(&full[st], ph);
+    const AdamBlock blk = ent[st];
+    const float Am = ent_abs[st][0], Av = ent_abs[st][1];
     float* rm = red_m[it & 1];
     float* rv = red_v[it & 1];
     auto refill = [&]() {  // after the absmax barrier: every thread has read stage st
@@ -280,7 +293,6 @@ __global__ void __launch_bounds__(DYN_NT, 3) adam8_dyn_kernel(const AdamBlock* _
       rAv = okv ? 1.0 / double(av_) : 0.0;
     };
     float am = 0.f, av = 0.f;
-    mbar_wait(&full[st], ph);
     const bool staged = adam_tma_ok(blk);
     const bool fast = staged || (blk.len == ADAM_TILE && blk.cols == blk.len && (blk.state_off & 3) == 0 &&
                                  (blk.grad_off & 3) == 0 && (blk.param_off & 3) == 0);
