@@ -1,6 +1,6 @@
 # round 2 final check on 4 GPUs: multi-GPU parity, bench N=4 (N=2 and the NCCL baselines ran on earlier boxes:
 # profiles/r2/final3m), NVLink counters at N=4 (single process driving the 4 GPUs)
-O=gpurun_out/final4m; mkdir -p $O
+O=gpurun_out/final7m; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 1200 python -m pytest tests/test_gpu_multi.py tests/test_gpu_fullsize.py -q -m gpu > $O/pytest_multi.log 2>&1; echo multi_rc=$?; tail -2 $O/pytest_multi.log
 timeout 720 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29814 bench.py --gpus 4 --watchdog 650 > $O/bench_n4.json 2> $O/bench_n4.err; echo bench_n4_rc=$?
